@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: grid points solved per second (fp64) for BASELINE config 4 on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--cfg C]
+
+A step is one full direct solve (forward 2D DST-I -> per-mode Thomas along z ->
+inverse 2D DST-I) of the config's seeded synthetic RHS. N=1: the whole grid
+on one GPU; N>1 (torchrun, one rank per GPU): z-slabs, NCCL all-to-all to
+y-slabs for the z-solves and back (the reference's Partitioned geometry),
+strong scaling of the same grid. Rank 0 prints ONE JSON line.
+
+`value` times device-resident data with CUDA events (inputs, 8.6 GB, are far
+larger than L2). `e2e` goes through the C-ABI host-buffer entry
+(hfb_solve_host: pinned H2D, solve, D2H). `cpu_baseline` times the oracle
+port (numpy/scipy, all host threads) on a bounded slab of the same planes.
+`--impl reference` times that CPU port alone (the reference is Python: there
+is no compiled oracle/_ref).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid points solved/sec (fp64) at 1/2/4/8 B200; % of HBM/NVLink roofline"
+ALG_BYTES_PER_PT = 48  # 3 stages x (8 B read + 8 B write)
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cfg", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-planes", type=int, default=64)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def workload_config(w, n_gpus):
+    return {"workload": f"cfg{w.cfg}: {WORKLOAD_TEXT[w.cfg]}", "n": w.n,
+            "points": w.n ** 3, "scheme": getattr(w.scheme, "value", "table"),
+            "rhs": w.rhs_kind, "seed": w.seed,
+            "parallelism": "single" if n_gpus == 1 else f"zslab{n_gpus}+nccl_alltoall",
+            "l2_flush": f"inputs {w.n ** 3 * 8 / 1e9:.1f} GB >> 126 MB L2 (no flush needed)"}
+
+
+WORKLOAD_TEXT = {
+    1: "4th-order Helmholtz 31^3, k=10(1+0.5 sin pi z)",
+    2: "6th-order Helmholtz 127^3, k=10(1+0.5 sin pi z)",
+    3: "6th-order Helmholtz 511^3, k=40(1+0.3 sin 2 pi z), F~N(0,1)",
+    4: "4th-order conv-diff 1023^3, -lap u + 1.5 u_z (gamma=-1.5), F~U[-1,1]",
+    5: "general 27-pt table 2047^3, seeded rows, centre=1.5 sum|off|, F~N(0,1)",
+}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    import torch.distributed as dist
+    if n_gpus > 1 or "RANK" in os.environ:
+        if not dist.is_initialized():
+            local = int(os.environ.get("LOCAL_RANK", 0))
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return dist.get_rank(), dist.get_world_size(), int(os.environ.get("LOCAL_RANK", 0))
+    return 0, 1, 0
+
+
+def oracle_baseline(w, planes, workers):
+    """Oracle port on the first `planes` z-planes (full n x n planes) of the workload."""
+    from oracle import helm_oracle as orc
+    from paper_1912_03565_b200 import stencil as st
+    import paper_1912_03565_b200 as hb
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, (planes + 1) / (w.n + 1)), w.n, w.n, planes)
+    if isinstance(w.scheme, hb.StencilTable):
+        T = tuple(t[:planes] for t in (w.scheme.A, w.scheme.B, w.scheme.C, w.scheme.D))
+    else:
+        prof = w.profile
+        k = lambda a: np.real(np.asarray(a))[:planes + 2]
+        T = orc.weight_table(w.scheme.value, k(prof.k2), k(prof.k2_z), k(prof.k2_zz),
+                             complex(prof.gamma).real, (g.h_x, g.h_y, g.h_z), planes)
+    cx, cy = orc.mode_cosines(w.n, w.n)
+    from paper_1912_03565_b200 import workloads as wl
+    F = wl.host_rhs(w, planes=planes)
+    orc.solve(F[:2], tuple(t[:2] for t in T), cx, cy, workers=workers)  # warm the FFT plans
+    t0 = time.perf_counter()
+    orc.solve(F, T, cx, cy, workers=workers)
+    dt = time.perf_counter() - t0
+    del st
+    return planes * w.n * w.n / dt, dt
+
+
+def run_reference(args):
+    rank, world, _ = (0, 1, 0)
+    if args.gpus > 1 or "RANK" in os.environ:
+        rank = int(os.environ.get("RANK", 0))
+        if rank != 0:
+            return
+    from paper_1912_03565_b200 import workloads as wl
+    w = wl.workload(args.cfg)
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle_baseline(w, max(2, args.cpu_planes // 4), cores)
+    vals = []
+    for _ in range(args.steps):
+        v, dt = oracle_baseline(w, args.cpu_planes, cores)
+        vals.append(v)
+    value = statistics.median(vals)
+    sample = (f"{args.cpu_planes} of {w.n} z-planes (full {w.n}x{w.n} planes) per step, "
+              f"oracle port numpy/scipy DUCC0, {cores} threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pts/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": args.cpu_planes * w.n * w.n / value * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": workload_config(w, args.gpus),
+            "cpu_baseline": {"value": value, "unit": "pts/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "pts/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import ctypes
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_03565_b200 as hb
+    from paper_1912_03565_b200 import _native, workloads as wl
+    from paper_1912_03565_b200.tridiag import device_coefficients
+
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    w = wl.workload(args.cfg)
+    n = w.n
+    lib = _native.load_library()
+    multi = world > 1
+
+    def barrier():
+        if multi:
+            dist.barrier(device_ids=[local])
+
+    if not multi:
+        plan = _native.get_plan(n, n, n, dev)
+        device_coefficients(plan, w.scheme, w.profile, w.grid)
+        F = wl.device_rhs(w, dev)
+        U = torch.empty_like(F)
+        work = plan.workspace(0)
+        st = plan.stream()
+
+        def step():
+            _native.check(lib.hfb_solve(plan.handle, _native.ptr(F), _native.ptr(U),
+                                        _native.ptr(work), st), "solve")
+    else:
+        from paper_1912_03565_b200 import distributed as hd
+        ex = hb.make_exchange_plan(w.grid, world)
+        z0, z1 = ex.partition.z_ranges[rank]
+        g = torch.Generator(device=dev)
+        g.manual_seed(w.seed * 1000 + rank)
+        F = torch.rand((z1 - z0, n, n), generator=g, device=dev, dtype=torch.float64)
+        F.mul_(2.0).sub_(1.0)
+
+        def step():
+            hd.solve_partitioned(F, w.scheme, w.profile, w.grid)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    if not multi:
+        plan.fetch_status()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    l0 = lib.hfb_launch_count()
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    barrier()
+    launches = int(lib.hfb_launch_count() - l0)
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if multi:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    points = n ** 3
+    value = points / (ms / 1e3)
+
+    # ---- end to end through the C-ABI host-buffer entry (pinned H2D + solve + D2H)
+    e2e = None
+    if not args.no_e2e:
+        if not multi:
+            hin = torch.empty(F.shape, dtype=torch.float64, pin_memory=True)
+            hin.copy_(F)
+            hout = torch.empty_like(hin).pin_memory()
+            status = _native.HfbStatus()
+            _native.check(lib.hfb_solve_host(plan.handle, _native.ptr(hin), _native.ptr(hout),
+                                             _native.ptr(work), st, ctypes.byref(status)), "e2e")
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                _native.check(lib.hfb_solve_host(plan.handle, _native.ptr(hin),
+                                                 _native.ptr(hout), _native.ptr(work), st,
+                                                 ctypes.byref(status)), "e2e")
+            e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+            nbytes = F.numel() * 8
+            del hin, hout
+        else:
+            from paper_1912_03565_b200 import distributed as hd
+            hin = F.cpu().pin_memory()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                d = hin.to(dev, non_blocking=True)
+                u = hd.solve_partitioned(d, w.scheme, w.profile, w.grid)
+                u.cpu()
+            barrier()
+            e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+            tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+            nbytes = F.numel() * 8
+        e2e = {"value": points / e2e_s, "unit": "pts/s", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "ms_per_step": e2e_s * 1e3,
+               "path": "C-ABI hfb_solve_host (pinned host buffers)" if not multi
+               else "pinned H2D + solve_partitioned + D2H per rank"}
+
+    if rank != 0:
+        if multi:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    achieved = ALG_BYTES_PER_PT * points / (ms / 1e3) / 1e9 / (world if multi else 1)
+    traffic = None
+    prof_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof_path):
+        try:
+            traffic = json.load(open(prof_path)).get(f"cfg{args.cfg}_bytes_per_step")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "whole solve pipeline (all launches of one step)",
+                "alg_bytes_per_point": ALG_BYTES_PER_PT, "peak_source": peak_src}
+    cpu = None
+    if not args.no_cpu and not multi:
+        cores = os.cpu_count() or 1
+        v, dt = oracle_baseline(w, args.cpu_planes, cores)
+        cpu = {"value": v, "unit": "pts/s", "cores": cores, "kind": "port",
+               "sample": f"{args.cpu_planes} of {n} z-planes (full {n}x{n} planes), "
+                         f"{dt:.1f} s, numpy/scipy oracle"}
+    line = {"metric": METRIC, "value": value, "unit": "pts/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, generated on device)",
+            "config": workload_config(w, world), "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "device": torch.cuda.get_device_name(dev)}
+    print(json.dumps(line), flush=True)
+    if multi:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

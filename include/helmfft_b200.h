@@ -1,0 +1,175 @@
+/*
+ * helmfft_b200.h — C-ABI of the B200 (sm_100a) hot path of the arXiv 1912.03565
+ * direct solver: forward orthonormal 2D DST-I of every z-plane, N_x*N_y
+ * independent tridiagonal (Thomas) solves along z, inverse 2D DST-I, plus the
+ * compact-scheme RHS operators and the 27-point operator used for folding and
+ * residuals.
+ *
+ * The reference (`helmfft`, pure Python on numpy/scipy) has no FFI; its
+ * boundary is the Python API. Each entry point below replaces one reference
+ * operator and is bound from Python through ctypes
+ * (paper_1912_03565_b200/_native.py; INTEGRATION.md shows the stub a helmfft
+ * maintainer would add). Conventions:
+ *
+ *  - every array is fp64 real, C order (n_z, n_y, n_x), x fastest — the
+ *    row ordering of reference assembly.py:32-34 / oracle.py:27-29;
+ *  - device pointers are borrowed for the duration of the call; all work is
+ *    enqueued on `stream` (a cudaStream_t passed as void*, NULL = legacy);
+ *  - workspaces are allocated by the caller (PyTorch) with the size that
+ *    hfb_workspace_bytes() reports;
+ *  - calls return an hfb_code; singular pivots are detected on the device and
+ *    reported by hfb_status_fetch() (the only synchronising call).
+ */
+#ifndef HELMFFT_B200_H
+#define HELMFFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HFB_OK = 0,
+  HFB_ERR_ARGUMENT = 1,      /* ValueError: shapes, extents            */
+  HFB_ERR_RANGE = 2,         /* IndexError: plane / pencil ranges      */
+  HFB_ERR_SINGULAR = 3,      /* SingularSystemError(n, m)              */
+  HFB_ERR_PARTITION = 4,     /* InvalidPartitionError                  */
+  HFB_ERR_EXCHANGE = 5,      /* ExchangeError(sender, receiver)        */
+  HFB_ERR_CUDA = 6,          /* CUDA runtime failure                   */
+  HFB_ERR_NO_COEFFICIENTS = 7
+} hfb_code;
+
+/* Error payload; mirrors the reference exceptions (errors.py:1-31). */
+typedef struct {
+  int code;
+  int64_t l;        /* 1-based row level of the vanishing pivot            */
+  int64_t m;        /* 1-based global sine mode along y                   */
+  int64_t n;        /* 1-based sine mode along x                          */
+  int sender;
+  int receiver;
+  char msg[256];
+} hfb_status;
+
+typedef struct hfb_plan hfb_plan;
+
+/* Library version string. */
+const char* hfb_version(void);
+
+/* Human-readable text for an hfb_code. */
+const char* hfb_strerror(int code);
+
+/* Number of kernels this library has launched in the process (all plans). */
+uint64_t hfb_launch_count(void);
+
+/* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.
+ * Replaces spectral.make_plan (spectral.py:46-51) and carries the per-row
+ * coefficient table that tridiag.solve_slab builds on every call
+ * (tridiag.py:112-123). Twiddle, sine and (for N+1 not a power of two)
+ * dense DST-I tables are built here. */
+int hfb_plan_create(int n_x, int n_y, int n_z, int device, hfb_plan** out);
+int hfb_plan_destroy(hfb_plan* plan);
+
+/* Upload the row coefficient table and mode cosines.
+ * table: n_z * 12 doubles, row l (0-based) holds, for level offset k = 0,1,2
+ *        (levels l-1, l, l+1), the weights (a, b, c, d) — i.e.
+ *        table[l*12 + k*4 + {0,1,2,3}] = A[l,k], B[l,k], C[l,k], D[l,k]
+ *        of stencil.coefficient_table (stencil.py:177-195);
+ * cx: n_x cosines cos(pi n/(n_x+1)), cy: n_y cosines (stencil.py:219-223);
+ * pivot_threshold: PIVOT_RTOL * max|table| (tridiag.py:22, 136-137). */
+int hfb_plan_set_coefficients(hfb_plan* plan, const double* table, const double* cx,
+                              const double* cy, double pivot_threshold);
+
+/* Workspace sizes in bytes. op: 0 = hfb_solve, 1 = hfb_transform_stack,
+ * 2 = hfb_solve_slab (for the full n_y modes). */
+size_t hfb_workspace_bytes(const hfb_plan* plan, int op);
+
+/* Orthonormal 2D DST-I (x-pass then y-pass) of planes [z0, z1) in place.
+ * Replaces spectral.transform_stack (spectral.py:75-91). */
+int hfb_transform_stack(hfb_plan* plan, double* data, int z0, int z1, void* work,
+                        void* stream);
+
+/* 1D passes on all planes, restricted to a y-range (x-pass) or an x-range
+ * (y-pass). Replace spectral.transform_lines_x/y (spectral.py:94-111). */
+int hfb_transform_lines_x(hfb_plan* plan, double* data, int y0, int y1, void* work,
+                          void* stream);
+int hfb_transform_lines_y(hfb_plan* plan, double* data, int x0, int x1, void* work,
+                          void* stream);
+
+/* Thomas sweep over a (n_z, m_count, n_x) slab in place; local row j is
+ * global mode m_offset + j. Replaces tridiag.solve_slab/_sweep
+ * (tridiag.py:112-167). Pivot failures are latched for hfb_status_fetch. */
+int hfb_solve_slab(hfb_plan* plan, double* slab, int m_count, int m_offset, void* work,
+                   void* stream);
+
+/* Batched Thomas on explicit bands (tridiag.solve_system, tridiag.py:59-90):
+ * sub/diag/sup/x are (nsys, n) doubles, or (nsys, n) interleaved complex when
+ * is_complex != 0; x is overwritten with the solution; cp_ws has x's size.
+ * thr[s] = PIVOT_RTOL * max band magnitude of system s; the first vanishing
+ * pivot is latched into *err as s*n + row (caller initialises *err = ~0). */
+int hfb_solve_bands(const double* sub, const double* diag, const double* sup, double* x,
+                    double* cp_ws, int n, int nsys, int is_complex, const double* thr,
+                    unsigned long long* err, void* stream);
+
+/* Full solve: U = V_z-solve(V F), V = 2D DST-I. rhs and out may alias
+ * (in place). Replaces the Sequential/SharedWorkers branch of
+ * solver.solve_discrete (solver.py:293-317) after the Dirichlet fold. */
+int hfb_solve(hfb_plan* plan, const double* rhs, double* out, void* work, void* stream);
+
+/* Same as hfb_solve with host (ideally pinned) buffers: H2D, solve, D2H,
+ * synchronised, pivot status reported in *status (may be NULL). */
+int hfb_solve_host(hfb_plan* plan, const double* host_rhs, double* host_out, void* work,
+                   void* stream, hfb_status* status);
+
+/* Synchronise `stream`, report (and clear) a latched singular pivot. */
+int hfb_status_fetch(hfb_plan* plan, void* stream, hfb_status* status);
+
+/* Fourth-order RHS operator F = h_z^2 (f/2 + (1/12) sum of the 6 face
+ * neighbours) of f sampled on the closed (n_z+2, n_y+2, n_x+2) grid.
+ * Replaces the FOURTH_ORDER branch of assembly.build_rhs (assembly.py:183-193). */
+int hfb_rhs_fourth(hfb_plan* plan, const double* f_closed, double* rhs, double h_z2,
+                   void* stream);
+
+/* Pointwise RHS combinations of sampled fields (assembly.py:180-181, 195-224).
+ * kind 2: F = hz2*f. kind 6: fields = {f, lap_f, d4_f, f_xxyy, f_xxzz, f_yyzz,
+ * f_z}, params = {h2, k2[1..nz] ptr unused}. See hfb_rhs_sixth/cd4. */
+int hfb_rhs_second(hfb_plan* plan, const double* f, double* rhs, double h_z2, void* stream);
+int hfb_rhs_sixth(hfb_plan* plan, const double* f, const double* lap, const double* d4,
+                  const double* fxxyy, const double* fxxzz, const double* fyyzz,
+                  const double* fz, const double* k2_levels /* n_z */,
+                  const double* k2z_levels /* n_z */, double h2, double* rhs, void* stream);
+int hfb_rhs_convdiff(hfb_plan* plan, const double* f, const double* fxx, const double* fyy,
+                     const double* fz, const double* fzz, double hx2, double hy2, double hz2,
+                     double gamma, double* rhs, void* stream);
+
+/* 27-point operator on a closed-box array ext (n_z+2, n_y+2, n_x+2):
+ * out = A*ext restricted to the interior, with the reference's term order and
+ * zero-column skipping (assembly.py:229-244). term_mask bit (k*9 + o) enables
+ * level offset k (0..2) and plane offset o in the order a(-1,-1),(1,-1),(-1,1),
+ * (1,1), b(-1,0),(1,0), c(0,-1),(0,1), d(0,0). mode 0: out = A ext;
+ * mode 1: out = rhs - A ext (Dirichlet fold, assembly.py:258-274). */
+int hfb_apply27(hfb_plan* plan, const double* ext, const double* rhs, double* out,
+                uint32_t term_mask, int mode, void* stream);
+
+/* Sum of squares of (A*u - F) with zero boundary (assembly.py:277-289):
+ * u, F interior arrays; partial sums written to `partial` (length returned by
+ * hfb_residual_partials()). */
+int hfb_residual_partials(const hfb_plan* plan);
+int hfb_residual_sq(hfb_plan* plan, const double* u, const double* rhs, double* partial,
+                    uint32_t term_mask, void* stream);
+
+/* z-slab -> send-buffer pack and receive-buffer -> z-slab unpack for the
+ * partitioned exchange (solver.py:146-201). y_starts has parts+1 entries
+ * (prefix of the y-ranges). Forward: send[q] = slab[:, y-range(q), :]
+ * contiguous, blocks concatenated in ascending q. Inverse: recv blocks
+ * (kpz, kpy(q), n_x) concatenated in ascending q -> slab[:, y-range(q), :]. */
+int hfb_pack_yblocks(hfb_plan* plan, const double* slab, double* send, int kpz,
+                     const int* y_starts, int parts, void* stream);
+int hfb_unpack_yblocks(hfb_plan* plan, const double* recv, double* slab, int kpz,
+                       const int* y_starts, int parts, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HELMFFT_B200_H */

@@ -1,0 +1,280 @@
+// C-ABI entry points: plan lifetime, coefficient upload, transform / tridiag
+// / full-solve drivers and status reporting. See include/helmfft_b200.h.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "hfb_internal.cuh"
+
+namespace hfb {
+static thread_local cudaError_t g_last_cuda = cudaSuccess;
+static std::atomic<unsigned long long> g_launches{0};
+void set_last_cuda(cudaError_t e) { g_last_cuda = e; }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace hfb
+
+extern "C" uint64_t hfb_launch_count(void) { return hfb::g_launches.load(); }
+
+using namespace hfb;
+
+static int ilog2_exact(int m) {
+  if (m < 2 || (m & (m - 1))) return -1;
+  int k = 0;
+  while ((1 << k) < m) ++k;
+  return k;
+}
+
+static int build_fft_tables(int n, double2** tw, double** sn, double* scale) {
+  const int M = n + 1;
+  std::vector<double2> t(M);
+  for (int k = 0; k < M; ++k) {
+    // exp(-2 pi i k / M) with the angle reduced to [0, pi/4]-symmetric form
+    const double a = 2.0 * M_PI * (double)k / (double)M;
+    t[k] = make_double2(std::cos(a), -std::sin(a));
+  }
+  // exact values at the quarter points
+  t[0] = make_double2(1.0, 0.0);
+  if (M % 4 == 0) {
+    t[M / 4] = make_double2(0.0, -1.0);
+    t[M / 2] = make_double2(-1.0, 0.0);
+    t[3 * M / 4] = make_double2(0.0, 1.0);
+  } else if (M % 2 == 0) {
+    t[M / 2] = make_double2(-1.0, 0.0);
+  }
+  std::vector<double> s(M / 2 + 1);
+  for (int j = 0; j <= M / 2; ++j) s[j] = std::sin(M_PI * (double)j / (double)M);
+  s[0] = 0.0;
+  s[M / 2] = 1.0;
+  HFB_CUDA(cudaMalloc(tw, sizeof(double2) * M));
+  HFB_CUDA(cudaMalloc(sn, sizeof(double) * (M / 2 + 1)));
+  HFB_CUDA(cudaMemcpy(*tw, t.data(), sizeof(double2) * M, cudaMemcpyHostToDevice));
+  HFB_CUDA(cudaMemcpy(*sn, s.data(), sizeof(double) * (M / 2 + 1), cudaMemcpyHostToDevice));
+  *scale = std::sqrt(2.0 / (double)M);
+  return HFB_OK;
+}
+
+static int build_dense(int n, double** out) {
+  const long long M = n + 1;
+  std::vector<double> S((size_t)n * n);
+  const double sc = std::sqrt(2.0 / (double)M);
+  for (int a = 1; a <= n; ++a)
+    for (int b = 1; b <= n; ++b) {
+      const long long r = ((long long)a * b) % (2 * M);  // sin is 2M-periodic in r
+      S[(size_t)(a - 1) * n + (b - 1)] = sc * std::sin(M_PI * (double)r / (double)M);
+    }
+  HFB_CUDA(cudaMalloc(out, sizeof(double) * S.size()));
+  HFB_CUDA(cudaMemcpy(*out, S.data(), sizeof(double) * S.size(), cudaMemcpyHostToDevice));
+  return HFB_OK;
+}
+
+extern "C" const char* hfb_version(void) { return "helmfft_b200 0.1.0 (sm_100a)"; }
+
+extern "C" const char* hfb_strerror(int code) {
+  switch (code) {
+    case HFB_OK: return "ok";
+    case HFB_ERR_ARGUMENT: return "invalid argument";
+    case HFB_ERR_RANGE: return "range outside extents";
+    case HFB_ERR_SINGULAR: return "vanishing pivot (singular spectral system)";
+    case HFB_ERR_PARTITION: return "invalid partition";
+    case HFB_ERR_EXCHANGE: return "exchange failure";
+    case HFB_ERR_CUDA: return cudaGetErrorString(hfb::g_last_cuda);
+    case HFB_ERR_NO_COEFFICIENTS: return "plan has no coefficients";
+    default: return "unknown error";
+  }
+}
+
+extern "C" int hfb_plan_destroy(hfb_plan* p) {
+  if (!p) return HFB_OK;
+  cudaSetDevice(p->device);
+  cudaFree(p->tw_x);
+  cudaFree(p->sn_x);
+  cudaFree(p->tw_y);
+  cudaFree(p->sn_y);
+  cudaFree(p->dense_x);
+  cudaFree(p->dense_y);
+  cudaFree(p->coef);
+  cudaFree(p->cx);
+  cudaFree(p->cy);
+  cudaFree(p->err);
+  cudaFree(p->ystarts);
+  cudaFree(p->dev_io);
+  std::free(p);
+  return HFB_OK;
+}
+
+extern "C" int hfb_plan_create(int nx, int ny, int nz, int device, hfb_plan** out) {
+  if (!out || nx < 1 || ny < 1 || nz < 1) return HFB_ERR_ARGUMENT;
+  *out = nullptr;
+  hfb_plan* p = (hfb_plan*)std::calloc(1, sizeof(hfb_plan));
+  if (!p) return HFB_ERR_ARGUMENT;
+  p->nx = nx;
+  p->ny = ny;
+  p->nz = nz;
+  p->device = device;
+  int rc = HFB_OK;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    std::free(p);
+    return HFB_ERR_CUDA;
+  }
+  p->logMx = ilog2_exact(nx + 1);
+  p->logMy = ilog2_exact(ny + 1);
+  if (p->logMx >= 0)
+    rc = build_fft_tables(nx, &p->tw_x, &p->sn_x, &p->scale_x);
+  else
+    rc = build_dense(nx, &p->dense_x);
+  if (!rc) {
+    if (p->logMy >= 0)
+      rc = build_fft_tables(ny, &p->tw_y, &p->sn_y, &p->scale_y);
+    else
+      rc = build_dense(ny, &p->dense_y);
+  }
+  if (!rc && cudaMalloc(&p->err, sizeof(unsigned long long)) != cudaSuccess) rc = HFB_ERR_CUDA;
+  if (!rc && cudaMemset(p->err, 0xff, sizeof(unsigned long long)) != cudaSuccess) rc = HFB_ERR_CUDA;
+  if (rc) {
+    hfb_plan_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return HFB_OK;
+}
+
+extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const double* cx,
+                                         const double* cy, double thr) {
+  if (!p || !table || !cx || !cy) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  const size_t nlev = (size_t)p->nz * 12;
+  // device layout: [scaled (4a,2b,2c,d) x nz*3][raw (a,b,c,d) x nz*3]
+  std::vector<double> buf(2 * nlev);
+  for (size_t e = 0; e < nlev; e += 4) {
+    buf[e + 0] = 4.0 * table[e + 0];
+    buf[e + 1] = 2.0 * table[e + 1];
+    buf[e + 2] = 2.0 * table[e + 2];
+    buf[e + 3] = table[e + 3];
+  }
+  std::memcpy(buf.data() + nlev, table, sizeof(double) * nlev);
+  if (!p->coef) HFB_CUDA(cudaMalloc(&p->coef, sizeof(double) * 2 * nlev));
+  if (!p->cx) HFB_CUDA(cudaMalloc(&p->cx, sizeof(double) * p->nx));
+  if (!p->cy) HFB_CUDA(cudaMalloc(&p->cy, sizeof(double) * p->ny));
+  HFB_CUDA(cudaMemcpy(p->coef, buf.data(), sizeof(double) * 2 * nlev, cudaMemcpyHostToDevice));
+  HFB_CUDA(cudaMemcpy(p->cx, cx, sizeof(double) * p->nx, cudaMemcpyHostToDevice));
+  HFB_CUDA(cudaMemcpy(p->cy, cy, sizeof(double) * p->ny, cudaMemcpyHostToDevice));
+  p->thr = thr;
+  p->have_coef = 1;
+  return HFB_OK;
+}
+
+extern "C" size_t hfb_workspace_bytes(const hfb_plan* p, int op) {
+  if (!p) return 0;
+  const size_t vol = (size_t)p->nx * p->ny * p->nz;
+  const size_t dense = dense_tmp_elems(p, p->nz);
+  switch (op) {
+    case 0: return sizeof(double) * (vol + dense);  // cp + dense temp
+    case 1: return sizeof(double) * dense;
+    case 2: return sizeof(double) * vol;
+    default: return 0;
+  }
+}
+
+static int transform_range(hfb_plan* p, const double* src, double* dst, int z0, int z1,
+                           double* tmp, cudaStream_t st) {
+  int rc = launch_dst_x(p, src, dst, z0, z1, 0, p->ny, tmp, st);
+  if (rc) return rc;
+  return launch_dst_y(p, dst, dst, z0, z1, 0, p->nx, tmp, st);
+}
+
+extern "C" int hfb_transform_stack(hfb_plan* p, double* data, int z0, int z1, void* work,
+                                   void* stream) {
+  if (!p || !data) return HFB_ERR_ARGUMENT;
+  if (z0 < 0 || z0 > z1 || z1 > p->nz) return HFB_ERR_RANGE;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return transform_range(p, data, data, z0, z1, (double*)work, (cudaStream_t)stream);
+}
+
+extern "C" int hfb_transform_lines_x(hfb_plan* p, double* data, int y0, int y1, void* work,
+                                     void* stream) {
+  if (!p || !data) return HFB_ERR_ARGUMENT;
+  if (y0 < 0 || y0 > y1 || y1 > p->ny) return HFB_ERR_RANGE;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return launch_dst_x(p, data, data, 0, p->nz, y0, y1, (double*)work, (cudaStream_t)stream);
+}
+
+extern "C" int hfb_transform_lines_y(hfb_plan* p, double* data, int x0, int x1, void* work,
+                                     void* stream) {
+  if (!p || !data) return HFB_ERR_ARGUMENT;
+  if (x0 < 0 || x0 > x1 || x1 > p->nx) return HFB_ERR_RANGE;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return launch_dst_y(p, data, data, 0, p->nz, x0, x1, (double*)work, (cudaStream_t)stream);
+}
+
+extern "C" int hfb_solve_slab(hfb_plan* p, double* slab, int m_count, int m_offset, void* work,
+                              void* stream) {
+  if (!p || !slab || !work) return HFB_ERR_ARGUMENT;
+  if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
+  if (m_count < 0 || m_offset < 0 || m_offset + m_count > p->ny) return HFB_ERR_RANGE;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return launch_thomas(p, slab, m_count, m_offset, (double*)work, (cudaStream_t)stream);
+}
+
+extern "C" int hfb_solve(hfb_plan* p, const double* rhs, double* out, void* work, void* stream) {
+  if (!p || !rhs || !out || !work) return HFB_ERR_ARGUMENT;
+  if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
+  HFB_CUDA(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t vol = (size_t)p->nx * p->ny * p->nz;
+  double* cpw = (double*)work;
+  double* tmp = dense_tmp_elems(p, p->nz) ? cpw + vol : nullptr;
+  int rc = transform_range(p, rhs, out, 0, p->nz, tmp, st);
+  if (rc) return rc;
+  rc = launch_thomas(p, out, p->ny, 0, cpw, st);
+  if (rc) return rc;
+  return transform_range(p, out, out, 0, p->nz, tmp, st);
+}
+
+extern "C" int hfb_status_fetch(hfb_plan* p, void* stream, hfb_status* s) {
+  if (!p) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long key = ~0ULL;
+  HFB_CUDA(cudaMemcpyAsync(&key, p->err, sizeof(key), cudaMemcpyDeviceToHost, st));
+  HFB_CUDA(cudaStreamSynchronize(st));
+  if (s) std::memset(s, 0, sizeof(*s));
+  if (key == ~0ULL) return HFB_OK;
+  HFB_CUDA(cudaMemsetAsync(p->err, 0xff, sizeof(unsigned long long), st));
+  HFB_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long nx = p->nx, ny = p->ny;
+  const long long n = (long long)(key % nx);
+  const long long m = (long long)((key / nx) % ny);
+  const long long l = (long long)(key / (nx * ny));
+  if (s) {
+    s->code = HFB_ERR_SINGULAR;
+    s->l = l + 1;
+    s->m = m + 1;
+    s->n = n + 1;
+    std::snprintf(s->msg, sizeof(s->msg), "vanishing pivot at row %lld for mode (n=%lld, m=%lld)",
+                  l + 1, n + 1, m + 1);
+  }
+  return HFB_ERR_SINGULAR;
+}
+
+extern "C" int hfb_solve_host(hfb_plan* p, const double* hin, double* hout, void* work,
+                              void* stream, hfb_status* s) {
+  if (!p || !hin || !hout || !work) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = sizeof(double) * (size_t)p->nx * p->ny * p->nz;
+  if (p->dev_io_bytes < bytes) {
+    if (p->dev_io) cudaFree(p->dev_io);
+    p->dev_io = nullptr;
+    p->dev_io_bytes = 0;
+    HFB_CUDA(cudaMalloc(&p->dev_io, bytes));
+    p->dev_io_bytes = bytes;
+  }
+  HFB_CUDA(cudaMemcpyAsync(p->dev_io, hin, bytes, cudaMemcpyHostToDevice, st));
+  int rc = hfb_solve(p, p->dev_io, p->dev_io, work, stream);
+  if (rc) return rc;
+  HFB_CUDA(cudaMemcpyAsync(hout, p->dev_io, bytes, cudaMemcpyDeviceToHost, st));
+  return hfb_status_fetch(p, stream, s);
+}

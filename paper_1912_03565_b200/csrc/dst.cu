@@ -1,0 +1,243 @@
+// Batched orthonormal DST-I along x (contiguous lines) and along y (strided
+// columns) — kernels (b)/(d) of the north star, replacing
+// spectral.dst_lines / transform_stack / transform_lines_x/y
+// (reference spectral.py:54-111).
+//
+// Power-of-two N+1: one complex Stockham FFT per pair of real lines, in
+// shared memory (hfb_internal.cuh). Other N: dense DST-I matrix product
+// (fp64 GEMM, S symmetric), out of place through a temporary.
+#include <algorithm>
+
+#include "hfb_internal.cuh"
+
+namespace hfb {
+
+// Threads per transform group for length M.
+static inline int group_threads(int M) { return M >= 8 ? M / 8 : 1; }
+
+struct LineSet {
+  // rows y0 + 2k, y0 + 2k + 1 of one plane form pair k; pairs never straddle
+  // planes, so a plane range never changes which rows share an FFT (results
+  // are bitwise independent of how the planes are split)
+  int z0, y0, nrow, ppp;  // ppp = pairs per plane = ceil(nrow / 2)
+  long long npairs;
+  long long ld, ps;       // row and plane strides (elements)
+};
+
+// x-pass: CTA = B groups of G threads; group f transforms one row pair as one
+// complex FFT (real part = even row, imaginary part = odd row).
+__global__ void __launch_bounds__(512) dst_x_fft_kernel(const double* __restrict__ src,
+                                                         double* __restrict__ dst, LineSet s,
+                                                         int N, FftCtx c, int B) {
+  extern __shared__ double2 smem[];
+  const int f = threadIdx.x / c.G, g = threadIdx.x % c.G;
+  double2* buf = smem + f * (c.M + 1);
+  double2* wsum = smem + B * (c.M + 1);
+  const long long pair = (long long)blockIdx.x * B + f;
+  const bool live = pair < s.npairs;
+  const long long pl = live ? s.z0 + pair / s.ppp : 0;
+  const int r0 = live ? 2 * (int)(pair % s.ppp) : 0;
+  const bool v0 = live, v1 = live && r0 + 1 < s.nrow;
+  const long long o0 = pl * s.ps + (long long)(s.y0 + r0) * s.ld;
+  const long long o1 = o0 + s.ld;
+  for (int j = g; j < N; j += c.G) {
+    const double x = v0 ? src[o0 + j] : 0.0;
+    const double y = v1 ? src[o1 + j] : 0.0;
+    buf[j + 1] = make_double2(x, y);
+  }
+  __syncthreads();
+  dst_core(buf, c, g, wsum);
+  for (int p = g; p < N; p += c.G) {
+    const double2 o = buf[p];
+    if (v0) dst[o0 + p] = o.x;
+    if (v1) dst[o1 + p] = o.y;
+  }
+}
+
+// y-pass: CTA = one plane x a tile of 2B columns; group f transforms the
+// column pair (c0 + 2f, c0 + 2f + 1) as one complex FFT. Loads and stores
+// are row-major over the tile (coalesced), staged through shared memory.
+__global__ void __launch_bounds__(512) dst_y_fft_kernel(const double* __restrict__ src,
+                                                         double* __restrict__ dst, int z0,
+                                                         int x0, int x1, long long ld,
+                                                         long long ps, int N, FftCtx c, int B) {
+  extern __shared__ double2 smem[];
+  const int f = threadIdx.x / c.G, g = threadIdx.x % c.G;
+  const int W = 2 * B;
+  double2* wsum = smem + B * (c.M + 1);
+  double* sb = reinterpret_cast<double*>(smem);
+  const long long plane = z0 + blockIdx.y;
+  const int col0 = x0 + blockIdx.x * W;
+  const int ncols = min(W, x1 - col0);
+  const double* P = src + plane * ps + col0;
+  double* Q = dst + plane * ps + col0;
+  const int total = N * W;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int row = e / W, col = e - row * W;
+    const double v = col < ncols ? P[row * ld + col] : 0.0;
+    sb[2 * ((col >> 1) * (c.M + 1) + row + 1) + (col & 1)] = v;
+  }
+  __syncthreads();
+  dst_core(smem + f * (c.M + 1), c, g, wsum);
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int row = e / W, col = e - row * W;
+    if (col < ncols) Q[row * ld + col] = sb[2 * ((col >> 1) * (c.M + 1) + row) + (col & 1)];
+  }
+}
+
+// ------------------------------------------------------------ dense path
+// C[b] = A[b] * B[b], row-major, Mr x Kd times Kd x Nc; 64x64 tiles, 256
+// threads, 4x4 outputs per thread.
+__global__ void __launch_bounds__(256) dgemm_batched_kernel(
+    int Mr, int Nc, int Kd, const double* __restrict__ A, long long lda, long long sA,
+    const double* __restrict__ Bm, long long ldb, long long sB, double* __restrict__ C,
+    long long ldc, long long sC) {
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int b = blockIdx.z;
+  A += b * sA;
+  Bm += b * sB;
+  C += b * sC;
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+  const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < Kd; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int kk = e % 16, r = e / 16;  // A tile: 64 rows x 16 k
+      const int gr = row0 + r, gk = k0 + kk;
+      As[kk][r] = (gr < Mr && gk < Kd) ? A[gr * lda + gk] : 0.0;
+      const int cc = e % 64, kb = e / 64;  // B tile: 16 k x 64 cols
+      const int gk2 = k0 + kb, gc = col0 + cc;
+      Bs[kb][cc] = (gk2 < Kd && gc < Nc) ? Bm[gk2 * ldb + gc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][tr + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tc + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = row0 + tr + 16 * i, cc = col0 + tc + 16 * j;
+      if (r < Mr && cc < Nc) C[r * ldc + cc] = acc[i][j];
+    }
+}
+
+// Copy a (planes x rows x cols) region between two arrays of equal strides.
+__global__ void copy_region_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                   int rows, int cols, long long ld, long long ps,
+                                   long long off) {
+  const long long pl = blockIdx.y;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)rows * cols;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cols, cc = e % cols;
+    const long long o = off + pl * ps + r * ld + cc;
+    dst[o] = src[o];
+  }
+}
+
+size_t dense_tmp_elems(const hfb_plan* p, int nplanes) {
+  if (p->logMx >= 0 && p->logMy >= 0) return 0;
+  return (size_t)nplanes * p->ny * p->nx;
+}
+
+static FftCtx make_ctx(int M, int logM, const double2* tw, const double* sn, double scale) {
+  FftCtx c;
+  c.M = M;
+  c.logM = logM;
+  c.G = group_threads(M);
+  c.tw = tw;
+  c.sn = sn;
+  c.scale = scale;
+  return c;
+}
+
+int launch_dst_x(hfb_plan* p, const double* src, double* dst, int z0, int z1, int y0, int y1,
+                 double* tmp, cudaStream_t st) {
+  const int nz = z1 - z0, nr = y1 - y0;
+  if (nz <= 0 || nr <= 0) return HFB_OK;
+  const long long ld = p->nx, ps = (long long)p->ny * p->nx;
+  if (p->logMx >= 0) {
+    const int M = p->nx + 1;
+    FftCtx c = make_ctx(M, p->logMx, p->tw_x, p->sn_x, p->scale_x);
+    const int B = std::max(1, 256 / c.G);
+    const int threads = B * c.G;
+    LineSet s;
+    s.z0 = z0;
+    s.y0 = y0;
+    s.nrow = nr;
+    s.ppp = (nr + 1) / 2;
+    s.npairs = (long long)nz * s.ppp;
+    s.ld = ld;
+    s.ps = ps;
+    const long long blocks = (s.npairs + B - 1) / B;
+    const size_t sm = (size_t)(B * (M + 1) + threads / 32 + 1) * sizeof(double2);
+    if (sm > 48 * 1024)
+      HFB_CUDA(cudaFuncSetAttribute(dst_x_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sm));
+    dst_x_fft_kernel<<<(unsigned)blocks, threads, sm, st>>>(src, dst, s, p->nx, c, B);
+    HFB_LAUNCHED();
+    return HFB_OK;
+  }
+  // dense: out_l[rows y0..y1) = in_l[rows] * S_x
+  if (!tmp) return HFB_ERR_ARGUMENT;
+  const double* A = src + (long long)z0 * ps + (long long)y0 * ld;
+  double* C = tmp + (long long)z0 * ps + (long long)y0 * ld;
+  dim3 grid((p->nx + 63) / 64, (nr + 63) / 64, nz);
+  dgemm_batched_kernel<<<grid, 256, 0, st>>>(nr, p->nx, p->nx, A, ld, ps, p->dense_x, p->nx, 0, C,
+                                             ld, ps);
+  HFB_LAUNCHED();
+  dim3 cg(std::max(1, std::min(1024, (nr * p->nx + 255) / 256)), nz);
+  copy_region_kernel<<<cg, 256, 0, st>>>(tmp, dst, nr, p->nx, ld, ps,
+                                         (long long)z0 * ps + (long long)y0 * ld);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+int launch_dst_y(hfb_plan* p, const double* src, double* dst, int z0, int z1, int x0, int x1,
+                 double* tmp, cudaStream_t st) {
+  const int nz = z1 - z0, ncol = x1 - x0;
+  if (nz <= 0 || ncol <= 0) return HFB_OK;
+  const long long ld = p->nx, ps = (long long)p->ny * p->nx;
+  if (p->logMy >= 0) {
+    const int M = p->ny + 1;
+    FftCtx c = make_ctx(M, p->logMy, p->tw_y, p->sn_y, p->scale_y);
+    int B = std::max(1, 512 / c.G);
+    B = std::min(B, 32);
+    B = std::min(B, (ncol + 1) / 2 > 0 ? (ncol + 1) / 2 : 1);
+    while (B * c.G < 32) ++B;  // keep whole warps
+    const int threads = B * c.G;
+    const size_t sm = (size_t)(B * (M + 1) + threads / 32 + 1) * sizeof(double2);
+    if (sm > 48 * 1024)
+      HFB_CUDA(cudaFuncSetAttribute(dst_y_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sm));
+    dim3 grid((ncol + 2 * B - 1) / (2 * B), nz);
+    dst_y_fft_kernel<<<grid, threads, sm, st>>>(src, dst, z0, x0, x1, ld, ps, p->ny, c, B);
+    HFB_LAUNCHED();
+    return HFB_OK;
+  }
+  if (!tmp) return HFB_ERR_ARGUMENT;
+  const double* Bp = src + (long long)z0 * ps + x0;
+  double* C = tmp + (long long)z0 * ps + x0;
+  dim3 grid((ncol + 63) / 64, (p->ny + 63) / 64, nz);
+  dgemm_batched_kernel<<<grid, 256, 0, st>>>(p->ny, ncol, p->ny, p->dense_y, p->ny, 0, Bp, ld, ps,
+                                             C, ld, ps);
+  HFB_LAUNCHED();
+  dim3 cg(std::max(1, std::min(1024, (p->ny * ncol + 255) / 256)), nz);
+  copy_region_kernel<<<cg, 256, 0, st>>>(tmp, dst, p->ny, ncol, ld, ps, (long long)z0 * ps + x0);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+}  // namespace hfb

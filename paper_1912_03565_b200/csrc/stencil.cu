@@ -1,0 +1,329 @@
+// Compact-scheme RHS operators (kernel (a) of the north star), the 27-point
+// operator used for the Dirichlet fold and residuals, and the z-slab <->
+// y-block pack/unpack of the partitioned exchange.
+//
+// RHS and 27-point kernels use explicit round-to-nearest intrinsics (no FMA
+// contraction) and the reference's exact term order, so for real data they
+// reproduce the reference's numpy results bit for bit (the complex
+// arithmetic of the reference reduces to these real operations when the
+// imaginary parts are zero).
+#include "hfb_internal.cuh"
+
+namespace hfb {
+
+#define DADD __dadd_rn
+#define DMUL __dmul_rn
+
+// assembly.py:183-193: F = hz2 * (0.5*core + (xm + xp + ym + yp + zm + zp) * (1/12))
+__global__ void rhs_fourth_kernel(const double* __restrict__ f, double* __restrict__ F, int nx,
+                                  int ny, int nz, double hz2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y, l = blockIdx.z;
+  if (i >= nx) return;
+  const long long X = nx + 2, XY = (long long)(nx + 2) * (ny + 2);
+  const long long c = (long long)(l + 1) * XY + (long long)(j + 1) * X + (i + 1);
+  double nb = DADD(__ldg(&f[c - 1]), __ldg(&f[c + 1]));
+  nb = DADD(nb, __ldg(&f[c - X]));
+  nb = DADD(nb, __ldg(&f[c + X]));
+  nb = DADD(nb, __ldg(&f[c - XY]));
+  nb = DADD(nb, __ldg(&f[c + XY]));
+  // the reference divides a complex128 array by 12.0, which numpy evaluates
+  // as a product with the reciprocal 1/12
+  const double v = DADD(DMUL(0.5, __ldg(&f[c])), DMUL(nb, 1.0 / 12.0));
+  F[((long long)l * ny + j) * nx + i] = DMUL(hz2, v);
+}
+
+// assembly.py:180-181
+__global__ void rhs_second_kernel(const double* __restrict__ f, double* __restrict__ F,
+                                  long long n, double hz2) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    F[e] = DMUL(hz2, f[e]);
+}
+
+// assembly.py:195-213 (uniform grid, h = h_z):
+// rhs = h2*(f + (h2/12) lap + (h4/360) d4 + (h4/90) mixed)
+//       - ((h4/20) k2) f + ((h2 h4/60) k2z) fz
+__global__ void rhs_sixth_kernel(const double* __restrict__ f, const double* __restrict__ lap,
+                                 const double* __restrict__ d4, const double* __restrict__ fxxyy,
+                                 const double* __restrict__ fxxzz,
+                                 const double* __restrict__ fyyzz,
+                                 const double* __restrict__ fz, const double* __restrict__ k2,
+                                 const double* __restrict__ k2z, double h2, long long plane,
+                                 long long n, double* __restrict__ F) {
+  const double h4 = DMUL(h2, h2);
+  const double c1 = __ddiv_rn(h2, 12.0), c2 = __ddiv_rn(h4, 360.0), c3 = __ddiv_rn(h4, 90.0);
+  const double c4 = __ddiv_rn(h4, 20.0), c5 = __ddiv_rn(DMUL(h2, h4), 60.0);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long l = e / plane;
+    const double mixed = DADD(DADD(fxxyy[e], fxxzz[e]), fyyzz[e]);
+    double in = DADD(f[e], DMUL(c1, lap[e]));
+    in = DADD(in, DMUL(c2, d4[e]));
+    in = DADD(in, DMUL(c3, mixed));
+    double r = DMUL(h2, in);
+    r = __dsub_rn(r, DMUL(DMUL(c4, k2[l]), f[e]));
+    r = DADD(r, DMUL(DMUL(c5, k2z[l]), fz[e]));
+    F[e] = r;
+  }
+}
+
+// assembly.py:215-224:
+// rhs = hz2*(f + (hx2/12) fxx + (hy2/12) fyy + (hz2/12)(gamma fz + fzz))
+__global__ void rhs_convdiff_kernel(const double* __restrict__ f, const double* __restrict__ fxx,
+                                    const double* __restrict__ fyy, const double* __restrict__ fz,
+                                    const double* __restrict__ fzz, double hx2, double hy2,
+                                    double hz2, double gamma, long long n,
+                                    double* __restrict__ F) {
+  const double a = __ddiv_rn(hx2, 12.0), b = __ddiv_rn(hy2, 12.0), c = __ddiv_rn(hz2, 12.0);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    double in = DADD(f[e], DMUL(a, fxx[e]));
+    in = DADD(in, DMUL(b, fyy[e]));
+    in = DADD(in, DMUL(c, DADD(DMUL(gamma, fz[e]), fzz[e])));
+    F[e] = DMUL(hz2, in);
+  }
+}
+
+// 27-point operator on a closed box (assembly.py:229-244). Raw weights
+// (a, b, c, d) per level and offset, in the reference's term order:
+// for dl in (-1, 0, 1): for (di, dj) in _PLANE_OFFSETS (assembly.py:20-25).
+__constant__ int c_off_di[9] = {-1, 1, -1, 1, -1, 1, 0, 0, 0};
+__constant__ int c_off_dj[9] = {-1, -1, 1, 1, 0, 0, -1, 1, 0};
+__constant__ int c_off_w[9] = {0, 0, 0, 0, 1, 1, 2, 2, 3};  // a a a a b b c c d
+
+__device__ __forceinline__ double apply27_point(const double* __restrict__ ext,
+                                                const double* __restrict__ raw, int i, int j,
+                                                int l, long long X, long long XY,
+                                                uint32_t mask) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const long long zb = (long long)(l + k) * XY;  // level l + (k-1), closed index +1
+#pragma unroll
+    for (int o = 0; o < 9; ++o) {
+      if (mask & (1u << (k * 9 + o))) {
+        const double wgt = __ldg(&raw[(long long)l * 12 + k * 4 + c_off_w[o]]);
+        const double v = __ldg(&ext[zb + (long long)(j + 1 + c_off_dj[o]) * X + (i + 1 + c_off_di[o])]);
+        acc = DADD(acc, DMUL(wgt, v));
+      }
+    }
+  }
+  return acc;
+}
+
+// mode 0: out = A ext; mode 1: out = rhs - A ext (fold_dirichlet, assembly.py:258-274)
+__global__ void apply27_kernel(const double* __restrict__ ext, const double* __restrict__ rhs,
+                               double* __restrict__ out, const double* __restrict__ raw, int nx,
+                               int ny, int nz, uint32_t mask, int mode) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y, l = blockIdx.z;
+  if (i >= nx) return;
+  const long long X = nx + 2, XY = (long long)(nx + 2) * (ny + 2);
+  const double v = apply27_point(ext, raw, i, j, l, X, XY, mask);
+  const long long o = ((long long)l * ny + j) * nx + i;
+  out[o] = mode == 0 ? v : __dsub_rn(rhs[o], v);
+}
+
+// Residual sum of squares with a zero boundary: u is interior-only, so the
+// neighbour fetch is bounds-checked instead of padded (assembly.py:277-289).
+__global__ void residual_sq_kernel(const double* __restrict__ u, const double* __restrict__ F,
+                                   const double* __restrict__ raw, int nx, int ny, int nz,
+                                   uint32_t mask, double* __restrict__ partial) {
+  __shared__ double red[256 / 32];
+  const long long n = (long long)nx * ny * nz;
+  double s = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % nx);
+    const int j = (int)((e / nx) % ny);
+    const int l = (int)(e / ((long long)nx * ny));
+    double acc = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const int ll = l + k - 1;
+      for (int o = 0; o < 9; ++o) {
+        if (!(mask & (1u << (k * 9 + o)))) continue;
+        const int ii = i + c_off_di[o], jj = j + c_off_dj[o];
+        double v = 0.0;
+        if (ll >= 0 && ll < nz && jj >= 0 && jj < ny && ii >= 0 && ii < nx)
+          v = u[((long long)ll * ny + jj) * nx + ii];
+        acc = DADD(acc, DMUL(raw[(long long)l * 12 + k * 4 + c_off_w[o]], v));
+      }
+    }
+    const double r = acc - F[e];
+    s = fma(r, r, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 256 / 32; ++w) t += red[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+// slab (kpz, ny, nx) -> send blocks (kpz, kpy(q), nx), ascending q
+__global__ void pack_yblocks_kernel(const double* __restrict__ slab, double* __restrict__ send,
+                                    int kpz, int ny, int nx, const int* __restrict__ ys,
+                                    int parts) {
+  const long long total = (long long)kpz * ny * nx;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % nx);
+    const int j = (int)((e / nx) % ny);
+    const int l = (int)(e / ((long long)nx * ny));
+    int q = 0;
+    while (q + 1 < parts && j >= ys[q + 1]) ++q;
+    const int y0 = ys[q], kpy = ys[q + 1] - ys[q];
+    const long long base = (long long)kpz * y0 * nx;  // blocks before q
+    send[base + ((long long)l * kpy + (j - y0)) * nx + i] = slab[e];
+  }
+}
+
+__global__ void unpack_yblocks_kernel(const double* __restrict__ recv, double* __restrict__ slab,
+                                      int kpz, int ny, int nx, const int* __restrict__ ys,
+                                      int parts) {
+  const long long total = (long long)kpz * ny * nx;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % nx);
+    const int j = (int)((e / nx) % ny);
+    const int l = (int)(e / ((long long)nx * ny));
+    int q = 0;
+    while (q + 1 < parts && j >= ys[q + 1]) ++q;
+    const int y0 = ys[q], kpy = ys[q + 1] - ys[q];
+    const long long base = (long long)kpz * y0 * nx;
+    slab[e] = recv[base + ((long long)l * kpy + (j - y0)) * nx + i];
+  }
+}
+
+}  // namespace hfb
+
+// ------------------------------------------------------------------ C-ABI
+using namespace hfb;
+
+static unsigned grid_for(long long n, int threads) {
+  long long b = (n + threads - 1) / threads;
+  if (b > 148LL * 64) b = 148LL * 64;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+extern "C" int hfb_rhs_fourth(hfb_plan* p, const double* f, double* F, double hz2,
+                              void* stream) {
+  if (!p || !f || !F) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  dim3 grid((p->nx + 127) / 128, p->ny, p->nz);
+  rhs_fourth_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(f, F, p->nx, p->ny, p->nz, hz2);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+extern "C" int hfb_rhs_second(hfb_plan* p, const double* f, double* F, double hz2,
+                              void* stream) {
+  if (!p || !f || !F) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  const long long n = (long long)p->nx * p->ny * p->nz;
+  rhs_second_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(f, F, n, hz2);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+extern "C" int hfb_rhs_sixth(hfb_plan* p, const double* f, const double* lap, const double* d4,
+                             const double* fxxyy, const double* fxxzz, const double* fyyzz,
+                             const double* fz, const double* k2, const double* k2z, double h2,
+                             double* F, void* stream) {
+  if (!p || !f || !lap || !d4 || !fxxyy || !fxxzz || !fyyzz || !fz || !k2 || !k2z || !F)
+    return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  const long long plane = (long long)p->nx * p->ny, n = plane * p->nz;
+  rhs_sixth_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      f, lap, d4, fxxyy, fxxzz, fyyzz, fz, k2, k2z, h2, plane, n, F);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+extern "C" int hfb_rhs_convdiff(hfb_plan* p, const double* f, const double* fxx,
+                                const double* fyy, const double* fz, const double* fzz,
+                                double hx2, double hy2, double hz2, double gamma, double* F,
+                                void* stream) {
+  if (!p || !f || !fxx || !fyy || !fz || !fzz || !F) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  const long long n = (long long)p->nx * p->ny * p->nz;
+  rhs_convdiff_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      f, fxx, fyy, fz, fzz, hx2, hy2, hz2, gamma, n, F);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+// raw table pointer: the plan keeps the scaled (4a,2b,2c,d) copy for the
+// Thomas sweep and the raw (a,b,c,d) copy right after it.
+extern "C" int hfb_apply27(hfb_plan* p, const double* ext, const double* rhs, double* out,
+                           uint32_t mask, int mode, void* stream) {
+  if (!p || !ext || !out || (mode == 1 && !rhs)) return HFB_ERR_ARGUMENT;
+  if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
+  HFB_CUDA(cudaSetDevice(p->device));
+  dim3 grid((p->nx + 127) / 128, p->ny, p->nz);
+  apply27_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(ext, rhs, out, p->coef + 12LL * p->nz,
+                                                         p->nx, p->ny, p->nz, mask, mode);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+extern "C" int hfb_residual_partials(const hfb_plan* p) {
+  (void)p;
+  return 148 * 8;
+}
+
+extern "C" int hfb_residual_sq(hfb_plan* p, const double* u, const double* F, double* partial,
+                               uint32_t mask, void* stream) {
+  if (!p || !u || !F || !partial) return HFB_ERR_ARGUMENT;
+  if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
+  HFB_CUDA(cudaSetDevice(p->device));
+  residual_sq_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+      u, F, p->coef + 12LL * p->nz, p->nx, p->ny, p->nz, mask, partial);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+static int upload_ystarts(hfb_plan* p, const int* ys, int parts, cudaStream_t st) {
+  if (p->ystarts_cap < parts + 1) {
+    if (p->ystarts) cudaFree(p->ystarts);
+    p->ystarts = nullptr;
+    HFB_CUDA(cudaMalloc(&p->ystarts, sizeof(int) * (parts + 1)));
+    p->ystarts_cap = parts + 1;
+  }
+  HFB_CUDA(cudaMemcpyAsync(p->ystarts, ys, sizeof(int) * (parts + 1), cudaMemcpyHostToDevice, st));
+  return HFB_OK;
+}
+
+extern "C" int hfb_pack_yblocks(hfb_plan* p, const double* slab, double* send, int kpz,
+                                const int* ys, int parts, void* stream) {
+  if (!p || !slab || !send || !ys || parts < 1 || kpz < 0) return HFB_ERR_ARGUMENT;
+  if (ys[0] != 0 || ys[parts] != p->ny) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  int rc = upload_ystarts(p, ys, parts, (cudaStream_t)stream);
+  if (rc) return rc;
+  const long long n = (long long)kpz * p->ny * p->nx;
+  if (n == 0) return HFB_OK;
+  pack_yblocks_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      slab, send, kpz, p->ny, p->nx, p->ystarts, parts);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+extern "C" int hfb_unpack_yblocks(hfb_plan* p, const double* recv, double* slab, int kpz,
+                                  const int* ys, int parts, void* stream) {
+  if (!p || !slab || !recv || !ys || parts < 1 || kpz < 0) return HFB_ERR_ARGUMENT;
+  if (ys[0] != 0 || ys[parts] != p->ny) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  int rc = upload_ystarts(p, ys, parts, (cudaStream_t)stream);
+  if (rc) return rc;
+  const long long n = (long long)kpz * p->ny * p->nx;
+  if (n == 0) return HFB_OK;
+  unpack_yblocks_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      recv, slab, kpz, p->ny, p->nx, p->ystarts, parts);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}

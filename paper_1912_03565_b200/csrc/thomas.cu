@@ -1,0 +1,198 @@
+// Per-mode tridiagonal (Thomas) solves along z — kernel (c) of the north
+// star, replacing tridiag._sweep (reference tridiag.py:126-167) with the
+// plane-operator eigenvalues fused in (stencil.eigenvalue_plane,
+// stencil.py:226-234).
+//
+// One thread per sine mode (m, n); consecutive threads take consecutive n,
+// so every z-level access is a coalesced row segment. Eigenvalues are
+// generated on the fly from the per-level weights (4a, 2b, 2c, d) and the
+// mode cosines: lambda = 4a cx cy + 2b cx + 2c cy + d. The forward sweep
+// stores the super-diagonal ratios cp in a workspace of the slab's size
+// (tridiag.py:153 `cp = np.empty_like(w)`); the back substitution reads them.
+//
+// Pivot screening (tridiag.py:142-151): |denom| < threshold latches the key
+// (l, m, n) with an atomicMin, so the reported failure is the first row l,
+// then the smallest m, then the smallest n — np.argwhere order.
+#include "hfb_internal.cuh"
+
+namespace hfb {
+
+__device__ __forceinline__ double eig(const double* __restrict__ co, double cx, double cy,
+                                      double cxy) {
+  // co = (4a, 2b, 2c, d) of one level
+  const double2 w0 = __ldg(reinterpret_cast<const double2*>(co));
+  const double2 w1 = __ldg(reinterpret_cast<const double2*>(co) + 1);
+  return fma(w0.x, cxy, fma(w0.y, cx, fma(w1.x, cy, w1.y)));
+}
+
+__device__ __forceinline__ double rcp(double d) { return 1.0 / d; }
+
+__device__ __forceinline__ void latch(unsigned long long* err, long long l, long long m,
+                                      long long n, long long ny_total, long long nx) {
+  const unsigned long long key =
+      ((unsigned long long)l * (unsigned long long)ny_total + (unsigned long long)m) *
+          (unsigned long long)nx +
+      (unsigned long long)n;
+  atomicMin(err, key);
+}
+
+struct ThomasArgs {
+  int nz, mloc, nx, ny_total, m_off;
+  long long plane;  // mloc * nx
+  const double* coef;
+  const double* cx;
+  const double* cy;
+  double thr;
+  unsigned long long* err;
+};
+
+__global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w,
+                                                           double* __restrict__ cpw,
+                                                           ThomasArgs a) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= a.plane) return;
+  const int ml = (int)(t / a.nx), n = (int)(t - (long long)ml * a.nx);
+  const double cxv = __ldg(&a.cx[n]);
+  const double cyv = __ldg(&a.cy[a.m_off + ml]);
+  const double cxy = cxv * cyv;
+  const long long P = a.plane;
+  // row 0
+  double den = eig(a.coef + 4, cxv, cyv, cxy);
+  if (fabs(den) < a.thr) latch(a.err, 0, a.m_off + ml, n, a.ny_total, a.nx);
+  double r = rcp(den);
+  double c = eig(a.coef + 8, cxv, cyv, cxy) * r;
+  double x = w[t] * r;
+  w[t] = x;
+  cpw[t] = c;
+  for (int l = 1; l < a.nz; ++l) {
+    const double* co = a.coef + (long long)l * 12;
+    const double lo = eig(co, cxv, cyv, cxy);
+    den = fma(-lo, c, eig(co + 4, cxv, cyv, cxy));
+    if (fabs(den) < a.thr) latch(a.err, l, a.m_off + ml, n, a.ny_total, a.nx);
+    r = rcp(den);
+    const long long o = (long long)l * P + t;
+    x = fma(-lo, x, w[o]) * r;
+    w[o] = x;
+    if (l < a.nz - 1) {
+      c = eig(co + 8, cxv, cyv, cxy) * r;
+      cpw[o] = c;
+    }
+  }
+  // back substitution; x holds W[nz-1]
+  for (int l = a.nz - 2; l >= 0; --l) {
+    const long long o = (long long)l * P + t;
+    x = fma(-cpw[o], x, w[o]);
+    w[o] = x;
+  }
+}
+
+int launch_thomas(hfb_plan* p, double* slab, int mloc, int m_off, double* cpw, cudaStream_t st) {
+  if (mloc <= 0) return HFB_OK;
+  ThomasArgs a;
+  a.nz = p->nz;
+  a.mloc = mloc;
+  a.nx = p->nx;
+  a.ny_total = p->ny;
+  a.m_off = m_off;
+  a.plane = (long long)mloc * p->nx;
+  a.coef = p->coef;
+  a.cx = p->cx;
+  a.cy = p->cy;
+  a.thr = p->thr;
+  a.err = p->err;
+  const long long blocks = (a.plane + 255) / 256;
+  thomas_slab_kernel<<<(unsigned)blocks, 256, 0, st>>>(slab, cpw, a);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+}  // namespace hfb
+
+// ----------------------------------------------------------------------
+// Batched Thomas on explicit bands (tridiag.solve_system, tridiag.py:59-90).
+// Arrays are (nsys, n) real or (nsys, n) complex interleaved (re, im).
+// thr[s] = PIVOT_RTOL * band scale of system s; the first failing row of
+// each system is latched as s * n + row (min over systems).
+namespace hfb {
+
+template <bool CPLX>
+struct Num;
+template <>
+struct Num<false> {
+  typedef double T;
+  static __device__ T ld(const double* p, long long i) { return p[i]; }
+  static __device__ void st(double* p, long long i, T v) { p[i] = v; }
+  static __device__ T sub(T a, T b) { return a - b; }
+  static __device__ T mul(T a, T b) { return a * b; }
+  static __device__ T div(T a, T b) { return a / b; }
+  static __device__ double mag(T a) { return fabs(a); }
+};
+template <>
+struct Num<true> {
+  typedef double2 T;
+  static __device__ T ld(const double* p, long long i) {
+    return reinterpret_cast<const double2*>(p)[i];
+  }
+  static __device__ void st(double* p, long long i, T v) { reinterpret_cast<double2*>(p)[i] = v; }
+  static __device__ T sub(T a, T b) { return csub(a, b); }
+  static __device__ T mul(T a, T b) { return cmul(a, b); }
+  static __device__ T div(T a, T b) {
+    const double s = 1.0 / fma(b.x, b.x, b.y * b.y);
+    return make_double2(fma(a.x, b.x, a.y * b.y) * s, fma(a.y, b.x, -a.x * b.y) * s);
+  }
+  static __device__ double mag(T a) { return hypot(a.x, a.y); }
+};
+
+template <bool CPLX>
+__global__ void bands_kernel(const double* __restrict__ sub, const double* __restrict__ diag,
+                             const double* __restrict__ sup, double* __restrict__ x,
+                             double* __restrict__ cpw, int n, int nsys,
+                             const double* __restrict__ thr, unsigned long long* err) {
+  typedef Num<CPLX> K;
+  typedef typename K::T T;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nsys) return;
+  const long long b = (long long)s * n;
+  T c = K::ld(sup, b), den = K::ld(diag, b), xv;
+  bool bad = K::mag(den) < thr[s];
+  long long first = bad ? 0 : -1;
+  c = K::div(c, den);
+  xv = K::div(K::ld(x, b), den);
+  K::st(cpw, b, c);
+  K::st(x, b, xv);
+  for (int l = 1; l < n; ++l) {
+    const T lo = K::ld(sub, b + l);
+    den = K::sub(K::ld(diag, b + l), K::mul(lo, c));
+    if (first < 0 && K::mag(den) < thr[s]) first = l;
+    if (l < n - 1) {
+      c = K::div(K::ld(sup, b + l), den);
+      K::st(cpw, b + l, c);
+    }
+    xv = K::div(K::sub(K::ld(x, b + l), K::mul(lo, xv)), den);
+    K::st(x, b + l, xv);
+  }
+  for (int l = n - 2; l >= 0; --l) {
+    xv = K::sub(K::ld(x, b + l), K::mul(K::ld(cpw, b + l), xv));
+    K::st(x, b + l, xv);
+  }
+  if (first >= 0) atomicMin(err, (unsigned long long)(b + first));
+}
+
+}  // namespace hfb
+
+extern "C" int hfb_solve_bands(const double* sub, const double* diag, const double* sup,
+                               double* x, double* cpw, int n, int nsys, int is_complex,
+                               const double* thr, unsigned long long* err, void* stream) {
+  if (!sub || !diag || !sup || !x || !cpw || !thr || !err || n < 1 || nsys < 0)
+    return HFB_ERR_ARGUMENT;
+  if (nsys == 0) return HFB_OK;
+  const int blocks = (nsys + 127) / 128;
+  if (is_complex)
+    hfb::bands_kernel<true><<<blocks, 128, 0, (cudaStream_t)stream>>>(sub, diag, sup, x, cpw, n,
+                                                                       nsys, thr, err);
+  else
+    hfb::bands_kernel<false><<<blocks, 128, 0, (cudaStream_t)stream>>>(sub, diag, sup, x, cpw, n,
+                                                                        nsys, thr, err);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}

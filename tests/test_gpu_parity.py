@@ -1,0 +1,390 @@
+"""Parity of the sm_100a path against the oracle and the reference's goldens.
+
+All tests call through the C-ABI (ctypes) on cuda:0. Tolerances: the north
+star's 1e-10 relative L2 is the bar; the measured noise floor is ~1e-14, so
+tighter tolerances are asserted where the arithmetic allows (stated inline).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1912_03565_b200 as hb
+from oracle import helm_oracle as orc
+from paper_1912_03565_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+PI = math.pi
+TOL = 1e-10  # north_star: relative L2 vs the reference CPU solver
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def oracle_table(scheme_key, prof, g):
+    return orc.weight_table(scheme_key, np.real(prof.k2), np.real(prof.k2_z),
+                            np.real(prof.k2_zz), complex(prof.gamma).real,
+                            (g.h_x, g.h_y, g.h_z), g.n_z)
+
+
+# ---------------------------------------------------------------- DST-I
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 15, 31, 63, 125, 127])
+def test_dst2d_matches_reference_goldens(golden, cuda, n):
+    out = hb.dst2d(hb.make_plan(n, n), golden[f"dst2d_in_{n}"])
+    assert np.abs(out - golden[f"dst2d_out_{n}"]).max() < 1e-13 * max(1, np.abs(out).max())
+
+
+@pytest.mark.parametrize("nx,ny,nz", [(255, 255, 3), (511, 127, 2), (1023, 1023, 1),
+                                      (2047, 31, 2), (31, 2047, 1), (9, 7, 6), (64, 33, 4)])
+def test_transform_stack_vs_scipy(cuda, nx, ny, nz):
+    rng = np.random.default_rng(nx + ny + nz)
+    data = rng.standard_normal((nz, ny, nx))
+    f = hb.Field3D(data.copy())
+    hb.transform_stack(hb.make_plan(nx, ny), f)
+    ref = orc.dst_stack(data, workers=4)
+    assert np.abs(f.values - ref).max() < 1e-13 * np.abs(ref).max()
+
+
+def test_basis_vector_and_single_mode(cuda):
+    out = hb.dst_lines(np.array([1.0, 0.0, 0.0]), axis=0)
+    assert np.allclose(out, [0.5, 1 / math.sqrt(2), 0.5], atol=1e-15)
+    n_x, n_y, n0, m0 = 8, 6, 3, 2
+    i, j = np.arange(1, n_x + 1), np.arange(1, n_y + 1)
+    plane = np.sin(PI * m0 * j / (n_y + 1))[:, None] * np.sin(PI * n0 * i / (n_x + 1))[None, :]
+    out = hb.dst2d(hb.make_plan(n_x, n_y), plane)
+    expect = np.zeros_like(out)
+    expect[m0 - 1, n0 - 1] = math.sqrt((n_x + 1) * (n_y + 1)) / 2.0
+    assert np.abs(out - expect).max() < 1e-12
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 8, 9, 31, 125, 127, 511])
+def test_involution_and_norm(cuda, n):
+    rng = np.random.default_rng(n)
+    plane = rng.standard_normal((n, n))
+    plan = hb.make_plan(n, n)
+    once = hb.dst2d(plan, plane)
+    twice = hb.dst2d(plan, once)
+    assert np.abs(twice - plane).max() <= 1e-13 * np.abs(plane).max()
+    assert np.linalg.norm(once) == pytest.approx(np.linalg.norm(plane), rel=1e-13)
+
+
+def test_dense_reference_path(cuda):
+    rng = np.random.default_rng(3)
+    plane = rng.standard_normal((32, 64))
+    plan = hb.make_plan(64, 32)
+    assert np.abs(hb.dst2d(plan, plane) - hb.dst2d_reference(plan, plane)).max() < 1e-12
+
+
+def test_transform_disjoint_halves_bitwise(cuda):
+    rng = np.random.default_rng(9)
+    data = rng.standard_normal((8, 6, 7))
+    full, halves = hb.Field3D(data.copy()), hb.Field3D(data.copy())
+    plan = hb.make_plan(7, 6)
+    hb.transform_stack(plan, full)
+    hb.transform_stack(plan, halves, (0, 3))
+    hb.transform_stack(plan, halves, (3, 8))
+    assert np.array_equal(full.values, halves.values)
+    data = rng.standard_normal((8, 63, 127))
+    full, halves = hb.Field3D(data.copy()), hb.Field3D(data.copy())
+    plan = hb.make_plan(127, 63)
+    hb.transform_stack(plan, full)
+    hb.transform_stack(plan, halves, (0, 3))
+    hb.transform_stack(plan, halves, (3, 8))
+    assert np.array_equal(full.values, halves.values)
+
+
+def test_transform_ranges_validated(cuda):
+    f = hb.Field3D(np.zeros((4, 3, 3)))
+    with pytest.raises(IndexError):
+        hb.transform_stack(hb.make_plan(3, 3), f, (0, 5))
+    data = np.random.default_rng(2).standard_normal((3, 4, 4))
+    f = hb.Field3D(data.copy())
+    hb.transform_stack(hb.make_plan(4, 4), f, (1, 1))
+    assert np.array_equal(f.values, data)
+
+
+def test_line_batches_match_planes(cuda):
+    rng = np.random.default_rng(5)
+    data = rng.standard_normal((5, 63, 31))
+    a, b = data.copy(), data.copy()
+    hb.transform_stack(hb.make_plan(31, 63), a)
+    hb.transform_lines_x(b, (0, 40))
+    hb.transform_lines_x(b, (40, 63))
+    hb.transform_lines_y(b, (0, 17))
+    hb.transform_lines_y(b, (17, 31))
+    assert np.abs(a - b).max() < 1e-13 * np.abs(a).max()
+
+
+# ---------------------------------------------------------------- Thomas
+def test_solve_system_known_answers(cuda):
+    sys_ = hb.SpectralSystem(1, 1, np.array([0, -1, -1.0]), np.array([2, 2, 2.0]),
+                             np.array([-1, -1, 0.0]))
+    assert np.allclose(hb.solve_system(sys_, np.array([1.0, 0, 0])), [0.75, 0.5, 0.25],
+                       atol=1e-15)
+    rng = np.random.default_rng(11)
+    n = 50
+    diag = 4.0 + rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    sub = rng.standard_normal(n) * 0.5 + 0.3j
+    sup = rng.standard_normal(n) * 0.5 - 0.2j
+    sub[0] = sup[-1] = 0
+    rhs = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    x = hb.solve_system(hb.SpectralSystem(1, 1, sub, diag, sup), rhs)
+    A = np.diag(diag) + np.diag(sub[1:], -1) + np.diag(sup[:-1], 1)
+    expect = np.linalg.solve(A, rhs)
+    assert np.abs(x - expect).max() < 1e-12 * np.abs(expect).max()
+    with pytest.raises(hb.SingularSystemError):
+        hb.solve_system(hb.SpectralSystem(1, 1, np.array([0, 1.0]), np.array([0, 1.0]),
+                                          np.array([1.0, 0])), np.array([1.0, 1.0]))
+
+
+@pytest.mark.parametrize("key,scheme", [("2", hb.SchemeKind.SECOND_ORDER),
+                                        ("4", hb.SchemeKind.FOURTH_ORDER),
+                                        ("6", hb.SchemeKind.SIXTH_ORDER)])
+def test_solve_all_vs_oracle_sweep(cuda, key, scheme):
+    g = wl.unit_grid(31)
+    prof = wl.profile_a(g)
+    data = orc.dst_stack(np.random.default_rng(23).standard_normal(g.shape))
+    dev = data.copy()
+    hb.solve_all(dev, scheme, prof, g)
+    ref = orc.thomas_sweep(data.copy(), oracle_table(key, prof, g), *orc.mode_cosines(31, 31))
+    assert rel_l2(dev, ref) < 1e-14
+
+
+def test_solve_all_disjoint_ranges_bitwise(cuda):
+    g = hb.make_grid(hb.Domain(0, PI, 0, PI, 0, PI), 5, 6, 4)
+    prof = hb.constant_profile(3.0, g)
+    data = np.random.default_rng(17).standard_normal(g.shape)
+    full, split = data.copy(), data.copy()
+    hb.solve_all(full, hb.SchemeKind.FOURTH_ORDER, prof, g)
+    hb.solve_all(split, hb.SchemeKind.FOURTH_ORDER, prof, g, (0, 2))
+    hb.solve_all(split, hb.SchemeKind.FOURTH_ORDER, prof, g, (2, 6))
+    assert np.array_equal(full, split)
+
+
+def test_resonance_reports_reference_mode(golden, cuda):
+    k2, n, m = golden["resonance"]
+    g = hb.make_grid(hb.Domain(0, PI, 0, PI, 0, PI), 5, 6, 4)
+    with pytest.raises(hb.SingularSystemError) as err:
+        hb.solve_discrete(hb.Field3D(np.ones(g.shape)), hb.BoundaryData.zero(),
+                          hb.SchemeKind.SECOND_ORDER, hb.constant_profile(k2, g), g)
+    assert (err.value.n, err.value.m) == (int(n), int(m))
+    g1 = hb.make_grid(hb.Domain(0, PI, 0, PI, 0, PI), 1, 1, 1)
+    with pytest.raises(hb.SingularSystemError) as err:
+        hb.solve_discrete(hb.Field3D(np.ones(g1.shape)), hb.BoundaryData.zero(),
+                          hb.SchemeKind.SECOND_ORDER, hb.constant_profile(6.0 / g1.h_z**2, g1), g1)
+    assert (err.value.n, err.value.m) == (1, 1)
+
+
+# ---------------------------------------------------------- full solves
+def solve(F, scheme, prof, g, config=None):
+    u, t = hb.solve_discrete(hb.Field3D(F), hb.BoundaryData.zero(), scheme, prof, g,
+                             config or hb.SolverConfig())
+    return u.values, t
+
+
+def test_cfg1_uniform_rhs(golden, cuda):
+    w = wl.workload(1)
+    u, t = solve(wl.host_rhs(w), w.scheme, w.profile, w.grid)
+    assert rel_l2(u, golden["cfg1_U"]) < 1e-13
+    assert t.total_s >= t.transform_s + t.tridiag_s
+
+
+def test_cfg1_manufactured_through_rhs_operator(golden, cuda):
+    w = wl.workload(1)
+    F = hb.build_rhs(w.scheme, wl.manufactured_source(), w.profile, w.grid)
+    g = w.grid
+    x = g.x_nodes(closed=True)[None, None, :]
+    y = g.y_nodes(closed=True)[None, :, None]
+    z = g.z_nodes(closed=True)[:, None, None]
+    f_closed = np.broadcast_to(wl.manufactured_source().f(x, y, z), (33, 33, 33))
+    assert np.array_equal(F.values, orc.rhs_fourth(f_closed, g.h_z))  # K1 bit-exact
+    assert np.abs(F.values - golden["cfg1A_F"]).max() <= 1e-15 * np.abs(golden["cfg1A_F"]).max()
+    u, _ = solve(F.values, w.scheme, w.profile, w.grid)
+    assert rel_l2(u, golden["cfg1A_U"]) < 1e-13
+
+
+def test_cfg2_full_size_against_reference_summaries(golden, cuda):
+    w = wl.workload(2)
+    u, _ = solve(wl.host_rhs(w), w.scheme, w.profile, w.grid)
+    assert rel_l2(u[63], golden["cfg2_U_plane63"]) < 1e-13
+    assert rel_l2(u[::8, ::8, ::8], golden["cfg2_U_sub8"]) < 1e-13
+    nrm, mx, sm = golden["cfg2_U_norms"]
+    assert abs(np.linalg.norm(u) - nrm) < 1e-12 * nrm
+
+
+def test_cfg2_sixth_order_rhs_and_solve(golden, cuda):
+    g = wl.unit_grid(31)
+    prof = wl.profile_a(g)
+    F = hb.build_rhs(hb.SchemeKind.SIXTH_ORDER, wl.manufactured_source(), prof, g)
+    assert np.abs(F.values - golden["cfg2A_n31_F"]).max() <= 1e-14 * np.abs(F.values).max()
+    u, _ = solve(F.values, hb.SchemeKind.SIXTH_ORDER, prof, g)
+    assert rel_l2(u, golden["cfg2A_n31_U"]) < 1e-13
+
+
+def test_convergence_orders(golden, cuda):
+    """4th/6th-order rates on the manufactured solution (31^3 / 63^3 / 127^3)."""
+    rows = golden["convergence"]
+    src = wl.manufactured_source()
+    for key, scheme in (("4", hb.SchemeKind.FOURTH_ORDER), ("6", hb.SchemeKind.SIXTH_ORDER)):
+        errs = []
+        for n in (31, 63, 127):
+            g = wl.unit_grid(n)
+            prof = wl.profile_a(g)
+            F = hb.build_rhs(scheme, src, prof, g)
+            u, _ = solve(F.values, scheme, prof, g)
+            x = g.x_nodes()[None, None, :]
+            y = g.y_nodes()[None, :, None]
+            z = g.z_nodes()[:, None, None]
+            exact = wl.manufactured_u(x, y, z)
+            errs.append(np.abs(u - exact).max())
+            ref = rows[(rows[:, 0] == float(key)) & (rows[:, 1] == n)][0]
+            assert errs[-1] == pytest.approx(ref[2], rel=1e-6)
+        orders = [math.log(errs[i] / errs[i + 1]) / math.log(2 * (n1 + 1) / (2 * (n0 + 1)))
+                  for i, (n0, n1) in enumerate(((31, 63), (63, 127)))]
+        lo, hi = (3.7, 4.3) if key == "4" else (5.6, 6.4)
+        assert all(lo <= o <= hi for o in orders), orders
+
+
+def test_cd4_and_general_table(golden, cuda):
+    g = wl.unit_grid(15)
+    u, _ = solve(golden["cd4_n15_F"], hb.SchemeKind.CONVECTION_DIFFUSION_4,
+                 hb.constant_profile(0.0, g, gamma=-1.5), g)
+    assert rel_l2(u, golden["cd4_n15_U"]) < 1e-13
+    T = golden["gen_n15_table"]
+    u, _ = solve(golden["gen_n15_F"], hb.StencilTable(*T), hb.constant_profile(0.0, g), g)
+    assert rel_l2(u, golden["gen_n15_U"]) < 1e-13
+
+
+def test_anisotropic_dense_path(golden, cuda):
+    g = hb.make_grid(hb.Domain(0, PI, 0, 2.0, 0, 1.0), 9, 7, 6)
+    u, _ = solve(golden["aniso_F"], hb.SchemeKind.FOURTH_ORDER, hb.constant_profile(2.0, g), g)
+    assert rel_l2(u, golden["aniso_U"]) < 1e-13
+
+
+@pytest.mark.parametrize("cfg,planes", [(3, 511), (4, 64)])
+def test_large_configs_vs_oracle(cuda, cfg, planes):
+    """cfg3 at full size; cfg4 on a 64-plane slab of the full 1023^2 planes (the
+    oracle needs ~4 GB and minutes for the full 1023^3)."""
+    w = wl.workload(cfg)
+    # a slab keeps the full grid's step h = 1/(n+1): z-extent (planes + 1) h
+    g = w.grid if planes == w.n else hb.make_grid(
+        hb.Domain(0, 1, 0, 1, 0, (planes + 1) / (w.n + 1)), w.n, w.n, planes)
+    prof = w.profile if planes == w.n else hb.CoefficientProfile(
+        k2=np.zeros(planes + 2, complex), k2_z=np.zeros(planes + 2, complex),
+        k2_zz=np.zeros(planes + 2, complex), gamma=w.profile.gamma)
+    F = wl.host_rhs(w, planes=planes)
+    u, _ = solve(F, w.scheme, prof, g)
+    key = w.scheme.value
+    ref = orc.solve(F, oracle_table(key, prof, g), *orc.mode_cosines(g.n_x, g.n_y), workers=8)
+    err = rel_l2(u, ref)
+    print(f"cfg{cfg} rel L2 vs oracle: {err:.3e}")
+    assert err < TOL
+    assert err < 1e-12
+
+
+def test_partitioned_and_shared_modes_bitwise(cuda):
+    g = hb.make_grid(hb.Domain(0, PI, 0, 2.0, 0, 1.0), 15, 31, 12)
+    prof = hb.constant_profile(5.0, g)
+    F = np.random.default_rng(59).standard_normal(g.shape)
+    ref, _ = solve(F, hb.SchemeKind.FOURTH_ORDER, prof, g)
+    for cfg in (hb.SolverConfig(mode=hb.SharedWorkers(2)), hb.SolverConfig(mode=hb.Partitioned(1)),
+                hb.SolverConfig(mode=hb.Partitioned(3)), hb.SolverConfig(mode=hb.Partitioned(4, 2)),
+                hb.SolverConfig(mode=hb.Device())):
+        u, t = solve(F, hb.SchemeKind.FOURTH_ORDER, prof, g, cfg)
+        assert np.abs(u - ref).max() <= 1e-13, cfg
+        if isinstance(cfg.mode, hb.Partitioned):
+            assert np.array_equal(u, ref)
+            assert t.exchange_s >= 0.0
+
+
+def test_repeat_runs_bitwise_and_input_untouched(cuda):
+    w = wl.workload(1)
+    F = wl.host_rhs(w)
+    keep = F.copy()
+    u1, _ = solve(F, w.scheme, w.profile, w.grid)
+    u2, _ = solve(F, w.scheme, w.profile, w.grid)
+    assert np.array_equal(u1, u2) and np.array_equal(F, keep)
+
+
+def test_linearity_and_complex_rhs(cuda):
+    w = wl.workload(1)
+    rng = np.random.default_rng(29)
+    f1, f2 = rng.standard_normal(w.grid.shape), rng.standard_normal(w.grid.shape)
+    u1, _ = solve(f1, w.scheme, w.profile, w.grid)
+    u2, _ = solve(f2, w.scheme, w.profile, w.grid)
+    uc, _ = solve(f1 + 1j * f2, w.scheme, w.profile, w.grid)
+    assert np.abs(uc.real - u1).max() <= 1e-15 * np.abs(u1).max() * 10
+    assert np.abs(uc.imag - u2).max() <= 1e-15 * np.abs(u2).max() * 10
+    ul, _ = solve(0.7 * f1 - 1.3 * f2, w.scheme, w.profile, w.grid)
+    assert np.abs(ul - (0.7 * u1 - 1.3 * u2)).max() < 1e-12 * np.abs(ul).max()
+
+
+def test_zero_rhs_and_device_tensors(cuda):
+    import torch
+    w = wl.workload(1)
+    u, _ = solve(np.zeros(w.grid.shape), w.scheme, w.profile, w.grid)
+    assert not np.any(u)
+    F = wl.host_rhs(w)
+    t = torch.from_numpy(F).to(cuda)
+    ut, _ = hb.solve_discrete(hb.Field3D(t), hb.BoundaryData.zero(), w.scheme, w.profile, w.grid)
+    assert ut.values.is_cuda
+    u, _ = solve(F, w.scheme, w.profile, w.grid)
+    assert np.array_equal(ut.values.cpu().numpy(), u)
+
+
+# ---------------------------------------------------- 27-point operator
+def test_apply_fold_residual_vs_oracle(cuda):
+    g = hb.make_grid(hb.Domain(0, PI, 0, 2.0, 0, 1.0), 9, 7, 6)
+    prof = hb.constant_profile(2.0, g)
+    rng = np.random.default_rng(43)
+    box = rng.standard_normal((8, 9, 11))
+    T = oracle_table("4", prof, g)
+    bnd = hb.BoundaryData.from_array(box)
+    ext = bnd.closed_box(g).real
+    rhs = rng.standard_normal(g.shape)
+    folded = hb.fold_dirichlet(hb.Field3D(rhs), bnd, hb.SchemeKind.FOURTH_ORDER, prof, g)
+    assert np.array_equal(folded.values, rhs - orc.accumulate27(ext, T))  # bit-exact
+    u = rng.standard_normal(g.shape)
+    au = hb.apply_stencil(hb.Field3D(u), hb.BoundaryData.zero(), hb.SchemeKind.FOURTH_ORDER,
+                          prof, g)
+    e2 = np.zeros((8, 9, 11))
+    e2[1:-1, 1:-1, 1:-1] = u
+    assert np.array_equal(au.values, orc.accumulate27(e2, T))
+    r = hb.residual_l2(hb.Field3D(u), hb.Field3D(rhs), hb.SchemeKind.FOURTH_ORDER, prof, g)
+    assert r == pytest.approx(orc.residual_l2(u, rhs, T), rel=1e-12)
+
+
+def test_nonzero_boundary_solve_vs_dense(cuda):
+    """solve with folded Dirichlet data reproduces the dense 27-diagonal LU (test_solver.py:160-171)."""
+    g = hb.make_grid(hb.Domain(0, PI, 0, PI, 0, PI), 6, 6, 6)
+    prof = hb.constant_profile(2.0, g)
+    rng = np.random.default_rng(41)
+    F = rng.standard_normal(g.shape)
+    box = rng.standard_normal((8, 8, 8))
+    u, _ = hb.solve_discrete(hb.Field3D(F), hb.BoundaryData.from_array(box),
+                             hb.SchemeKind.FOURTH_ORDER, prof, g)
+    T = oracle_table("4", prof, g)
+    n = 216
+    A = np.zeros((n, n))
+    for c in range(n):
+        e = np.zeros(n)
+        e[c] = 1.0
+        ext = np.zeros((8, 8, 8))
+        ext[1:-1, 1:-1, 1:-1] = e.reshape(6, 6, 6)
+        A[:, c] = orc.accumulate27(ext, T).ravel()
+    ext = np.array(box)
+    ext[1:-1, 1:-1, 1:-1] = 0
+    rhs = F - orc.accumulate27(ext, T)
+    expect = np.linalg.solve(A, rhs.ravel()).reshape(6, 6, 6)
+    assert np.abs(u.values - expect).max() < 1e-12 * np.abs(expect).max()
+
+
+def test_cfg3_residual_at_full_size(cuda):
+    """Size-independent property at 511^3: ||A U - F|| / ||F|| at roundoff."""
+    import torch
+    w = wl.workload(3)
+    F = wl.device_rhs(w, cuda)
+    u, _ = hb.solve_discrete(hb.Field3D(F), hb.BoundaryData.zero(), w.scheme, w.profile, w.grid)
+    r = hb.residual_l2(u, hb.Field3D(F), w.scheme, w.profile, w.grid)
+    assert r / float(torch.linalg.norm(F)) < 1e-12
