@@ -230,6 +230,7 @@ class _EventClock:
         self.marks[name] = ev
 
     def seconds(self, a, b):
+        self.marks[b].synchronize()
         return self.marks[a].elapsed_time(self.marks[b]) / 1e3
 
 
