@@ -39,7 +39,10 @@ def real_parts(arr):
 def upload(host, device):
     """float64 host array -> contiguous float64 device tensor."""
     torch = _torch()
-    t = torch.from_numpy(np.ascontiguousarray(host, dtype=np.float64))
+    arr = np.ascontiguousarray(host, dtype=np.float64)
+    if not arr.flags.writeable:
+        arr = arr.copy()
+    t = torch.from_numpy(arr)
     return t.to(device=device, non_blocking=False)
 
 
