@@ -169,10 +169,10 @@ extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const
 extern "C" size_t hfb_workspace_bytes(const hfb_plan* p, int op) {
   if (!p) return 0;
   const size_t vol = (size_t)p->nx * p->ny * p->nz;
-  const size_t dense = dense_tmp_elems(p, p->nz);
+  const size_t tw = transform_work_elems(p, p->nz);
   switch (op) {
-    case 0: return sizeof(double) * (vol + dense);  // cp + dense temp
-    case 1: return sizeof(double) * dense;
+    case 0: return sizeof(double) * (vol + tw);  // cp + transform scratch
+    case 1: return sizeof(double) * tw;
     case 2: return sizeof(double) * vol;
     default: return 0;
   }
@@ -180,9 +180,7 @@ extern "C" size_t hfb_workspace_bytes(const hfb_plan* p, int op) {
 
 static int transform_range(hfb_plan* p, const double* src, double* dst, int z0, int z1,
                            double* tmp, cudaStream_t st) {
-  int rc = launch_dst_x(p, src, dst, z0, z1, 0, p->ny, tmp, st);
-  if (rc) return rc;
-  return launch_dst_y(p, dst, dst, z0, z1, 0, p->nx, tmp, st);
+  return transform_planes(p, src, dst, z0, z1, tmp, st);
 }
 
 extern "C" int hfb_transform_stack(hfb_plan* p, double* data, int z0, int z1, void* work,
@@ -225,7 +223,7 @@ extern "C" int hfb_solve(hfb_plan* p, const double* rhs, double* out, void* work
   cudaStream_t st = (cudaStream_t)stream;
   const size_t vol = (size_t)p->nx * p->ny * p->nz;
   double* cpw = (double*)work;
-  double* tmp = dense_tmp_elems(p, p->nz) ? cpw + vol : nullptr;
+  double* tmp = transform_work_elems(p, p->nz) ? cpw + vol : nullptr;
   int rc = transform_range(p, rhs, out, 0, p->nz, tmp, st);
   if (rc) return rc;
   rc = launch_thomas(p, out, p->ny, 0, cpw, st);

@@ -168,6 +168,11 @@ int launch_dst_x(hfb_plan* p, const double* src, double* dst, int z0, int z1, in
   const int nz = z1 - z0, nr = y1 - y0;
   if (nz <= 0 || nr <= 0) return HFB_OK;
   const long long ld = p->nx, ps = (long long)p->ny * p->nx;
+  if (dst16_ok(p->nx + 1)) {
+    const long long off = (long long)y0 * ld;
+    return launch_dst16(p->tw_x, p->sn_x, p->scale_x, p->nx + 1, src + off, dst + off, z0, nz,
+                        nr, ld, ps, ld, ps, false, st);
+  }
   if (p->logMx >= 0) {
     const int M = p->nx + 1;
     FftCtx c = make_ctx(M, p->logMx, p->tw_x, p->sn_x, p->scale_x);
@@ -238,6 +243,36 @@ int launch_dst_y(hfb_plan* p, const double* src, double* dst, int z0, int z1, in
   copy_region_kernel<<<cg, 256, 0, st>>>(tmp, dst, p->ny, ncol, ld, ps, (long long)z0 * ps + x0);
   HFB_LAUNCHED();
   return HFB_OK;
+}
+
+// Transposed scratch line stride for y-lines (even, >= ny).
+static long long tran_ld(const hfb_plan* p) { return (p->ny + 1) & ~1LL; }
+
+static bool tran_path(const hfb_plan* p) { return dst16_ok(p->nx + 1) && dst16_ok(p->ny + 1); }
+
+size_t transform_work_elems(const hfb_plan* p, int nplanes) {
+  if (tran_path(p)) return (size_t)nplanes * p->nx * tran_ld(p);
+  return dense_tmp_elems(p, nplanes);
+}
+
+int transform_planes(hfb_plan* p, const double* src, double* dst, int z0, int z1, double* work,
+                     cudaStream_t st) {
+  const int nz = z1 - z0;
+  if (nz <= 0) return HFB_OK;
+  if (!tran_path(p)) {
+    int rc = launch_dst_x(p, src, dst, z0, z1, 0, p->ny, work, st);
+    if (rc) return rc;
+    return launch_dst_y(p, dst, dst, z0, z1, 0, p->nx, work, st);
+  }
+  if (!work) return HFB_ERR_ARGUMENT;
+  // x-pass: rows (l, j, :) -> scratch (l, n, j) ; y-pass: scratch lines
+  // (l, n, :) -> natural (l, m, n). Scratch planes are indexed from 0.
+  const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), pst = ldt * p->nx;
+  int rc = launch_dst16(p->tw_x, p->sn_x, p->scale_x, p->nx + 1, src + (long long)z0 * ps,
+                        work, 0, nz, p->ny, p->nx, ps, ldt, pst, true, st);
+  if (rc) return rc;
+  return launch_dst16(p->tw_y, p->sn_y, p->scale_y, p->ny + 1, work, dst + (long long)z0 * ps,
+                      0, nz, p->nx, ldt, pst, p->nx, ps, true, st);
 }
 
 }  // namespace hfb
