@@ -170,8 +170,9 @@ int launch_dst_x(hfb_plan* p, const double* src, double* dst, int z0, int z1, in
   const long long ld = p->nx, ps = (long long)p->ny * p->nx;
   if (dst16_ok(p->nx + 1)) {
     const long long off = (long long)y0 * ld;
-    return launch_dst16(p->tw_x, p->sn_x, p->scale_x, p->nx + 1, src + off, dst + off, z0, nz,
-                        nr, ld, ps, ld, ps, false, st);
+    return launch_dst16(p->tw_x, p->sn_x, p->scale_x, p->nx + 1, src + off,
+                        src + (long long)p->nz * ps, dst + off, z0, nz, nr, ld, ps, ld, ps, false,
+                        st);
   }
   if (p->logMx >= 0) {
     const int M = p->nx + 1;
@@ -269,10 +270,11 @@ int transform_planes(hfb_plan* p, const double* src, double* dst, int z0, int z1
   // (l, n, :) -> natural (l, m, n). Scratch planes are indexed from 0.
   const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), pst = ldt * p->nx;
   int rc = launch_dst16(p->tw_x, p->sn_x, p->scale_x, p->nx + 1, src + (long long)z0 * ps,
-                        work, 0, nz, p->ny, p->nx, ps, ldt, pst, true, st);
+                        src + (long long)p->nz * ps, work, 0, nz, p->ny, p->nx, ps, ldt, pst,
+                        true, st);
   if (rc) return rc;
-  return launch_dst16(p->tw_y, p->sn_y, p->scale_y, p->ny + 1, work, dst + (long long)z0 * ps,
-                      0, nz, p->nx, ldt, pst, p->nx, ps, true, st);
+  return launch_dst16(p->tw_y, p->sn_y, p->scale_y, p->ny + 1, work, work + nz * pst,
+                      dst + (long long)z0 * ps, 0, nz, p->nx, ldt, pst, p->nx, ps, true, st);
 }
 
 }  // namespace hfb
