@@ -22,6 +22,13 @@
 
 namespace hfb {
 
+struct Fft16 {
+  int M, p, T;                     // length, log2, threads per group
+  const double2* __restrict__ tw;  // tw[k] = exp(-2 pi i k/M)
+  const double* __restrict__ sn;   // sin(pi j/M), j <= M/2
+  double scale;                    // sqrt(2/M)
+};
+
 struct StreamArgs {
   const double* src;
   double* dst;
@@ -51,12 +58,12 @@ __device__ __forceinline__ RowRef batch_row(const StreamArgs& a, long long batch
   return x;
 }
 
-template <bool TRAN>
+template <int P, bool TRAN>
 __global__ void __launch_bounds__(128, 3) dst16_stream_kernel(StreamArgs a, Fft16 c) {
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_delta[2][16];
   __shared__ int s_tail[2][16];
-  const int T = c.T;
+  constexpr int T = F16<P>::T;
   const int f = threadIdx.x / T, t = threadIdx.x - f * T;
   double2* wsum = reinterpret_cast<double2*>(sm + 2LL * a.NF * a.gbuf);
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + (blockDim.x / 32 + 1));
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(128, 3) dst16_stream_kernel(StreamArgs a, Fft1
     const double* g0 = a.src + x0.plane * a.in_ps + (long long)x0.row * a.in_ld;
     const double* g1 = a.src + x1.plane * a.in_ps + (long long)x1.row * a.in_ld;
     double2 v[16];
-    dst16_pre(v, c, t, [&](int e) -> double2 {
+    dst16_pre<P>(v, c.sn, t, [&](int e) -> double2 {
       const int p = e - 1;
       double xr = 0.0, xi = 0.0;
       if (x0.valid) xr = (t0 && p == last) ? __ldg(g0 + p) : r0[p];
@@ -143,9 +150,9 @@ __global__ void __launch_bounds__(128, 3) dst16_stream_kernel(StreamArgs a, Fft1
     });
     __syncthreads();  // staged rows consumed: the group buffer becomes FFT scratch
     double2* sb = reinterpret_cast<double2*>(gb);
-    fft16_forward(v, sb, c, t);
+    fft16_forward<P>(v, sb, c.tw, t);
     double2 ev[8], od[8];
-    dst16_post(v, sb, wsum, c, t, ev, od);
+    dst16_post<P>(v, sb, wsum, c.scale, t, ev, od);
     __syncthreads();
     // stage rows [2f, 2f+1] x positions
     double* q0 = gb;
@@ -186,6 +193,22 @@ __global__ void __launch_bounds__(128, 3) dst16_stream_kernel(StreamArgs a, Fft1
 
 bool dst16_ok(int M) { return M >= 16 && M <= 4096 && (M & (M - 1)) == 0; }
 
+template <int P, bool TRAN>
+static int launch_stream(const StreamArgs& a, const Fft16& c, int threads, size_t sm,
+                         cudaStream_t st) {
+  HFB_CUDA(cudaFuncSetAttribute(dst16_stream_kernel<P, TRAN>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per_sm = 1;
+  HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dst16_stream_kernel<P, TRAN>,
+                                                         threads, sm));
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long blocks = std::min<long long>(a.nbatch, (long long)sms * std::max(per_sm, 1));
+  dst16_stream_kernel<P, TRAN><<<(unsigned)blocks, threads, sm, st>>>(a, c);
+  return HFB_OK;
+}
+
 // Lines (plane z0.., nrow lines each, line stride in_ld, plane stride in_ps)
 // -> ROW (out_ld line stride) or TRAN (out_ld position stride).
 // src_end: one past the last element that may be read from src.
@@ -215,37 +238,29 @@ int launch_dst16(const double2* tw, const double* sn, double scale, int M, const
   a.out_ld = out_ld;
   a.out_ps = out_ps;
   a.N = M - 1;
-  a.NF = std::max(1, std::min(128 / c.T, 8));  // <= 128 threads (launch bounds)
-  while (a.NF * c.T < 32) ++a.NF;
+  a.NF = std::max(1, std::min(128 / c.T, 8));  // <= 128 threads, <= 16 rows per batch
   a.nbatch = (a.npairs + a.NF - 1) / a.NF;
   a.rowslot = ((a.N + 2) + 1) & ~1;
   a.stage_ld = (a.N % 2 == 1) ? a.N + 2 : a.N + 1;
-  a.gbuf = std::max({2 * a.rowslot, 2 * (pad16(M) + 1), 2 * a.stage_ld});
+  a.gbuf = std::max({2 * a.rowslot, 2 * (pad16(M) + 1), 2 * a.stage_ld});  // doubles
   a.gbuf = (a.gbuf + 1) & ~1;
   const int threads = a.NF * c.T;
   const size_t sm = (size_t)2 * a.NF * a.gbuf * sizeof(double) +
                     (threads / 32 + 1) * sizeof(double2) + 2 * sizeof(uint64_t);
   int per_sm = 1;
-  if (tran) {
-    HFB_CUDA(cudaFuncSetAttribute(dst16_stream_kernel<true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dst16_stream_kernel<true>,
-                                                           threads, sm));
-  } else {
-    HFB_CUDA(cudaFuncSetAttribute(dst16_stream_kernel<false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dst16_stream_kernel<false>,
-                                                           threads, sm));
+  int rc = HFB_OK;
+  switch (c.p) {
+#define HFB_P(PP)                                                                 \
+  case PP:                                                                        \
+    rc = tran ? launch_stream<PP, true>(a, c, threads, sm, st)                    \
+              : launch_stream<PP, false>(a, c, threads, sm, st);                  \
+    break;
+    HFB_P(4) HFB_P(5) HFB_P(6) HFB_P(7) HFB_P(8) HFB_P(9) HFB_P(10) HFB_P(11) HFB_P(12)
+#undef HFB_P
+    default: return HFB_ERR_ARGUMENT;
   }
-  int sms = 148;
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long blocks = std::min<long long>(a.nbatch, (long long)sms * std::max(per_sm, 1));
-  if (tran)
-    dst16_stream_kernel<true><<<(unsigned)blocks, threads, sm, st>>>(a, c);
-  else
-    dst16_stream_kernel<false><<<(unsigned)blocks, threads, sm, st>>>(a, c);
+  (void)per_sm;
+  if (rc) return rc;
   HFB_LAUNCHED();
   return HFB_OK;
 }

@@ -1,4 +1,6 @@
-// Register-resident DST-I engine for M = N+1 = 2^p, 16 <= M <= 4096.
+// Register-resident DST-I engine for M = N+1 = 2^P, 16 <= M <= 4096, with the
+// transform length a compile-time constant (all strides, twiddle steps and
+// shared-memory padding fold to immediates).
 //
 // One transform group = T = M/16 threads; thread t holds the 16 complex
 // values x[t + T*i] (the "cyclic" distribution). Stockham passes of radix 16
@@ -8,37 +10,34 @@
 // The last pass leaves its outputs in the same cyclic slots, so the FFT
 // needs (#passes - 1) exchanges: 2 for M = 512..4096.
 //
-// DST-I pre/post-processing (see hfb_internal.cuh for the algebra):
+// DST-I pre/post-processing (algebra in hfb_internal.cuh):
 //   pre : b_e = s_e (a_e + a_{M-e}) + (a_e - a_{M-e})/2 from the loader;
 //   post: B in registers -> C_k, D_k (k < M/2) with B_{M-k} read back from
 //         shared memory; odd outputs are a prefix sum over k done on
 //         contiguous k-segments (local scan + group scan), then handed back
-//         in the cyclic order so every store of a warp is contiguous.
+//         in the cyclic order.
 #pragma once
 #include "hfb_internal.cuh"
 
 namespace hfb {
 
-__host__ __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+__host__ __device__ __forceinline__ constexpr int pad16(int i) { return i + (i >> 4); }
 
-// multiply by w16^e (forward: exp(-2 pi i e / 16)), e in 0..9 (compile time)
+// multiply by w16^E (forward: exp(-2 pi i E / 16))
 template <int E>
 __device__ __forceinline__ double2 mul_w16(double2 a) {
   constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
   constexpr double r = 0.70710678118654752440;
-  if (E == 0) return a;
-  if (E == 4) return cmul_mi(a);
-  if (E == 8) return make_double2(-a.x, -a.y);
-  if (E == 2) return make_double2(r * (a.x + a.y), r * (a.y - a.x));
-  if (E == 6) return make_double2(r * (a.y - a.x), -r * (a.x + a.y));
-  // generic: w = (cos, -sin) of 2 pi E / 16
-  const double wc = (E == 1) ? c1 : (E == 3) ? s1 : (E == 9) ? -c1 : 0.0;
-  const double ws = (E == 1) ? s1 : (E == 3) ? c1 : (E == 9) ? -s1 : 0.0;
-  // (a.x + i a.y)(wc - i ws)
+  if constexpr (E == 0) return a;
+  if constexpr (E == 4) return cmul_mi(a);
+  if constexpr (E == 2) return make_double2(r * (a.x + a.y), r * (a.y - a.x));
+  if constexpr (E == 6) return make_double2(r * (a.y - a.x), -r * (a.x + a.y));
+  constexpr double wc = (E == 1) ? c1 : (E == 3) ? s1 : -c1;  // E = 1, 3, 9
+  constexpr double ws = (E == 1) ? s1 : (E == 3) ? c1 : -s1;
   return make_double2(fma(a.x, wc, a.y * ws), fma(a.y, wc, -a.x * ws));
 }
 
-// in-place 16-point forward DFT of v[0..16) (4 x 4 decomposition)
+// in-place 16-point forward DFT (4 x 4 decomposition)
 __device__ __forceinline__ void dft16(double2* v) {
   double2 y[16];
 #pragma unroll
@@ -48,16 +47,15 @@ __device__ __forceinline__ void dft16(double2* v) {
 #pragma unroll
     for (int q2 = 0; q2 < 4; ++q2) y[u1 * 4 + q2] = q[q2];
   }
-  // twiddle y[u1][q2] *= w16^(u1*q2)
-  y[1 * 4 + 1] = mul_w16<1>(y[5]);
-  y[1 * 4 + 2] = mul_w16<2>(y[6]);
-  y[1 * 4 + 3] = mul_w16<3>(y[7]);
-  y[2 * 4 + 1] = mul_w16<2>(y[9]);
-  y[2 * 4 + 2] = mul_w16<4>(y[10]);
-  y[2 * 4 + 3] = mul_w16<6>(y[11]);
-  y[3 * 4 + 1] = mul_w16<3>(y[13]);
-  y[3 * 4 + 2] = mul_w16<6>(y[14]);
-  y[3 * 4 + 3] = mul_w16<9>(y[15]);
+  y[5] = mul_w16<1>(y[5]);
+  y[6] = mul_w16<2>(y[6]);
+  y[7] = mul_w16<3>(y[7]);
+  y[9] = mul_w16<2>(y[9]);
+  y[10] = mul_w16<4>(y[10]);
+  y[11] = mul_w16<6>(y[11]);
+  y[13] = mul_w16<3>(y[13]);
+  y[14] = mul_w16<6>(y[14]);
+  y[15] = mul_w16<9>(y[15]);
 #pragma unroll
   for (int q2 = 0; q2 < 4; ++q2) {
     double2 q[4] = {y[q2], y[4 + q2], y[8 + q2], y[12 + q2]};
@@ -67,29 +65,29 @@ __device__ __forceinline__ void dft16(double2* v) {
   }
 }
 
-struct Fft16 {
-  int M, p, T;                     // length, log2, threads per group
-  const double2* __restrict__ tw;  // tw[k] = exp(-2 pi i k/M)
-  const double* __restrict__ sn;   // sin(pi j/M), j <= M/2
-  double scale;                    // sqrt(2/M)
+template <int P>
+struct F16 {
+  static constexpr int M = 1 << P;
+  static constexpr int T = M / 16;
+  static constexpr int FULL = P / 4;
+  static constexpr int REM = P % 4;
+  static constexpr int BUF = pad16(M) + 1;  // double2 slots of a group buffer
 };
 
-// One radix-R Stockham pass on the cyclic registers (R in {2,4,8,16}).
-// Butterflies j = t + T*b (b < 16/R) take slots b + u*(16/R).
-template <int R>
-__device__ __forceinline__ void pass_regs(double2* v, const Fft16& c, int L, int t) {
-  constexpr int NB = 16 / R;
-  const int twstep = c.M / (L * R);
+// One radix-R Stockham pass (stride L) on the cyclic registers.
+template <int P, int R, int L>
+__device__ __forceinline__ void pass_regs(double2* v, const double2* __restrict__ tw, int t) {
+  constexpr int M = F16<P>::M, T = F16<P>::T, NB = 16 / R, TWSTEP = M / (L * R);
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    const int j = t + c.T * b;
+    const int j = t + T * b;
     const int k = j & (L - 1);
     double2 w[R];
 #pragma unroll
     for (int u = 0; u < R; ++u) w[u] = v[b + u * NB];
-    if (L > 1) {
+    if constexpr (L > 1) {
 #pragma unroll
-      for (int u = 1; u < R; ++u) w[u] = cmul(w[u], __ldg(&c.tw[u * k * twstep]));
+      for (int u = 1; u < R; ++u) w[u] = cmul(w[u], __ldg(&tw[u * k * TWSTEP]));
     }
     if constexpr (R == 16) {
       dft16(w);
@@ -101,83 +99,75 @@ __device__ __forceinline__ void pass_regs(double2* v, const Fft16& c, int L, int
   }
 }
 
-// Write a pass's outputs (Stockham destination order) to shared memory.
-template <int R>
-__device__ __forceinline__ void pass_store(const double2* v, double2* sb, const Fft16& c, int L,
-                                           int t) {
-  constexpr int NB = 16 / R;
+// Store the outputs of a radix-16 pass in Stockham order, then reload cyclic.
+template <int P, int L>
+__device__ __forceinline__ void exchange16(double2* v, double2* sb, int t) {
+  constexpr int T = F16<P>::T;
+  const int k = t & (L - 1);
+  const int base = (t - k) * 16 + k;
 #pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const int j = t + c.T * b;
-    const int k = j & (L - 1);
-    const int base = (j - k) * R + k;
+  for (int u = 0; u < 16; ++u) sb[pad16(base + u * L)] = v[u];
+  __syncthreads();
 #pragma unroll
-    for (int u = 0; u < R; ++u) sb[pad16(base + u * L)] = v[b + u * NB];
+  for (int i = 0; i < 16; ++i) v[i] = sb[pad16(t + T * i)];
+  __syncthreads();
+}
+
+// Full forward FFT: cyclic natural-order input -> cyclic natural-order output.
+template <int P>
+__device__ __forceinline__ void fft16_forward(double2* v, double2* sb,
+                                              const double2* __restrict__ tw, int t) {
+  using G = F16<P>;
+  pass_regs<P, 16, 1>(v, tw, t);
+  if constexpr (G::FULL >= 2) {
+    exchange16<P, 1>(v, sb, t);
+    pass_regs<P, 16, 16>(v, tw, t);
+  }
+  if constexpr (G::FULL >= 3) {
+    exchange16<P, 16>(v, sb, t);
+    pass_regs<P, 16, 256>(v, tw, t);
+  }
+  if constexpr (G::REM > 0) {
+    constexpr int L = 1 << (4 * G::FULL);
+    exchange16<P, L / 16>(v, sb, t);
+    pass_regs<P, (1 << G::REM), L>(v, tw, t);
   }
 }
 
-__device__ __forceinline__ void load_cyclic(double2* v, const double2* sb, const Fft16& c, int t) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = sb[pad16(t + c.T * i)];
-}
-
-// Full forward FFT: v (cyclic, natural input order) -> v (cyclic, natural
-// output order). sb: this group's padded buffer (>= pad16(M) slots). `bar`
-// synchronises all groups of the CTA (every thread must call).
-__device__ __forceinline__ void fft16_forward(double2* v, double2* sb, const Fft16& c, int t) {
-  const int full = c.p / 4;     // radix-16 passes
-  const int rem = c.p - 4 * full;  // final radix 2^rem (0 = none)
-  int L = 1;
-  for (int s = 0; s < full; ++s) {
-    pass_regs<16>(v, c, L, t);
-    const bool last = (s == full - 1) && rem == 0;
-    if (!last) {
-      pass_store<16>(v, sb, c, L, t);
-      __syncthreads();
-      load_cyclic(v, sb, c, t);
-      __syncthreads();
-    }
-    L *= 16;
-  }
-  if (rem == 1) pass_regs<2>(v, c, L, t);
-  else if (rem == 2) pass_regs<4>(v, c, L, t);
-  else if (rem == 3) pass_regs<8>(v, c, L, t);
-}
-
-// Exclusive scan over the T threads of a group (T a power of two, groups
-// are T-aligned runs of threadIdx.x). wsum: >= blockDim/32 slots.
-__device__ __forceinline__ double2 group_scan16(double2 v, int t, int T, double2* wsum) {
+// Exclusive scan over the T threads of a group (T-aligned runs of threadIdx).
+template <int T>
+__device__ __forceinline__ double2 group_scan(double2 v, int t, double2* wsum) {
+  constexpr int W = T < 32 ? T : 32;
   const int lane = threadIdx.x & 31;
-  const int width = T < 32 ? T : 32;
   double2 inc = v;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    if (o < width) {
-      const double tx = __shfl_up_sync(0xffffffffu, inc.x, o, width);
-      const double ty = __shfl_up_sync(0xffffffffu, inc.y, o, width);
-      if ((lane & (width - 1)) >= o) {
-        inc.x += tx;
-        inc.y += ty;
-      }
+  for (int o = 1; o < W; o <<= 1) {
+    const double tx = __shfl_up_sync(0xffffffffu, inc.x, o, W);
+    const double ty = __shfl_up_sync(0xffffffffu, inc.y, o, W);
+    if ((lane & (W - 1)) >= o) {
+      inc.x += tx;
+      inc.y += ty;
     }
   }
   double2 ex = csub(inc, v);
-  if (T > 32) {
+  if constexpr (T > 32) {
     const int warp = threadIdx.x >> 5;
     if (lane == 31) wsum[warp] = inc;
     __syncthreads();
     const int w0 = (threadIdx.x - t) >> 5;
-    for (int w = w0; w < warp; ++w) ex = cadd(ex, wsum[w]);
+#pragma unroll
+    for (int w = 0; w < T / 32 - 1; ++w)
+      if (w0 + w < warp) ex = cadd(ex, wsum[w0 + w]);
   }
   return ex;
 }
 
-// DST post-processing. In: v = B (cyclic). Out: for i < 8 (k = t + T*i < M/2):
-// ev[i] = sqrt(2/M) S_{2k} (= D_k; meaningless for k = 0) and od[i] =
-// sqrt(2/M) S_{2k+1}. sb: group buffer; wsum: CTA scratch. M >= 16.
+// DST post-processing. In: v = B (cyclic). Out: for i < 8 (k = t + T i):
+// ev[i] = scale * S_{2k} (D_k; unused for k = 0), od[i] = scale * S_{2k+1}.
+template <int P>
 __device__ __forceinline__ void dst16_post(const double2* v, double2* sb, double2* wsum,
-                                           const Fft16& c, int t, double2* ev, double2* od) {
-  const int M = c.M, T = c.T;
+                                           double scale, int t, double2* ev, double2* od) {
+  constexpr int M = F16<P>::M, T = F16<P>::T;
 #pragma unroll
   for (int i = 0; i < 16; ++i) sb[pad16(t + T * i)] = v[i];
   __syncthreads();
@@ -188,33 +178,32 @@ __device__ __forceinline__ void dst16_post(const double2* v, double2* sb, double
     const double2 bk = v[i];
     const double2 bm = sb[pad16((M - k) & (M - 1))];
     C[i] = make_double2(0.5 * (bk.x + bm.x), 0.5 * (bk.y + bm.y));
-    ev[i] = make_double2(-0.5 * c.scale * (bk.y - bm.y), 0.5 * c.scale * (bk.x - bm.x));
+    ev[i] = make_double2(-0.5 * scale * (bk.y - bm.y), 0.5 * scale * (bk.x - bm.x));
   }
   if (t == 0) C[0] = cscale(C[0], 0.5);
-  __syncthreads();  // all B_{M-k} reads done before C overwrites the buffer
+  __syncthreads();
 #pragma unroll
   for (int i = 0; i < 8; ++i) sb[pad16(t + T * i)] = C[i];
   __syncthreads();
-  // contiguous segment k in [8t, 8t + 8): local inclusive scan
   double2 seg[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) seg[s] = sb[pad16(8 * t + s)];
 #pragma unroll
   for (int s = 1; s < 8; ++s) seg[s] = cadd(seg[s], seg[s - 1]);
-  const double2 off = group_scan16(seg[7], t, T, wsum);
-  __syncthreads();  // segment reads (and wsum reads) done before P overwrites
+  const double2 off = group_scan<T>(seg[7], t, wsum);
+  __syncthreads();
 #pragma unroll
   for (int s = 0; s < 8; ++s) sb[pad16(8 * t + s)] = cadd(seg[s], off);
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < 8; ++i) od[i] = cscale(sb[pad16(t + T * i)], c.scale);
+  for (int i = 0; i < 8; ++i) od[i] = cscale(sb[pad16(t + T * i)], scale);
 }
 
-// Pre-processing from a loader giving a_e for e in [1, M-1] (0 outside):
-// v[i] = b_{t + T i}.
-template <class Load>
-__device__ __forceinline__ void dst16_pre(double2* v, const Fft16& c, int t, Load&& load) {
-  const int M = c.M, T = c.T, H = M >> 1;
+// Pre-processing: v[i] = b_{t + T i} from a loader of a_e, e in [1, M-1].
+template <int P, class Load>
+__device__ __forceinline__ void dst16_pre(double2* v, const double* __restrict__ sn, int t,
+                                          Load&& load) {
+  constexpr int M = F16<P>::M, T = F16<P>::T, H = M / 2;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const int e = t + T * i;
@@ -225,7 +214,7 @@ __device__ __forceinline__ void dst16_pre(double2* v, const Fft16& c, int t, Loa
       v[i] = make_double2(2.0 * a.x, 2.0 * a.y);
     } else {
       const double2 p = load(e), q = load(M - e);
-      const double s = __ldg(&c.sn[e < H ? e : M - e]);
+      const double s = __ldg(&sn[e < H ? e : M - e]);
       const double sx = (p.x + q.x) * s, sy = (p.y + q.y) * s;
       v[i] = make_double2(fma(0.5, p.x - q.x, sx), fma(0.5, p.y - q.y, sy));
     }
