@@ -6,15 +6,15 @@
 // 1D TMA bulk copies (cp.async.bulk + mbarrier, double-buffered), so the HBM
 // latency of batch i+1 overlaps the FFT of batch i. Rows need not be 16-byte
 // aligned: the copy starts at the aligned address below the row and the
-// consumer skips the leading element.
+// consumer skips the leading element; a copy that would read past the end of
+// the source array is shortened and thread 0 patches the last element.
+// Thread 0 also resolves every row's input/output addresses per batch into
+// shared memory, so the transform threads do no index division.
 //
 // Output, staged through shared memory:
-//   ROW  : out[plane][row][pos] — each group stores its own two rows,
-//          coalesced;
+//   ROW  : out[plane][row][pos] — each group stores its own two rows;
 //   TRAN : out[plane][pos][row] — lines become columns; a warp stores 2NF
 //          consecutive rows of 32/(2NF) positions.
-// The x-pass uses TRAN into a padded scratch (lines of the y-pass); the
-// y-pass uses TRAN back into the natural (m, n) order.
 #include <algorithm>
 
 #include "fft16.cuh"
@@ -36,33 +36,23 @@ struct StreamArgs {
   int z0, nrow, ppp;      // first plane, lines per plane, pairs per plane
   long long npairs, nbatch;
   long long in_ld, in_ps, out_ld, out_ps;
-  int N, NF;
-  int rowslot;   // doubles per staged input row (even, >= N + 2)
+  int N, NF, logW;        // line length, groups per CTA, log2(2 NF)
+  int rowslot;   // doubles per staged input row (even, >= N + 4)
   int gbuf;      // doubles per group buffer per stage
   int stage_ld;  // output staging row stride (odd, >= N)
 };
 
-struct RowRef {
-  long long plane;
-  int row;
-  bool valid;
-};
+constexpr int kMaxRows = 16;  // 2 * NF
 
-__device__ __forceinline__ RowRef batch_row(const StreamArgs& a, long long batch, int r) {
-  RowRef x;
-  const long long pr = batch * a.NF + (r >> 1);
-  x.valid = pr < a.npairs;
-  x.plane = x.valid ? a.z0 + pr / a.ppp : 0;
-  x.row = x.valid ? 2 * (int)(pr % a.ppp) + (r & 1) : 0;
-  x.valid = x.valid && x.row < a.nrow;
-  return x;
-}
+struct BatchMeta {
+  long long out[2][kMaxRows];  // output base offset of each row, -1 if absent
+  int delta[2][kMaxRows];      // staged-row offset (doubles) of element 0
+};
 
 template <int P, bool TRAN>
 __global__ void __launch_bounds__(128, 3) dst16_stream_kernel(StreamArgs a, Fft16 c) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ int s_delta[2][16];
-  __shared__ int s_tail[2][16];
+  __shared__ BatchMeta meta;
   constexpr int T = F16<P>::T;
   const int f = threadIdx.x / T, t = threadIdx.x - f * T;
   double2* wsum = reinterpret_cast<double2*>(sm + 2LL * a.NF * a.gbuf);
@@ -76,46 +66,49 @@ __global__ void __launch_bounds__(128, 3) dst16_stream_kernel(StreamArgs a, Fft1
   }
   __syncthreads();
 
-  // thread 0: start the bulk copies of `batch` into stage s. Row r is copied
-  // from the 16-byte aligned address at or below its start; `delta` is the
-  // number of leading doubles to skip; a row whose rounded-up copy would read
-  // past src_end drops its last 16 bytes and the consumer loads the tail.
-  auto row_copy = [&](long long batch, int r, const double*& A16, uint32_t& S, int& d,
-                      int& tail) {
-    const RowRef x = batch_row(a, batch, r);
-    S = 0;
-    d = 0;
-    tail = 0;
-    if (!x.valid) return;
-    const double* A = a.src + x.plane * a.in_ps + (long long)x.row * a.in_ld;
-    A16 = reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(A) & ~uintptr_t(15));
-    d = (int)(A - A16);
-    S = (uint32_t)((8 * (a.N + d) + 15) & ~15);
-    if (A16 + S / 8 > a.src_end) {
-      S -= 16;
-      tail = 1;
-    }
-  };
+  // thread 0: resolve the rows of `batch` and start their bulk copies into
+  // stage s (staged row r at gbuf(s, r/2) + (r&1)*rowslot + 2, 16-B aligned)
   auto issue = [&](long long batch, int s) {
     uint32_t total = 0;
+    const int rows = 2 * a.NF;
 #pragma unroll 1
-    for (int r = 0; r < 2 * a.NF; ++r) {
-      const double* A16;
-      uint32_t S;
-      int d, tail;
-      row_copy(batch, r, A16, S, d, tail);
-      total += S;
-      s_delta[s][r] = d;
-      s_tail[s][r] = tail;
-    }
-    mbar_arrive_expect_tx(&bar[s], total);
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1) mbar_arrive_expect_tx(&bar[s], total);
 #pragma unroll 1
-    for (int r = 0; r < 2 * a.NF; ++r) {
-      const double* A16;
-      uint32_t S;
-      int d, tail;
-      row_copy(batch, r, A16, S, d, tail);
-      if (S) bulk_g2s(gbuf(s, r >> 1) + (r & 1) * a.rowslot, A16, S, &bar[s]);
+      for (int r = 0; r < rows; ++r) {
+        const long long pr = batch * a.NF + (r >> 1);
+        int row = 0;
+        long long plane = 0;
+        bool valid = pr < a.npairs;
+        if (valid) {
+          plane = a.z0 + pr / a.ppp;
+          row = 2 * (int)(pr % a.ppp) + (r & 1);
+          valid = row < a.nrow;
+        }
+        if (!valid) {
+          if (pass == 0) {
+            meta.out[s][r] = -1;
+            meta.delta[s][r] = 2;
+          }
+          continue;
+        }
+        const double* A = a.src + plane * a.in_ps + (long long)row * a.in_ld;
+        const double* A16 =
+            reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(A) & ~uintptr_t(15));
+        const int d = (int)(A - A16);
+        uint32_t S = (uint32_t)((8 * (a.N + d) + 15) & ~15);
+        const bool cut = A16 + S / 8 > a.src_end;
+        if (cut) S -= 16;
+        double* dstrow = gbuf(s, r >> 1) + (r & 1) * a.rowslot + 2;
+        if (pass == 0) {
+          total += S;
+          meta.delta[s][r] = 2 + d;
+          meta.out[s][r] = TRAN ? plane * a.out_ps + row : plane * a.out_ps + row * a.out_ld;
+          if (cut) dstrow[d + a.N - 1] = __ldg(A + a.N - 1);  // not covered by the copy
+        } else {
+          bulk_g2s(dstrow, A16, S, &bar[s]);
+        }
+      }
     }
   };
 
@@ -133,28 +126,19 @@ __global__ void __launch_bounds__(128, 3) dst16_stream_kernel(StreamArgs a, Fft1
     if (s == 0) phase0 ^= 1; else phase1 ^= 1;
 
     double* gb = gbuf(s, f);
-    const RowRef x0 = batch_row(a, batch, 2 * f), x1 = batch_row(a, batch, 2 * f + 1);
-    const double* r0 = gb + s_delta[s][2 * f];
-    const double* r1 = gb + a.rowslot + s_delta[s][2 * f + 1];
-    const bool t0 = s_tail[s][2 * f], t1 = s_tail[s][2 * f + 1];
-    const int last = a.N - 1;
-    const double* g0 = a.src + x0.plane * a.in_ps + (long long)x0.row * a.in_ld;
-    const double* g1 = a.src + x1.plane * a.in_ps + (long long)x1.row * a.in_ld;
+    const double* r0 = gb + meta.delta[s][2 * f] - 1;            // a_e at r0[e]
+    const double* r1 = gb + a.rowslot + meta.delta[s][2 * f + 1] - 1;
+    const bool v0 = meta.out[s][2 * f] >= 0, v1 = meta.out[s][2 * f + 1] >= 0;
     double2 v[16];
     dst16_pre<P>(v, c.sn, t, [&](int e) -> double2 {
-      const int p = e - 1;
-      double xr = 0.0, xi = 0.0;
-      if (x0.valid) xr = (t0 && p == last) ? __ldg(g0 + p) : r0[p];
-      if (x1.valid) xi = (t1 && p == last) ? __ldg(g1 + p) : r1[p];
-      return make_double2(xr, xi);
+      return make_double2(v0 ? r0[e] : 0.0, v1 ? r1[e] : 0.0);
     });
-    __syncthreads();  // staged rows consumed: the group buffer becomes FFT scratch
+    group_sync<T>(f);  // staged rows consumed: the group buffer becomes FFT scratch
     double2* sb = reinterpret_cast<double2*>(gb);
-    fft16_forward<P>(v, sb, c.tw, t);
+    fft16_forward<P>(v, sb, c.tw, t, f);
     double2 ev[8], od[8];
-    dst16_post<P>(v, sb, wsum, c.scale, t, ev, od);
-    __syncthreads();
-    // stage rows [2f, 2f+1] x positions
+    dst16_post<P>(v, sb, wsum, c.scale, t, f, ev, od);
+    group_sync<T>(f);
     double* q0 = gb;
     double* q1 = gb + a.stage_ld;
 #pragma unroll
@@ -167,23 +151,22 @@ __global__ void __launch_bounds__(128, 3) dst16_stream_kernel(StreamArgs a, Fft1
       q0[2 * k] = od[i].x;
       q1[2 * k] = od[i].y;
     }
-    __syncthreads();
     if (!TRAN) {
-      double* o0 = a.dst + x0.plane * a.out_ps + (long long)x0.row * a.out_ld;
-      double* o1 = a.dst + x1.plane * a.out_ps + (long long)x1.row * a.out_ld;
+      group_sync<T>(f);
+      const long long b0 = meta.out[s][2 * f], b1 = meta.out[s][2 * f + 1];
       for (int p = t; p < a.N; p += T) {
-        if (x0.valid) o0[p] = q0[p];
-        if (x1.valid) o1[p] = q1[p];
+        if (b0 >= 0) a.dst[b0 + p] = q0[p];
+        if (b1 >= 0) a.dst[b1 + p] = q1[p];
       }
     } else {
+      __syncthreads();
       const int W = 2 * a.NF;
       const int total = a.N * W;
       for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        const int pos = e / W, r = e - pos * W;
-        const RowRef x = batch_row(a, batch, r);
-        if (!x.valid) continue;
-        a.dst[x.plane * a.out_ps + (long long)pos * a.out_ld + x.row] =
-            gbuf(s, r >> 1)[(r & 1) * a.stage_ld + pos];
+        const int pos = e >> a.logW, r = e & (W - 1);
+        const long long base = meta.out[s][r];
+        if (base < 0) continue;
+        a.dst[base + (long long)pos * a.out_ld] = gbuf(s, r >> 1)[(r & 1) * a.stage_ld + pos];
       }
     }
     __syncthreads();  // stage s is free for the prefetch issued next iteration
@@ -238,28 +221,28 @@ int launch_dst16(const double2* tw, const double* sn, double scale, int M, const
   a.out_ld = out_ld;
   a.out_ps = out_ps;
   a.N = M - 1;
-  a.NF = std::max(1, std::min(128 / c.T, 8));  // <= 128 threads, <= 16 rows per batch
+  a.NF = std::max(1, std::min(128 / c.T, kMaxRows / 2));  // <= 128 threads
+  a.logW = 0;
+  while ((1 << a.logW) < 2 * a.NF) ++a.logW;
   a.nbatch = (a.npairs + a.NF - 1) / a.NF;
-  a.rowslot = ((a.N + 2) + 1) & ~1;
+  a.rowslot = ((a.N + 4) + 1) & ~1;
   a.stage_ld = (a.N % 2 == 1) ? a.N + 2 : a.N + 1;
   a.gbuf = std::max({2 * a.rowslot, 2 * (pad16(M) + 1), 2 * a.stage_ld});  // doubles
   a.gbuf = (a.gbuf + 1) & ~1;
   const int threads = a.NF * c.T;
   const size_t sm = (size_t)2 * a.NF * a.gbuf * sizeof(double) +
                     (threads / 32 + 1) * sizeof(double2) + 2 * sizeof(uint64_t);
-  int per_sm = 1;
   int rc = HFB_OK;
   switch (c.p) {
-#define HFB_P(PP)                                                                 \
-  case PP:                                                                        \
-    rc = tran ? launch_stream<PP, true>(a, c, threads, sm, st)                    \
-              : launch_stream<PP, false>(a, c, threads, sm, st);                  \
+#define HFB_P(PP)                                                              \
+  case PP:                                                                     \
+    rc = tran ? launch_stream<PP, true>(a, c, threads, sm, st)                 \
+              : launch_stream<PP, false>(a, c, threads, sm, st);               \
     break;
     HFB_P(4) HFB_P(5) HFB_P(6) HFB_P(7) HFB_P(8) HFB_P(9) HFB_P(10) HFB_P(11) HFB_P(12)
 #undef HFB_P
     default: return HFB_ERR_ARGUMENT;
   }
-  (void)per_sm;
   if (rc) return rc;
   HFB_LAUNCHED();
   return HFB_OK;

@@ -65,6 +65,17 @@ __device__ __forceinline__ void dft16(double2* v) {
   }
 }
 
+// Barrier over one transform group: a named barrier (id 1 + f, T threads)
+// when the group is whole warps, else the CTA barrier.
+template <int T>
+__device__ __forceinline__ void group_sync(int f) {
+  if constexpr (T >= 32) {
+    asm volatile("bar.sync %0, %1;" ::"r"(f + 1), "n"(T) : "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
 template <int P>
 struct F16 {
   static constexpr int M = 1 << P;
@@ -101,42 +112,42 @@ __device__ __forceinline__ void pass_regs(double2* v, const double2* __restrict_
 
 // Store the outputs of a radix-16 pass in Stockham order, then reload cyclic.
 template <int P, int L>
-__device__ __forceinline__ void exchange16(double2* v, double2* sb, int t) {
+__device__ __forceinline__ void exchange16(double2* v, double2* sb, int t, int f) {
   constexpr int T = F16<P>::T;
   const int k = t & (L - 1);
   const int base = (t - k) * 16 + k;
 #pragma unroll
   for (int u = 0; u < 16; ++u) sb[pad16(base + u * L)] = v[u];
-  __syncthreads();
+  group_sync<T>(f);
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = sb[pad16(t + T * i)];
-  __syncthreads();
+  group_sync<T>(f);
 }
 
 // Full forward FFT: cyclic natural-order input -> cyclic natural-order output.
 template <int P>
 __device__ __forceinline__ void fft16_forward(double2* v, double2* sb,
-                                              const double2* __restrict__ tw, int t) {
+                                              const double2* __restrict__ tw, int t, int f) {
   using G = F16<P>;
   pass_regs<P, 16, 1>(v, tw, t);
   if constexpr (G::FULL >= 2) {
-    exchange16<P, 1>(v, sb, t);
+    exchange16<P, 1>(v, sb, t, f);
     pass_regs<P, 16, 16>(v, tw, t);
   }
   if constexpr (G::FULL >= 3) {
-    exchange16<P, 16>(v, sb, t);
+    exchange16<P, 16>(v, sb, t, f);
     pass_regs<P, 16, 256>(v, tw, t);
   }
   if constexpr (G::REM > 0) {
     constexpr int L = 1 << (4 * G::FULL);
-    exchange16<P, L / 16>(v, sb, t);
+    exchange16<P, L / 16>(v, sb, t, f);
     pass_regs<P, (1 << G::REM), L>(v, tw, t);
   }
 }
 
 // Exclusive scan over the T threads of a group (T-aligned runs of threadIdx).
 template <int T>
-__device__ __forceinline__ double2 group_scan(double2 v, int t, double2* wsum) {
+__device__ __forceinline__ double2 group_scan(double2 v, int t, int f, double2* wsum) {
   constexpr int W = T < 32 ? T : 32;
   const int lane = threadIdx.x & 31;
   double2 inc = v;
@@ -153,7 +164,7 @@ __device__ __forceinline__ double2 group_scan(double2 v, int t, double2* wsum) {
   if constexpr (T > 32) {
     const int warp = threadIdx.x >> 5;
     if (lane == 31) wsum[warp] = inc;
-    __syncthreads();
+    group_sync<T>(f);
     const int w0 = (threadIdx.x - t) >> 5;
 #pragma unroll
     for (int w = 0; w < T / 32 - 1; ++w)
@@ -166,11 +177,12 @@ __device__ __forceinline__ double2 group_scan(double2 v, int t, double2* wsum) {
 // ev[i] = scale * S_{2k} (D_k; unused for k = 0), od[i] = scale * S_{2k+1}.
 template <int P>
 __device__ __forceinline__ void dst16_post(const double2* v, double2* sb, double2* wsum,
-                                           double scale, int t, double2* ev, double2* od) {
+                                           double scale, int t, int f, double2* ev,
+                                           double2* od) {
   constexpr int M = F16<P>::M, T = F16<P>::T;
 #pragma unroll
   for (int i = 0; i < 16; ++i) sb[pad16(t + T * i)] = v[i];
-  __syncthreads();
+  group_sync<T>(f);
   double2 C[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -181,25 +193,27 @@ __device__ __forceinline__ void dst16_post(const double2* v, double2* sb, double
     ev[i] = make_double2(-0.5 * scale * (bk.y - bm.y), 0.5 * scale * (bk.x - bm.x));
   }
   if (t == 0) C[0] = cscale(C[0], 0.5);
-  __syncthreads();
+  group_sync<T>(f);
 #pragma unroll
   for (int i = 0; i < 8; ++i) sb[pad16(t + T * i)] = C[i];
-  __syncthreads();
+  group_sync<T>(f);
   double2 seg[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) seg[s] = sb[pad16(8 * t + s)];
 #pragma unroll
   for (int s = 1; s < 8; ++s) seg[s] = cadd(seg[s], seg[s - 1]);
-  const double2 off = group_scan<T>(seg[7], t, wsum);
-  __syncthreads();
+  const double2 off = group_scan<T>(seg[7], t, f, wsum);
+  group_sync<T>(f);
 #pragma unroll
   for (int s = 0; s < 8; ++s) sb[pad16(8 * t + s)] = cadd(seg[s], off);
-  __syncthreads();
+  group_sync<T>(f);
 #pragma unroll
   for (int i = 0; i < 8; ++i) od[i] = cscale(sb[pad16(t + T * i)], scale);
 }
 
-// Pre-processing: v[i] = b_{t + T i} from a loader of a_e, e in [1, M-1].
+// Pre-processing: v[i] = b_{t + T i} from a loader of a_e (e in [1, M-1]); the
+// loader may return garbage for e = 0 and e = M (selected away here). The one
+// formula also covers b_0 = 0 (s_0 = 0, a_0 = a_M = 0) and b_{M/2} = 2 a_{M/2}.
 template <int P, class Load>
 __device__ __forceinline__ void dst16_pre(double2* v, const double* __restrict__ sn, int t,
                                           Load&& load) {
@@ -207,17 +221,15 @@ __device__ __forceinline__ void dst16_pre(double2* v, const double* __restrict__
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const int e = t + T * i;
-    if (e == 0) {
-      v[i] = make_double2(0.0, 0.0);
-    } else if (e == H) {
-      const double2 a = load(e);
-      v[i] = make_double2(2.0 * a.x, 2.0 * a.y);
-    } else {
-      const double2 p = load(e), q = load(M - e);
-      const double s = __ldg(&sn[e < H ? e : M - e]);
-      const double sx = (p.x + q.x) * s, sy = (p.y + q.y) * s;
-      v[i] = make_double2(fma(0.5, p.x - q.x, sx), fma(0.5, p.y - q.y, sy));
+    double2 p = load(e), q = load(M - e);
+    if (i == 0) {
+      const bool z = (t == 0);
+      p = z ? make_double2(0.0, 0.0) : p;
+      q = z ? make_double2(0.0, 0.0) : q;
     }
+    const double s = __ldg(&sn[e <= H ? e : M - e]);
+    const double sx = (p.x + q.x) * s, sy = (p.y + q.y) * s;
+    v[i] = make_double2(fma(0.5, p.x - q.x, sx), fma(0.5, p.y - q.y, sy));
   }
 }
 
