@@ -170,8 +170,9 @@ extern "C" size_t hfb_workspace_bytes(const hfb_plan* p, int op) {
   if (!p) return 0;
   const size_t vol = (size_t)p->nx * p->ny * p->nz;
   const size_t tw = transform_work_elems(p, p->nz);
+  const size_t fw = fused_work_elems(p);
   switch (op) {
-    case 0: return sizeof(double) * (vol + tw);  // cp + transform scratch
+    case 0: return sizeof(double) * (fw ? fw : vol + tw);  // fused, or cp + scratch
     case 1: return sizeof(double) * tw;
     case 2: return sizeof(double) * vol;
     default: return 0;
@@ -221,6 +222,7 @@ extern "C" int hfb_solve(hfb_plan* p, const double* rhs, double* out, void* work
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
   HFB_CUDA(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (fused_work_elems(p)) return solve_fused(p, rhs, out, (double*)work, st);
   const size_t vol = (size_t)p->nx * p->ny * p->nz;
   double* cpw = (double*)work;
   double* tmp = transform_work_elems(p, p->nz) ? cpw + vol : nullptr;
