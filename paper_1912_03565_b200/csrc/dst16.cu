@@ -196,9 +196,20 @@ __global__ void __launch_bounds__(128, 3) dst16_stream_kernel(StreamArgs a, Fft1
         double* rr = q ? r1 : r0;
         const double* cpr = a.cp + plane * a.in_ps + (long long)row * a.in_ld;
         double* wcr = a.wc + (long long)row * a.in_ld;
-        for (int p = t; p < a.N; p += T) {
-          double w = rr[p + 1];
-          if (!top) w = fma(-__ldg(cpr + p), wcr[p], w);
+        constexpr int NPOS = F16<P>::M - 1;
+        constexpr int J = (NPOS + T - 1) / T;
+        double cv[J], wv[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int p = t + T * j;
+          cv[j] = (!top && p < NPOS) ? __ldg(cpr + p) : 0.0;
+          wv[j] = (!top && p < NPOS) ? wcr[p] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int p = t + T * j;
+          if (p >= NPOS) continue;
+          const double w = fma(-cv[j], wv[j], rr[p + 1]);
           rr[p + 1] = w;
           wcr[p] = w;
         }
@@ -253,17 +264,27 @@ __global__ void __launch_bounds__(128, 3) dst16_stream_kernel(StreamArgs a, Fft1
         double* co_out = a.cp + o;
         const double* xprev = xo - a.out_ps;
         const double* cprev = co_out - a.out_ps;
-        for (int p = t; p < a.N; p += T) {
+        // positions p = t + T j: the carry loads of all j are issued together
+        constexpr int NPOS = F16<P>::M - 1;
+        constexpr int J = (NPOS + T - 1) / T;
+        double xc[J], cc[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int p = t + T * j;
+          xc[j] = (!first && p < NPOS) ? xprev[p] : 0.0;
+          cc[j] = (!first && p < NPOS) ? cprev[p] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int p = t + T * j;
+          if (p >= NPOS) continue;
           const double cyv = __ldg(a.cy + p);
           const double lo = eig(co, cxv, cyv), di = eig(co + 4, cxv, cyv);
-          double den = di, rhs = qq[p];
-          if (!first) {
-            den = fma(-lo, cprev[p], di);
-            rhs = fma(-lo, xprev[p], rhs);
-          }
+          const double den = fma(-lo, cc[j], di);
+          const double rhs = fma(-lo, xc[j], qq[p]);
           if (fabs(den) < a.thr) {
             const unsigned long long key =
-                ((unsigned long long)lvl * (unsigned long long)a.N + (unsigned long long)p) *
+                ((unsigned long long)lvl * (unsigned long long)NPOS + (unsigned long long)p) *
                     (unsigned long long)a.nrow +
                 (unsigned long long)row;
             atomicMin(a.err, key);
@@ -333,6 +354,9 @@ int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {
   a.out_ps = k.out_ps;
   a.N = k.M - 1;
   a.NF = std::max(1, std::min(128 / c.T, kMaxRows / 2));  // <= 128 threads
+  // fused modes: each CTA carries one row group through every plane, so use
+  // the smallest groups (most independent chains)
+  if (k.mode == kYFwd || k.mode == kYBwd) a.NF = std::max(1, std::min(a.NF, 32 / c.T));
   a.G = (a.ppp + a.NF - 1) / a.NF;
   a.logW = 0;
   while ((1 << a.logW) < 2 * a.NF) ++a.logW;
