@@ -256,81 +256,75 @@ size_t transform_work_elems(const hfb_plan* p, int nplanes) {
   return dense_tmp_elems(p, nplanes);
 }
 
-// Fused solve workspace: S / x' (nz x nx x ldt), cp (same), W carry (nx x ldt).
+// Transposed-pipeline solve workspace: S (nz x nx x ldt) and cp (same).
 size_t fused_work_elems(const hfb_plan* p) {
   if (!tran_path(p)) return 0;
-  const size_t pst = (size_t)p->nx * tran_ld(p);
-  return 2 * pst * p->nz + pst;
+  return 2 * (size_t)p->nx * tran_ld(p) * p->nz;
 }
 
-// Four persistent launches:
-//   1. x-DST      F (l, j, i)            -> S (l, n, j)       [TRAN]
-//   2. y-DST + forward Thomas  S (l, n, .) -> x' (l, n, m) in place, cp
-//   3. back substitution + y-DST  x' -> W -> out (l, j, n)    [TRAN]
-//   4. x-DST      out (l, j, .)          -> out (l, j, i)     [ROW, in place]
+// Five launches:
+//   1. x-DST      F (l, j, i)     -> S (l, n, j)        [TRAN]
+//   2. y-DST      S (l, n, .)     -> S (l, n, m)        [ROW, in place]
+//   3. Thomas     per mode (n, m) along l on S, cp workspace
+//   4. y-DST      S (l, n, .)     -> out (l, j, n)      [TRAN]
+//   5. x-DST      out (l, j, .)   -> out (l, j, i)      [ROW, in place]
 int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaStream_t st) {
   const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), pst = ldt * p->nx;
   double* S = work;
   double* CP = S + pst * p->nz;
-  double* WC = CP + pst * p->nz;
-  Dst16Call k = {};
-  k.tw = p->tw_x;
-  k.sn = p->sn_x;
-  k.scale = p->scale_x;
-  k.M = p->nx + 1;
-  k.mode = 1;
-  k.src = rhs;
-  k.src_end = rhs + p->nz * ps;
-  k.dst = S;
-  k.nz = p->nz;
-  k.nrow = p->ny;
-  k.in_ld = p->nx;
-  k.in_ps = ps;
-  k.out_ld = ldt;
-  k.out_ps = pst;
-  int rc = launch_dst16_mode(k, st);
-  if (rc) return rc;
-
-  Dst16Call y = {};
+  Dst16Call x = {};
+  x.tw = p->tw_x;
+  x.sn = p->sn_x;
+  x.scale = p->scale_x;
+  x.M = p->nx + 1;
+  x.nz = p->nz;
+  Dst16Call y = x;
   y.tw = p->tw_y;
   y.sn = p->sn_y;
   y.scale = p->scale_y;
   y.M = p->ny + 1;
-  y.mode = 2;
+  // 1
+  x.mode = 1;
+  x.src = rhs;
+  x.src_end = rhs + p->nz * ps;
+  x.dst = S;
+  x.nrow = p->ny;
+  x.in_ld = p->nx;
+  x.in_ps = ps;
+  x.out_ld = ldt;
+  x.out_ps = pst;
+  int rc = launch_dst16_mode(x, st);
+  if (rc) return rc;
+  // 2
+  y.mode = 0;
   y.src = S;
   y.src_end = S + p->nz * pst;
   y.dst = S;
-  y.nz = p->nz;
   y.nrow = p->nx;
   y.in_ld = ldt;
   y.in_ps = pst;
   y.out_ld = ldt;
   y.out_ps = pst;
-  y.cp = CP;
-  y.wc = WC;
-  y.coef = p->coef;
-  y.cx = p->cx;
-  y.cy = p->cy;
-  y.thr = p->thr;
-  y.err = p->err;
-  y.nz_total = p->nz;
   rc = launch_dst16_mode(y, st);
   if (rc) return rc;
-
-  y.mode = 3;
+  // 3
+  rc = launch_thomas_tran(p, S, CP, ldt, st);
+  if (rc) return rc;
+  // 4
+  y.mode = 1;
   y.dst = out;
   y.out_ld = p->nx;
   y.out_ps = ps;
   rc = launch_dst16_mode(y, st);
   if (rc) return rc;
-
-  k.mode = 0;
-  k.src = out;
-  k.src_end = out + p->nz * ps;
-  k.dst = out;
-  k.out_ld = p->nx;
-  k.out_ps = ps;
-  return launch_dst16_mode(k, st);
+  // 5
+  x.mode = 0;
+  x.src = out;
+  x.src_end = out + p->nz * ps;
+  x.dst = out;
+  x.out_ld = p->nx;
+  x.out_ps = ps;
+  return launch_dst16_mode(x, st);
 }
 
 int transform_planes(hfb_plan* p, const double* src, double* dst, int z0, int z1, double* work,

@@ -1,0 +1,291 @@
+// Register-resident DST-I engine, E = 16 or 32 complex values per thread,
+// transform length M = N+1 = 2^P a compile-time constant (E <= M <= 4096).
+//
+// A transform group = T = M/E threads; thread t holds x[t + T*i], i < E (the
+// "cyclic" distribution). Stockham passes of radix E (and one final smaller
+// radix) run in registers; between passes the values go through a padded
+// shared buffer (one pad slot per 16, so the strided Stockham writes and the
+// cyclic reads are bank-conflict free). The last pass leaves its outputs in
+// the same cyclic slots: an M = 1024 transform with E = 32 is one warp, two
+// radix-32 passes and a single exchange.
+//
+// DST-I pre/post-processing (algebra in hfb_internal.cuh):
+//   pre : b_e = s_e (a_e + a_{M-e}) + (a_e - a_{M-e})/2 (b_0 = 0 and
+//         b_{M/2} = 2 a_{M/2} fall out of the same formula);
+//   post: B goes to shared memory once; thread t then reads its contiguous
+//         k-segment [SEG t, SEG t + SEG) (SEG = E/2) together with the mirror
+//         values B_{M-k}, forms C_k and D_k, scans C over the segment and the
+//         segment totals over the group, and emits the 2 SEG consecutive
+//         outputs S_{2k} (position 2k-1) and S_{2k+1} (position 2k).
+#pragma once
+#include "hfb_internal.cuh"
+
+namespace hfb {
+
+__host__ __device__ __forceinline__ constexpr int pad16(int i) { return i + (i >> 4); }
+__host__ __device__ __forceinline__ constexpr int pad32(int i) { return i + (i >> 5); }
+
+// cos(pi k / 16) for any integer k (exact decimal expansions of the 32nd roots)
+__host__ __device__ __forceinline__ constexpr double c32(int k) {
+  constexpr double tab[9] = {1.0,
+                             0.98078528040323044913,
+                             0.92387953251128675613,
+                             0.83146961230254523708,
+                             0.70710678118654752440,
+                             0.55557023301960222474,
+                             0.38268343236508977173,
+                             0.19509032201612826785,
+                             0.0};
+  const int m = ((k % 32) + 32) % 32;
+  return m <= 8 ? tab[m] : m <= 16 ? -tab[16 - m] : m <= 24 ? -tab[m - 16] : tab[32 - m];
+}
+
+// multiply by w_N^E = exp(-2 pi i E / N) for a compile-time (N, E), N | 32
+template <int N, int E>
+__device__ __forceinline__ double2 mul_wn(double2 a) {
+  constexpr int e = ((E % N) + N) % N;
+  constexpr double r = 0.70710678118654752440;
+  if constexpr (e == 0) {
+    return a;
+  } else if constexpr (4 * e == N) {  // -i
+    return cmul_mi(a);
+  } else if constexpr (2 * e == N) {  // -1
+    return make_double2(-a.x, -a.y);
+  } else if constexpr (4 * e == 3 * N) {  // +i
+    return make_double2(-a.y, a.x);
+  } else if constexpr (8 * e == N) {  // (1 - i)/sqrt2
+    return make_double2(r * (a.x + a.y), r * (a.y - a.x));
+  } else if constexpr (8 * e == 3 * N) {  // (-1 - i)/sqrt2
+    return make_double2(r * (a.y - a.x), -r * (a.x + a.y));
+  } else {
+    constexpr int K = e * (32 / N);  // angle 2 pi e / N = pi K / 16
+    constexpr double wc = c32(K), ws = c32(K - 8);  // cos, sin
+    return make_double2(fma(a.x, wc, a.y * ws), fma(a.y, wc, -a.x * ws));
+  }
+}
+
+// in-place forward DFT of R values (natural order in and out)
+template <int R>
+__device__ __forceinline__ void dftR(double2* v);
+
+template <>
+__device__ __forceinline__ void dftR<2>(double2* v) {
+  dft_fwd<2>(v);
+}
+template <>
+__device__ __forceinline__ void dftR<4>(double2* v) {
+  dft_fwd<4>(v);
+}
+template <>
+__device__ __forceinline__ void dftR<8>(double2* v) {
+  dft_fwd<8>(v);
+}
+
+// R = N1 * N2 split: u = u1 + N1 u2, q = N2 q1 + q2
+template <int N1, int N2>
+__device__ __forceinline__ void dft_split(double2* v) {
+  constexpr int R = N1 * N2;
+  double2 y[R];
+#pragma unroll
+  for (int u1 = 0; u1 < N1; ++u1) {
+    double2 q[N2];
+#pragma unroll
+    for (int u2 = 0; u2 < N2; ++u2) q[u2] = v[u1 + N1 * u2];
+    dftR<N2>(q);
+#pragma unroll
+    for (int q2 = 0; q2 < N2; ++q2) y[u1 * N2 + q2] = q[q2];
+  }
+  // twiddle y[u1][q2] *= w_R^(u1 q2)
+#pragma unroll
+  for (int u1 = 1; u1 < N1; ++u1) {
+#pragma unroll
+    for (int q2 = 1; q2 < N2; ++q2) {
+      // unrolled constant exponent via a switch on the product
+      double2& z = y[u1 * N2 + q2];
+      switch (u1 * q2) {
+#define HFB_TW(EE) \
+  case EE: z = mul_wn<R, EE>(z); break;
+        HFB_TW(1) HFB_TW(2) HFB_TW(3) HFB_TW(4) HFB_TW(5) HFB_TW(6) HFB_TW(7) HFB_TW(8)
+        HFB_TW(9) HFB_TW(10) HFB_TW(12) HFB_TW(14) HFB_TW(15) HFB_TW(18) HFB_TW(21)
+#undef HFB_TW
+        default: break;
+      }
+    }
+  }
+#pragma unroll
+  for (int q2 = 0; q2 < N2; ++q2) {
+    double2 q[N1];
+#pragma unroll
+    for (int u1 = 0; u1 < N1; ++u1) q[u1] = y[u1 * N2 + q2];
+    dftR<N1>(q);
+#pragma unroll
+    for (int q1 = 0; q1 < N1; ++q1) v[N2 * q1 + q2] = q[q1];
+  }
+}
+
+template <>
+__device__ __forceinline__ void dftR<16>(double2* v) {
+  dft_split<4, 4>(v);
+}
+template <>
+__device__ __forceinline__ void dftR<32>(double2* v) {
+  dft_split<4, 8>(v);
+}
+
+template <int T>
+__device__ __forceinline__ void group_sync(int f) {
+  if constexpr (T == 32) {
+    __syncwarp();
+  } else if constexpr (T > 32) {
+    asm volatile("bar.sync %0, %1;" ::"r"(f + 1), "n"(T) : "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
+template <int P, int E>
+struct FE {
+  static constexpr int M = 1 << P;
+  static constexpr int T = M / E;
+  static constexpr int LE = (E == 32) ? 5 : 4;
+  static constexpr int FULL = P / LE;
+  static constexpr int REM = P % LE;
+  static constexpr int BUF = pad16(M) + 1;  // double2 slots of a group buffer
+  static constexpr int SEG = E / 2;
+};
+
+// One radix-R Stockham pass (stride L) on the cyclic registers.
+template <int P, int E, int R, int L>
+__device__ __forceinline__ void pass_regs(double2* v, const double2* __restrict__ tw, int t) {
+  constexpr int M = FE<P, E>::M, T = FE<P, E>::T, NB = E / R, TWSTEP = M / (L * R);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int j = t + T * b;
+    const int k = j & (L - 1);
+    double2 w[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) w[u] = v[b + u * NB];
+    if constexpr (L > 1) {
+#pragma unroll
+      for (int u = 1; u < R; ++u) w[u] = cmul(w[u], __ldg(&tw[u * k * TWSTEP]));
+    }
+    dftR<R>(w);
+#pragma unroll
+    for (int u = 0; u < R; ++u) v[b + u * NB] = w[u];
+  }
+}
+
+// Store a radix-E pass's outputs in Stockham order, then reload cyclic.
+template <int P, int E, int L>
+__device__ __forceinline__ void exchangeE(double2* v, double2* sb, int t, int f) {
+  constexpr int T = FE<P, E>::T;
+  const int k = t & (L - 1);
+  const int base = (t - k) * E + k;
+#pragma unroll
+  for (int u = 0; u < E; ++u) sb[pad16(base + u * L)] = v[u];
+  group_sync<T>(f);
+#pragma unroll
+  for (int i = 0; i < E; ++i) v[i] = sb[pad16(t + T * i)];
+  group_sync<T>(f);
+}
+
+template <int P, int E>
+__device__ __forceinline__ void fftE_forward(double2* v, double2* sb,
+                                             const double2* __restrict__ tw, int t, int f) {
+  using G = FE<P, E>;
+  pass_regs<P, E, E, 1>(v, tw, t);
+  if constexpr (G::FULL >= 2) {
+    exchangeE<P, E, 1>(v, sb, t, f);
+    pass_regs<P, E, E, E>(v, tw, t);
+  }
+  if constexpr (G::FULL >= 3) {
+    exchangeE<P, E, E>(v, sb, t, f);
+    pass_regs<P, E, E, E * E>(v, tw, t);
+  }
+  if constexpr (G::REM > 0) {
+    constexpr int L = 1 << (G::LE * G::FULL);
+    exchangeE<P, E, L / E>(v, sb, t, f);
+    pass_regs<P, E, (1 << G::REM), L>(v, tw, t);
+  }
+}
+
+// Exclusive scan over the T threads of a group (T-aligned runs of threadIdx).
+template <int T>
+__device__ __forceinline__ double2 group_scanE(double2 v, int t, int f, double2* wsum) {
+  constexpr int W = T < 32 ? T : 32;
+  const int lane = threadIdx.x & 31;
+  double2 inc = v;
+#pragma unroll
+  for (int o = 1; o < W; o <<= 1) {
+    const double tx = __shfl_up_sync(0xffffffffu, inc.x, o, W);
+    const double ty = __shfl_up_sync(0xffffffffu, inc.y, o, W);
+    if ((lane & (W - 1)) >= o) {
+      inc.x += tx;
+      inc.y += ty;
+    }
+  }
+  double2 ex = csub(inc, v);
+  if constexpr (T > 32) {
+    const int warp = threadIdx.x >> 5;
+    if (lane == 31) wsum[warp] = inc;
+    group_sync<T>(f);
+    const int w0 = (threadIdx.x - t) >> 5;
+#pragma unroll
+    for (int w = 0; w < T / 32 - 1; ++w)
+      if (w0 + w < warp) ex = cadd(ex, wsum[w0 + w]);
+  }
+  return ex;
+}
+
+// DST post-processing: v = B (cyclic) -> the 2*SEG outputs of thread t, i.e.
+// positions 2k-1 and 2k for k in [SEG t, SEG t + SEG), scaled by sqrt(2/M):
+// out[2s] = S_{2k} (position 2k-1; meaningless for k = 0), out[2s+1] =
+// S_{2k+1} (position 2k), k = SEG t + s. sb is left free for the caller.
+template <int P, int E>
+__device__ __forceinline__ void dstE_post(const double2* v, double2* sb, double2* wsum,
+                                          double scale, int t, int f, double2* out) {
+  constexpr int M = FE<P, E>::M, T = FE<P, E>::T, SEG = FE<P, E>::SEG;
+#pragma unroll
+  for (int i = 0; i < E; ++i) sb[pad16(t + T * i)] = v[i];
+  group_sync<T>(f);
+  const int k0 = SEG * t;
+  double2 run = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s = 0; s < SEG; ++s) {
+    const int k = k0 + s;
+    const double2 bk = sb[pad16(k)];
+    const double2 bm = sb[pad16((M - k) & (M - 1))];
+    double2 C = make_double2(0.5 * (bk.x + bm.x), 0.5 * (bk.y + bm.y));
+    if (k == 0) C = cscale(C, 0.5);
+    run = cadd(run, C);
+    out[2 * s] = make_double2(-0.5 * scale * (bk.y - bm.y), 0.5 * scale * (bk.x - bm.x));
+    out[2 * s + 1] = run;  // inclusive prefix within the segment (unscaled)
+  }
+  const double2 off = group_scanE<T>(run, t, f, wsum);
+#pragma unroll
+  for (int s = 0; s < SEG; ++s) out[2 * s + 1] = cscale(cadd(out[2 * s + 1], off), scale);
+  group_sync<T>(f);  // every B read is done: sb may be reused
+}
+
+// Pre-processing: v[i] = b_{t + T i} from a loader of a_e (e in [1, M-1]); the
+// loader may return garbage for e = 0 and e = M (selected away here).
+template <int P, int E, class Load>
+__device__ __forceinline__ void dstE_pre(double2* v, const double* __restrict__ sn, int t,
+                                         Load&& load) {
+  constexpr int M = FE<P, E>::M, T = FE<P, E>::T, H = M / 2;
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int e = t + T * i;
+    double2 p = load(e), q = load(M - e);
+    if (i == 0) {
+      const bool z = (t == 0);
+      p = z ? make_double2(0.0, 0.0) : p;
+      q = z ? make_double2(0.0, 0.0) : q;
+    }
+    const double s = __ldg(&sn[e <= H ? e : M - e]);
+    const double sx = (p.x + q.x) * s, sy = (p.y + q.y) * s;
+    v[i] = make_double2(fma(0.5, p.x - q.x, sx), fma(0.5, p.y - q.y, sy));
+  }
+}
+
+}  // namespace hfb

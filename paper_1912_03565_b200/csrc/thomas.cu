@@ -37,8 +37,9 @@ __device__ __forceinline__ void latch(unsigned long long* err, long long l, long
 }
 
 struct ThomasArgs {
-  int nz, mloc, nx, ny_total, m_off;
-  long long plane;  // mloc * nx
+  int nz, nrows, ncols, nx, ny_total, m_off, swap;
+  long long ld, ps;   // row stride and plane stride of the data
+  long long nmodes;   // nrows * ncols
   const double* coef;
   const double* cx;
   const double* cy;
@@ -46,64 +47,87 @@ struct ThomasArgs {
   unsigned long long* err;
 };
 
+// Thread per mode. Natural layout (swap = 0): rows are y-modes m_off + r,
+// columns x-modes n. Transposed layout (swap = 1, the (l, n, m) order of the
+// two-pass transform): rows are x-modes n, columns y-modes m.
 __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w,
                                                            double* __restrict__ cpw,
                                                            ThomasArgs a) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= a.plane) return;
-  const int ml = (int)(t / a.nx), n = (int)(t - (long long)ml * a.nx);
+  if (t >= a.nmodes) return;
+  const int r = (int)(t / a.ncols), col = (int)(t - (long long)r * a.ncols);
+  const int n = a.swap ? r : col;
+  const int m = a.swap ? col : a.m_off + r;
   const double cxv = __ldg(&a.cx[n]);
-  const double cyv = __ldg(&a.cy[a.m_off + ml]);
+  const double cyv = __ldg(&a.cy[m]);
   const double cxy = cxv * cyv;
-  const long long P = a.plane;
-  // row 0
+  const long long P = a.ps;
+  const long long t0 = (long long)r * a.ld + col;
   double den = eig(a.coef + 4, cxv, cyv, cxy);
-  if (fabs(den) < a.thr) latch(a.err, 0, a.m_off + ml, n, a.ny_total, a.nx);
-  double r = rcp(den);
-  double c = eig(a.coef + 8, cxv, cyv, cxy) * r;
-  double x = w[t] * r;
-  w[t] = x;
-  cpw[t] = c;
+  if (fabs(den) < a.thr) latch(a.err, 0, m, n, a.ny_total, a.nx);
+  double rr = rcp(den);
+  double c = eig(a.coef + 8, cxv, cyv, cxy) * rr;
+  double x = w[t0] * rr;
+  w[t0] = x;
+  cpw[t0] = c;
+#pragma unroll 4
   for (int l = 1; l < a.nz; ++l) {
     const double* co = a.coef + (long long)l * 12;
+    const long long o = (long long)l * P + t0;
+    const double wl = w[o];
     const double lo = eig(co, cxv, cyv, cxy);
     den = fma(-lo, c, eig(co + 4, cxv, cyv, cxy));
-    if (fabs(den) < a.thr) latch(a.err, l, a.m_off + ml, n, a.ny_total, a.nx);
-    r = rcp(den);
-    const long long o = (long long)l * P + t;
-    x = fma(-lo, x, w[o]) * r;
+    if (fabs(den) < a.thr) latch(a.err, l, m, n, a.ny_total, a.nx);
+    rr = rcp(den);
+    x = fma(-lo, x, wl) * rr;
     w[o] = x;
     if (l < a.nz - 1) {
-      c = eig(co + 8, cxv, cyv, cxy) * r;
+      c = eig(co + 8, cxv, cyv, cxy) * rr;
       cpw[o] = c;
     }
   }
   // back substitution; x holds W[nz-1]
+#pragma unroll 4
   for (int l = a.nz - 2; l >= 0; --l) {
-    const long long o = (long long)l * P + t;
+    const long long o = (long long)l * P + t0;
     x = fma(-cpw[o], x, w[o]);
     w[o] = x;
   }
 }
 
-int launch_thomas(hfb_plan* p, double* slab, int mloc, int m_off, double* cpw, cudaStream_t st) {
-  if (mloc <= 0) return HFB_OK;
+static int launch_thomas_layout(hfb_plan* p, double* data, double* cpw, int nrows, int ncols,
+                                long long ld, long long ps, int m_off, int swap,
+                                cudaStream_t st) {
+  if (nrows <= 0 || ncols <= 0) return HFB_OK;
   ThomasArgs a;
   a.nz = p->nz;
-  a.mloc = mloc;
+  a.nrows = nrows;
+  a.ncols = ncols;
   a.nx = p->nx;
   a.ny_total = p->ny;
   a.m_off = m_off;
-  a.plane = (long long)mloc * p->nx;
+  a.swap = swap;
+  a.ld = ld;
+  a.ps = ps;
+  a.nmodes = (long long)nrows * ncols;
   a.coef = p->coef;
   a.cx = p->cx;
   a.cy = p->cy;
   a.thr = p->thr;
   a.err = p->err;
-  const long long blocks = (a.plane + 255) / 256;
-  thomas_slab_kernel<<<(unsigned)blocks, 256, 0, st>>>(slab, cpw, a);
+  const long long blocks = (a.nmodes + 255) / 256;
+  thomas_slab_kernel<<<(unsigned)blocks, 256, 0, st>>>(data, cpw, a);
   HFB_LAUNCHED();
   return HFB_OK;
+}
+
+int launch_thomas(hfb_plan* p, double* slab, int mloc, int m_off, double* cpw, cudaStream_t st) {
+  return launch_thomas_layout(p, slab, cpw, mloc, p->nx, p->nx, (long long)mloc * p->nx, m_off,
+                              0, st);
+}
+
+int launch_thomas_tran(hfb_plan* p, double* data, double* cpw, long long ld, cudaStream_t st) {
+  return launch_thomas_layout(p, data, cpw, p->nx, p->ny, ld, ld * p->nx, 0, 1, st);
 }
 
 }  // namespace hfb
