@@ -63,6 +63,10 @@ const char* hfb_strerror(int code);
 /* Number of kernels this library has launched in the process (all plans). */
 uint64_t hfb_launch_count(void);
 
+/* Performance knobs (no effect on results): key 0 = DST engine width
+ * (16 or 32 values per thread), key 1 = transform groups per CTA (0 = auto). */
+void hfb_set_tuning(int key, int value);
+
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.
  * Replaces spectral.make_plan (spectral.py:46-51) and carries the per-row
  * coefficient table that tridiag.solve_slab builds on every call

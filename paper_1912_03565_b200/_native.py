@@ -45,6 +45,7 @@ SIGNATURES = {
     "hfb_version": (ctypes.c_char_p, []),
     "hfb_strerror": (ctypes.c_char_p, [_i]),
     "hfb_launch_count": (ctypes.c_uint64, []),
+    "hfb_set_tuning": (None, [_i, _i]),
     "hfb_plan_create": (_i, [_i, _i, _i, _i, ctypes.POINTER(_vp)]),
     "hfb_plan_destroy": (_i, [_vp]),
     "hfb_plan_set_coefficients": (_i, [_vp, _vp, _vp, _vp, _d]),

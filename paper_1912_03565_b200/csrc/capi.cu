@@ -18,6 +18,8 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 extern "C" uint64_t hfb_launch_count(void) { return hfb::g_launches.load(); }
 
+extern "C" void hfb_set_tuning(int key, int value) { hfb::set_tuning(key, value); }
+
 using namespace hfb;
 
 static int ilog2_exact(int m) {

@@ -211,11 +211,15 @@ static int launch_stream(const StreamArgs& a, const FftArgs& c, int threads, siz
   return HFB_OK;
 }
 
-template <int P>
-static int launch_p(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStream_t st) {
-  constexpr int E = (P >= 5) ? 32 : 16;
+// tuning knobs (hfb_set_tuning): engine width E for M >= 32 and groups per CTA
+static int g_tune_E = 16;
+static int g_tune_NF = 0;
+
+template <int P, int E>
+static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStream_t st) {
   constexpr int T = FE<P, E>::T;
   a.NF = std::max(1, std::min(128 / T, kMaxRows / 2));  // <= 128 threads per CTA
+  if (g_tune_NF > 0) a.NF = std::max(1, std::min(g_tune_NF, std::min(128 / T, kMaxRows / 2)));
   a.G = (a.ppp + a.NF - 1) / a.NF;
   a.logW = 0;
   while ((1 << a.logW) < 2 * a.NF) ++a.logW;
@@ -229,6 +233,19 @@ static int launch_p(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStre
                     (threads / 32 + 1) * sizeof(double2) + 2 * sizeof(uint64_t);
   if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, threads, sm, st);
   return launch_stream<P, E, kRow>(a, c, threads, sm, st);
+}
+
+template <int P>
+static int launch_p(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStream_t st) {
+  if constexpr (P >= 5) {
+    if (g_tune_E == 32) return launch_pe<P, 32>(k, a, c, st);
+  }
+  return launch_pe<P, 16>(k, a, c, st);
+}
+
+void set_tuning(int key, int value) {
+  if (key == 0) g_tune_E = (value == 32) ? 32 : 16;
+  if (key == 1) g_tune_NF = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

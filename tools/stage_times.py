@@ -49,3 +49,20 @@ for name, fn in stages.items():
     ms = e0.elapsed_time(e1) / a.reps
     print(f"{name:22s} {ms:9.3f} ms  {pts / ms / 1e6:10.3e} pts/s  "
           f"{16 * pts / ms / 1e6:8.1f} GB/s at 16 B/pt")
+
+if os.environ.get("HFB_SWEEP"):
+    for E in (16, 32):
+        for NF in (0, 1, 2, 4):
+            lib.hfb_set_tuning(0, E)
+            lib.hfb_set_tuning(1, NF)
+            for name in ("dst_x (all rows)", "stack (x^T + y^T)"):
+                fn = stages[name]
+                fn()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(a.reps):
+                    fn()
+                e1.record()
+                torch.cuda.synchronize()
+                print(f"E={E} NF={NF} {name:20s} {e0.elapsed_time(e1) / a.reps:8.3f} ms")
