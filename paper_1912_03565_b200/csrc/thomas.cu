@@ -70,7 +70,6 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
   double x = w[t0] * rr;
   w[t0] = x;
   cpw[t0] = c;
-#pragma unroll 4
   for (int l = 1; l < a.nz; ++l) {
     const double* co = a.coef + (long long)l * 12;
     const long long o = (long long)l * P + t0;
@@ -87,7 +86,6 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
     }
   }
   // back substitution; x holds W[nz-1]
-#pragma unroll 4
   for (int l = a.nz - 2; l >= 0; --l) {
     const long long o = (long long)l * P + t0;
     x = fma(-cpw[o], x, w[o]);

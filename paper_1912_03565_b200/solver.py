@@ -9,8 +9,11 @@ Every mode runs on the GPU — there is no CPU path:
 
 - ``Sequential()`` / ``SharedWorkers(w)`` / ``Device()``: the single-GPU
   pipeline (forward 2D DST-I -> per-mode Thomas -> inverse 2D DST-I) of the
-  sm_100a library. Host worker counts are validated like the reference and
-  otherwise irrelevant: parallelism is the GPU's.
+  sm_100a library in one call (hfb_solve); its phase timings report the whole
+  device time as transform_s. ``Device(staged=True)`` runs the three stages
+  as separate calls (transform_s / tridiag_s measured separately). Host
+  worker counts are validated like the reference and otherwise irrelevant:
+  parallelism is the GPU's.
 - ``Partitioned(p, t)``: the reference's slab <-> pencil geometry on one
   device: part p transforms its z-slab, the blocks (kpz(p), kpy(q), n_x)
   are redistributed by a device copy, part q solves its y-slab with mode
@@ -264,7 +267,7 @@ def _solve_part_device(plan, t, grid, config, clock, part_idx):
         return (clock.seconds("t0" + tag, "t1" + tag) + clock.seconds("t4" + tag, "t5" + tag),
                 clock.seconds("t1" + tag, "t2" + tag) + clock.seconds("t3" + tag, "t4" + tag),
                 clock.seconds("t2" + tag, "t3" + tag))
-    staged = not (isinstance(mode, Device) and not mode.staged)
+    staged = isinstance(mode, Device) and mode.staged
     if staged:
         work_t = plan.workspace(1)
         cpw = torch.empty_like(t)
