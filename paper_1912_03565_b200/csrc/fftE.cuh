@@ -154,6 +154,34 @@ struct FE {
   static constexpr int SEG = E / 2;
 };
 
+// Twiddles w^u, u = 1..R-1, of w = tw[k*S] (w^u = tw[u*k*S]) from at most two
+// table loads: w^2, w^3 by products, and for R = 16 the fourth powers loaded
+// directly so every factor is at most three roundings from the table.
+template <int R>
+__device__ __forceinline__ void twiddle_powers(const double2* __restrict__ tw, int ks,
+                                               double2* wp) {
+  wp[1] = __ldg(&tw[ks]);
+  if constexpr (R >= 4) {
+    wp[2] = cmul(wp[1], wp[1]);
+    wp[3] = cmul(wp[2], wp[1]);
+  }
+  if constexpr (R == 8) {
+    wp[4] = cmul(wp[2], wp[2]);
+    wp[5] = cmul(wp[4], wp[1]);
+    wp[6] = cmul(wp[4], wp[2]);
+    wp[7] = cmul(wp[4], wp[3]);
+  }
+  if constexpr (R == 16) {
+    wp[4] = __ldg(&tw[4 * ks]);
+    wp[8] = cmul(wp[4], wp[4]);
+    wp[12] = cmul(wp[8], wp[4]);
+#pragma unroll
+    for (int a4 = 4; a4 < 16; a4 += 4)
+#pragma unroll
+      for (int b = 1; b < 4; ++b) wp[a4 + b] = cmul(wp[a4], wp[b]);
+  }
+}
+
 // One radix-R Stockham pass (stride L) on the cyclic registers.
 template <int P, int E, int R, int L>
 __device__ __forceinline__ void pass_regs(double2* v, const double2* __restrict__ tw, int t) {
@@ -166,8 +194,10 @@ __device__ __forceinline__ void pass_regs(double2* v, const double2* __restrict_
 #pragma unroll
     for (int u = 0; u < R; ++u) w[u] = v[b + u * NB];
     if constexpr (L > 1) {
+      double2 wp[R];
+      twiddle_powers<R>(tw, k * TWSTEP, wp);
 #pragma unroll
-      for (int u = 1; u < R; ++u) w[u] = cmul(w[u], __ldg(&tw[u * k * TWSTEP]));
+      for (int u = 1; u < R; ++u) w[u] = cmul(w[u], wp[u]);
     }
     dftR<R>(w);
 #pragma unroll
@@ -273,6 +303,8 @@ template <int P, int E, class Load>
 __device__ __forceinline__ void dstE_pre(double2* v, const double* __restrict__ sn, int t,
                                          Load&& load) {
   constexpr int M = FE<P, E>::M, T = FE<P, E>::T, H = M / 2;
+  // E = 16: sin(pi (t + T i)/M) = sin(pi t/M) cos(pi i/16) + cos(pi t/M) sin(pi i/16)
+  const double st = __ldg(&sn[t]), ct = __ldg(&sn[H - t]);
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const int e = t + T * i;
@@ -282,7 +314,12 @@ __device__ __forceinline__ void dstE_pre(double2* v, const double* __restrict__ 
       p = z ? make_double2(0.0, 0.0) : p;
       q = z ? make_double2(0.0, 0.0) : q;
     }
-    const double s = __ldg(&sn[e <= H ? e : M - e]);
+    double s;
+    if constexpr (E == 16) {
+      s = fma(st, c32(i), ct * c32(i - 8));
+    } else {
+      s = __ldg(&sn[e <= H ? e : M - e]);
+    }
     const double sx = (p.x + q.x) * s, sy = (p.y + q.y) * s;
     v[i] = make_double2(fma(0.5, p.x - q.x, sx), fma(0.5, p.y - q.y, sy));
   }
