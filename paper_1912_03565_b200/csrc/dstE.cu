@@ -179,27 +179,13 @@ __global__ void __launch_bounds__(128, 3) dstE_stream_kernel(StreamArgs a, FftAr
     } else {
       __syncthreads();
       const int W = 2 * a.NF;
-      if ((blockDim.x & (W - 1)) == 0) {
-        // each thread keeps one row: lanes cover W rows x (32/W) positions
-        const int r = threadIdx.x & (W - 1);
+      const int total = a.N * W;
+      for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        const int pos = e >> a.logW, r = e & (W - 1);
         const int row = meta.row[s][r];
-        if (row >= 0) {
-          const double* src = gbuf(s, r >> 1) + (r & 1) * a.stage_ld;
-          const int pstep = blockDim.x >> a.logW;
-          int pos = threadIdx.x >> a.logW;
-          double* d = a.dst + plane * a.out_ps + row + (long long)pos * a.out_ld;
-          const long long dstep = (long long)pstep * a.out_ld;
-          for (; pos < a.N; pos += pstep, d += dstep) *d = src[pad32(pos + 1)];
-        }
-      } else {
-        const int total = a.N * W;
-        for (int e = threadIdx.x; e < total; e += blockDim.x) {
-          const int pos = e >> a.logW, r = e & (W - 1);
-          const int row = meta.row[s][r];
-          if (row < 0) continue;
-          a.dst[plane * a.out_ps + (long long)pos * a.out_ld + row] =
-              gbuf(s, r >> 1)[(r & 1) * a.stage_ld + pad32(pos + 1)];
-        }
+        if (row < 0) continue;
+        a.dst[plane * a.out_ps + (long long)pos * a.out_ld + row] =
+            gbuf(s, r >> 1)[(r & 1) * a.stage_ld + pad32(pos + 1)];
       }
     }
     __syncthreads();  // stage s is free for the prefetch issued next iteration
