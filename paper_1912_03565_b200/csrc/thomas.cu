@@ -50,6 +50,8 @@ struct ThomasArgs {
 // Thread per mode. Natural layout (swap = 0): rows are y-modes m_off + r,
 // columns x-modes n. Transposed layout (swap = 1, the (l, n, m) order of the
 // two-pass transform): rows are x-modes n, columns y-modes m.
+constexpr int KCP = 8;  // cp checkpoint interval (levels)
+
 __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w,
                                                            double* __restrict__ cpw,
                                                            ThomasArgs a) {
@@ -63,13 +65,16 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
   const double cxy = cxv * cyv;
   const long long P = a.ps;
   const long long t0 = (long long)r * a.ld + col;
+  // Forward elimination. cp depends on the matrix only, so it is stored just
+  // at the last level of every block of KCP levels (cpw slot = l / KCP) and
+  // recomputed, bit for bit, block by block during the back substitution.
   double den = eig(a.coef + 4, cxv, cyv, cxy);
   if (fabs(den) < a.thr) latch(a.err, 0, m, n, a.ny_total, a.nx);
   double rr = rcp(den);
   double c = eig(a.coef + 8, cxv, cyv, cxy) * rr;
   double x = w[t0] * rr;
   w[t0] = x;
-  cpw[t0] = c;
+  if (KCP == 1 && a.nz > 1) cpw[t0] = c;
   for (int l = 1; l < a.nz; ++l) {
     const double* co = a.coef + (long long)l * 12;
     const long long o = (long long)l * P + t0;
@@ -82,14 +87,35 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
     w[o] = x;
     if (l < a.nz - 1) {
       c = eig(co + 8, cxv, cyv, cxy) * rr;
-      cpw[o] = c;
+      if ((l % KCP) == KCP - 1) cpw[(long long)(l / KCP) * P + t0] = c;
     }
   }
-  // back substitution; x holds W[nz-1]
-  for (int l = a.nz - 2; l >= 0; --l) {
-    const long long o = (long long)l * P + t0;
-    x = fma(-cpw[o], x, w[o]);
-    w[o] = x;
+  // back substitution over blocks [b*KCP, b*KCP + KCP), descending; x = W[nz-1]
+  for (int b = (a.nz - 2) / KCP; b >= 0; --b) {
+    const int l0 = b * KCP;
+    double cb[KCP];
+    double cprev = (b > 0) ? cpw[(long long)(b - 1) * P + t0] : 0.0;
+#pragma unroll
+    for (int i = 0; i < KCP; ++i) {
+      const int l = l0 + i;
+      if (l < a.nz - 1) {
+        const double* co = a.coef + (long long)l * 12;
+        const double dl = (l == 0) ? eig(co + 4, cxv, cyv, cxy)
+                                   : fma(-eig(co, cxv, cyv, cxy), cprev,
+                                         eig(co + 4, cxv, cyv, cxy));
+        cprev = eig(co + 8, cxv, cyv, cxy) * rcp(dl);
+        cb[i] = cprev;
+      }
+    }
+#pragma unroll
+    for (int i = KCP - 1; i >= 0; --i) {
+      const int l = l0 + i;
+      if (l < a.nz - 1) {
+        const long long o = (long long)l * P + t0;
+        x = fma(-cb[i], x, w[o]);
+        w[o] = x;
+      }
+    }
   }
 }
 
