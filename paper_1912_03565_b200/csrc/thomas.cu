@@ -75,10 +75,18 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
   double x = w[t0] * rr;
   w[t0] = x;
   if (KCP == 1 && a.nz > 1) cpw[t0] = c;
+  // the right-hand sides do not depend on the recurrence: keep KCP loads in
+  // flight (a register ring refilled KCP levels ahead)
+  double ring[KCP];
+#pragma unroll
+  for (int i = 0; i < KCP; ++i) ring[i] = (1 + i < a.nz) ? w[(long long)(1 + i) * P + t0] : 0.0;
   for (int l = 1; l < a.nz; ++l) {
     const double* co = a.coef + (long long)l * 12;
     const long long o = (long long)l * P + t0;
-    const double wl = w[o];
+    const double wl = ring[0];
+#pragma unroll
+    for (int i = 0; i < KCP - 1; ++i) ring[i] = ring[i + 1];
+    ring[KCP - 1] = (l + KCP < a.nz) ? w[(long long)(l + KCP) * P + t0] : 0.0;
     const double lo = eig(co, cxv, cyv, cxy);
     den = fma(-lo, c, eig(co + 4, cxv, cyv, cxy));
     if (fabs(den) < a.thr) latch(a.err, l, m, n, a.ny_total, a.nx);
@@ -91,10 +99,27 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
     }
   }
   // back substitution over blocks [b*KCP, b*KCP + KCP), descending; x = W[nz-1]
-  for (int b = (a.nz - 2) / KCP; b >= 0; --b) {
+  const int bmax = (a.nz - 2) / KCP;
+  double wb[KCP], cnext = 0.0;
+  if (bmax >= 0) {
+#pragma unroll
+    for (int i = 0; i < KCP; ++i) {
+      const int l = bmax * KCP + i;
+      wb[i] = (l < a.nz - 1) ? w[(long long)l * P + t0] : 0.0;
+    }
+    cnext = (bmax > 0) ? cpw[(long long)(bmax - 1) * P + t0] : 0.0;
+  }
+  for (int b = bmax; b >= 0; --b) {
     const int l0 = b * KCP;
-    double cb[KCP];
-    double cprev = (b > 0) ? cpw[(long long)(b - 1) * P + t0] : 0.0;
+    double cb[KCP], wcur[KCP];
+    double cprev = cnext;
+#pragma unroll
+    for (int i = 0; i < KCP; ++i) wcur[i] = wb[i];
+    if (b > 0) {  // prefetch the next (lower) block while this one is recomputed
+#pragma unroll
+      for (int i = 0; i < KCP; ++i) wb[i] = w[(long long)(l0 - KCP + i) * P + t0];
+      cnext = (b > 1) ? cpw[(long long)(b - 2) * P + t0] : 0.0;
+    }
 #pragma unroll
     for (int i = 0; i < KCP; ++i) {
       const int l = l0 + i;
@@ -111,9 +136,8 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
     for (int i = KCP - 1; i >= 0; --i) {
       const int l = l0 + i;
       if (l < a.nz - 1) {
-        const long long o = (long long)l * P + t0;
-        x = fma(-cb[i], x, w[o]);
-        w[o] = x;
+        x = fma(-cb[i], x, wcur[i]);
+        w[(long long)l * P + t0] = x;
       }
     }
   }
