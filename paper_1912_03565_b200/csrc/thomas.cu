@@ -80,21 +80,34 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
   double ring[KCP];
 #pragma unroll
   for (int i = 0; i < KCP; ++i) ring[i] = (1 + i < a.nz) ? w[(long long)(1 + i) * P + t0] : 0.0;
+  // the eigenvalues of level l + 1 are generated while level l is eliminated
+  // (they do not depend on the recurrence either)
+  double lo_n = 0.0, di_n = 0.0, up_n = 0.0;
+  if (a.nz > 1) {
+    lo_n = eig(a.coef + 12, cxv, cyv, cxy);
+    di_n = eig(a.coef + 16, cxv, cyv, cxy);
+    up_n = eig(a.coef + 20, cxv, cyv, cxy);
+  }
   for (int l = 1; l < a.nz; ++l) {
-    const double* co = a.coef + (long long)l * 12;
     const long long o = (long long)l * P + t0;
     const double wl = ring[0];
 #pragma unroll
     for (int i = 0; i < KCP - 1; ++i) ring[i] = ring[i + 1];
     ring[KCP - 1] = (l + KCP < a.nz) ? w[(long long)(l + KCP) * P + t0] : 0.0;
-    const double lo = eig(co, cxv, cyv, cxy);
-    den = fma(-lo, c, eig(co + 4, cxv, cyv, cxy));
+    const double lo = lo_n, di = di_n, up = up_n;
+    if (l + 1 < a.nz) {
+      const double* cn = a.coef + (long long)(l + 1) * 12;
+      lo_n = eig(cn, cxv, cyv, cxy);
+      di_n = eig(cn + 4, cxv, cyv, cxy);
+      up_n = eig(cn + 8, cxv, cyv, cxy);
+    }
+    den = fma(-lo, c, di);
     if (fabs(den) < a.thr) latch(a.err, l, m, n, a.ny_total, a.nx);
     rr = rcp(den);
     x = fma(-lo, x, wl) * rr;
     w[o] = x;
     if (l < a.nz - 1) {
-      c = eig(co + 8, cxv, cyv, cxy) * rr;
+      c = up * rr;
       if ((l % KCP) == KCP - 1) cpw[(long long)(l / KCP) * P + t0] = c;
     }
   }
