@@ -72,14 +72,17 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
   if (fabs(den) < a.thr) latch(a.err, 0, m, n, a.ny_total, a.nx);
   double rr = rcp(den);
   double c = eig(a.coef + 8, cxv, cyv, cxy) * rr;
-  double x = w[t0] * rr;
-  w[t0] = x;
+  // streamed data is evict-first (__ldcs/__stcs) so the per-level weights stay
+  // in L1 for every mode of the CTA
+  double x = __ldcs(w + t0) * rr;
+  __stcs(w + t0, x);
   if (KCP == 1 && a.nz > 1) cpw[t0] = c;
   // the right-hand sides do not depend on the recurrence: keep KCP loads in
   // flight (a register ring refilled KCP levels ahead)
   double ring[KCP];
 #pragma unroll
-  for (int i = 0; i < KCP; ++i) ring[i] = (1 + i < a.nz) ? w[(long long)(1 + i) * P + t0] : 0.0;
+  for (int i = 0; i < KCP; ++i)
+    ring[i] = (1 + i < a.nz) ? __ldcs(w + (long long)(1 + i) * P + t0) : 0.0;
   // the eigenvalues of level l + 1 are generated while level l is eliminated
   // (they do not depend on the recurrence either)
   double lo_n = 0.0, di_n = 0.0, up_n = 0.0;
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
     const double wl = ring[0];
 #pragma unroll
     for (int i = 0; i < KCP - 1; ++i) ring[i] = ring[i + 1];
-    ring[KCP - 1] = (l + KCP < a.nz) ? w[(long long)(l + KCP) * P + t0] : 0.0;
+    ring[KCP - 1] = (l + KCP < a.nz) ? __ldcs(w + (long long)(l + KCP) * P + t0) : 0.0;
     const double lo = lo_n, di = di_n, up = up_n;
     if (l + 1 < a.nz) {
       const double* cn = a.coef + (long long)(l + 1) * 12;
@@ -105,7 +108,7 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
     if (fabs(den) < a.thr) latch(a.err, l, m, n, a.ny_total, a.nx);
     rr = rcp(den);
     x = fma(-lo, x, wl) * rr;
-    w[o] = x;
+    __stcs(w + o, x);
     if (l < a.nz - 1) {
       c = up * rr;
       if ((l % KCP) == KCP - 1) cpw[(long long)(l / KCP) * P + t0] = c;
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
 #pragma unroll
     for (int i = 0; i < KCP; ++i) {
       const int l = bmax * KCP + i;
-      wb[i] = (l < a.nz - 1) ? w[(long long)l * P + t0] : 0.0;
+      wb[i] = (l < a.nz - 1) ? __ldcs(w + (long long)l * P + t0) : 0.0;
     }
     cnext = (bmax > 0) ? cpw[(long long)(bmax - 1) * P + t0] : 0.0;
   }
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
     for (int i = 0; i < KCP; ++i) wcur[i] = wb[i];
     if (b > 0) {  // prefetch the next (lower) block while this one is recomputed
 #pragma unroll
-      for (int i = 0; i < KCP; ++i) wb[i] = w[(long long)(l0 - KCP + i) * P + t0];
+      for (int i = 0; i < KCP; ++i) wb[i] = __ldcs(w + (long long)(l0 - KCP + i) * P + t0);
       cnext = (b > 1) ? cpw[(long long)(b - 2) * P + t0] : 0.0;
     }
 #pragma unroll
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(256) thomas_slab_kernel(double* __restrict__ w
       const int l = l0 + i;
       if (l < a.nz - 1) {
         x = fma(-cb[i], x, wcur[i]);
-        w[(long long)l * P + t0] = x;
+        __stcs(w + (long long)l * P + t0, x);
       }
     }
   }
