@@ -308,7 +308,7 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
   rc = launch_dst16_mode(y, st);
   if (rc) return rc;
   // 3
-  rc = launch_thomas_tran(p, S, CP, ldt, st);
+  rc = launch_thomas_tma(p, S, CP, ldt, st);
   if (rc) return rc;
   // 4
   y.mode = 1;

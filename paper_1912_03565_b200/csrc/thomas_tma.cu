@@ -1,0 +1,204 @@
+// Streaming Thomas sweep for the transposed, padded (l, n, m) layout of the
+// one-call solve: kernel (c) fed by the TMA engine.
+//
+// A CTA owns a contiguous block of BM = 256 modes (one row segment: fixed x-mode
+// n, y-modes m0..m0+255) and walks the levels in chunks of K = 8. Every chunk's
+// 8 rows (and the chunk's 8 x 12 stencil weights) arrive by 1D bulk copies into
+// a 3-stage shared-memory ring, two chunks ahead of the compute; results leave
+// by 1D bulk stores. The memory-level parallelism therefore comes from the
+// copy engine (~32 KB in flight per CTA), not from thread occupancy, which is
+// what the plain thread-per-mode sweep lacks (its per-level loads sit inside
+// the recurrence's latency chain).
+//
+// Arithmetic is the same as thomas.cu (bitwise): cp is kept only at the last
+// level of each chunk (cpk, one plane per chunk) and recomputed per chunk in
+// the back substitution, 34 B/point of HBM traffic instead of 48.
+#include "hfb_internal.cuh"
+#include "tma.cuh"
+
+namespace hfb {
+
+namespace {
+constexpr int BM = 256;  // modes per CTA block = threads
+constexpr int K = 8;     // levels per chunk
+constexpr int S = 3;     // ring stages
+
+struct TmaArgs {
+  double* w;           // data (l, n, m): x' / W in place
+  double* cpk;         // checkpoints: plane q holds cp at level q*K + K - 1
+  const double* coef;  // [l][k][(4a, 2b, 2c, d)]
+  const double* cx;
+  const double* cy;
+  int nz, nrows, ncols, nbpr;  // levels, rows (n), cols (m), blocks per row
+  long long ld, ps;            // row / plane strides (doubles), ld even
+  double thr;
+  unsigned long long* err;
+  int nx, ny_total;
+};
+
+__device__ __forceinline__ double eig_s(const double* co, double cx, double cy, double cxy) {
+  return fma(co[0], cxy, fma(co[1], cx, fma(co[2], cy, co[3])));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
+  extern __shared__ __align__(16) double dyn[];
+  double(*sdat)[K][BM] = reinterpret_cast<double(*)[K][BM]>(dyn);
+  double(*scoef)[K * 12] = reinterpret_cast<double(*)[K * 12]>(dyn + S * K * BM);
+  __shared__ uint64_t bar[S];
+  const int tid = threadIdx.x;
+  const int nchunk = (a.nz + K - 1) / K;
+  const int ntask = 2 * nchunk;  // forward chunks ascending, then backward descending
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  uint32_t phase[S] = {0, 0, 0};
+
+  for (long long blk = blockIdx.x; blk < (long long)a.nrows * a.nbpr; blk += gridDim.x) {
+    const int n = (int)(blk / a.nbpr);
+    const int m0 = (int)(blk % a.nbpr) * BM;
+    const int cols = min(BM, a.ncols - m0);
+    const uint32_t rowbytes = (uint32_t)(((cols + 1) & ~1) * 8);  // ld is even
+    double* base = a.w + (long long)n * a.ld + m0;
+    auto chunk_of = [&](int task) { return task < nchunk ? task : ntask - 1 - task; };
+    // thread 0: bring chunk `task` into stage s
+    auto issue = [&](int task, int s) {
+      const int c = chunk_of(task);
+      const int l0 = c * K, nl = min(K, a.nz - l0);
+      mbar_arrive_expect_tx(&bar[s], nl * rowbytes + (uint32_t)(nl * 12 * 8));
+      for (int i = 0; i < nl; ++i)
+        bulk_g2s(&sdat[s][i][0], base + (long long)(l0 + i) * a.ps, rowbytes, &bar[s]);
+      bulk_g2s(&scoef[s][0], a.coef + (long long)l0 * 12, (uint32_t)(nl * 12 * 8), &bar[s]);
+    };
+    const bool live = tid < cols;
+    const int m = m0 + tid;
+    const double cxv = __ldg(a.cx + n);
+    const double cyv = live ? __ldg(a.cy + m) : 0.0;
+    const double cxy = cxv * cyv;
+    double* ck = a.cpk + (long long)n * a.ld + m0 + tid;
+
+    // The last forward chunk stays in its stage and is the first backward chunk
+    // (no store, no reload), so stages run task % S forward and (task-1) % S
+    // backward.
+    auto stage_of = [&](int task) { return task < nchunk ? task % S : (task - 1) % S; };
+    auto needs_load = [&](int task) { return task != nchunk; };
+    if (tid == 0) {
+      issue(0, stage_of(0));
+      if (ntask > 1 && needs_load(1)) issue(1, stage_of(1));
+    }
+    double c = 0.0, x = 0.0, cknext = 0.0;
+    for (int task = 0; task < ntask; ++task) {
+      const int s = stage_of(task);
+      if (tid == 0 && task + 2 < ntask && needs_load(task + 2)) {
+        // backward reloads must see the forward stores; otherwise only the
+        // stage's previous store has to be done reading shared memory
+        if (task + 2 > nchunk) bulk_wait<0>(); else bulk_wait_read<0>();
+        fence_proxy_async_smem();
+        issue(task + 2, stage_of(task + 2));
+      }
+      if (needs_load(task)) {
+        mbar_wait(&bar[s], phase[s]);
+        phase[s] ^= 1;
+      }
+      const int cidx = chunk_of(task);
+      const int l0 = cidx * K, nl = min(K, a.nz - l0);
+      const double* co = &scoef[s][0];
+      if (task < nchunk) {
+        // forward elimination over levels l0 .. l0 + nl - 1
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          if (i < nl) {
+            const int l = l0 + i;
+            const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
+            const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
+            const double up = eig_s(co + i * 12 + 8, cxv, cyv, cxy);
+            const double den = (l == 0) ? di : fma(-lo, c, di);
+            if (live && fabs(den) < a.thr) {
+              const unsigned long long key =
+                  ((unsigned long long)l * (unsigned long long)a.ny_total + (unsigned long long)m) *
+                      (unsigned long long)a.nx +
+                  (unsigned long long)n;
+              atomicMin(a.err, key);
+            }
+            const double rr = 1.0 / den;
+            x = ((l == 0) ? sdat[s][i][tid] : fma(-lo, x, sdat[s][i][tid])) * rr;
+            sdat[s][i][tid] = x;
+            if (l < a.nz - 1) {
+              c = up * rr;
+              if (i == K - 1 && live) ck[(long long)cidx * a.ps] = c;
+            }
+          }
+        }
+        if (live && task == nchunk - 1 && nchunk > 1) cknext = ck[(long long)(nchunk - 2) * a.ps];
+      } else {
+        // back substitution over levels l0 + nl - 1 .. l0 (x holds W at the level above)
+        double cprev = cknext;
+        if (cidx >= 2 && live) cknext = ck[(long long)(cidx - 2) * a.ps];
+        double cb[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          const int l = l0 + i;
+          if (i < nl && l < a.nz - 1) {
+            const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
+            const double dl = (l == 0) ? di : fma(-eig_s(co + i * 12, cxv, cyv, cxy), cprev, di);
+            cprev = eig_s(co + i * 12 + 8, cxv, cyv, cxy) * (1.0 / dl);
+            cb[i] = cprev;
+          }
+        }
+#pragma unroll
+        for (int i = K - 1; i >= 0; --i) {
+          const int l = l0 + i;
+          if (i < nl && l < a.nz - 1) {
+            x = fma(-cb[i], x, sdat[s][i][tid]);
+            sdat[s][i][tid] = x;
+          }
+        }
+      }
+      __syncthreads();  // every thread's results for this chunk are in sdat[s]
+      if (tid == 0 && task != nchunk - 1) {
+        fence_proxy_async_smem();
+        for (int i = 0; i < nl; ++i)
+          bulk_s2g(base + (long long)(l0 + i) * a.ps, &sdat[s][i][0], rowbytes);
+        bulk_commit();
+      }
+    }
+    if (tid == 0) bulk_wait<0>();  // stores done before the stages are refilled
+    __syncthreads();
+  }
+}
+
+int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, cudaStream_t st) {
+  if (p->nz < 1) return HFB_OK;
+  TmaArgs a;
+  a.w = data;
+  a.cpk = cpk;
+  a.coef = p->coef;
+  a.cx = p->cx;
+  a.cy = p->cy;
+  a.nz = p->nz;
+  a.nrows = p->nx;
+  a.ncols = p->ny;
+  a.nbpr = (p->ny + BM - 1) / BM;
+  a.ld = ld;
+  a.ps = ld * p->nx;
+  a.thr = p->thr;
+  a.err = p->err;
+  a.nx = p->nx;
+  a.ny_total = p->ny;
+  const size_t sm = sizeof(double) * (size_t)S * (K * BM + K * 12);
+  HFB_CUDA(cudaFuncSetAttribute(thomas_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sm));
+  int per_sm = 1, sms = 148, dev = 0;
+  HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, thomas_tma_kernel, BM, sm));
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long work = (long long)a.nrows * a.nbpr;
+  const long long blocks = std::min<long long>(work, (long long)sms * std::max(per_sm, 1));
+  thomas_tma_kernel<<<(unsigned)blocks, BM, sm, st>>>(a);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+}  // namespace hfb

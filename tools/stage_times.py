@@ -32,8 +32,7 @@ stages = {
     "dst_x (all rows)": lambda: lib.hfb_transform_lines_x(h, P(F), 0, n, P(None), st),
     "dst_y (all cols)": lambda: lib.hfb_transform_lines_y(h, P(F), 0, n, P(None), st),
     "thomas (all modes)": lambda: lib.hfb_solve_slab(h, P(F), n, 0, P(cpw), st),
-    "stack (x^T + y^T)": lambda: lib.hfb_transform_stack(h, P(F), 0, n, P(work), st),
-    "full solve": lambda: lib.hfb_solve(h, P(F), P(U), P(work), st),
+    "stack (x^T + y^T)": lambda: lib.hfb_transform_stack(h, P(F), 0, n, P(work), st),    "full solve": lambda: lib.hfb_solve(h, P(F), P(U), P(work), st),
 }
 pts = n ** 3
 for name, fn in stages.items():
