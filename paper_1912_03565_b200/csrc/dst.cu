@@ -259,7 +259,9 @@ size_t transform_work_elems(const hfb_plan* p, int nplanes) {
 // Transposed-pipeline solve workspace: S (nz x nx x ldt) and cp (same).
 size_t fused_work_elems(const hfb_plan* p) {
   if (!tran_path(p)) return 0;
-  return 2 * (size_t)p->nx * tran_ld(p) * p->nz;
+  const size_t pst = (size_t)p->nx * tran_ld(p);
+  const size_t nck = (p->nz + kThomasChunk - 1) / kThomasChunk;  // cp checkpoint planes
+  return pst * (p->nz + nck);
 }
 
 // Five launches:

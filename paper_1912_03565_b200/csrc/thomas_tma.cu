@@ -20,7 +20,7 @@ namespace hfb {
 
 namespace {
 constexpr int BM = 256;  // modes per CTA block = threads
-constexpr int K = 8;     // levels per chunk
+constexpr int K = kThomasChunk;  // levels per chunk
 constexpr int S = 3;     // ring stages
 
 struct TmaArgs {
