@@ -64,7 +64,10 @@ const char* hfb_strerror(int code);
 uint64_t hfb_launch_count(void);
 
 /* Performance knobs (no effect on results): key 0 = DST engine width
- * (16 or 32 values per thread), key 1 = transform groups per CTA (0 = auto). */
+ * (16 or 32 values per thread), key 1 = transform groups per CTA (0 = auto),
+ * key 2 = L2 promotion of the column (tensor-box) loads: 0 none, 1 64 B,
+ * 2 128 B (default), 3 256 B; key 3 = batch order: 0 interleaved over CTAs
+ * (default), 1 contiguous runs per CTA. */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.
@@ -88,6 +91,13 @@ int hfb_plan_set_coefficients(hfb_plan* plan, const double* table, const double*
 /* Workspace sizes in bytes. op: 0 = hfb_solve, 1 = hfb_transform_stack,
  * 2 = hfb_solve_slab (for the full n_y modes). */
 size_t hfb_workspace_bytes(const hfb_plan* plan, int op);
+
+/* Layout of the hfb_solve workspace (no effect on results): 0 = fast (two
+ * padded scratch volumes; every DST pass reads and writes whole rows or
+ * tensor-map column boxes), 1 = lean (one padded scratch volume; the forward
+ * x-pass writes transposed). hfb_workspace_bytes(plan, 0) reports the size for
+ * the current mode, which hfb_solve then expects. Default 0. */
+int hfb_plan_set_workspace_mode(hfb_plan* plan, int lean);
 
 /* Orthonormal 2D DST-I (x-pass then y-pass) of planes [z0, z1) in place.
  * Replaces spectral.transform_stack (spectral.py:75-91). */

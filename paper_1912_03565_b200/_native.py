@@ -46,6 +46,7 @@ SIGNATURES = {
     "hfb_strerror": (ctypes.c_char_p, [_i]),
     "hfb_launch_count": (ctypes.c_uint64, []),
     "hfb_set_tuning": (None, [_i, _i]),
+    "hfb_plan_set_workspace_mode": (_i, [_vp, _i]),
     "hfb_plan_create": (_i, [_i, _i, _i, _i, ctypes.POINTER(_vp)]),
     "hfb_plan_destroy": (_i, [_vp]),
     "hfb_plan_set_coefficients": (_i, [_vp, _vp, _vp, _vp, _d]),
@@ -175,11 +176,25 @@ class DevicePlan:
         self._coef_key = key
 
     def workspace(self, op):
+        """Device workspace for op (see hfb_workspace_bytes). For the one-call
+        solve (op 0) the fast two-volume layout is tried first; when it does
+        not fit, the plan switches to the lean one-volume layout."""
         torch = _torch()
         nbytes = int(self.lib.hfb_workspace_bytes(self.handle, op))
         if nbytes == 0:
             return None
+        try:
+            return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        except torch.OutOfMemoryError:
+            if op != 0:
+                raise
+        torch.cuda.empty_cache()
+        check(self.lib.hfb_plan_set_workspace_mode(self.handle, 1), "set_workspace_mode")
+        nbytes = int(self.lib.hfb_workspace_bytes(self.handle, op))
         return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+
+    def set_workspace_mode(self, lean):
+        check(self.lib.hfb_plan_set_workspace_mode(self.handle, int(lean)), "set_workspace_mode")
 
     def stream(self):
         return current_stream(self.device)

@@ -168,6 +168,12 @@ extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const
   return HFB_OK;
 }
 
+extern "C" int hfb_plan_set_workspace_mode(hfb_plan* p, int lean) {
+  if (!p || lean < 0 || lean > 1) return HFB_ERR_ARGUMENT;
+  p->ws_lean = lean;
+  return HFB_OK;
+}
+
 extern "C" size_t hfb_workspace_bytes(const hfb_plan* p, int op) {
   if (!p) return 0;
   const size_t vol = (size_t)p->nx * p->ny * p->nz;

@@ -256,24 +256,38 @@ size_t transform_work_elems(const hfb_plan* p, int nplanes) {
   return dense_tmp_elems(p, nplanes);
 }
 
-// Transposed-pipeline solve workspace: S (nz x nx x ldt) and cp (same).
-size_t fused_work_elems(const hfb_plan* p) {
-  if (!tran_path(p)) return 0;
-  const size_t pst = (size_t)p->nx * tran_ld(p);
-  const size_t nck = (p->nz + kThomasChunk - 1) / kThomasChunk;  // cp checkpoint planes
-  return pst * (p->nz + nck);
+// One-call solve scratch. Every scratch plane holds either (j, n) rows of
+// stride ldx or (n, m) rows of stride ldt (both even, so rows are 16-byte
+// aligned for the bulk copies and strides are legal for tensor maps); the cp
+// checkpoints take one plane per kThomasChunk levels.
+//   fast: S1 (x-pass output) + S2 (y-pass output, Thomas, inverse y-pass) + cp
+//   lean: S + cp (the forward x-pass writes columns: transposing stores)
+static long long x_ld(const hfb_plan* p) { return (p->nx + 1) & ~1LL; }
+static long long fused_plane(const hfb_plan* p) {
+  return std::max(x_ld(p) * p->ny, tran_ld(p) * p->nx);
 }
 
-// Five launches:
-//   1. x-DST      F (l, j, i)     -> S (l, n, j)        [TRAN]
-//   2. y-DST      S (l, n, .)     -> S (l, n, m)        [ROW, in place]
-//   3. Thomas     per mode (n, m) along l on S, cp workspace
-//   4. y-DST      S (l, n, .)     -> out (l, j, n)      [TRAN]
-//   5. x-DST      out (l, j, .)   -> out (l, j, i)      [ROW, in place]
+size_t fused_work_elems(const hfb_plan* p) {
+  if (!tran_path(p)) return 0;
+  const size_t nck = (p->nz + kThomasChunk - 1) / kThomasChunk;
+  const size_t arrays = p->ws_lean ? 1 : 2;
+  return (size_t)fused_plane(p) * (arrays * p->nz + nck);
+}
+
+// Five launches. Fast layout:
+//   1. x-DST   F (l, j, i)    -> S1 (l, j, n)   [ROW: rows in, rows out]
+//   2. y-DST   S1 columns n   -> S2 (l, n, m)   [TLOAD: tensor-box columns in, rows out]
+//   3. Thomas  per mode (n, m) along l, in place on S2, cp checkpoints
+//   4. y-DST   S2 (l, n, .)   -> S2 (l, n, j)   [ROW, in place]
+//   5. x-DST   S2 columns j   -> out (l, j, i)  [TLOAD]
+// Lean layout replaces 1-2 by an x-pass with transposing stores F -> S (l, n, j)
+// and a y-pass in place on S.
 int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaStream_t st) {
-  const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), pst = ldt * p->nx;
-  double* S = work;
-  double* CP = S + pst * p->nz;
+  const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), ldx = x_ld(p);
+  const long long pst = fused_plane(p);
+  double* S1 = work;
+  double* S2 = p->ws_lean ? work : work + pst * p->nz;
+  double* CP = S2 + pst * p->nz;
   Dst16Call x = {};
   x.tw = p->tw_x;
   x.sn = p->sn_x;
@@ -285,44 +299,57 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
   y.sn = p->sn_y;
   y.scale = p->scale_y;
   y.M = p->ny + 1;
+  int rc;
   // 1
-  x.mode = 1;
   x.src = rhs;
   x.src_end = rhs + p->nz * ps;
-  x.dst = S;
   x.nrow = p->ny;
   x.in_ld = p->nx;
   x.in_ps = ps;
-  x.out_ld = ldt;
-  x.out_ps = pst;
-  int rc = launch_dst16_mode(x, st);
-  if (rc) return rc;
+  if (p->ws_lean) {
+    x.mode = 1;  // TRAN: F rows -> S2 (l, n, j)
+    x.dst = S2;
+    x.out_ld = ldt;
+    x.out_ps = pst;
+  } else {
+    x.mode = 0;  // ROW: F rows -> S1 (l, j, n)
+    x.dst = S1;
+    x.out_ld = ldx;
+    x.out_ps = pst;
+  }
+  if ((rc = launch_dst16_mode(x, st))) return rc;
   // 2
-  y.mode = 0;
-  y.src = S;
-  y.src_end = S + p->nz * pst;
-  y.dst = S;
   y.nrow = p->nx;
-  y.in_ld = ldt;
-  y.in_ps = pst;
+  y.dst = S2;
   y.out_ld = ldt;
   y.out_ps = pst;
-  rc = launch_dst16_mode(y, st);
-  if (rc) return rc;
+  if (p->ws_lean) {
+    y.mode = 0;  // ROW in place on S2
+    y.src = S2;
+    y.in_ld = ldt;
+  } else {
+    y.mode = 2;  // TLOAD: S1 columns -> S2 rows
+    y.src = S1;
+    y.in_ld = ldx;
+  }
+  y.src_end = y.src + p->nz * pst;
+  y.in_ps = pst;
+  if ((rc = launch_dst16_mode(y, st))) return rc;
   // 3
-  rc = launch_thomas_tma(p, S, CP, ldt, st);
-  if (rc) return rc;
+  if ((rc = launch_thomas_tma(p, S2, CP, ldt, pst, st))) return rc;
   // 4
-  y.mode = 1;
-  y.dst = out;
-  y.out_ld = p->nx;
-  y.out_ps = ps;
-  rc = launch_dst16_mode(y, st);
-  if (rc) return rc;
+  y.mode = 0;
+  y.src = S2;
+  y.src_end = S2 + p->nz * pst;
+  y.in_ld = ldt;
+  if ((rc = launch_dst16_mode(y, st))) return rc;
   // 5
-  x.mode = 0;
-  x.src = out;
-  x.src_end = out + p->nz * ps;
+  x.mode = 2;
+  x.src = S2;
+  x.src_end = S2 + p->nz * pst;
+  x.nrow = p->ny;
+  x.in_ld = ldt;
+  x.in_ps = pst;
   x.dst = out;
   x.out_ld = p->nx;
   x.out_ps = ps;

@@ -1,28 +1,41 @@
-// DST-I along contiguous lines with the register-resident engine (fftE.cuh).
+// DST-I along lines with the register-resident engine (fftE.cuh).
 //
-// Persistent CTAs, each holding NF transform groups (one warp per group for
-// M = 1024). A batch is one plane's row group: NF line pairs (2NF lines; pair
-// k = rows (2k, 2k+1), never straddling a plane). Input rows are prefetched
-// one batch ahead into shared memory with 1D TMA bulk copies (cp.async.bulk +
-// mbarrier, double-buffered), so the HBM latency of batch i+1 overlaps the
-// transform of batch i. Rows need not be 16-byte aligned: the copy starts at
-// the aligned address below the row and the consumer skips the leading
-// element; a copy that would read past the end of the source array is
-// shortened and thread 0 patches the last element. Thread 0 resolves every
-// row's addresses per batch into shared memory.
+// Persistent CTAs, each holding NF transform groups (one group = M/16
+// threads). A batch is one plane's block of W = 2NF consecutive lines (pair k
+// = lines (2k, 2k+1), never straddling a plane). The next batch is prefetched
+// into shared memory by the TMA engine while the current one is transformed
+// (mbarrier, double-buffered stages), so HBM latency overlaps the arithmetic.
 //
-// Output, staged through shared memory (rows padded one slot per 32):
-//   ROW  : out[plane][row][pos] — each group stores its own two rows;
-//   TRAN : out[plane][pos][row] — lines become columns; a warp stores 2NF
-//          consecutive rows of 32/(2NF) positions.
+// Input modes:
+//   ROW, TRAN : lines are contiguous rows, fetched with 1D bulk copies. Rows
+//               need not be 16-byte aligned: the copy starts at the aligned
+//               address below the row and the consumer skips the leading
+//               element; a copy that would read past the end of the source is
+//               shortened and thread 0 patches the last element.
+//   TLOAD     : lines are COLUMNS of a padded (plane, pos, line) array, fetched
+//               as 3D tensor boxes [pos][W] (cp.async.bulk.tensor); the
+//               transposition happens in the TMA engine and each thread reads
+//               its line pair as one double2 per position.
+// Output (staged through shared memory as (line 2f, line 2f+1) double2 pairs,
+// XOR-swizzled so both the per-thread segment writes and the reads are
+// conflict-free):
+//   ROW, TLOAD : out[plane][line][pos] — each group stores its own two lines;
+//   TRAN       : out[plane][pos][line] — lines become columns; consecutive
+//                threads store consecutive (pos, pair) double2 values.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "fftE.cuh"
 #include "tma.cuh"
 
 namespace hfb {
 
-enum { kRow = 0, kTran = 1 };  // Dst16Call::mode
+enum { kRow = 0, kTran = 1, kTload = 2 };  // Dst16Call::mode
 
 struct FftArgs {
   const double2* __restrict__ tw;  // tw[k] = exp(-2 pi i k/M)
@@ -35,25 +48,38 @@ struct StreamArgs {
   double* dst;
   const double* src_end;  // one past the last readable element of src
   int z0, nz;             // first plane, plane count
-  int nrow, ppp, G;       // lines per plane, pairs per plane, row groups per plane
+  int nrow, ppp, G;       // lines per plane, pairs per plane, line blocks per plane
   long long in_ld, in_ps, out_ld, out_ps;
-  int N, NF, logW;        // line length, groups per CTA, log2(2 NF)
-  int rowslot;   // doubles per staged input row (even, >= N + 4)
-  int gbuf;      // doubles per group buffer per stage
-  int stage_ld;  // output staging row stride (odd, > pad32(N + 1))
+  int N, NF, logNF;       // line length, groups per CTA, log2(NF)
+  int rowslot;            // doubles per staged input row (even, >= N + 4)
+  int gbuf;               // doubles per group buffer (== 16/NF mod 16)
+  int stage;              // doubles per stage (multiple of 128: 1-KB aligned swizzle atoms)
+  int nbox, boxn;         // TLOAD: boxes per batch and their extent along the line
+  int vec_out;            // TRAN: (line 2k, 2k+1) pairs are 16-byte aligned in dst
+  long long per;          // batches per CTA (contiguous runs), 0 = interleaved
 };
 
 constexpr int kMaxRows = 16;  // 2 * NF
 
 struct BatchMeta {
   long long plane[2];
-  int row[2][kMaxRows];    // row index within the plane, -1 if absent
-  int delta[2][kMaxRows];  // staged-row offset (doubles) of element 0
+  int row[2][kMaxRows];    // line index within the plane, -1 if absent
+  int delta[2][kMaxRows];  // staged-row offset (doubles) of element 0 (ROW/TRAN)
 };
 
+// Batch `it` of this CTA: interleaved (b = blockIdx + it * grid) or, with
+// a.per > 0, a contiguous run of a.per batches per CTA (consecutive line blocks
+// of one plane in a row, so a TLOAD CTA reuses the L2 lines its previous box
+// fetched).
 __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long long& plane,
                                          int& g) {
-  const long long b = blockIdx.x + it * gridDim.x;
+  long long b;
+  if (a.per > 0) {
+    if (it >= a.per) return false;
+    b = (long long)blockIdx.x * a.per + it;
+  } else {
+    b = blockIdx.x + it * gridDim.x;
+  }
   if (b >= (long long)a.nz * a.G) return false;
   plane = a.z0 + b / a.G;
   g = (int)(b % a.G);
@@ -61,14 +87,20 @@ __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long
 }
 
 template <int P, int E, int MODE>
-__global__ void __launch_bounds__(128, 3) dstE_stream_kernel(StreamArgs a, FftArgs c) {
-  extern __shared__ __align__(16) double sm[];
+__global__ void __launch_bounds__(128, 3)
+    dstE_stream_kernel(StreamArgs a, FftArgs c, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(16) double sm_raw[];
   __shared__ BatchMeta meta;
-  constexpr int T = FE<P, E>::T, SEG = FE<P, E>::SEG;
+  constexpr int M = FE<P, E>::M, T = FE<P, E>::T, SEG = FE<P, E>::SEG, Q = 2 * SEG;
+  constexpr int LQ = FE<P, E>::LE;  // log2(Q)
+  // 1-KB aligned base (swizzle atoms of the TLOAD boxes); offset arithmetic on
+  // the shared array keeps every access an LDS/STS (no generic loads)
+  double* sm = sm_raw + (((smem_u32(sm_raw) + 1023u) & ~1023u) - smem_u32(sm_raw)) / 8;
   const int f = threadIdx.x / T, t = threadIdx.x - f * T;
-  double2* wsum = reinterpret_cast<double2*>(sm + 2LL * a.NF * a.gbuf);
+  double2* wsum = reinterpret_cast<double2*>(sm + 2LL * a.stage);
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + (blockDim.x / 32 + 1));
-  auto gbuf = [&](int s, int g) { return sm + ((long long)s * a.NF + g) * a.gbuf; };
+  auto gbuf = [&](int s, int g) { return sm + (long long)s * a.stage + (long long)g * a.gbuf; };
+  const int W = 2 * a.NF;
 
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -77,44 +109,54 @@ __global__ void __launch_bounds__(128, 3) dstE_stream_kernel(StreamArgs a, FftAr
   }
   __syncthreads();
 
-  // thread 0: resolve the rows of batch `it` and start their bulk copies into
-  // stage s (staged row r at gbuf(s, r/2) + (r&1)*rowslot + 2, 16-B aligned)
+  // thread 0: resolve the lines of batch `it` and start their copies into stage s
   auto issue = [&](long long it, int s) {
     long long plane;
     int g;
     batch_of(a, it, plane, g);
     meta.plane[s] = plane;
-    uint32_t total = 0;
-    const int rows = 2 * a.NF;
+    if constexpr (MODE == kTload) {
+      for (int r = 0; r < W; ++r) {
+        const int row = g * W + r;
+        meta.row[s][r] = row < a.nrow ? row : -1;
+      }
+      mbar_arrive_expect_tx(&bar[s], (uint32_t)(a.nbox * a.boxn * W * 8));
+      for (int b = 0; b < a.nbox; ++b)
+        tensor_g2s_3d(gbuf(s, 0) + (long long)b * a.boxn * W, &tmap, g * W, b * a.boxn,
+                      (int)plane, &bar[s]);
+    } else {
+      // staged row r at gbuf(s, r/2) + (r&1)*rowslot + 2 (16-B aligned)
+      uint32_t total = 0;
 #pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 1) mbar_arrive_expect_tx(&bar[s], total);
+      for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) mbar_arrive_expect_tx(&bar[s], total);
 #pragma unroll 1
-      for (int r = 0; r < rows; ++r) {
-        const int k = g * a.NF + (r >> 1);
-        const int row = 2 * k + (r & 1);
-        if (k >= a.ppp || row >= a.nrow) {
-          if (pass == 0) {
-            meta.row[s][r] = -1;
-            meta.delta[s][r] = 2;
+        for (int r = 0; r < W; ++r) {
+          const int k = g * a.NF + (r >> 1);
+          const int row = 2 * k + (r & 1);
+          if (k >= a.ppp || row >= a.nrow) {
+            if (pass == 0) {
+              meta.row[s][r] = -1;
+              meta.delta[s][r] = 2;
+            }
+            continue;
           }
-          continue;
-        }
-        const double* A = a.src + plane * a.in_ps + (long long)row * a.in_ld;
-        const double* A16 =
-            reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(A) & ~uintptr_t(15));
-        const int d = (int)(A - A16);
-        uint32_t S = (uint32_t)((8 * (a.N + d) + 15) & ~15);
-        const bool cut = A16 + S / 8 > a.src_end;
-        if (cut) S -= 16;
-        double* dstrow = gbuf(s, r >> 1) + (r & 1) * a.rowslot + 2;
-        if (pass == 0) {
-          total += S;
-          meta.row[s][r] = row;
-          meta.delta[s][r] = 2 + d;
-          if (cut) dstrow[d + a.N - 1] = __ldg(A + a.N - 1);  // not covered by the copy
-        } else {
-          bulk_g2s(dstrow, A16, S, &bar[s]);
+          const double* A = a.src + plane * a.in_ps + (long long)row * a.in_ld;
+          const double* A16 =
+              reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(A) & ~uintptr_t(15));
+          const int d = (int)(A - A16);
+          uint32_t S = (uint32_t)((8 * (a.N + d) + 15) & ~15);
+          const bool cut = A16 + S / 8 > a.src_end;
+          if (cut) S -= 16;
+          double* dstrow = gbuf(s, r >> 1) + (r & 1) * a.rowslot + 2;
+          if (pass == 0) {
+            total += S;
+            meta.row[s][r] = row;
+            meta.delta[s][r] = 2 + d;
+            if (cut) dstrow[d + a.N - 1] = __ldg(A + a.N - 1);  // not covered by the copy
+          } else {
+            bulk_g2s(dstrow, A16, S, &bar[s]);
+          }
         }
       }
     }
@@ -145,47 +187,63 @@ __global__ void __launch_bounds__(128, 3) dstE_stream_kernel(StreamArgs a, FftAr
     double* gb = gbuf(s, f);
     const int row0 = meta.row[s][2 * f], row1 = meta.row[s][2 * f + 1];
     const bool v0 = row0 >= 0, v1 = row1 >= 0;
-    const double* r0 = gb + meta.delta[s][2 * f] - 1;  // a_e at r0[e]
-    const double* r1 = gb + a.rowslot + meta.delta[s][2 * f + 1] - 1;
 
     double2 v[E];
-    dstE_pre<P, E>(v, c.sn, t, [&](int e) -> double2 {
-      return make_double2(v0 ? r0[e] : 0.0, v1 ? r1[e] : 0.0);
-    });
-    group_sync<T>(f);  // staged rows consumed: the group buffer becomes FFT scratch
+    if constexpr (MODE == kTload) {
+      // box [pos][W]: a_e of lines (2f, 2f+1) is the double2 at pos e - 1
+      // (absent lines and positions >= N were zero-filled by the TMA engine)
+      // (the box is swizzled: 16-byte granule g sits at g ^ ((g >> 3) & (NF - 1)))
+      const double2* bx = reinterpret_cast<const double2*>(gbuf(s, 0));
+      dstE_pre<P, E>(v, c.sn, t, [&](int e) -> double2 {
+        const int gr = ((e + M - 1) & (M - 1)) * a.NF + f;
+        return bx[gr ^ ((gr >> 3) & (a.NF - 1))];
+      });
+      __syncthreads();  // the box interleaves all groups' lines
+    } else {
+      const double* r0 = gb + meta.delta[s][2 * f] - 1;  // a_e at r0[e]
+      const double* r1 = gb + a.rowslot + meta.delta[s][2 * f + 1] - 1;
+      dstE_pre<P, E>(v, c.sn, t, [&](int e) -> double2 {
+        return make_double2(v0 ? r0[e] : 0.0, v1 ? r1[e] : 0.0);
+      });
+      group_sync<T>(f);  // staged rows consumed: the group buffer becomes FFT scratch
+    }
     double2* sb = reinterpret_cast<double2*>(gb);
     fftE_forward<P, E>(v, sb, c.tw, t, f);
-    double2 out[2 * SEG];
+    double2 out[Q];
     dstE_post<P, E>(v, sb, wsum, c.scale, t, f, out);
-    // stage: position p of row q at gb[q * stage_ld + pad32(p + 1)]
-    double* q0 = gb;
-    double* q1 = gb + a.stage_ld;
+    // stage: output position p of the pair at slot swz<LQ>(p)
+    double2* st2 = reinterpret_cast<double2*>(gb);
 #pragma unroll
-    for (int j = 0; j < 2 * SEG; ++j) {
-      const int idx = pad32(2 * SEG * t + j);  // position 2 SEG t + j - 1, shifted by one
-      if (t > 0 || j > 0) {
-        q0[idx] = out[j].x;
-        q1[idx] = out[j].y;
-      }
+    for (int j = 0; j < Q; ++j) {
+      const int p = Q * t + j - 1;
+      if (p >= 0) st2[swz<LQ>(p)] = out[j];
     }
-    if constexpr (MODE == kRow) {
-      group_sync<T>(f);
-      const long long b0 = plane * a.out_ps + (long long)row0 * a.out_ld;
-      const long long b1 = plane * a.out_ps + (long long)row1 * a.out_ld;
-      for (int p = t; p < a.N; p += T) {
-        if (v0) a.dst[b0 + p] = q0[pad32(p + 1)];
-        if (v1) a.dst[b1 + p] = q1[pad32(p + 1)];
+    if constexpr (MODE == kTran) {
+      __syncthreads();
+      const int total = a.N << a.logNF;
+      double* ob = a.dst + plane * a.out_ps;
+      for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        const int pos = e >> a.logNF, gg = e & (a.NF - 1);
+        const int r0 = meta.row[s][2 * gg];
+        if (r0 < 0) continue;
+        const bool has1 = meta.row[s][2 * gg + 1] >= 0;
+        const double2 val = lds128(reinterpret_cast<const double2*>(gbuf(s, gg)) + swz<LQ>(pos));
+        double* o = ob + (long long)pos * a.out_ld + r0;
+        if (a.vec_out && has1) {
+          *reinterpret_cast<double2*>(o) = val;
+        } else {
+          o[0] = val.x;
+          if (has1) o[1] = val.y;
+        }
       }
     } else {
-      __syncthreads();
-      const int W = 2 * a.NF;
-      const int total = a.N * W;
-      for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        const int pos = e >> a.logW, r = e & (W - 1);
-        const int row = meta.row[s][r];
-        if (row < 0) continue;
-        a.dst[plane * a.out_ps + (long long)pos * a.out_ld + row] =
-            gbuf(s, r >> 1)[(r & 1) * a.stage_ld + pad32(pos + 1)];
+      group_sync<T>(f);
+      double* o0 = a.dst + plane * a.out_ps + (long long)row0 * a.out_ld;
+      double* o1 = a.dst + plane * a.out_ps + (long long)row1 * a.out_ld;
+      for (int p = t; p < a.N; p += T) {
+        const double2 val = lds128(&st2[swz<LQ>(p)]);
+        if (v0) o0[p] = val.x;
+        if (v1) o1[p] = val.y;
       }
     }
     __syncthreads();  // stage s is free for the prefetch issued next iteration
@@ -195,49 +253,120 @@ __global__ void __launch_bounds__(128, 3) dstE_stream_kernel(StreamArgs a, FftAr
 
 bool dst16_ok(int M) { return M >= 16 && M <= 4096 && (M & (M - 1)) == 0; }
 
-template <int P, int E, int MODE>
-static int launch_stream(const StreamArgs& a, const FftArgs& c, int threads, size_t sm,
-                         cudaStream_t st) {
-  auto kern = dstE_stream_kernel<P, E, MODE>;
-  HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  int per_sm = 1;
-  HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, sm));
-  int sms = 148, dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long work = (long long)a.nz * a.G;
-  const long long blocks = std::min<long long>(work, (long long)sms * std::max(per_sm, 1));
-  kern<<<(unsigned)blocks, threads, sm, st>>>(a, c);
-  return HFB_OK;
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
 }
 
 // tuning knobs (hfb_set_tuning): engine width E for M >= 32 and groups per CTA
 static int g_tune_E = 16;
 static int g_tune_NF = 0;
+static int g_tune_l2 = 2;     // TLOAD tensor-map L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
+static int g_tune_order = 0;  // batch order: 0 interleaved, 1 contiguous runs per CTA
+
+template <int P, int E, int MODE>
+static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
+                         int threads, size_t sm, cudaStream_t st) {
+  auto kern = dstE_stream_kernel<P, E, MODE>;
+  HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared));
+  int per_sm = 1;
+  HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, sm));
+  if (getenv("HFB_DEBUG"))
+    fprintf(stderr, "dstE<P=%d,E=%d,mode=%d>: %d threads, %zu B smem, %d CTAs/SM\n", P, E, MODE,
+            threads, sm, per_sm);
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long work = (long long)a.nz * a.G;
+  long long blocks = std::min<long long>(work, (long long)sms * std::max(per_sm, 1));
+  StreamArgs b = a;
+  b.per = 0;
+  if (g_tune_order == 1) {
+    b.per = (work + blocks - 1) / blocks;
+    blocks = (work + b.per - 1) / b.per;
+  }
+  kern<<<(unsigned)blocks, threads, sm, st>>>(b, c, tmap);
+  return HFB_OK;
+}
 
 template <int P, int E>
 static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStream_t st) {
-  constexpr int T = FE<P, E>::T;
-  a.NF = std::max(1, std::min(128 / T, kMaxRows / 2));  // <= 128 threads per CTA
-  if (g_tune_NF > 0) a.NF = std::max(1, std::min(g_tune_NF, std::min(128 / T, kMaxRows / 2)));
+  using G = FE<P, E>;
+  constexpr int T = G::T, M = G::M;
+  int nf = std::max(1, std::min(128 / T, kMaxRows / 2));  // <= 128 threads per CTA
+  if (g_tune_NF > 0) nf = std::max(1, std::min(g_tune_NF, nf));
+  a.NF = 1;
+  a.logNF = 0;
+  while (2 * a.NF <= nf) {
+    a.NF *= 2;
+    ++a.logNF;
+  }
+  const int W = 2 * a.NF;
   a.G = (a.ppp + a.NF - 1) / a.NF;
-  a.logW = 0;
-  while ((1 << a.logW) < 2 * a.NF) ++a.logW;
   a.rowslot = ((a.N + 4) + 1) & ~1;
-  a.stage_ld = pad32(a.N + 1) + 1;
-  if (a.stage_ld % 2 == 0) ++a.stage_ld;
-  a.gbuf = std::max({2 * a.rowslot, 2 * FE<P, E>::BUF, 2 * a.stage_ld});  // doubles
-  a.gbuf = (a.gbuf + 1) & ~1;
+  int gb = std::max(2 * a.rowslot, 2 * G::BUF);
+  const int want = 16 / a.NF;  // group offsets spread over the 8 16-byte bank groups
+  while (gb % 16 != want % 16) ++gb;
+  a.gbuf = gb;
+  long long stage = (long long)a.NF * a.gbuf;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (k.mode == kTload) {
+    a.boxn = std::min(256, M);
+    a.nbox = M / a.boxn;
+    stage = std::max<long long>(stage, (long long)a.nbox * a.boxn * W);
+    auto enc = tensor_encoder();
+    if (!enc) return HFB_ERR_CUDA;
+    if ((reinterpret_cast<uintptr_t>(a.src) & 15) || (a.in_ld & 1) || (a.in_ps & 1))
+      return HFB_ERR_ARGUMENT;
+    cuuint64_t dims[3] = {(cuuint64_t)a.nrow, (cuuint64_t)a.N, (cuuint64_t)(a.z0 + a.nz)};
+    cuuint64_t strides[2] = {(cuuint64_t)a.in_ld * 8, (cuuint64_t)a.in_ps * 8};
+    cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)a.boxn, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(a.src), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     a.NF == 8   ? CU_TENSOR_MAP_SWIZZLE_128B
+                     : a.NF == 4 ? CU_TENSOR_MAP_SWIZZLE_64B
+                     : a.NF == 2 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : CU_TENSOR_MAP_SWIZZLE_NONE,
+                     g_tune_l2 == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                     : g_tune_l2 == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                     : g_tune_l2 == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                      : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return HFB_ERR_ARGUMENT;
+  }
+  a.stage = (int)((stage + 127) & ~127LL);
+  a.vec_out = (k.mode == kTran) && !(reinterpret_cast<uintptr_t>(a.dst) & 15) &&
+              !(a.out_ld & 1) && !(a.out_ps & 1);
   const int threads = a.NF * T;
-  const size_t sm = (size_t)2 * a.NF * a.gbuf * sizeof(double) +
+  const size_t sm = 1024 + (size_t)2 * a.stage * sizeof(double) +
                     (threads / 32 + 1) * sizeof(double2) + 2 * sizeof(uint64_t);
-  if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, threads, sm, st);
-  return launch_stream<P, E, kRow>(a, c, threads, sm, st);
+  if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, tmap, threads, sm, st);
+  if (k.mode == kTload) return launch_stream<P, E, kTload>(a, c, tmap, threads, sm, st);
+  return launch_stream<P, E, kRow>(a, c, tmap, threads, sm, st);
 }
 
 template <int P>
 static int launch_p(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStream_t st) {
-  if constexpr (P >= 5) {
+  // E = 32 on request, and whenever E = 16 would need more than 128 threads
+  // per line pair (M = 4096)
+  if constexpr (P >= 12) {
+    return launch_pe<P, 32>(k, a, c, st);
+  } else if constexpr (P >= 5) {
     if (g_tune_E == 32) return launch_pe<P, 32>(k, a, c, st);
   }
   return launch_pe<P, 16>(k, a, c, st);
@@ -246,11 +375,13 @@ static int launch_p(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStre
 void set_tuning(int key, int value) {
   if (key == 0) g_tune_E = (value == 32) ? 32 : 16;
   if (key == 1) g_tune_NF = value;
+  if (key == 2) g_tune_l2 = value;
+  if (key == 3) g_tune_order = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {
   if (k.nz <= 0 || k.nrow <= 0) return HFB_OK;
-  if (k.mode != kRow && k.mode != kTran) return HFB_ERR_ARGUMENT;
+  if (k.mode != kRow && k.mode != kTran && k.mode != kTload) return HFB_ERR_ARGUMENT;
   int p = 0;
   while ((1 << p) < k.M) ++p;
   FftArgs c;

@@ -3,11 +3,11 @@
 //
 // A transform group = T = M/E threads; thread t holds x[t + T*i], i < E (the
 // "cyclic" distribution). Stockham passes of radix E (and one final smaller
-// radix) run in registers; between passes the values go through a padded
-// shared buffer (one pad slot per 16, so the strided Stockham writes and the
-// cyclic reads are bank-conflict free). The last pass leaves its outputs in
-// the same cyclic slots: an M = 1024 transform with E = 32 is one warp, two
-// radix-32 passes and a single exchange.
+// radix) run in registers; between passes the values go through a shared
+// buffer whose slots are XOR-swizzled (swz), so the strided Stockham writes and
+// the cyclic reads are bank-conflict free without padding. The last pass
+// leaves its outputs in the same cyclic slots: an M = 1024 transform with
+// E = 32 is one warp, two radix-32 passes and a single exchange.
 //
 // DST-I pre/post-processing (algebra in hfb_internal.cuh):
 //   pre : b_e = s_e (a_e + a_{M-e}) + (a_e - a_{M-e})/2 (b_0 = 0 and
@@ -21,9 +21,6 @@
 #include "hfb_internal.cuh"
 
 namespace hfb {
-
-__host__ __device__ __forceinline__ constexpr int pad16(int i) { return i + (i >> 4); }
-__host__ __device__ __forceinline__ constexpr int pad32(int i) { return i + (i >> 5); }
 
 // cos(pi k / 16) for any integer k (exact decimal expansions of the 32nd roots)
 __host__ __device__ __forceinline__ constexpr double c32(int k) {
@@ -150,13 +147,24 @@ struct FE {
   static constexpr int LE = (E == 32) ? 5 : 4;
   static constexpr int FULL = P / LE;
   static constexpr int REM = P % LE;
-  static constexpr int BUF = pad16(M) + 1;  // double2 slots of a group buffer
   static constexpr int SEG = E / 2;
+  static constexpr int BUF = M;  // double2 slots of a group buffer (XOR-swizzled, no pads)
 };
 
+// Bank-conflict-free placement without padding: the low three bits of a
+// 16-byte slot index are XORed with bits [S, S+3). Accesses whose threads
+// stride by 2^S slots (the Stockham scatter, the k-segment reads of the post-
+// processing) and accesses by 8 consecutive slots both hit 8 distinct bank
+// groups, and the map is a bijection inside every aligned block of 8 slots.
+template <int S>
+__device__ __forceinline__ constexpr int swz(int i) {
+  return i ^ ((i >> S) & 7);
+}
+
 // Twiddles w^u, u = 1..R-1, of w = tw[k*S] (w^u = tw[u*k*S]) from at most two
-// table loads: w^2, w^3 by products, and for R = 16 the fourth powers loaded
-// directly so every factor is at most three roundings from the table.
+// table loads: w^2, w^3 by products, and for R = 16 (32) the fourth (and
+// sixteenth) powers loaded directly so every factor is at most three (four)
+// roundings from the table.
 template <int R>
 __device__ __forceinline__ void twiddle_powers(const double2* __restrict__ tw, int ks,
                                                double2* wp) {
@@ -171,7 +179,7 @@ __device__ __forceinline__ void twiddle_powers(const double2* __restrict__ tw, i
     wp[6] = cmul(wp[4], wp[2]);
     wp[7] = cmul(wp[4], wp[3]);
   }
-  if constexpr (R == 16) {
+  if constexpr (R >= 16) {
     wp[4] = __ldg(&tw[4 * ks]);
     wp[8] = cmul(wp[4], wp[4]);
     wp[12] = cmul(wp[8], wp[4]);
@@ -179,6 +187,11 @@ __device__ __forceinline__ void twiddle_powers(const double2* __restrict__ tw, i
     for (int a4 = 4; a4 < 16; a4 += 4)
 #pragma unroll
       for (int b = 1; b < 4; ++b) wp[a4 + b] = cmul(wp[a4], wp[b]);
+  }
+  if constexpr (R == 32) {
+    wp[16] = __ldg(&tw[16 * ks]);
+#pragma unroll
+    for (int r = 1; r < 16; ++r) wp[16 + r] = cmul(wp[16], wp[r]);
   }
 }
 
@@ -211,11 +224,12 @@ __device__ __forceinline__ void exchangeE(double2* v, double2* sb, int t, int f)
   constexpr int T = FE<P, E>::T;
   const int k = t & (L - 1);
   const int base = (t - k) * E + k;
+  constexpr int LE = FE<P, E>::LE;
 #pragma unroll
-  for (int u = 0; u < E; ++u) sb[pad16(base + u * L)] = v[u];
+  for (int u = 0; u < E; ++u) sb[swz<LE>(base + u * L)] = v[u];
   group_sync<T>(f);
 #pragma unroll
-  for (int i = 0; i < E; ++i) v[i] = sb[pad16(t + T * i)];
+  for (int i = 0; i < E; ++i) v[i] = sb[swz<LE>(t + T * i)];
   group_sync<T>(f);
 }
 
@@ -274,17 +288,17 @@ __device__ __forceinline__ double2 group_scanE(double2 v, int t, int f, double2*
 template <int P, int E>
 __device__ __forceinline__ void dstE_post(const double2* v, double2* sb, double2* wsum,
                                           double scale, int t, int f, double2* out) {
-  constexpr int M = FE<P, E>::M, T = FE<P, E>::T, SEG = FE<P, E>::SEG;
+  constexpr int M = FE<P, E>::M, T = FE<P, E>::T, SEG = FE<P, E>::SEG, LS = FE<P, E>::LE - 1;
 #pragma unroll
-  for (int i = 0; i < E; ++i) sb[pad16(t + T * i)] = v[i];
+  for (int i = 0; i < E; ++i) sb[swz<LS>(t + T * i)] = v[i];
   group_sync<T>(f);
   const int k0 = SEG * t;
   double2 run = make_double2(0.0, 0.0);
 #pragma unroll
   for (int s = 0; s < SEG; ++s) {
     const int k = k0 + s;
-    const double2 bk = sb[pad16(k)];
-    const double2 bm = sb[pad16((M - k) & (M - 1))];
+    const double2 bk = sb[swz<LS>(k)];
+    const double2 bm = sb[swz<LS>((M - k) & (M - 1))];
     double2 C = make_double2(0.5 * (bk.x + bm.x), 0.5 * (bk.y + bm.y));
     if (k == 0) C = cscale(C, 0.5);
     run = cadd(run, C);

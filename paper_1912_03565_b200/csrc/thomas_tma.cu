@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
     mbar_fence_init();
   }
   __syncthreads();
-  uint32_t phase[S] = {0, 0, 0};
+  uint32_t phase = 0;  // bit s: parity of stage s
 
   for (long long blk = blockIdx.x; blk < (long long)a.nrows * a.nbpr; blk += gridDim.x) {
     const int n = (int)(blk / a.nbpr);
@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
         issue(task + 2, stage_of(task + 2));
       }
       if (needs_load(task)) {
-        mbar_wait(&bar[s], phase[s]);
-        phase[s] ^= 1;
+        mbar_wait(&bar[s], (phase >> s) & 1u);
+        phase ^= 1u << s;
       }
       const int cidx = chunk_of(task);
       const int l0 = cidx * K, nl = min(K, a.nz - l0);
@@ -169,7 +169,8 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
   }
 }
 
-int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, cudaStream_t st) {
+int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, long long ps,
+                      cudaStream_t st) {
   if (p->nz < 1) return HFB_OK;
   TmaArgs a;
   a.w = data;
@@ -182,7 +183,7 @@ int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, cuda
   a.ncols = p->ny;
   a.nbpr = (p->ny + BM - 1) / BM;
   a.ld = ld;
-  a.ps = ld * p->nx;
+  a.ps = ps;
   a.thr = p->thr;
   a.err = p->err;
   a.nx = p->nx;

@@ -396,3 +396,63 @@ def test_cfg3_residual_at_full_size(cuda):
     r = hb.residual_l2(u, hb.Field3D(F), w.scheme, w.profile, w.grid)
     # roundoff floor eps * ||A|| ||U|| / ||F||; ||U|| >> ||F|| near resonance
     assert r / float(torch.linalg.norm(F)) < 1e-11
+
+
+# ------------------------------------------------- engine tuning variants
+@pytest.fixture
+def tuning():
+    lib = hb._native.load_library()
+    yield lib.hfb_set_tuning
+    lib.hfb_set_tuning(0, 16)
+    lib.hfb_set_tuning(1, 0)
+    lib.hfb_set_tuning(2, 2)
+    lib.hfb_set_tuning(3, 0)
+
+
+@pytest.mark.parametrize("knobs", [((0, 32),), ((0, 32), (1, 2)), ((0, 32), (1, 1)), ((1, 1),),
+                                   ((2, 0),), ((2, 3),), ((3, 1),)])
+def test_tuning_variants_match_oracle(cuda, tuning, knobs):
+    """Performance knobs change the FFT factorisation or the CTA shape, never
+    the result beyond rounding: transforms (row, transposed-store and
+    tensor-box column paths) and one-call solves against the oracle."""
+    for k, v in knobs:
+        tuning(k, v)
+    rng = np.random.default_rng(7)
+    for nx, ny, nz in [(255, 255, 3), (63, 127, 5), (1023, 63, 2), (31, 4095, 1)]:
+        data = rng.standard_normal((nz, ny, nx))
+        f = hb.Field3D(data.copy())
+        hb.transform_stack(hb.make_plan(nx, ny), f)
+        ref = orc.dst_stack(data, workers=4)
+        assert np.abs(f.values - ref).max() < 1e-13 * np.abs(ref).max()
+    w = wl.workload(1)
+    F = wl.host_rhs(w)
+    u, _ = solve(F, w.scheme, w.profile, w.grid)
+    ref = orc.solve(F, oracle_table(w.scheme.value, w.profile, w.grid),
+                    *orc.mode_cosines(w.grid.n_x, w.grid.n_y))
+    assert rel_l2(u, ref) < PARITY
+
+
+@pytest.mark.parametrize("shape", [(31, 31, 31), (127, 63, 33), (255, 15, 9)])
+def test_lean_workspace_bitwise_equal_fast(cuda, shape):
+    """The lean one-volume workspace (transposing x-pass stores) and the fast
+    two-volume one (row/tensor-box passes) run the same per-line arithmetic."""
+    import torch
+    nx, ny, nz = shape
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+    prof = hb.constant_profile(3.0, g)
+    F = torch.from_numpy(np.random.default_rng(nx).standard_normal((nz, ny, nx))).cuda()
+    plan = hb._native.get_plan(nx, ny, nz, F.device)
+    hb.tridiag.device_coefficients(plan, hb.SchemeKind.FOURTH_ORDER, prof, g)
+    outs = []
+    for lean in (0, 1):
+        plan.set_workspace_mode(lean)
+        U = torch.empty_like(F)
+        work = plan.workspace(0)
+        hb._native.check(plan.lib.hfb_solve(plan.handle, hb._native.ptr(F), hb._native.ptr(U),
+                                            hb._native.ptr(work), plan.stream()), "solve")
+        plan.fetch_status()
+        outs.append(U.cpu().numpy())
+    plan.set_workspace_mode(0)
+    assert np.array_equal(outs[0], outs[1])
+    ref = orc.solve(F.cpu().numpy(), oracle_table("4", prof, g), *orc.mode_cosines(nx, ny))
+    assert rel_l2(outs[0], ref) < PARITY

@@ -16,6 +16,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=4)
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--tune", default="", help="key=value,... passed to hfb_set_tuning")
+ap.add_argument("--time", action="store_true", help="print the mean solve time (CUDA events)")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 w = wl.workload(a.cfg, a.n)
@@ -25,9 +27,29 @@ device_coefficients(plan, w.scheme, w.profile, w.grid)
 F = wl.device_rhs(w, dev)
 U = torch.empty_like(F)
 work = plan.workspace(0)
-for _ in range(a.reps):
+for kv in filter(None, a.tune.split(",")):
+    k, v = kv.split("=")
+    plan.lib.hfb_set_tuning(int(k), int(v))
+
+
+def solve():
     _native.check(plan.lib.hfb_solve(plan.handle, _native.ptr(F), _native.ptr(U),
                                      _native.ptr(work), plan.stream()), "solve")
+
+
+if a.time:
+    solve()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.reps):
+        solve()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"tune={a.tune} n={n} ms/solve={e0.elapsed_time(e1) / a.reps:.3f}")
+else:
+    for _ in range(a.reps):
+        solve()
 plan.fetch_status()
 torch.cuda.synchronize()
 print("ok", float(U.abs().max()))
