@@ -66,8 +66,9 @@ uint64_t hfb_launch_count(void);
 /* Performance knobs (no effect on results): key 0 = DST engine width
  * (16 or 32 values per thread), key 1 = transform groups per CTA (0 = auto),
  * key 2 = L2 promotion of the column (tensor-box) loads: 0 none, 1 64 B,
- * 2 128 B (default), 3 256 B; key 3 = batch order: 0 interleaved over CTAs
- * (default), 1 contiguous runs per CTA. */
+ * 2 128 B (default), 3 256 B; key 3 = batch order: 0 auto (interleaved over
+ * CTAs; column passes in runs of one 128-byte line), 1 one contiguous run per
+ * CTA, R >= 2 interleaved runs of R batches. */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.

@@ -74,12 +74,14 @@ _lib = None
 _lock = threading.Lock()
 
 
-def load_library(path=LIB_PATH):
-    """Load (once) and type the C-ABI library; raises NativeUnavailableError."""
+def load_library(path=None):
+    """Load (once) and type the C-ABI library; raises NativeUnavailableError.
+    HFB_LIBRARY overrides the in-tree path (A/B builds of the same ABI)."""
     global _lib
     with _lock:
         if _lib is not None:
             return _lib
+        path = path or os.environ.get("HFB_LIBRARY") or LIB_PATH
         if not os.path.exists(path):
             raise NativeUnavailableError(
                 f"{path} is missing: build it with `make` (or __graft_entry__.build())")

@@ -56,7 +56,8 @@ struct StreamArgs {
   int stage;              // doubles per stage (multiple of 128: 1-KB aligned swizzle atoms)
   int nbox, boxn;         // TLOAD: boxes per batch and their extent along the line
   int vec_out;            // TRAN: (line 2k, 2k+1) pairs are 16-byte aligned in dst
-  long long per;          // batches per CTA (contiguous runs), 0 = interleaved
+  long long per;          // batches per CTA (one contiguous run), 0 = interleaved
+  int run;                // > 1: interleaved runs of `run` consecutive batches
 };
 
 constexpr int kMaxRows = 16;  // 2 * NF
@@ -67,16 +68,18 @@ struct BatchMeta {
   int delta[2][kMaxRows];  // staged-row offset (doubles) of element 0 (ROW/TRAN)
 };
 
-// Batch `it` of this CTA: interleaved (b = blockIdx + it * grid) or, with
-// a.per > 0, a contiguous run of a.per batches per CTA (consecutive line blocks
-// of one plane in a row, so a TLOAD CTA reuses the L2 lines its previous box
-// fetched).
+// Batch `it` of this CTA: interleaved (b = blockIdx + it * grid), interleaved
+// runs of a.run consecutive batches (a TLOAD CTA then reads the neighbouring
+// columns of the 128-byte lines its previous box fetched while they are still
+// in L2), or one contiguous run of a.per batches per CTA.
 __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long long& plane,
                                          int& g) {
   long long b;
   if (a.per > 0) {
     if (it >= a.per) return false;
     b = (long long)blockIdx.x * a.per + it;
+  } else if (a.run > 1) {
+    b = ((it / a.run) * gridDim.x + blockIdx.x) * a.run + it % a.run;
   } else {
     b = blockIdx.x + it * gridDim.x;
   }
@@ -162,6 +165,8 @@ __global__ void __launch_bounds__(128, 3)
     }
   };
 
+  EngineTw<P, E> etw;
+  engine_tw<P, E>(c.tw, c.sn, t, etw);
   int s = 0;
   uint32_t phase0 = 0, phase1 = 0;
   {
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(128, 3)
       // (absent lines and positions >= N were zero-filled by the TMA engine)
       // (the box is swizzled: 16-byte granule g sits at g ^ ((g >> 3) & (NF - 1)))
       const double2* bx = reinterpret_cast<const double2*>(gbuf(s, 0));
-      dstE_pre<P, E>(v, c.sn, t, [&](int e) -> double2 {
+      dstE_pre<P, E>(v, c.sn, etw, t, [&](int e) -> double2 {
         const int gr = ((e + M - 1) & (M - 1)) * a.NF + f;
         return bx[gr ^ ((gr >> 3) & (a.NF - 1))];
       });
@@ -202,13 +207,13 @@ __global__ void __launch_bounds__(128, 3)
     } else {
       const double* r0 = gb + meta.delta[s][2 * f] - 1;  // a_e at r0[e]
       const double* r1 = gb + a.rowslot + meta.delta[s][2 * f + 1] - 1;
-      dstE_pre<P, E>(v, c.sn, t, [&](int e) -> double2 {
+      dstE_pre<P, E>(v, c.sn, etw, t, [&](int e) -> double2 {
         return make_double2(v0 ? r0[e] : 0.0, v1 ? r1[e] : 0.0);
       });
       group_sync<T>(f);  // staged rows consumed: the group buffer becomes FFT scratch
     }
     double2* sb = reinterpret_cast<double2*>(gb);
-    fftE_forward<P, E>(v, sb, c.tw, t, f);
+    fftE_forward<P, E>(v, sb, etw, t, f);
     double2 out[Q];
     dstE_post<P, E>(v, sb, wsum, c.scale, t, f, out);
     // stage: output position p of the pair at slot swz<LQ>(p)
@@ -273,7 +278,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
 static int g_tune_E = 16;
 static int g_tune_NF = 0;
 static int g_tune_l2 = 2;     // TLOAD tensor-map L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
-static int g_tune_order = 0;  // batch order: 0 interleaved, 1 contiguous runs per CTA
+static int g_tune_order = 0;  // batch order: 0 auto, 1 one run per CTA, R >= 2 runs of R
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
@@ -294,9 +299,14 @@ static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMa
   long long blocks = std::min<long long>(work, (long long)sms * std::max(per_sm, 1));
   StreamArgs b = a;
   b.per = 0;
+  b.run = 1;
   if (g_tune_order == 1) {
     b.per = (work + blocks - 1) / blocks;
     blocks = (work + b.per - 1) / b.per;
+  } else if (g_tune_order >= 2) {
+    b.run = g_tune_order;
+  } else if (MODE == kTload) {
+    b.run = 2;  // pairs of neighbouring column blocks (measured best at W = 4)
   }
   kern<<<(unsigned)blocks, threads, sm, st>>>(b, c, tmap);
   return HFB_OK;

@@ -161,14 +161,62 @@ __device__ __forceinline__ constexpr int swz(int i) {
   return i ^ ((i >> S) & 7);
 }
 
-// Twiddles w^u, u = 1..R-1, of w = tw[k*S] (w^u = tw[u*k*S]) from at most two
-// table loads: w^2, w^3 by products, and for R = 16 (32) the fourth (and
-// sixteenth) powers loaded directly so every factor is at most three (four)
-// roundings from the table.
+// multiply by w_N^e for an e that is a compile-time constant after unrolling
+template <int N>
+__device__ __forceinline__ double2 mul_wn_at(double2 a, int e) {
+  switch (e & 31) {
+#define HFB_W(EE) \
+  case EE: return mul_wn<N, EE>(a);
+    HFB_W(0) HFB_W(1) HFB_W(2) HFB_W(3) HFB_W(4) HFB_W(5) HFB_W(6) HFB_W(7) HFB_W(8) HFB_W(9)
+    HFB_W(10) HFB_W(11) HFB_W(12) HFB_W(13) HFB_W(14) HFB_W(15) HFB_W(16) HFB_W(17) HFB_W(18)
+    HFB_W(19) HFB_W(20) HFB_W(21) HFB_W(22) HFB_W(23) HFB_W(24) HFB_W(25) HFB_W(26) HFB_W(27)
+    HFB_W(28) HFB_W(29) HFB_W(30) HFB_W(31)
+#undef HFB_W
+  }
+  return a;
+}
+
+// Per-thread twiddle bases, loaded once per kernel (they depend only on the
+// thread's place in its group, not on the data): for the pass of stride L and
+// radix R, w = tw[k M/(L R)] with k = t mod L, plus w^4 (R >= 16) and w^16
+// (R = 32) straight from the table; the sine pair of the pre-processing.
+template <int P, int E>
+struct EngineTw {
+  double2 w1[3], w4[3], w16[3];  // by pass index (0 = the L = 1 pass: unused)
+  double st, ct;                 // sin(pi t/M), cos(pi t/M)
+};
+
+template <int P, int E, int R, int L>
+__device__ __forceinline__ void tw_base(const double2* __restrict__ tw, int t, double2& w1,
+                                        double2& w4, double2& w16) {
+  constexpr int M = FE<P, E>::M, TWSTEP = M / (L * R);
+  const int k = t & (L - 1);
+  w1 = __ldg(&tw[k * TWSTEP]);
+  if constexpr (R >= 16) w4 = __ldg(&tw[4 * k * TWSTEP]);
+  if constexpr (R == 32) w16 = __ldg(&tw[16 * k * TWSTEP]);
+}
+
+template <int P, int E>
+__device__ __forceinline__ void engine_tw(const double2* __restrict__ tw,
+                                          const double* __restrict__ sn, int t,
+                                          EngineTw<P, E>& w) {
+  using G = FE<P, E>;
+  if constexpr (G::FULL >= 2) tw_base<P, E, E, E>(tw, t, w.w1[1], w.w4[1], w.w16[1]);
+  if constexpr (G::FULL >= 3) tw_base<P, E, E, E * E>(tw, t, w.w1[2], w.w4[2], w.w16[2]);
+  if constexpr (G::REM > 0) {
+    constexpr int L = 1 << (G::LE * G::FULL);
+    tw_base<P, E, (1 << G::REM), L>(tw, t, w.w1[G::FULL], w.w4[G::FULL], w.w16[G::FULL]);
+  }
+  w.st = __ldg(&sn[t]);
+  w.ct = __ldg(&sn[G::M / 2 - t]);
+}
+
+// Twiddles w^u, u = 1..R-1, from w (and w^4, w^16 for R >= 16, 32): w^2, w^3
+// by products, so every factor is at most four roundings from the table.
 template <int R>
-__device__ __forceinline__ void twiddle_powers(const double2* __restrict__ tw, int ks,
+__device__ __forceinline__ void twiddle_powers(double2 w1, double2 w4, double2 w16,
                                                double2* wp) {
-  wp[1] = __ldg(&tw[ks]);
+  wp[1] = w1;
   if constexpr (R >= 4) {
     wp[2] = cmul(wp[1], wp[1]);
     wp[3] = cmul(wp[2], wp[1]);
@@ -180,7 +228,7 @@ __device__ __forceinline__ void twiddle_powers(const double2* __restrict__ tw, i
     wp[7] = cmul(wp[4], wp[3]);
   }
   if constexpr (R >= 16) {
-    wp[4] = __ldg(&tw[4 * ks]);
+    wp[4] = w4;
     wp[8] = cmul(wp[4], wp[4]);
     wp[12] = cmul(wp[8], wp[4]);
 #pragma unroll
@@ -189,26 +237,28 @@ __device__ __forceinline__ void twiddle_powers(const double2* __restrict__ tw, i
       for (int b = 1; b < 4; ++b) wp[a4 + b] = cmul(wp[a4], wp[b]);
   }
   if constexpr (R == 32) {
-    wp[16] = __ldg(&tw[16 * ks]);
+    wp[16] = w16;
 #pragma unroll
     for (int r = 1; r < 16; ++r) wp[16 + r] = cmul(wp[16], wp[r]);
   }
 }
 
-// One radix-R Stockham pass (stride L) on the cyclic registers.
+// One radix-R Stockham pass (stride L) on the cyclic registers. With NB = E/R
+// butterflies per thread (the final, smaller-radix pass), butterfly b's base
+// is tw[t + T b] = w * w_E^b: one rotation by a compile-time root.
 template <int P, int E, int R, int L>
-__device__ __forceinline__ void pass_regs(double2* v, const double2* __restrict__ tw, int t) {
-  constexpr int M = FE<P, E>::M, T = FE<P, E>::T, NB = E / R, TWSTEP = M / (L * R);
+__device__ __forceinline__ void pass_regs(double2* v, double2 w1, double2 w4, double2 w16) {
+  constexpr int NB = E / R;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    const int j = t + T * b;
-    const int k = j & (L - 1);
     double2 w[R];
 #pragma unroll
     for (int u = 0; u < R; ++u) w[u] = v[b + u * NB];
     if constexpr (L > 1) {
+      static_assert(NB == 1 || FE<P, E>::T * NB == L, "shared twiddle base");
       double2 wp[R];
-      twiddle_powers<R>(tw, k * TWSTEP, wp);
+      twiddle_powers<R>(b ? mul_wn_at<E>(w1, b) : w1, b ? mul_wn_at<E>(w4, 4 * b) : w4,
+                        b ? mul_wn_at<E>(w16, 16 * b) : w16, wp);
 #pragma unroll
       for (int u = 1; u < R; ++u) w[u] = cmul(w[u], wp[u]);
     }
@@ -234,22 +284,23 @@ __device__ __forceinline__ void exchangeE(double2* v, double2* sb, int t, int f)
 }
 
 template <int P, int E>
-__device__ __forceinline__ void fftE_forward(double2* v, double2* sb,
-                                             const double2* __restrict__ tw, int t, int f) {
+__device__ __forceinline__ void fftE_forward(double2* v, double2* sb, const EngineTw<P, E>& tw,
+                                             int t, int f) {
   using G = FE<P, E>;
-  pass_regs<P, E, E, 1>(v, tw, t);
+  const double2 z = make_double2(0.0, 0.0);
+  pass_regs<P, E, E, 1>(v, z, z, z);
   if constexpr (G::FULL >= 2) {
     exchangeE<P, E, 1>(v, sb, t, f);
-    pass_regs<P, E, E, E>(v, tw, t);
+    pass_regs<P, E, E, E>(v, tw.w1[1], tw.w4[1], tw.w16[1]);
   }
   if constexpr (G::FULL >= 3) {
     exchangeE<P, E, E>(v, sb, t, f);
-    pass_regs<P, E, E, E * E>(v, tw, t);
+    pass_regs<P, E, E, E * E>(v, tw.w1[2], tw.w4[2], tw.w16[2]);
   }
   if constexpr (G::REM > 0) {
     constexpr int L = 1 << (G::LE * G::FULL);
     exchangeE<P, E, L / E>(v, sb, t, f);
-    pass_regs<P, E, (1 << G::REM), L>(v, tw, t);
+    pass_regs<P, E, (1 << G::REM), L>(v, tw.w1[G::FULL], tw.w4[G::FULL], tw.w16[G::FULL]);
   }
 }
 
@@ -314,11 +365,11 @@ __device__ __forceinline__ void dstE_post(const double2* v, double2* sb, double2
 // Pre-processing: v[i] = b_{t + T i} from a loader of a_e (e in [1, M-1]); the
 // loader may return garbage for e = 0 and e = M (selected away here).
 template <int P, int E, class Load>
-__device__ __forceinline__ void dstE_pre(double2* v, const double* __restrict__ sn, int t,
-                                         Load&& load) {
+__device__ __forceinline__ void dstE_pre(double2* v, const double* __restrict__ sn,
+                                         const EngineTw<P, E>& tw, int t, Load&& load) {
   constexpr int M = FE<P, E>::M, T = FE<P, E>::T, H = M / 2;
   // E = 16: sin(pi (t + T i)/M) = sin(pi t/M) cos(pi i/16) + cos(pi t/M) sin(pi i/16)
-  const double st = __ldg(&sn[t]), ct = __ldg(&sn[H - t]);
+  const double st = tw.st, ct = tw.ct;
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const int e = t + T * i;

@@ -410,7 +410,7 @@ def tuning():
 
 
 @pytest.mark.parametrize("knobs", [((0, 32),), ((0, 32), (1, 2)), ((0, 32), (1, 1)), ((1, 1),),
-                                   ((2, 0),), ((2, 3),), ((3, 1),)])
+                                   ((2, 0),), ((2, 3),), ((3, 1),), ((3, 3),)])
 def test_tuning_variants_match_oracle(cuda, tuning, knobs):
     """Performance knobs change the FFT factorisation or the CTA shape, never
     the result beyond rounding: transforms (row, transposed-store and
