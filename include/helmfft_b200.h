@@ -68,7 +68,9 @@ uint64_t hfb_launch_count(void);
  * key 2 = L2 promotion of the column (tensor-box) loads: 0 none, 1 64 B,
  * 2 128 B (default), 3 256 B; key 3 = batch order: 0 auto (interleaved over
  * CTAs; column passes in runs of one 128-byte line), 1 one contiguous run per
- * CTA, R >= 2 interleaved runs of R batches. */
+ * CTA, R >= 2 interleaved runs of R batches; key 4 = row outputs by TMA
+ * tensor stores where the destination layout allows (1, default) or by
+ * thread stores (0). */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.

@@ -56,6 +56,7 @@ struct StreamArgs {
   int stage;              // doubles per stage (multiple of 128: 1-KB aligned swizzle atoms)
   int nbox, boxn;         // TLOAD: boxes per batch and their extent along the line
   int vec_out;            // TRAN: (line 2k, 2k+1) pairs are 16-byte aligned in dst
+  int tstore;             // ROW/TLOAD: outputs leave by TMA tensor stores (omap)
   long long per;          // batches per CTA (one contiguous run), 0 = interleaved
   int run;                // > 1: interleaved runs of `run` consecutive batches
 };
@@ -91,7 +92,8 @@ __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long
 
 template <int P, int E, int MODE>
 __global__ void __launch_bounds__(128, 3)
-    dstE_stream_kernel(StreamArgs a, FftArgs c, const __grid_constant__ CUtensorMap tmap) {
+    dstE_stream_kernel(StreamArgs a, FftArgs c, const __grid_constant__ CUtensorMap tmap,
+                       const __grid_constant__ CUtensorMap omap) {
   extern __shared__ __align__(16) double sm_raw[];
   __shared__ BatchMeta meta;
   constexpr int M = FE<P, E>::M, T = FE<P, E>::T, SEG = FE<P, E>::SEG, Q = 2 * SEG;
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__(128, 3)
       long long pl2;
       int g2;
       if (threadIdx.x == 0 && batch_of(a, it + 1, pl2, g2)) {
+        if (a.tstore) bulk_wait_read<0>();  // batch it-1's tensor stores read stage s^1
         fence_proxy_async_smem();
         issue(it + 1, s ^ 1);
       }
@@ -215,45 +218,77 @@ __global__ void __launch_bounds__(128, 3)
     double2* sb = reinterpret_cast<double2*>(gb);
     fftE_forward<P, E>(v, sb, etw, t, f);
     double2 out[Q];
-    dstE_post<P, E>(v, sb, wsum, c.scale, t, f, out);
-    // stage: output position p of the pair at slot swz<LQ>(p)
-    double2* st2 = reinterpret_cast<double2*>(gb);
+    if (MODE != kTran && a.tstore) {
+      // Segment-aligned outputs staged as the group's tensor box [2 lines]
+      // [M/16 segments][16] in the 128B-swizzle layout (granule h of smem row r
+      // at h ^ (r & 7): conflict-free, since thread t owns whole segments),
+      // then one TMA tensor store per group (issued by thread 0).
+      dstE_post_aligned<P, E>(v, sb, wsum, c.scale, t, f, out);
+      constexpr int NSEG = M / 16;
 #pragma unroll
-    for (int j = 0; j < Q; ++j) {
-      const int p = Q * t + j - 1;
-      if (p >= 0) st2[swz<LQ>(p)] = out[j];
-    }
-    if constexpr (MODE == kTran) {
-      __syncthreads();
-      const int total = a.N << a.logNF;
-      double* ob = a.dst + plane * a.out_ps;
-      for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        const int pos = e >> a.logNF, gg = e & (a.NF - 1);
-        const int r0 = meta.row[s][2 * gg];
-        if (r0 < 0) continue;
-        const bool has1 = meta.row[s][2 * gg + 1] >= 0;
-        const double2 val = lds128(reinterpret_cast<const double2*>(gbuf(s, gg)) + swz<LQ>(pos));
-        double* o = ob + (long long)pos * a.out_ld + r0;
-        if (a.vec_out && has1) {
-          *reinterpret_cast<double2*>(o) = val;
-        } else {
-          o[0] = val.x;
-          if (has1) o[1] = val.y;
+      for (int L = 0; L < 2; ++L) {
+#pragma unroll
+        for (int h = 0; h < Q / 2; ++h) {
+          const int pos = Q * t + 2 * h;
+          const int row = L * NSEG + (pos >> 4);
+          const int phys = row * 16 + 2 * (((pos >> 1) & 7) ^ (row & 7));
+          const double2 val = L == 0 ? make_double2(out[2 * h].x, out[2 * h + 1].x)
+                                     : make_double2(out[2 * h].y, out[2 * h + 1].y);
+          *reinterpret_cast<double2*>(gb + phys) = val;
         }
       }
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int gg = 0; gg < a.NF; ++gg) {
+          const int r0 = meta.row[s][2 * gg];
+          if (r0 >= 0) tensor_s2g_4d(&omap, 0, 0, r0, (int)plane, gbuf(s, gg));
+        }
+        bulk_commit();
+      }
     } else {
-      group_sync<T>(f);
-      double* o0 = a.dst + plane * a.out_ps + (long long)row0 * a.out_ld;
-      double* o1 = a.dst + plane * a.out_ps + (long long)row1 * a.out_ld;
-      for (int p = t; p < a.N; p += T) {
-        const double2 val = lds128(&st2[swz<LQ>(p)]);
-        if (v0) o0[p] = val.x;
-        if (v1) o1[p] = val.y;
+      dstE_post<P, E>(v, sb, wsum, c.scale, t, f, out);
+      // stage: output position p of the pair at slot swz<LQ>(p)
+      double2* st2 = reinterpret_cast<double2*>(gb);
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const int p = Q * t + j - 1;
+        if (p >= 0) st2[swz<LQ>(p)] = out[j];
+      }
+      if constexpr (MODE == kTran) {
+        __syncthreads();
+        const int total = a.N << a.logNF;
+        double* ob = a.dst + plane * a.out_ps;
+        for (int e = threadIdx.x; e < total; e += blockDim.x) {
+          const int pos = e >> a.logNF, gg = e & (a.NF - 1);
+          const int r0 = meta.row[s][2 * gg];
+          if (r0 < 0) continue;
+          const bool has1 = meta.row[s][2 * gg + 1] >= 0;
+          const double2 val =
+              lds128(reinterpret_cast<const double2*>(gbuf(s, gg)) + swz<LQ>(pos));
+          double* o = ob + (long long)pos * a.out_ld + r0;
+          if (a.vec_out && has1) {
+            *reinterpret_cast<double2*>(o) = val;
+          } else {
+            o[0] = val.x;
+            if (has1) o[1] = val.y;
+          }
+        }
+      } else {
+        group_sync<T>(f);
+        double* o0 = a.dst + plane * a.out_ps + (long long)row0 * a.out_ld;
+        double* o1 = a.dst + plane * a.out_ps + (long long)row1 * a.out_ld;
+        for (int p = t; p < a.N; p += T) {
+          const double2 val = lds128(&st2[swz<LQ>(p)]);
+          if (v0) o0[p] = val.x;
+          if (v1) o1[p] = val.y;
+        }
       }
     }
     __syncthreads();  // stage s is free for the prefetch issued next iteration
     s ^= 1;
   }
+  if (a.tstore && threadIdx.x == 0) bulk_wait<0>();  // smem stays valid until stored
 }
 
 bool dst16_ok(int M) { return M >= 16 && M <= 4096 && (M & (M - 1)) == 0; }
@@ -279,10 +314,11 @@ static int g_tune_E = 16;
 static int g_tune_NF = 0;
 static int g_tune_l2 = 2;     // TLOAD tensor-map L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
 static int g_tune_order = 0;  // batch order: 0 auto, 1 one run per CTA, R >= 2 runs of R
+static int g_tune_tstore = 1;  // row outputs by TMA tensor stores where the layout allows
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
-                         int threads, size_t sm, cudaStream_t st) {
+                         const CUtensorMap& omap, int threads, size_t sm, cudaStream_t st) {
   auto kern = dstE_stream_kernel<P, E, MODE>;
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -308,7 +344,7 @@ static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMa
   } else if (MODE == kTload) {
     b.run = 2;  // pairs of neighbouring column blocks (measured best at W = 4)
   }
-  kern<<<(unsigned)blocks, threads, sm, st>>>(b, c, tmap);
+  kern<<<(unsigned)blocks, threads, sm, st>>>(b, c, tmap, omap);
   return HFB_OK;
 }
 
@@ -328,9 +364,32 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   a.G = (a.ppp + a.NF - 1) / a.NF;
   a.rowslot = ((a.N + 4) + 1) & ~1;
   int gb = std::max(2 * a.rowslot, 2 * G::BUF);
-  const int want = 16 / a.NF;  // group offsets spread over the 8 16-byte bank groups
-  while (gb % 16 != want % 16) ++gb;
+  // tensor-store outputs: rows stored whole (position N lands in the row's
+  // padding, so ld >= M), 16-byte aligned rows and planes
+  a.tstore = (k.mode != kTran) && g_tune_tstore && M >= 16 && a.out_ld >= M &&
+             !(reinterpret_cast<uintptr_t>(a.dst) & 15) && !(a.out_ld & 1) && !(a.out_ps & 1);
+  if (a.tstore) {
+    gb = (gb + 127) & ~127;  // every group box 1-KB aligned (128B swizzle atoms)
+  } else {
+    const int want = 16 / a.NF;  // group offsets spread over the 8 16-byte bank groups
+    while (gb % 16 != want % 16) ++gb;
+  }
   a.gbuf = gb;
+  CUtensorMap omap;
+  memset(&omap, 0, sizeof(omap));
+  if (a.tstore) {
+    auto enc = tensor_encoder();
+    if (!enc) return HFB_ERR_CUDA;
+    cuuint64_t dims[4] = {16, (cuuint64_t)(M / 16), (cuuint64_t)a.nrow,
+                          (cuuint64_t)(a.z0 + a.nz)};
+    cuuint64_t strides[3] = {128, (cuuint64_t)a.out_ld * 8, (cuuint64_t)a.out_ps * 8};
+    cuuint32_t box[4] = {16, (cuuint32_t)(M / 16), 2, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, a.dst, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return HFB_ERR_ARGUMENT;
+  }
   long long stage = (long long)a.NF * a.gbuf;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
@@ -365,9 +424,9 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   const int threads = a.NF * T;
   const size_t sm = 1024 + (size_t)2 * a.stage * sizeof(double) +
                     (threads / 32 + 1) * sizeof(double2) + 2 * sizeof(uint64_t);
-  if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, tmap, threads, sm, st);
-  if (k.mode == kTload) return launch_stream<P, E, kTload>(a, c, tmap, threads, sm, st);
-  return launch_stream<P, E, kRow>(a, c, tmap, threads, sm, st);
+  if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, tmap, omap, threads, sm, st);
+  if (k.mode == kTload) return launch_stream<P, E, kTload>(a, c, tmap, omap, threads, sm, st);
+  return launch_stream<P, E, kRow>(a, c, tmap, omap, threads, sm, st);
 }
 
 template <int P>
@@ -387,6 +446,7 @@ void set_tuning(int key, int value) {
   if (key == 1) g_tune_NF = value;
   if (key == 2) g_tune_l2 = value;
   if (key == 3) g_tune_order = value;
+  if (key == 4) g_tune_tstore = value ? 1 : 0;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

@@ -362,6 +362,40 @@ __device__ __forceinline__ void dstE_post(const double2* v, double2* sb, double2
   group_sync<T>(f);  // every B read is done: sb may be reused
 }
 
+// Post-processing with segment-aligned ownership: thread t emits positions
+// [Q t, Q t + Q) (Q = 2 SEG) — out[2s] = S_{2k+1} (position 2k) and
+// out[2s+1] = S_{2k+2} = D_{k+1} (position 2k+1), k = SEG t + s — so every
+// thread owns whole 128-byte segments of the output line (for TMA tensor
+// stores). Costs one extra (B_k, B_{M-k}) read per thread for D_{SEG t + SEG}.
+template <int P, int E>
+__device__ __forceinline__ void dstE_post_aligned(const double2* v, double2* sb, double2* wsum,
+                                                  double scale, int t, int f, double2* out) {
+  constexpr int M = FE<P, E>::M, T = FE<P, E>::T, SEG = FE<P, E>::SEG, LS = FE<P, E>::LE - 1;
+#pragma unroll
+  for (int i = 0; i < E; ++i) sb[swz<LS>(t + T * i)] = v[i];
+  group_sync<T>(f);
+  const int k0 = SEG * t;
+  double2 run = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s = 0; s <= SEG; ++s) {
+    const int k = k0 + s;  // k <= M/2
+    const double2 bk = sb[swz<LS>(k & (M - 1))];
+    const double2 bm = sb[swz<LS>((M - k) & (M - 1))];
+    if (s > 0)
+      out[2 * s - 1] = make_double2(-0.5 * scale * (bk.y - bm.y), 0.5 * scale * (bk.x - bm.x));
+    if (s < SEG) {
+      double2 C = make_double2(0.5 * (bk.x + bm.x), 0.5 * (bk.y + bm.y));
+      if (k == 0) C = cscale(C, 0.5);
+      run = cadd(run, C);
+      out[2 * s] = run;  // inclusive prefix within the segment (unscaled)
+    }
+  }
+  const double2 off = group_scanE<T>(run, t, f, wsum);
+#pragma unroll
+  for (int s = 0; s < SEG; ++s) out[2 * s] = cscale(cadd(out[2 * s], off), scale);
+  group_sync<T>(f);  // every B read is done: sb may be reused
+}
+
 // Pre-processing: v[i] = b_{t + T i} from a loader of a_e (e in [1, M-1]); the
 // loader may return garbage for e = 0 and e = M (selected away here).
 template <int P, int E, class Load>

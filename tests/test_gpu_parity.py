@@ -407,10 +407,12 @@ def tuning():
     lib.hfb_set_tuning(1, 0)
     lib.hfb_set_tuning(2, 2)
     lib.hfb_set_tuning(3, 0)
+    lib.hfb_set_tuning(4, 1)
 
 
 @pytest.mark.parametrize("knobs", [((0, 32),), ((0, 32), (1, 2)), ((0, 32), (1, 1)), ((1, 1),),
-                                   ((2, 0),), ((2, 3),), ((3, 1),), ((3, 3),)])
+                                   ((2, 0),), ((2, 3),), ((3, 1),), ((3, 3),), ((4, 0),),
+                                   ((0, 32), (4, 0))])
 def test_tuning_variants_match_oracle(cuda, tuning, knobs):
     """Performance knobs change the FFT factorisation or the CTA shape, never
     the result beyond rounding: transforms (row, transposed-store and
