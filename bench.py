@@ -33,6 +33,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "grid points solved/sec (fp64) at 1/2/4/8 B200; % of HBM/NVLink roofline"
 ALG_BYTES_PER_PT = 48  # 3 stages x (8 B read + 8 B write)
+# Per launch of the one-call solve: every kernel reads and writes the volume
+# once (8 B + 8 B per point) — its algorithmic minimum as a separate launch.
+STAGE_ALG_BYTES = 16
+STAGES_FAST = ["dstE x rows F->S1", "dstE y columns S1->S2 (tensor boxes)",
+               "thomas_tma z-solve S2", "dstE inverse y rows S2", "dstE inverse x columns S2->U"]
+STAGES_LEAN = ["dstE x rows->columns F->S", "dstE y rows S", "thomas_tma z-solve S",
+               "dstE inverse y rows S", "dstE inverse x columns S->U"]
 FALLBACK_HBM = 6650.0
 
 
@@ -44,7 +51,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-planes", type=int, default=64)
+    ap.add_argument("--cpu-planes", type=int, default=None,
+                    help="z-planes of the oracle CPU sample (default: all n for the "
+                         "cpu_baseline, n/4 per step for --impl reference)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -175,6 +184,8 @@ def run_reference(args):
     from paper_1912_03565_b200 import workloads as wl
     w = wl.workload(args.cfg)
     cores = os.cpu_count() or 1
+    if args.cpu_planes is None:
+        args.cpu_planes = max(2, w.n // 4)
     for _ in range(args.warmup):
         oracle_baseline(w, max(2, args.cpu_planes // 4), cores)
     vals = []
@@ -221,7 +232,8 @@ def run_ours(args):
         plan = _native.get_plan(n, n, n, dev)
         device_coefficients(plan, w.scheme, w.profile, w.grid)
         F = wl.device_rhs(w, dev)
-        U = torch.empty_like(F)
+        # 2047^3 (137 GB in + out) only fits in place
+        U = F if args.cfg == 5 else torch.empty_like(F)
         work = plan.workspace(0)
         st = plan.stream()
 
@@ -248,6 +260,8 @@ def run_ours(args):
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
+    if not multi:  # per-launch CUDA events on the solve's stream, inside the timed region
+        _native.check(lib.hfb_stage_timing(plan.handle, args.steps), "stage_timing")
     l0 = lib.hfb_launch_count()
     barrier()
     torch.cuda.synchronize(dev)
@@ -260,6 +274,14 @@ def run_ours(args):
     barrier()
     launches = int(lib.hfb_launch_count() - l0)
     clocks = sampler.stop()
+    stage_ms = None
+    if not multi:
+        buf = (ctypes.c_float * (5 * args.steps))()
+        nslots = ctypes.c_int(0)
+        _native.check(lib.hfb_stage_times(plan.handle, buf, ctypes.byref(nslots)), "stage_times")
+        _native.check(lib.hfb_stage_timing(plan.handle, 0), "stage_timing")
+        k = nslots.value
+        stage_ms = [sum(buf[5 * r + i] for r in range(k)) / k for i in range(5)]
     ms = e0.elapsed_time(e1) / args.steps
     if multi:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -312,21 +334,42 @@ def run_ours(args):
         return
 
     peak, peak_src = peaks()
-    achieved = ALG_BYTES_PER_PT * points / (ms / 1e3) / 1e9 / (world if multi else 1)
-    traffic = None
+    pipe_achieved = ALG_BYTES_PER_PT * points / (ms / 1e3) / 1e9 / (world if multi else 1)
+    traffic_tab = {}
     prof_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof_path):
         try:
-            traffic = json.load(open(prof_path)).get(f"cfg{args.cfg}_bytes_per_step")
+            traffic_tab = json.load(open(prof_path)).get(f"cfg{args.cfg}", {})
         except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "kernel": "whole solve pipeline (all launches of one step)",
-                "alg_bytes_per_point": ALG_BYTES_PER_PT, "peak_source": peak_src}
+            traffic_tab = {}
+    pipeline = {"alg_bytes_per_point": ALG_BYTES_PER_PT, "achieved_GBs": pipe_achieved,
+                "frac": pipe_achieved / peak,
+                "definition": "SURVEY.md 8(d): 3 stages x (8 B read + 8 B write) per point "
+                              "over the whole step"}
+    if stage_ms is not None:
+        lean = bool(getattr(plan, "lean", False))
+        names = STAGES_LEAN if lean else STAGES_FAST
+        stages = [{"kernel": nm, "ms": t, "alg_bytes_per_point": STAGE_ALG_BYTES,
+                   "achieved_GBs": STAGE_ALG_BYTES * points / (t / 1e3) / 1e9,
+                   "traffic_bytes": traffic_tab.get(nm)}
+                  for nm, t in zip(names, stage_ms)]
+        dom = max(stages, key=lambda e: e["ms"])
+        roofline = {"bound": "hbm", "achieved": dom["achieved_GBs"], "peak": peak, "unit": "GB/s",
+                    "frac": dom["achieved_GBs"] / peak, "traffic": dom["traffic_bytes"],
+                    "kernel": dom["kernel"], "kernel_ms": dom["ms"],
+                    "alg_bytes_per_launch": STAGE_ALG_BYTES * points,
+                    "share_of_step": dom["ms"] / ms, "peak_source": peak_src,
+                    "stages": stages, "pipeline": pipeline}
+    else:
+        roofline = {"bound": "hbm", "achieved": pipe_achieved, "peak": peak, "unit": "GB/s",
+                    "frac": pipe_achieved / peak, "traffic": None,
+                    "kernel": "whole solve pipeline (all launches of one step, max over ranks)",
+                    "peak_source": peak_src, "pipeline": pipeline}
     cpu = None
     if not args.no_cpu and not multi:
         cores = os.cpu_count() or 1
+        if args.cpu_planes is None:
+            args.cpu_planes = n if args.cfg <= 4 else 128
         v, dt = oracle_baseline(w, args.cpu_planes, cores)
         cpu = {"value": v, "unit": "pts/s", "cores": cores, "kind": "port",
                "sample": f"{args.cpu_planes} of {n} z-planes (full {n}x{n} planes), "

@@ -102,6 +102,16 @@ size_t hfb_workspace_bytes(const hfb_plan* plan, int op);
  * the current mode, which hfb_solve then expects. Default 0. */
 int hfb_plan_set_workspace_mode(hfb_plan* plan, int lean);
 
+/* Per-stage CUDA events of the one-call solve (measurement only). With a ring
+ * of R > 0 slots, each hfb_solve records an event before its first and after
+ * each of its five launches on the caller's stream, in slot (solve count mod
+ * R); R = 0 disables and frees them. hfb_stage_times waits for the recorded
+ * slots and writes 5 durations (ms) per slot — the x-pass, y-pass, z-solve,
+ * inverse y-pass and inverse x-pass of DESIGN.md §4 — and the number of
+ * recorded slots (ms must hold 5 R floats). */
+int hfb_stage_timing(hfb_plan* plan, int ring);
+int hfb_stage_times(hfb_plan* plan, float* ms, int* nslots);
+
 /* Orthonormal 2D DST-I (x-pass then y-pass) of planes [z0, z1) in place.
  * Replaces spectral.transform_stack (spectral.py:75-91). */
 int hfb_transform_stack(hfb_plan* plan, double* data, int z0, int z1, void* work,

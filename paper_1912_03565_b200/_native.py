@@ -47,6 +47,8 @@ SIGNATURES = {
     "hfb_launch_count": (ctypes.c_uint64, []),
     "hfb_set_tuning": (None, [_i, _i]),
     "hfb_plan_set_workspace_mode": (_i, [_vp, _i]),
+    "hfb_stage_timing": (_i, [_vp, _i]),
+    "hfb_stage_times": (_i, [_vp, _vp, _vp]),
     "hfb_plan_create": (_i, [_i, _i, _i, _i, ctypes.POINTER(_vp)]),
     "hfb_plan_destroy": (_i, [_vp]),
     "hfb_plan_set_coefficients": (_i, [_vp, _vp, _vp, _vp, _d]),
@@ -155,6 +157,7 @@ class DevicePlan:
                   "plan_create")
         self.handle = handle
         self._coef_key = None
+        self.lean = False  # one-call solve workspace layout (hfb_plan_set_workspace_mode)
         self.lock = threading.RLock()
 
     def __del__(self):
@@ -191,12 +194,13 @@ class DevicePlan:
             if op != 0:
                 raise
         torch.cuda.empty_cache()
-        check(self.lib.hfb_plan_set_workspace_mode(self.handle, 1), "set_workspace_mode")
+        self.set_workspace_mode(True)
         nbytes = int(self.lib.hfb_workspace_bytes(self.handle, op))
         return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
 
     def set_workspace_mode(self, lean):
         check(self.lib.hfb_plan_set_workspace_mode(self.handle, int(lean)), "set_workspace_mode")
+        self.lean = bool(lean)
 
     def stream(self):
         return current_stream(self.device)

@@ -1,3 +1,4 @@
+#include <algorithm>
 // C-ABI entry points: plan lifetime, coefficient upload, transform / tridiag
 // / full-solve drivers and status reporting. See include/helmfft_b200.h.
 #include <atomic>
@@ -88,9 +89,18 @@ extern "C" const char* hfb_strerror(int code) {
   }
 }
 
+static void stage_events_free(hfb_plan* p) {
+  for (int i = 0; i < 6 * p->stage_ring; ++i) cudaEventDestroy(p->stage_ev[i]);
+  std::free(p->stage_ev);
+  p->stage_ev = nullptr;
+  p->stage_ring = 0;
+  p->stage_count = 0;
+}
+
 extern "C" int hfb_plan_destroy(hfb_plan* p) {
   if (!p) return HFB_OK;
   cudaSetDevice(p->device);
+  stage_events_free(p);
   cudaFree(p->tw_x);
   cudaFree(p->sn_x);
   cudaFree(p->tw_y);
@@ -165,6 +175,36 @@ extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const
   HFB_CUDA(cudaMemcpy(p->cy, cy, sizeof(double) * p->ny, cudaMemcpyHostToDevice));
   p->thr = thr;
   p->have_coef = 1;
+  return HFB_OK;
+}
+
+extern "C" int hfb_stage_timing(hfb_plan* p, int ring) {
+  if (!p || ring < 0) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  stage_events_free(p);
+  if (ring == 0) return HFB_OK;
+  p->stage_ev = (cudaEvent_t*)std::calloc(6 * (size_t)ring, sizeof(cudaEvent_t));
+  if (!p->stage_ev) return HFB_ERR_ARGUMENT;
+  for (int i = 0; i < 6 * ring; ++i) {
+    if (cudaEventCreate(&p->stage_ev[i]) != cudaSuccess) {
+      p->stage_ring = i / 6;
+      stage_events_free(p);
+      return HFB_ERR_CUDA;
+    }
+  }
+  p->stage_ring = ring;
+  return HFB_OK;
+}
+
+extern "C" int hfb_stage_times(hfb_plan* p, float* ms, int* nslots) {
+  if (!p || !ms || !nslots || !p->stage_ring) return HFB_ERR_ARGUMENT;
+  const long long n = std::min<long long>(p->stage_count, p->stage_ring);
+  for (long long r = 0; r < n; ++r) {
+    cudaEvent_t* e = p->stage_ev + 6 * r;
+    HFB_CUDA(cudaEventSynchronize(e[5]));
+    for (int i = 0; i < 5; ++i) HFB_CUDA(cudaEventElapsedTime(&ms[5 * r + i], e[i], e[i + 1]));
+  }
+  *nslots = (int)n;
   return HFB_OK;
 }
 

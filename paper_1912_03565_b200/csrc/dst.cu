@@ -300,6 +300,11 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
   y.scale = p->scale_y;
   y.M = p->ny + 1;
   int rc;
+  const int slot = p->stage_ring ? (int)(p->stage_count++ % p->stage_ring) : 0;
+  auto mark = [&](int i) {
+    if (p->stage_ring) cudaEventRecord(p->stage_ev[slot * 6 + i], st);
+  };
+  mark(0);
   // 1
   x.src = rhs;
   x.src_end = rhs + p->nz * ps;
@@ -318,6 +323,7 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
     x.out_ps = pst;
   }
   if ((rc = launch_dst16_mode(x, st))) return rc;
+  mark(1);
   // 2
   y.nrow = p->nx;
   y.dst = S2;
@@ -335,14 +341,17 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
   y.src_end = y.src + p->nz * pst;
   y.in_ps = pst;
   if ((rc = launch_dst16_mode(y, st))) return rc;
+  mark(2);
   // 3
   if ((rc = launch_thomas_tma(p, S2, CP, ldt, pst, st))) return rc;
+  mark(3);
   // 4
   y.mode = 0;
   y.src = S2;
   y.src_end = S2 + p->nz * pst;
   y.in_ld = ldt;
   if ((rc = launch_dst16_mode(y, st))) return rc;
+  mark(4);
   // 5
   x.mode = 2;
   x.src = S2;
@@ -353,7 +362,9 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
   x.dst = out;
   x.out_ld = p->nx;
   x.out_ps = ps;
-  return launch_dst16_mode(x, st);
+  if ((rc = launch_dst16_mode(x, st))) return rc;
+  mark(5);
+  return HFB_OK;
 }
 
 int transform_planes(hfb_plan* p, const double* src, double* dst, int z0, int z1, double* work,

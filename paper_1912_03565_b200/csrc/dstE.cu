@@ -90,8 +90,13 @@ __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long
   return true;
 }
 
+// E = 16: up to 128 threads (two line pairs of M = 1024), 3 CTAs per SM;
+// E = 32: up to 64 threads (one warp per pair) and the full register budget.
+template <int P, int E>
+constexpr int kMaxThreads = (E == 32 && (1 << P) <= 2048) ? 64 : 128;
+
 template <int P, int E, int MODE>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(kMaxThreads<P, E>, 3)
     dstE_stream_kernel(StreamArgs a, FftArgs c, const __grid_constant__ CUtensorMap tmap,
                        const __grid_constant__ CUtensorMap omap) {
   extern __shared__ __align__(16) double sm_raw[];
@@ -352,7 +357,7 @@ template <int P, int E>
 static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStream_t st) {
   using G = FE<P, E>;
   constexpr int T = G::T, M = G::M;
-  int nf = std::max(1, std::min(128 / T, kMaxRows / 2));  // <= 128 threads per CTA
+  int nf = std::max(1, std::min(kMaxThreads<P, E> / T, kMaxRows / 2));
   if (g_tune_NF > 0) nf = std::max(1, std::min(g_tune_NF, nf));
   a.NF = 1;
   a.logNF = 0;
