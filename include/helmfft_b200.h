@@ -92,7 +92,8 @@ int hfb_plan_set_coefficients(hfb_plan* plan, const double* table, const double*
                               const double* cy, double pivot_threshold);
 
 /* Workspace sizes in bytes. op: 0 = hfb_solve, 1 = hfb_transform_stack,
- * 2 = hfb_solve_slab (for the full n_y modes). */
+ * 2 = hfb_solve_slab (for the full n_y modes), 3 = hfb_solve_z,
+ * 4 = hfb_solve_slab_z (full n_y). */
 size_t hfb_workspace_bytes(const hfb_plan* plan, int op);
 
 /* Layout of the hfb_solve workspace (no effect on results): 0 = fast (two
@@ -185,6 +186,42 @@ int hfb_apply27(hfb_plan* plan, const double* ext, const double* rhs, double* ou
 int hfb_residual_partials(const hfb_plan* plan);
 int hfb_residual_sq(hfb_plan* plan, const double* u, const double* rhs, double* partial,
                     uint32_t term_mask, void* stream);
+
+/* ---- complex k(z): complex weight tables -------------
+ * The reference computes in complex128 throughout (grid.py:8-9, 126-129);
+ * complex fields travel as two real volumes (real, imaginary parts) in the
+ * usual C-order (n_z, n_y, n_x) layout.
+ *
+ * Complex row table: table_re / table_im hold the real and imaginary parts in
+ * the layout of hfb_plan_set_coefficients (stencil.coefficient_table with
+ * complex k^2, stencil.py:177-195); pivot_threshold = PIVOT_RTOL * max|entry|.
+ * A plan with a complex table rejects the real hfb_solve / hfb_solve_slab
+ * (HFB_ERR_ARGUMENT); hfb_plan_set_coefficients makes it real again. */
+int hfb_plan_set_coefficients_z(hfb_plan* plan, const double* table_re, const double* table_im,
+                                const double* cx, const double* cy, double pivot_threshold);
+
+/* One-call complex solve (solver.solve_discrete with complex k, solver.py:
+ * 278-317): forward 2D DST of both parts, complex per-mode Thomas along z
+ * (tridiag.py:126-167 in complex arithmetic), inverse 2D DST. Workspace:
+ * hfb_workspace_bytes(plan, 3). Pivot failures are latched for
+ * hfb_status_fetch. */
+int hfb_solve_z(hfb_plan* plan, const double* rhs_re, const double* rhs_im, double* out_re,
+                double* out_im, void* work, void* stream);
+
+/* Complex per-mode solves on a transformed natural-layout y-slab (solve_slab,
+ * tridiag.py:112-167). Workspace: 2 * m_count * n_x * n_z doubles
+ * (hfb_workspace_bytes(plan, 4) for the full n_y). */
+int hfb_solve_slab_z(hfb_plan* plan, double* re, double* im, int m_count, int m_offset,
+                     void* work, void* stream);
+
+/* hfb_apply27 / hfb_residual_sq with the complex table: complex fields as
+ * (re, im) pairs, each term w*v added in the reference's order. */
+int hfb_apply27_z(hfb_plan* plan, const double* ext_re, const double* ext_im,
+                  const double* rhs_re, const double* rhs_im, double* out_re, double* out_im,
+                  uint32_t term_mask, int mode, void* stream);
+int hfb_residual_sq_z(hfb_plan* plan, const double* u_re, const double* u_im,
+                      const double* rhs_re, const double* rhs_im, double* partial,
+                      uint32_t term_mask, void* stream);
 
 /* z-slab -> send-buffer pack and receive-buffer -> z-slab unpack for the
  * partitioned exchange (solver.py:146-201). y_starts has parts+1 entries

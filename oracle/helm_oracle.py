@@ -42,10 +42,14 @@ def _cdiv(x, c):
 def row_weights(scheme, k2, k2_z, k2_zz, gamma, h, l):
     """(a, b, c, d) at offsets (l-1, l, l+1) for row level l (1-based),
     restating stencil.py:70-161 one row at a time. h = (h_x, h_y, h_z);
-    k2, k2_z, k2_zz hold the n_z + 2 closed-grid samples (real)."""
+    k2, k2_z, k2_zz hold the n_z + 2 closed-grid samples (real, or complex for
+    complex k(z))."""
     hx, hy, hz = h
     r_zx, r_zy = hz**2 / hx**2, hz**2 / hy**2
-    a, b, c, d = (np.zeros(3) for _ in range(4))
+    # complex k^2 (complex k(z), SURVEY.md 8 f1): the same formulas in complex128
+    dt = complex if any(np.iscomplexobj(v) and np.any(np.imag(v)) for v in (k2, k2_z, k2_zz)) \
+        else float
+    a, b, c, d = (np.zeros(3, dtype=dt) for _ in range(4))
     if scheme == "2":  # stencil.py:70-82
         b[1], c[1] = r_zx, r_zy
         d[0] = d[2] = 1.0
@@ -196,8 +200,10 @@ def solve_line(sub, diag, sup, rhs):
 # -------------------------------------------------------- full pipeline
 def solve(F, table, cx, cy, workers=1):
     """Homogeneous-Dirichlet solve: DST -> Thomas -> DST (solver.py:293-317 with
-    the fold a copy, assembly.py:268-269). F is (n_z, n_y, n_x); returns U."""
-    w = dst_stack(np.array(F, dtype=np.float64), workers)
+    the fold a copy, assembly.py:268-269). F is (n_z, n_y, n_x); returns U
+    (complex when F or the table is complex: complex k(z))."""
+    cplx = np.iscomplexobj(F) or any(np.iscomplexobj(t) and np.any(np.imag(t)) for t in table)
+    w = dst_stack(np.array(F, dtype=complex if cplx else np.float64), workers)
     if workers <= 1:
         thomas_sweep(w, table, cx, cy)
     else:
@@ -223,7 +229,7 @@ def accumulate27(ext, table):
     """27-point operator on a closed box (assembly.py:20-25, 229-244), same term
     order and zero-column skipping. Returns the interior result."""
     n_z, n_y, n_x = (s - 2 for s in ext.shape)
-    out = np.zeros((n_z, n_y, n_x), dtype=ext.dtype)
+    out = np.zeros((n_z, n_y, n_x), dtype=np.result_type(ext, *table))
     for dl in (-1, 0, 1):
         k = dl + 1
         for (di, dj), wi in _PLANE_TERMS:

@@ -48,6 +48,11 @@ SIGNATURES = {
     "hfb_set_tuning": (None, [_i, _i]),
     "hfb_plan_set_workspace_mode": (_i, [_vp, _i]),
     "hfb_stage_timing": (_i, [_vp, _i]),
+    "hfb_plan_set_coefficients_z": (_i, [_vp, _vp, _vp, _vp, _vp, ctypes.c_double]),
+    "hfb_solve_z": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hfb_solve_slab_z": (_i, [_vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "hfb_apply27_z": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_uint32, _i, _vp]),
+    "hfb_residual_sq_z": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_uint32, _vp]),
     "hfb_stage_times": (_i, [_vp, _vp, _vp]),
     "hfb_plan_create": (_i, [_i, _i, _i, _i, ctypes.POINTER(_vp)]),
     "hfb_plan_destroy": (_i, [_vp]),
@@ -158,6 +163,7 @@ class DevicePlan:
         self.handle = handle
         self._coef_key = None
         self.lean = False  # one-call solve workspace layout (hfb_plan_set_workspace_mode)
+        self.complex_coef = False  # the uploaded table is complex (complex k(z))
         self.lock = threading.RLock()
 
     def __del__(self):
@@ -179,6 +185,21 @@ class DevicePlan:
             self.handle, packed.ctypes.data_as(_vp), cx.ctypes.data_as(_vp),
             cy.ctypes.data_as(_vp), float(threshold)), "set_coefficients")
         self._coef_key = key
+        self.complex_coef = False
+
+    def set_coefficients_z(self, packed_re, packed_im, cx, cy, threshold, key=None):
+        """Complex table (complex k(z)): real and imaginary parts, pack_table layout."""
+        if key is not None and key == self._coef_key:
+            return
+        re = np.ascontiguousarray(packed_re, dtype=np.float64)
+        im = np.ascontiguousarray(packed_im, dtype=np.float64)
+        cx = np.ascontiguousarray(cx, dtype=np.float64)
+        cy = np.ascontiguousarray(cy, dtype=np.float64)
+        check(self.lib.hfb_plan_set_coefficients_z(
+            self.handle, re.ctypes.data_as(_vp), im.ctypes.data_as(_vp), cx.ctypes.data_as(_vp),
+            cy.ctypes.data_as(_vp), float(threshold)), "set_coefficients_z")
+        self._coef_key = key
+        self.complex_coef = True
 
     def workspace(self, op):
         """Device workspace for op (see hfb_workspace_bytes). For the one-call
@@ -191,7 +212,7 @@ class DevicePlan:
         try:
             return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         except torch.OutOfMemoryError:
-            if op != 0:
+            if op not in (0, 3):
                 raise
         torch.cuda.empty_cache()
         self.set_workspace_mode(True)

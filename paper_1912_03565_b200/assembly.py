@@ -243,19 +243,30 @@ def _with_coefficients(plan, scheme, profile, grid):
 
 
 def _apply_parts(ext_parts, rhs_parts, scheme, profile, grid, mode, device):
-    """mode 0: A ext; mode 1: rhs - A ext; per real part; returns device tensors."""
+    """mode 0: A ext; mode 1: rhs - A ext; per real part (real table) or on the
+    (re, im) pair (complex table, complex k(z)); returns device tensors."""
     torch = dv._torch()
     plan = get_plan(grid.n_x, grid.n_y, grid.n_z, device)
     outs = []
+    zeros = lambda like_shape: torch.zeros(like_shape, dtype=torch.float64, device=device)
     with plan.lock:
         table = _with_coefficients(plan, scheme, profile, grid)
         mask = term_mask(table)
+        if plan.complex_coef:
+            ext = list(ext_parts) + [torch.zeros_like(ext_parts[0])] * (2 - len(ext_parts))
+            rhs = [None, None]
+            if mode == 1:
+                rhs = list(rhs_parts) + [zeros(grid.shape)] * (2 - len(rhs_parts))
+            outs = [torch.empty(grid.shape, dtype=torch.float64, device=device) for _ in range(2)]
+            check(plan.lib.hfb_apply27_z(plan.handle, ptr(ext[0]), ptr(ext[1]), ptr(rhs[0]),
+                                         ptr(rhs[1]), ptr(outs[0]), ptr(outs[1]), mask, mode,
+                                         plan.stream()), "apply27_z")
+            return outs
         for k in range(max(len(ext_parts), len(rhs_parts) if rhs_parts else 0)):
             ext = ext_parts[k] if k < len(ext_parts) else torch.zeros_like(ext_parts[0])
             rhs = None
             if mode == 1:
-                rhs = rhs_parts[k] if k < len(rhs_parts) else torch.zeros(
-                    grid.shape, dtype=torch.float64, device=device)
+                rhs = rhs_parts[k] if k < len(rhs_parts) else zeros(grid.shape)
             out = torch.empty(grid.shape, dtype=torch.float64, device=device)
             check(plan.lib.hfb_apply27(plan.handle, ptr(ext), ptr(rhs), ptr(out), mask, mode,
                                        plan.stream()), "apply27")
@@ -271,6 +282,8 @@ def _parts_of(values, device):
 
 def _result(outs, like):
     if dv.is_tensor(like):
+        if len(outs) > 1:
+            raise NotImplementedError("complex results (complex k(z)) need numpy fields")
         return Field3D(outs[0])
     return Field3D(dv.join_parts([dv.download(o) for o in outs], like))
 
@@ -324,6 +337,14 @@ def residual_l2(u: Field3D, rhs_folded: Field3D, scheme, profile: CoefficientPro
         table = _with_coefficients(plan, scheme, profile, grid)
         mask = term_mask(table)
         npart = int(plan.lib.hfb_residual_partials(plan.handle))
+        if plan.complex_coef:
+            u2 = list(u_parts) + [torch.zeros_like(u_parts[0])] * (2 - len(u_parts))
+            f2 = list(f_parts) + [torch.zeros_like(f_parts[0])] * (2 - len(f_parts))
+            partial = torch.empty(npart, dtype=torch.float64, device=device)
+            check(plan.lib.hfb_residual_sq_z(plan.handle, ptr(u2[0]), ptr(u2[1]), ptr(f2[0]),
+                                             ptr(f2[1]), ptr(partial), mask, plan.stream()),
+                  "residual_z")
+            return float(np.sqrt(float(partial.sum().item())))
         for k in range(max(len(u_parts), len(f_parts))):
             uk = u_parts[k] if k < len(u_parts) else torch.zeros_like(u_parts[0])
             fk = f_parts[k] if k < len(f_parts) else torch.zeros_like(f_parts[0])

@@ -108,6 +108,7 @@ extern "C" int hfb_plan_destroy(hfb_plan* p) {
   cudaFree(p->dense_x);
   cudaFree(p->dense_y);
   cudaFree(p->coef);
+  cudaFree(p->coef_i);
   cudaFree(p->cx);
   cudaFree(p->cy);
   cudaFree(p->err);
@@ -153,20 +154,42 @@ extern "C" int hfb_plan_create(int nx, int ny, int nz, int device, hfb_plan** ou
   return HFB_OK;
 }
 
-extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const double* cx,
-                                         const double* cy, double thr) {
-  if (!p || !table || !cx || !cy) return HFB_ERR_ARGUMENT;
-  HFB_CUDA(cudaSetDevice(p->device));
-  const size_t nlev = (size_t)p->nz * 12;
+static void scaled_table(const double* table, size_t nlev, double* buf) {
   // device layout: [scaled (4a,2b,2c,d) x nz*3][raw (a,b,c,d) x nz*3]
-  std::vector<double> buf(2 * nlev);
   for (size_t e = 0; e < nlev; e += 4) {
     buf[e + 0] = 4.0 * table[e + 0];
     buf[e + 1] = 2.0 * table[e + 1];
     buf[e + 2] = 2.0 * table[e + 2];
     buf[e + 3] = table[e + 3];
   }
-  std::memcpy(buf.data() + nlev, table, sizeof(double) * nlev);
+  std::memcpy(buf + nlev, table, sizeof(double) * nlev);
+}
+
+extern "C" int hfb_plan_set_coefficients_z(hfb_plan* p, const double* table_re,
+                                           const double* table_im, const double* cx,
+                                           const double* cy, double thr) {
+  if (!p || !table_im) return HFB_ERR_ARGUMENT;
+  int rc = hfb_plan_set_coefficients(p, table_re, cx, cy, thr);
+  if (rc) return rc;
+  const size_t nlev = (size_t)p->nz * 12;
+  std::vector<double> buf(2 * nlev);
+  scaled_table(table_im, nlev, buf.data());
+  if (!p->coef_i) HFB_CUDA(cudaMalloc(&p->coef_i, sizeof(double) * 2 * nlev));
+  HFB_CUDA(cudaMemcpy(p->coef_i, buf.data(), sizeof(double) * 2 * nlev, cudaMemcpyHostToDevice));
+  return HFB_OK;
+}
+
+extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const double* cx,
+                                         const double* cy, double thr) {
+  if (!p || !table || !cx || !cy) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  const size_t nlev = (size_t)p->nz * 12;
+  std::vector<double> buf(2 * nlev);
+  scaled_table(table, nlev, buf.data());
+  if (p->coef_i) {  // a real table replaces a complex one
+    cudaFree(p->coef_i);
+    p->coef_i = nullptr;
+  }
   if (!p->coef) HFB_CUDA(cudaMalloc(&p->coef, sizeof(double) * 2 * nlev));
   if (!p->cx) HFB_CUDA(cudaMalloc(&p->cx, sizeof(double) * p->nx));
   if (!p->cy) HFB_CUDA(cudaMalloc(&p->cy, sizeof(double) * p->ny));
@@ -223,6 +246,11 @@ extern "C" size_t hfb_workspace_bytes(const hfb_plan* p, int op) {
     case 0: return sizeof(double) * (fw ? fw : vol + tw);  // fused, or cp + scratch
     case 1: return sizeof(double) * tw;
     case 2: return sizeof(double) * vol;
+    case 3: {  // hfb_solve_z
+      const size_t fz = fused_work_elems_z(p);
+      return sizeof(double) * (fz ? fz : 2 * vol + tw);
+    }
+    case 4: return sizeof(double) * 2 * vol;  // hfb_solve_slab_z (full n_y modes)
     default: return 0;
   }
 }
@@ -260,6 +288,7 @@ extern "C" int hfb_solve_slab(hfb_plan* p, double* slab, int m_count, int m_offs
                               void* stream) {
   if (!p || !slab || !work) return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
+  if (p->coef_i) return HFB_ERR_ARGUMENT;  // complex table: hfb_solve_slab_z
   if (m_count < 0 || m_offset < 0 || m_offset + m_count > p->ny) return HFB_ERR_RANGE;
   HFB_CUDA(cudaSetDevice(p->device));
   return launch_thomas(p, slab, m_count, m_offset, (double*)work, (cudaStream_t)stream);
@@ -268,6 +297,7 @@ extern "C" int hfb_solve_slab(hfb_plan* p, double* slab, int m_count, int m_offs
 extern "C" int hfb_solve(hfb_plan* p, const double* rhs, double* out, void* work, void* stream) {
   if (!p || !rhs || !out || !work) return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
+  if (p->coef_i) return HFB_ERR_ARGUMENT;  // complex table: hfb_solve_z
   HFB_CUDA(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
   if (fused_work_elems(p)) return solve_fused(p, rhs, out, (double*)work, st);
@@ -279,6 +309,34 @@ extern "C" int hfb_solve(hfb_plan* p, const double* rhs, double* out, void* work
   rc = launch_thomas(p, out, p->ny, 0, cpw, st);
   if (rc) return rc;
   return transform_range(p, out, out, 0, p->nz, tmp, st);
+}
+
+extern "C" int hfb_solve_slab_z(hfb_plan* p, double* re, double* im, int m_count, int m_offset,
+                                void* work, void* stream) {
+  if (!p || !re || !im || !work) return HFB_ERR_ARGUMENT;
+  if (!p->have_coef || !p->coef_i) return HFB_ERR_NO_COEFFICIENTS;
+  if (m_count < 0 || m_offset < 0 || m_offset + m_count > p->ny) return HFB_ERR_RANGE;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return launch_thomas_slab_z(p, re, im, m_count, m_offset, (double*)work, (cudaStream_t)stream);
+}
+
+extern "C" int hfb_solve_z(hfb_plan* p, const double* rhs_re, const double* rhs_im,
+                           double* out_re, double* out_im, void* work, void* stream) {
+  if (!p || !rhs_re || !rhs_im || !out_re || !out_im || !work) return HFB_ERR_ARGUMENT;
+  if (!p->have_coef || !p->coef_i) return HFB_ERR_NO_COEFFICIENTS;
+  HFB_CUDA(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (fused_work_elems_z(p))
+    return solve_fused_z(p, rhs_re, rhs_im, out_re, out_im, (double*)work, st);
+  const size_t vol = (size_t)p->nx * p->ny * p->nz;
+  double* cpw = (double*)work;
+  double* tmp = transform_work_elems(p, p->nz) ? cpw + 2 * vol : nullptr;
+  int rc = transform_range(p, rhs_re, out_re, 0, p->nz, tmp, st);
+  if (!rc) rc = transform_range(p, rhs_im, out_im, 0, p->nz, tmp, st);
+  if (!rc) rc = launch_thomas_slab_z(p, out_re, out_im, p->ny, 0, cpw, st);
+  if (!rc) rc = transform_range(p, out_re, out_re, 0, p->nz, tmp, st);
+  if (!rc) rc = transform_range(p, out_im, out_im, 0, p->nz, tmp, st);
+  return rc;
 }
 
 extern "C" int hfb_status_fetch(hfb_plan* p, void* stream, hfb_status* s) {

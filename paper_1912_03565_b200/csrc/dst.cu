@@ -367,6 +367,106 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
   return HFB_OK;
 }
 
+// Complex-coefficient solve (complex k(z)): the DSTs are real-linear, so the
+// real and imaginary volumes are transformed separately by the same passes;
+// the z-solve couples them. Fast layout: S1 + S2 (re) + S3 (im) + cp (two
+// planes per chunk); lean: S2 + S3 + cp with transposing forward x-passes.
+size_t fused_work_elems_z(const hfb_plan* p) {
+  if (!tran_path(p)) return 0;
+  const size_t nck = (p->nz + kThomasChunk - 1) / kThomasChunk;
+  const size_t arrays = p->ws_lean ? 2 : 3;
+  return (size_t)fused_plane(p) * (arrays * p->nz + 2 * nck);
+}
+
+static int forward_2d(hfb_plan* p, const double* rhs, double* S1, double* S2, cudaStream_t st) {
+  const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), ldx = x_ld(p);
+  const long long pst = fused_plane(p);
+  Dst16Call x = {};
+  x.tw = p->tw_x;
+  x.sn = p->sn_x;
+  x.scale = p->scale_x;
+  x.M = p->nx + 1;
+  x.nz = p->nz;
+  Dst16Call y = x;
+  y.tw = p->tw_y;
+  y.sn = p->sn_y;
+  y.scale = p->scale_y;
+  y.M = p->ny + 1;
+  x.src = rhs;
+  x.src_end = rhs + p->nz * ps;
+  x.nrow = p->ny;
+  x.in_ld = p->nx;
+  x.in_ps = ps;
+  x.mode = p->ws_lean ? 1 : 0;
+  x.dst = p->ws_lean ? S2 : S1;
+  x.out_ld = p->ws_lean ? ldt : ldx;
+  x.out_ps = pst;
+  int rc = launch_dst16_mode(x, st);
+  if (rc) return rc;
+  y.nrow = p->nx;
+  y.dst = S2;
+  y.out_ld = ldt;
+  y.out_ps = pst;
+  y.mode = p->ws_lean ? 0 : 2;
+  y.src = p->ws_lean ? S2 : S1;
+  y.in_ld = p->ws_lean ? ldt : ldx;
+  y.src_end = y.src + p->nz * pst;
+  y.in_ps = pst;
+  return launch_dst16_mode(y, st);
+}
+
+static int inverse_2d(hfb_plan* p, double* S2, double* out, cudaStream_t st) {
+  const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p);
+  const long long pst = fused_plane(p);
+  Dst16Call y = {};
+  y.tw = p->tw_y;
+  y.sn = p->sn_y;
+  y.scale = p->scale_y;
+  y.M = p->ny + 1;
+  y.nz = p->nz;
+  Dst16Call x = y;
+  x.tw = p->tw_x;
+  x.sn = p->sn_x;
+  x.scale = p->scale_x;
+  x.M = p->nx + 1;
+  y.mode = 0;
+  y.src = S2;
+  y.src_end = S2 + p->nz * pst;
+  y.nrow = p->nx;
+  y.in_ld = ldt;
+  y.in_ps = pst;
+  y.dst = S2;
+  y.out_ld = ldt;
+  y.out_ps = pst;
+  int rc = launch_dst16_mode(y, st);
+  if (rc) return rc;
+  x.mode = 2;
+  x.src = S2;
+  x.src_end = S2 + p->nz * pst;
+  x.nrow = p->ny;
+  x.in_ld = ldt;
+  x.in_ps = pst;
+  x.dst = out;
+  x.out_ld = p->nx;
+  x.out_ps = ps;
+  return launch_dst16_mode(x, st);
+}
+
+int solve_fused_z(hfb_plan* p, const double* rhs_re, const double* rhs_im, double* out_re,
+                  double* out_im, double* work, cudaStream_t st) {
+  const long long pst = fused_plane(p), ldt = tran_ld(p);
+  double* S1 = work;
+  double* Sr = p->ws_lean ? work : work + pst * p->nz;
+  double* Si = Sr + pst * p->nz;
+  double* CP = Si + pst * p->nz;
+  int rc;
+  if ((rc = forward_2d(p, rhs_re, S1, Sr, st))) return rc;
+  if ((rc = forward_2d(p, rhs_im, S1, Si, st))) return rc;
+  if ((rc = launch_thomas_tma_z(p, Sr, Si, CP, ldt, pst, st))) return rc;
+  if ((rc = inverse_2d(p, Sr, out_re, st))) return rc;
+  return inverse_2d(p, Si, out_im, st);
+}
+
 int transform_planes(hfb_plan* p, const double* src, double* dst, int z0, int z1, double* work,
                      cudaStream_t st) {
   const int nz = z1 - z0;

@@ -163,6 +163,80 @@ __global__ void residual_sq_kernel(const double* __restrict__ u, const double* _
   }
 }
 
+// Complex weights (complex k(z)): out = A ext or rhs - A ext with complex
+// arithmetic, each term w * v = (wr vr - wi vi, wr vi + wi vr) added in the
+// reference's order (assembly.py:229-244 on complex128).
+__global__ void apply27_z_kernel(const double* __restrict__ er, const double* __restrict__ ei,
+                                 const double* __restrict__ rr, const double* __restrict__ ri,
+                                 double* __restrict__ outr, double* __restrict__ outi,
+                                 const double* __restrict__ rawr, const double* __restrict__ rawi,
+                                 int nx, int ny, int nz, uint32_t mask, int mode) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y, l = blockIdx.z;
+  if (i >= nx) return;
+  const long long X = nx + 2, XY = (long long)(nx + 2) * (ny + 2);
+  double ar = 0.0, ai = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    const long long zb = (long long)(l + k) * XY;
+    for (int o = 0; o < 9; ++o) {
+      if (!(mask & (1u << (k * 9 + o)))) continue;
+      const long long w = (long long)l * 12 + k * 4 + c_off_w[o];
+      const double wr = __ldg(&rawr[w]), wi = __ldg(&rawi[w]);
+      const long long e = zb + (long long)(j + 1 + c_off_dj[o]) * X + (i + 1 + c_off_di[o]);
+      const double vr = __ldg(&er[e]), vi = __ldg(&ei[e]);
+      ar = DADD(ar, __dsub_rn(DMUL(wr, vr), DMUL(wi, vi)));
+      ai = DADD(ai, DADD(DMUL(wr, vi), DMUL(wi, vr)));
+    }
+  }
+  const long long o = ((long long)l * ny + j) * nx + i;
+  outr[o] = mode == 0 ? ar : __dsub_rn(rr[o], ar);
+  outi[o] = mode == 0 ? ai : __dsub_rn(ri[o], ai);
+}
+
+// |A u - F|^2 partial sums (complex), zero boundary, as residual_sq_kernel.
+__global__ void residual_sq_z_kernel(const double* __restrict__ ur, const double* __restrict__ ui,
+                                     const double* __restrict__ Fr, const double* __restrict__ Fi,
+                                     const double* __restrict__ rawr,
+                                     const double* __restrict__ rawi, int nx, int ny, int nz,
+                                     uint32_t mask, double* __restrict__ partial) {
+  __shared__ double red[256 / 32];
+  const long long n = (long long)nx * ny * nz;
+  double s = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % nx);
+    const int j = (int)((e / nx) % ny);
+    const int l = (int)(e / ((long long)nx * ny));
+    double ar = 0.0, ai = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const int ll = l + k - 1;
+      for (int o = 0; o < 9; ++o) {
+        if (!(mask & (1u << (k * 9 + o)))) continue;
+        const int ii = i + c_off_di[o], jj = j + c_off_dj[o];
+        double vr = 0.0, vi = 0.0;
+        if (ll >= 0 && ll < nz && jj >= 0 && jj < ny && ii >= 0 && ii < nx) {
+          const long long q = ((long long)ll * ny + jj) * nx + ii;
+          vr = ur[q];
+          vi = ui[q];
+        }
+        const long long w = (long long)l * 12 + k * 4 + c_off_w[o];
+        ar = DADD(ar, __dsub_rn(DMUL(rawr[w], vr), DMUL(rawi[w], vi)));
+        ai = DADD(ai, DADD(DMUL(rawr[w], vi), DMUL(rawi[w], vr)));
+      }
+    }
+    const double dr = ar - Fr[e], di = ai - Fi[e];
+    s = fma(dr, dr, fma(di, di, s));
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 256 / 32; ++w) t += red[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
 // slab (kpz, ny, nx) -> send blocks (kpz, kpy(q), nx), ascending q
 __global__ void pack_yblocks_kernel(const double* __restrict__ slab, double* __restrict__ send,
                                     int kpz, int ny, int nx, const int* __restrict__ ys,
@@ -324,6 +398,34 @@ extern "C" int hfb_unpack_yblocks(hfb_plan* p, const double* recv, double* slab,
   if (n == 0) return HFB_OK;
   unpack_yblocks_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
       recv, slab, kpz, p->ny, p->nx, p->ystarts, parts);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+extern "C" int hfb_apply27_z(hfb_plan* p, const double* ext_re, const double* ext_im,
+                             const double* rhs_re, const double* rhs_im, double* out_re,
+                             double* out_im, uint32_t mask, int mode, void* stream) {
+  if (!p || !ext_re || !ext_im || !out_re || !out_im) return HFB_ERR_ARGUMENT;
+  if (mode == 1 && (!rhs_re || !rhs_im)) return HFB_ERR_ARGUMENT;
+  if (!p->have_coef || !p->coef_i) return HFB_ERR_NO_COEFFICIENTS;
+  HFB_CUDA(cudaSetDevice(p->device));
+  dim3 grid((p->nx + 127) / 128, p->ny, p->nz);
+  apply27_z_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(
+      ext_re, ext_im, rhs_re, rhs_im, out_re, out_im, p->coef + 12LL * p->nz,
+      p->coef_i + 12LL * p->nz, p->nx, p->ny, p->nz, mask, mode);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+extern "C" int hfb_residual_sq_z(hfb_plan* p, const double* u_re, const double* u_im,
+                                 const double* rhs_re, const double* rhs_im, double* partial,
+                                 uint32_t mask, void* stream) {
+  if (!p || !u_re || !u_im || !rhs_re || !rhs_im || !partial) return HFB_ERR_ARGUMENT;
+  if (!p->have_coef || !p->coef_i) return HFB_ERR_NO_COEFFICIENTS;
+  HFB_CUDA(cudaSetDevice(p->device));
+  residual_sq_z_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+      u_re, u_im, rhs_re, rhs_im, p->coef + 12LL * p->nz, p->coef_i + 12LL * p->nz, p->nx,
+      p->ny, p->nz, mask, partial);
   HFB_LAUNCHED();
   return HFB_OK;
 }

@@ -287,6 +287,51 @@ def _solve_part_device(plan, t, grid, config, clock, part_idx):
     return (clock.seconds("t0" + tag, "t1" + tag), 0.0, 0.0)
 
 
+def _solve_z_device(plan, tr, ti, grid, config, clock):
+    """Complex-coefficient solve (complex k(z)) of the (re, im) pair in place."""
+    torch = dv._torch()
+    mode = config.mode
+    lib, h = plan.lib, plan.handle
+    st = plan.stream()
+    n_z, n_y, n_x = grid.shape
+
+    def transform(z0=0, z1=n_z):
+        work_t = plan.workspace(1)
+        for t in (tr, ti):
+            check(lib.hfb_transform_stack(h, ptr(t), z0, z1, ptr(work_t), st), "transform")
+
+    if isinstance(mode, Partitioned) or (isinstance(mode, Device) and mode.staged):
+        parts = mode.parts if isinstance(mode, Partitioned) else 1
+        ex = make_exchange_plan(grid, parts)
+        clock.mark("z0")
+        for z0, z1 in ex.partition.z_ranges:
+            transform(z0, z1)
+        clock.mark("z1")
+        slabs = [(tr[:, y0:y1, :].contiguous(), ti[:, y0:y1, :].contiguous())
+                 for y0, y1 in ex.partition.y_ranges]
+        clock.mark("z2")
+        for (y0, y1), (sr, si) in zip(ex.partition.y_ranges, slabs):
+            cpw = torch.empty((2,) + tuple(sr.shape), dtype=torch.float64, device=sr.device)
+            check(lib.hfb_solve_slab_z(h, ptr(sr), ptr(si), y1 - y0, y0, ptr(cpw), st),
+                  "solve_slab_z")
+        clock.mark("z3")
+        for (y0, y1), (sr, si) in zip(ex.partition.y_ranges, slabs):
+            tr[:, y0:y1, :] = sr
+            ti[:, y0:y1, :] = si
+        clock.mark("z4")
+        for z0, z1 in ex.partition.z_ranges:
+            transform(z0, z1)
+        clock.mark("z5")
+        return (clock.seconds("z0", "z1") + clock.seconds("z4", "z5"),
+                clock.seconds("z1", "z2") + clock.seconds("z3", "z4"),
+                clock.seconds("z2", "z3"))
+    work = plan.workspace(3)
+    clock.mark("z0")
+    check(lib.hfb_solve_z(h, ptr(tr), ptr(ti), ptr(tr), ptr(ti), ptr(work), st), "solve_z")
+    clock.mark("z1")
+    return (clock.seconds("z0", "z1"), 0.0, 0.0)
+
+
 def solve_discrete(rhs: Field3D, boundary: BoundaryData, scheme, profile: CoefficientProfile,
                    grid: Grid3D, config: SolverConfig = SolverConfig()):
     """Solve the 27-point system for a prebuilt (unfolded) right-hand side (solver.py:278-399).
@@ -316,11 +361,19 @@ def solve_discrete(rhs: Field3D, boundary: BoundaryData, scheme, profile: Coeffi
         setup_s = time.perf_counter() - t_start
         clock = _EventClock(torch, device)
         transform_s = exchange_s = tridiag_s = 0.0
-        for k, t in enumerate(parts):
-            tr, ex, tri = _solve_part_device(plan, t, grid, config, clock, k)
-            transform_s += tr
-            exchange_s += ex
-            tridiag_s += tri
+        if plan.complex_coef:
+            if on_device:
+                raise NotImplementedError("complex k(z) needs numpy (complex) fields")
+            while len(parts) < 2:
+                parts.append(torch.zeros_like(parts[0]))
+            transform_s, exchange_s, tridiag_s = _solve_z_device(plan, parts[0], parts[1],
+                                                                 grid, config, clock)
+        else:
+            for k, t in enumerate(parts):
+                tr, ex, tri = _solve_part_device(plan, t, grid, config, clock, k)
+                transform_s += tr
+                exchange_s += ex
+                tridiag_s += tri
         plan.fetch_status()
     if on_device:
         out = Field3D(parts[0])

@@ -282,14 +282,29 @@ def pivot_threshold(table, rtol=1e-14):
     return rtol * max(float(np.abs(t).max()) for t in table)
 
 
+def is_complex_table(table) -> bool:
+    """True when some weight has a non-zero imaginary part (complex k(z))."""
+    return any(np.iscomplexobj(t) and np.any(np.imag(t)) for t in table)
+
+
 def pack_table(table) -> np.ndarray:
-    """(A, B, C, D) -> the C-ABI layout table[l*12 + k*4 + {a,b,c,d}] (float64)."""
+    """(A, B, C, D) -> the C-ABI layout table[l*12 + k*4 + {a,b,c,d}] (float64).
+    Complex tables go through pack_table_z."""
     A, B, C, D = (np.asarray(t) for t in table)
-    if any(np.iscomplexobj(t) and np.any(np.imag(t)) for t in (A, B, C, D)):
-        raise NotImplementedError(
-            "complex coefficients (complex k(z)) are not supported by the fp64-real kernels yet")
+    if is_complex_table((A, B, C, D)):
+        raise ValueError("complex table: use pack_table_z")
     packed = np.stack([np.real(t).astype(np.float64) for t in (A, B, C, D)], axis=-1)
     return np.ascontiguousarray(packed.reshape(-1))
+
+
+def pack_table_z(table):
+    """Complex (A, B, C, D) -> (real parts, imaginary parts), each in the
+    pack_table layout (hfb_plan_set_coefficients_z)."""
+    A, B, C, D = (np.asarray(t, dtype=complex) for t in table)
+    re = np.stack([t.real for t in (A, B, C, D)], axis=-1)
+    im = np.stack([t.imag for t in (A, B, C, D)], axis=-1)
+    return (np.ascontiguousarray(re.reshape(-1), dtype=np.float64),
+            np.ascontiguousarray(im.reshape(-1), dtype=np.float64))
 
 
 def term_mask(table) -> int:

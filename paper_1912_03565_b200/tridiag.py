@@ -16,8 +16,8 @@ from . import _device as dv
 from ._native import check, get_plan, load_library, ptr
 from .errors import SingularSystemError
 from .grid import CoefficientProfile, Grid3D
-from .stencil import (coefficient_table, coefficients_for, eigenvalue, mode_cosines,
-                      pack_table, pivot_threshold)
+from .stencil import (coefficient_table, coefficients_for, eigenvalue, is_complex_table,
+                      mode_cosines, pack_table, pack_table_z, pivot_threshold)
 
 PIVOT_RTOL = 1e-14
 
@@ -84,13 +84,19 @@ def solve_system(system: SpectralSystem, rhs) -> np.ndarray:
 
 
 def device_coefficients(plan, scheme, profile, grid):
-    """Upload the row table + cosines of (scheme, profile, grid) to a DevicePlan."""
+    """Upload the row table + cosines of (scheme, profile, grid) to a DevicePlan
+    (a complex table — complex k(z) — as real and imaginary parts)."""
     table = coefficient_table(scheme, profile, grid)
-    packed = pack_table(table)
     cx, cy = mode_cosines(grid)
     thr = pivot_threshold(table, PIVOT_RTOL)
-    key = (packed.tobytes(), grid.n_x, grid.n_y, thr)
-    plan.set_coefficients(packed, cx, cy, thr, key=key)
+    if is_complex_table(table):
+        re, im = pack_table_z(table)
+        key = (re.tobytes(), im.tobytes(), grid.n_x, grid.n_y, thr)
+        plan.set_coefficients_z(re, im, cx, cy, thr, key=key)
+    else:
+        packed = pack_table(table)
+        key = (packed.tobytes(), grid.n_x, grid.n_y, thr)
+        plan.set_coefficients(packed, cx, cy, thr, key=key)
     return table
 
 
@@ -99,10 +105,25 @@ def _slab_device(t, scheme, profile, grid, m_start):
     plan = get_plan(grid.n_x, grid.n_y, grid.n_z, t.device)
     with plan.lock:
         device_coefficients(plan, scheme, profile, grid)
+        if plan.complex_coef:
+            raise NotImplementedError("complex k(z) needs complex values: pass a complex "
+                                      "numpy slab")
         torch = dv._torch()
         work = torch.empty((n_z, m_count, n_x), dtype=torch.float64, device=t.device)
         check(plan.lib.hfb_solve_slab(plan.handle, ptr(t), m_count, m_start, ptr(work),
                                       plan.stream()), "solve_slab")
+        plan.fetch_status()
+
+
+def _slab_device_z(tr, ti, scheme, profile, grid, m_start):
+    n_z, m_count, n_x = tr.shape
+    plan = get_plan(grid.n_x, grid.n_y, grid.n_z, tr.device)
+    with plan.lock:
+        device_coefficients(plan, scheme, profile, grid)
+        torch = dv._torch()
+        work = torch.empty((2, n_z, m_count, n_x), dtype=torch.float64, device=tr.device)
+        check(plan.lib.hfb_solve_slab_z(plan.handle, ptr(tr), ptr(ti), m_count, m_start,
+                                        ptr(work), plan.stream()), "solve_slab_z")
         plan.fetch_status()
 
 
@@ -118,6 +139,15 @@ def solve_slab(values, scheme, profile: CoefficientProfile, grid: Grid3D,
         return
     torch = dv._torch()
     dev = torch.device("cuda", torch.cuda.current_device())
+    if is_complex_table(coefficient_table(scheme, profile, grid)):
+        if not np.iscomplexobj(values):
+            raise TypeError("complex k(z) needs a complex slab")
+        tr = dv.upload(np.ascontiguousarray(values.real), dev)
+        ti = dv.upload(np.ascontiguousarray(values.imag), dev)
+        _slab_device_z(tr, ti, scheme, profile, grid, m_start)
+        values.real[...] = dv.download(tr)
+        values.imag[...] = dv.download(ti)
+        return
     parts = []
     for part in dv.real_parts(values):
         t = dv.upload(part, dev)

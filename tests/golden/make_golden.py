@@ -179,6 +179,59 @@ def main():
     except hf.SingularSystemError as exc:
         out["resonance"] = np.array([k2, exc.n, exc.m])
 
+    # ---- complex k(z): complex profiles, complex fields
+    def zsolve(F, bnd, scheme, prof, grid):
+        b = hf.BoundaryData.zero() if bnd is None else hf.BoundaryData.from_array(bnd)
+        u, _ = hf.solve_discrete(hf.Field3D(np.asarray(F, complex)), b, scheme, prof, grid)
+        return u.values.copy()
+
+    zlev = np.linspace(0.0, 1.0, 33)
+    k2z4 = 100.0 * (1 + 0.5 * np.sin(np.pi * zlev)) ** 2 * (1 + 0.3j)
+    pz4 = hf.CoefficientProfile(k2=k2z4, k2_z=np.zeros(33, complex), k2_zz=np.zeros(33, complex))
+    rz = np.random.default_rng(101)
+    Fz4 = rz.standard_normal((31, 31, 31)) + 1j * rz.standard_normal((31, 31, 31))
+    out["z4_k2"] = k2z4  # F regenerates from default_rng(101) in the tests
+    out["z4_table"] = np.stack(hf.coefficient_table(hf.SchemeKind.FOURTH_ORDER, pz4, g31))
+    out["z4_U"] = zsolve(Fz4, None, hf.SchemeKind.FOURTH_ORDER, pz4, g31)
+
+    s = 1 + 0.3 * np.sin(2 * np.pi * zlev)
+    sz = 0.6 * np.pi * np.cos(2 * np.pi * zlev)
+    szz = -1.2 * np.pi ** 2 * np.sin(2 * np.pi * zlev)
+    c6 = 1600.0 * (1 + 0.2j)
+    pz6 = hf.CoefficientProfile(k2=c6 * s ** 2, k2_z=c6 * 2 * s * sz,
+                                k2_zz=c6 * 2 * (sz ** 2 + s * szz))
+    rz = np.random.default_rng(102)
+    Fz6 = rz.standard_normal((31, 31, 31)) + 1j * rz.standard_normal((31, 31, 31))
+    out["z6_k2"], out["z6_k2z"], out["z6_k2zz"] = pz6.k2, pz6.k2_z, pz6.k2_zz
+    # F regenerates from default_rng(102) in the tests
+    out["z6_U"] = zsolve(Fz6, None, hf.SchemeKind.SIXTH_ORDER, pz6, g31)
+
+    # non-cubic, power-of-two line lengths, complex Dirichlet data, real F
+    gzb = ref_grid(0, (0.0, 1.0, 0.0, 2.0, 0.0, 0.5), (15, 31, 9))
+    rz = np.random.default_rng(103)
+    k2b = 30.0 * (rz.standard_normal(11) + 1j * rz.standard_normal(11))
+    pzb = hf.CoefficientProfile(k2=k2b, k2_z=np.zeros(11, complex), k2_zz=np.zeros(11, complex))
+    Fzb = rz.standard_normal((9, 31, 15))
+    Bzb = rz.standard_normal((11, 33, 17)) + 1j * rz.standard_normal((11, 33, 17))
+    out["zb_k2"], out["zb_F"], out["zb_B"] = k2b, Fzb, Bzb
+    out["zb_U"] = zsolve(Fzb, Bzb, hf.SchemeKind.SECOND_ORDER, pzb, gzb)
+
+    # generic (non-power-of-two) sizes, every scheme but cd4: random complex
+    # profiles, fields and boundary (the reference's dense-oracle criterion,
+    # test_acceptance.py:161-186)
+    gd = ref_grid(0, (0.0, math.pi, 0.0, math.pi, 0.0, math.pi), (6, 6, 6))
+    rz = np.random.default_rng(104)
+    for key in ("2", "4", "6"):
+        prof = hf.CoefficientProfile(k2=rz.standard_normal(8) + 1j * rz.standard_normal(8),
+                                     k2_z=rz.standard_normal(8) + 0j,
+                                     k2_zz=rz.standard_normal(8) + 0j)
+        F = rz.standard_normal((6, 6, 6)) + 1j * rz.standard_normal((6, 6, 6))
+        B = rz.standard_normal((8, 8, 8)) + 1j * rz.standard_normal((8, 8, 8))
+        out[f"zd{key}_k2"], out[f"zd{key}_k2z"], out[f"zd{key}_k2zz"] = \
+            prof.k2, prof.k2_z, prof.k2_zz
+        out[f"zd{key}_F"], out[f"zd{key}_B"] = F, B
+        out[f"zd{key}_U"] = zsolve(F, B, ref_scheme(key), prof, gd)
+
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {os.path.getsize(path) / 1e6:.2f} MB, {len(out)} arrays")

@@ -458,3 +458,83 @@ def test_lean_workspace_bitwise_equal_fast(cuda, shape):
     assert np.array_equal(outs[0], outs[1])
     ref = orc.solve(F.cpu().numpy(), oracle_table("4", prof, g), *orc.mode_cosines(nx, ny))
     assert rel_l2(outs[0], ref) < PARITY
+
+
+# ------------------------------------------------------ complex k(z) (f1)
+ZSCHEME = {"2": hb.SchemeKind.SECOND_ORDER, "4": hb.SchemeKind.FOURTH_ORDER,
+           "6": hb.SchemeKind.SIXTH_ORDER}
+ZCASES = [("z4", "4"), ("z6", "6"), ("zb", "2"), ("zd2", "2"), ("zd4", "4"), ("zd6", "6")]
+
+
+def z_inputs(golden, name):
+    from _zcases import z_case, z_grid
+    dom, (nx, ny, nz) = z_grid(name)
+    g = hb.make_grid(hb.Domain(*dom), nx, ny, nz)
+    k2 = golden[f"{name}_k2"]
+    prof = hb.CoefficientProfile(k2=k2, k2_z=golden.get(f"{name}_k2z", np.zeros_like(k2)),
+                                 k2_zz=golden.get(f"{name}_k2zz", np.zeros_like(k2)))
+    key = dict(ZCASES)[name]
+    F, B, T, cs = z_case(golden, name, key)
+    bnd = hb.BoundaryData.zero() if B is None else hb.BoundaryData.from_array(B)
+    return g, prof, ZSCHEME[key], F, bnd
+
+
+@pytest.mark.parametrize("name", [c for c, _ in ZCASES])
+def test_complex_k_solves_vs_reference(golden, cuda, name):
+    """Complex k(z) through solve_discrete: complex tables, complex z-solve
+    (fused power-of-two path and the generic dense-DST path), complex fold."""
+    g, prof, scheme, F, bnd = z_inputs(golden, name)
+    u, _ = hb.solve_discrete(hb.Field3D(F), bnd, scheme, prof, g)
+    assert np.iscomplexobj(u.values)
+    assert rel_l2(u.values, golden[f"{name}_U"]) < PARITY
+
+
+@pytest.mark.parametrize("mode", ["staged", "partitioned"])
+def test_complex_k_modes_agree(golden, cuda, mode):
+    g, prof, scheme, F, bnd = z_inputs(golden, "z4")
+    cfg = hb.SolverConfig(mode=hb.Device(staged=True) if mode == "staged"
+                          else hb.Partitioned(parts=3))
+    u, _ = hb.solve_discrete(hb.Field3D(F), bnd, scheme, prof, g, cfg)
+    assert rel_l2(u.values, golden["z4_U"]) < PARITY
+    if mode == "partitioned":
+        us, _ = hb.solve_discrete(hb.Field3D(F), bnd, scheme, prof, g,
+                                  hb.SolverConfig(mode=hb.Device(staged=True)))
+        assert np.array_equal(u.values, us.values)
+
+
+def test_complex_k_residual_fold_and_guards(golden, cuda):
+    g, prof, scheme, F, bnd = z_inputs(golden, "zb")
+    Ff = hb.fold_dirichlet(hb.Field3D(F), bnd, scheme, prof, g)
+    u, _ = hb.solve_discrete(hb.Field3D(F), bnd, scheme, prof, g)
+    res = hb.residual_l2(u, Ff, scheme, prof, g)
+    assert res < 1e-11 * np.linalg.norm(Ff.values)
+    # A u (with the boundary) reproduces the unfolded rhs
+    Au = hb.apply_stencil(u, bnd, scheme, prof, g)
+    assert rel_l2(Au.values, F) < 1e-12
+    # the real entry points refuse a complex table
+    plan = hb._native.get_plan(g.n_x, g.n_y, g.n_z, hb._native._torch().device("cuda", 0))
+    hb.tridiag.device_coefficients(plan, scheme, prof, g)
+    assert plan.complex_coef
+    import torch
+    t = torch.zeros(g.shape, dtype=torch.float64, device="cuda")
+    work = plan.workspace(0)
+    assert plan.lib.hfb_solve(plan.handle, hb._native.ptr(t), hb._native.ptr(t),
+                              hb._native.ptr(work), plan.stream()) == 1
+
+
+@pytest.mark.parametrize("n", [255, 511])
+def test_complex_k_large_vs_oracle(cuda, n):
+    """Fused complex z-solve at 255^3 / 511^3 (64-plane slab) against the oracle."""
+    planes = 64
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, (planes + 1) / (n + 1)), n, n, planes)
+    z = np.linspace(0, (planes + 1) / (n + 1), planes + 2)
+    prof = hb.CoefficientProfile(k2=(200.0 + 50.0j) * (1 + 0.3 * np.sin(6 * z)),
+                                 k2_z=np.zeros(planes + 2, complex),
+                                 k2_zz=np.zeros(planes + 2, complex))
+    rng = np.random.default_rng(n)
+    F = rng.standard_normal((planes, n, n)) + 1j * rng.standard_normal((planes, n, n))
+    u, _ = hb.solve_discrete(hb.Field3D(F), hb.BoundaryData.zero(), hb.SchemeKind.FOURTH_ORDER,
+                             prof, g)
+    T = orc.weight_table("4", prof.k2, prof.k2_z, prof.k2_zz, 0.0, (g.h_x, g.h_y, g.h_z), planes)
+    ref = orc.solve(F, T, *orc.mode_cosines(n, n), workers=8)
+    assert rel_l2(u.values, ref) < TOL

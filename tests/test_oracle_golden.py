@@ -151,3 +151,20 @@ def test_oracle_is_bit_exact_on_cfg1(golden):
     T, g = cfg1_table()
     U = orc.solve(wl.host_rhs(wl.workload(1)), T, *orc.mode_cosines(31, 31))
     assert np.array_equal(U, golden["cfg1_U"])
+
+
+# ------------------------------------------------------ complex k(z) (f1)
+from _zcases import oracle_fold, z_case  # noqa: E402
+def test_complex_table_bitwise(golden):
+    F, B, T, _ = z_case(golden, "z4", "4")
+    assert np.array_equal(np.stack(T), golden["z4_table"])
+
+
+@pytest.mark.parametrize("name,key", [("z4", "4"), ("z6", "6"), ("zb", "2"), ("zd2", "2"),
+                                      ("zd4", "4"), ("zd6", "6")])
+def test_complex_solves_match_reference(golden, name, key):
+    """Complex k(z): the oracle's complex Thomas (reciprocal form) against the
+    reference's complex division — same algorithm, roundoff-level agreement."""
+    F, B, T, cs = z_case(golden, name, key)
+    U = orc.solve(oracle_fold(F, B, T), T, *cs)
+    assert rel_l2(U, golden[f"{name}_U"]) < 1e-12
