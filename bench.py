@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", type=int, default=4)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--cpu-planes", type=int, default=None,
                     help="z-planes of the oracle CPU sample (default: all n for the "
                          "cpu_baseline, n/4 per step for --impl reference)")
@@ -294,20 +294,37 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         if not multi:
-            hin = torch.empty(F.shape, dtype=torch.float64, pin_memory=True)
-            hin.copy_(F)
-            hout = torch.empty_like(hin).pin_memory()
+            # two pinned (input, output) pairs, as a caller streaming right-hand sides
+            hins = [torch.empty(F.shape, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+            houts = [torch.empty(F.shape, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+            for h in hins:
+                h.copy_(F)
             status = _native.HfbStatus()
-            _native.check(lib.hfb_solve_host(plan.handle, _native.ptr(hin), _native.ptr(hout),
-                                             _native.ptr(work), st, ctypes.byref(status)), "e2e")
+            # latency of one synchronous call (H2D + solve + D2H)
+            _native.check(lib.hfb_solve_host(plan.handle, _native.ptr(hins[0]),
+                                             _native.ptr(houts[0]), _native.ptr(work), st,
+                                             ctypes.byref(status)), "e2e")
             t0 = time.perf_counter()
-            for _ in range(args.e2e_steps):
-                _native.check(lib.hfb_solve_host(plan.handle, _native.ptr(hin),
-                                                 _native.ptr(hout), _native.ptr(work), st,
-                                                 ctypes.byref(status)), "e2e")
+            _native.check(lib.hfb_solve_host(plan.handle, _native.ptr(hins[0]),
+                                             _native.ptr(houts[0]), _native.ptr(work), st,
+                                             ctypes.byref(status)), "e2e")
+            sync_s = time.perf_counter() - t0
+            # throughput of pipelined calls (H2D of step k+1 and D2H of step k-1
+            # overlap the solve of step k); every step still copies its input in
+            # and its result out
+            _native.check(lib.hfb_solve_host_async(plan.handle, _native.ptr(hins[0]),
+                                                   _native.ptr(houts[0]), _native.ptr(work),
+                                                   st), "e2e")
+            _native.check(lib.hfb_host_sync(plan.handle, ctypes.byref(status)), "e2e")
+            t0 = time.perf_counter()
+            for k in range(args.e2e_steps):
+                _native.check(lib.hfb_solve_host_async(plan.handle, _native.ptr(hins[k % 2]),
+                                                       _native.ptr(houts[k % 2]),
+                                                       _native.ptr(work), st), "e2e")
+            _native.check(lib.hfb_host_sync(plan.handle, ctypes.byref(status)), "e2e")
             e2e_s = (time.perf_counter() - t0) / args.e2e_steps
             nbytes = F.numel() * 8
-            del hin, hout
+            del hins, houts
         else:
             from paper_1912_03565_b200 import distributed as hd
             hin = F.cpu().pin_memory()
@@ -325,8 +342,11 @@ def run_ours(args):
             nbytes = F.numel() * 8
         e2e = {"value": points / e2e_s, "unit": "pts/s", "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "ms_per_step": e2e_s * 1e3,
-               "path": "C-ABI hfb_solve_host (pinned host buffers)" if not multi
+               "path": "C-ABI hfb_solve_host_async, pinned host buffers, "
+                       f"{args.e2e_steps} pipelined steps + hfb_host_sync" if not multi
                else "pinned H2D + solve_partitioned + D2H per rank"}
+        if not multi:
+            e2e["sync_ms_per_step"] = sync_s * 1e3  # one blocking hfb_solve_host call
 
     if rank != 0:
         if multi:

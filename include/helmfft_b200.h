@@ -153,6 +153,17 @@ int hfb_solve_host(hfb_plan* plan, const double* host_rhs, double* host_out, voi
 /* Synchronise `stream`, report (and clear) a latched singular pivot. */
 int hfb_status_fetch(hfb_plan* plan, void* stream, hfb_status* status);
 
+/* Pipelined host-buffer solves for many right-hand sides (serving / time
+ * stepping): each call enqueues H2D of host_rhs, the solve (on `stream`) and
+ * D2H into host_out, and returns without waiting. The H2D of the next call and
+ * the D2H of the previous one run on the plan's own copy streams while this
+ * one solves; two device volumes alternate. Host buffers must be pinned and
+ * stay untouched until hfb_host_sync, which waits for every pending call and
+ * reports a latched pivot failure like hfb_status_fetch. */
+int hfb_solve_host_async(hfb_plan* plan, const double* host_rhs, double* host_out, void* work,
+                         void* stream);
+int hfb_host_sync(hfb_plan* plan, hfb_status* status);
+
 /* Fourth-order RHS operator F = h_z^2 (f/2 + (1/12) sum of the 6 face
  * neighbours) of f sampled on the closed (n_z+2, n_y+2, n_x+2) grid.
  * Replaces the FOURTH_ORDER branch of assembly.build_rhs (assembly.py:183-193). */

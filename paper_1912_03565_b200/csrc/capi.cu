@@ -114,6 +114,20 @@ extern "C" int hfb_plan_destroy(hfb_plan* p) {
   cudaFree(p->err);
   cudaFree(p->ystarts);
   cudaFree(p->dev_io);
+  if (p->pipe) {
+    HostPipe* q = p->pipe;
+    cudaStreamSynchronize(q->h2d);
+    cudaStreamSynchronize(q->d2h);
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(q->buf[b]);
+      cudaEventDestroy(q->h2d_done[b]);
+      cudaEventDestroy(q->solved[b]);
+      cudaEventDestroy(q->d2h_done[b]);
+    }
+    cudaStreamDestroy(q->h2d);
+    cudaStreamDestroy(q->d2h);
+    delete q;
+  }
   std::free(p);
   return HFB_OK;
 }
@@ -383,4 +397,66 @@ extern "C" int hfb_solve_host(hfb_plan* p, const double* hin, double* hout, void
   if (rc) return rc;
   HFB_CUDA(cudaMemcpyAsync(hout, p->dev_io, bytes, cudaMemcpyDeviceToHost, st));
   return hfb_status_fetch(p, stream, s);
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined host solves: H2D of call k+1 and D2H of call k-1 run on their own
+// copy streams (separate copy engines) while call k solves on the caller's
+// stream; two device volumes alternate. Host buffers must be pinned and stay
+// valid until hfb_host_sync.
+static int host_pipe(hfb_plan* p, size_t bytes) {
+  if (p->pipe && p->pipe->bytes >= bytes) return HFB_OK;
+  if (p->pipe) {
+    HFB_CUDA(cudaStreamSynchronize(p->pipe->h2d));
+    HFB_CUDA(cudaStreamSynchronize(p->pipe->d2h));
+    for (int b = 0; b < 2; ++b) cudaFree(p->pipe->buf[b]);
+  } else {
+    p->pipe = new HostPipe();
+    HostPipe* q = p->pipe;
+    HFB_CUDA(cudaStreamCreateWithFlags(&q->h2d, cudaStreamNonBlocking));
+    HFB_CUDA(cudaStreamCreateWithFlags(&q->d2h, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      HFB_CUDA(cudaEventCreateWithFlags(&q->h2d_done[b], cudaEventDisableTiming));
+      HFB_CUDA(cudaEventCreateWithFlags(&q->solved[b], cudaEventDisableTiming));
+      HFB_CUDA(cudaEventCreateWithFlags(&q->d2h_done[b], cudaEventDisableTiming));
+      HFB_CUDA(cudaEventRecord(q->d2h_done[b], q->d2h));
+    }
+  }
+  HostPipe* q = p->pipe;
+  q->bytes = 0;
+  for (int b = 0; b < 2; ++b) HFB_CUDA(cudaMalloc(&q->buf[b], bytes));
+  q->bytes = bytes;
+  return HFB_OK;
+}
+
+extern "C" int hfb_solve_host_async(hfb_plan* p, const double* hin, double* hout, void* work,
+                                    void* stream) {
+  if (!p || !hin || !hout || !work) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = sizeof(double) * (size_t)p->nx * p->ny * p->nz;
+  int rc = host_pipe(p, bytes);
+  if (rc) return rc;
+  HostPipe* q = p->pipe;
+  const int b = q->next;
+  q->next ^= 1;
+  HFB_CUDA(cudaStreamWaitEvent(q->h2d, q->d2h_done[b], 0));
+  HFB_CUDA(cudaMemcpyAsync(q->buf[b], hin, bytes, cudaMemcpyHostToDevice, q->h2d));
+  HFB_CUDA(cudaEventRecord(q->h2d_done[b], q->h2d));
+  HFB_CUDA(cudaStreamWaitEvent(st, q->h2d_done[b], 0));
+  if ((rc = hfb_solve(p, q->buf[b], q->buf[b], work, stream))) return rc;
+  HFB_CUDA(cudaEventRecord(q->solved[b], st));
+  HFB_CUDA(cudaStreamWaitEvent(q->d2h, q->solved[b], 0));
+  HFB_CUDA(cudaMemcpyAsync(hout, q->buf[b], bytes, cudaMemcpyDeviceToHost, q->d2h));
+  HFB_CUDA(cudaEventRecord(q->d2h_done[b], q->d2h));
+  return HFB_OK;
+}
+
+extern "C" int hfb_host_sync(hfb_plan* p, hfb_status* s) {
+  if (!p) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  if (!p->pipe) return hfb_status_fetch(p, nullptr, s);
+  HFB_CUDA(cudaStreamSynchronize(p->pipe->h2d));
+  HFB_CUDA(cudaStreamSynchronize(p->pipe->d2h));
+  return hfb_status_fetch(p, p->pipe->d2h, s);
 }

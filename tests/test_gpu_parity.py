@@ -538,3 +538,33 @@ def test_complex_k_large_vs_oracle(cuda, n):
     T = orc.weight_table("4", prof.k2, prof.k2_z, prof.k2_zz, 0.0, (g.h_x, g.h_y, g.h_z), planes)
     ref = orc.solve(F, T, *orc.mode_cosines(n, n), workers=8)
     assert rel_l2(u.values, ref) < TOL
+
+
+def test_pipelined_host_solves_match_blocking(cuda):
+    """hfb_solve_host_async: several right-hand sides in flight (two device
+    volumes, copy streams) give exactly the blocking hfb_solve_host results."""
+    import ctypes
+    import torch
+    w = wl.workload(1)
+    n = w.n
+    plan = hb._native.get_plan(n, n, n, torch.device("cuda", 0))
+    hb.tridiag.device_coefficients(plan, w.scheme, w.profile, w.grid)
+    work = plan.workspace(0)
+    st = plan.stream()
+    rng = np.random.default_rng(5)
+    ins = [torch.from_numpy(rng.standard_normal((n, n, n))).pin_memory() for _ in range(5)]
+    outs = [torch.empty_like(x).pin_memory() for x in ins]
+    ref = [torch.empty_like(x).pin_memory() for x in ins]
+    status = hb._native.HfbStatus()
+    lib, ptr = plan.lib, hb._native.ptr
+    for x, r in zip(ins, ref):
+        hb._native.check(lib.hfb_solve_host(plan.handle, ptr(x), ptr(r), ptr(work), st,
+                                            ctypes.byref(status)), "host")
+    for x, o in zip(ins, outs):
+        hb._native.check(lib.hfb_solve_host_async(plan.handle, ptr(x), ptr(o), ptr(work), st),
+                         "async")
+    hb._native.check(lib.hfb_host_sync(plan.handle, ctypes.byref(status)), "sync")
+    for o, r in zip(outs, ref):
+        assert torch.equal(o, r)
+    T = oracle_table(w.scheme.value, w.profile, w.grid)
+    assert rel_l2(outs[3].numpy(), orc.solve(ins[3].numpy(), T, *orc.mode_cosines(n, n))) < 1e-12
