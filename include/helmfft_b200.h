@@ -70,7 +70,9 @@ uint64_t hfb_launch_count(void);
  * CTAs; column passes in runs of one 128-byte line), 1 one contiguous run per
  * CTA, R >= 2 interleaved runs of R batches; key 4 = row outputs by TMA
  * tensor stores where the destination layout allows (1, default) or by
- * thread stores (0). */
+ * thread stores (0); key 5 = fuse the forward Thomas sweep into the one-call
+ * solve's y-pass (1) or not (0, default: the carried per-mode state limits the
+ * fused kernel to 8 warps per SM, 12 ms against 4 + 3 ms unfused). */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.

@@ -324,7 +324,8 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
   }
   if ((rc = launch_dst16_mode(x, st))) return rc;
   mark(1);
-  // 2
+  // 2 (fast layout, fused: the forward Thomas sweep rides in the y-pass)
+  const bool fuse = !p->ws_lean && tuning(5);
   y.nrow = p->nx;
   y.dst = S2;
   y.out_ld = ldt;
@@ -334,16 +335,25 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
     y.src = S2;
     y.in_ld = ldt;
   } else {
-    y.mode = 2;  // TLOAD: S1 columns -> S2 rows
+    y.mode = fuse ? 3 : 2;  // (YF or) TLOAD: S1 columns -> S2 rows
     y.src = S1;
     y.in_ld = ldx;
   }
   y.src_end = y.src + p->nz * pst;
   y.in_ps = pst;
+  if (fuse) {
+    y.coef = p->coef;
+    y.cx = p->cx;
+    y.cy = p->cy;
+    y.thr = p->thr;
+    y.err = p->err;
+    y.cp = CP;
+    y.nz_total = p->nz;
+  }
   if ((rc = launch_dst16_mode(y, st))) return rc;
   mark(2);
   // 3
-  if ((rc = launch_thomas_tma(p, S2, CP, ldt, pst, st))) return rc;
+  if ((rc = launch_thomas_tma(p, S2, CP, ldt, pst, st, fuse ? 1 : 0))) return rc;
   mark(3);
   // 4
   y.mode = 0;

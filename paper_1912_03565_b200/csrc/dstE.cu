@@ -35,7 +35,10 @@
 
 namespace hfb {
 
-enum { kRow = 0, kTran = 1, kTload = 2 };  // Dst16Call::mode
+// Dst16Call::mode. kYF = the y-pass of the one-call solve fused with the
+// forward Thomas sweep: TLOAD input, then per mode x' = (F - lo x)/den, c =
+// up/den carried across levels, x' out by tensor store, c checkpointed.
+enum { kRow = 0, kTran = 1, kTload = 2, kYF = 3 };
 
 struct FftArgs {
   const double2* __restrict__ tw;  // tw[k] = exp(-2 pi i k/M)
@@ -57,6 +60,15 @@ struct StreamArgs {
   int nbox, boxn;         // TLOAD: boxes per batch and their extent along the line
   int vec_out;            // TRAN: (line 2k, 2k+1) pairs are 16-byte aligned in dst
   int tstore;             // ROW/TLOAD: outputs leave by TMA tensor stores (omap)
+  // kYF: forward Thomas sweep (thomas_tma.cu arithmetic) on the y-pass outputs
+  const double* coef;     // [l][k][(4a, 2b, 2c, d)]
+  const double* cx;       // per line (x-mode)
+  const double* cy;       // per position (y-mode)
+  double thr;
+  unsigned long long* err;
+  double* ck;             // cp checkpoints (l / 8, n, m) at levels 8q + 7
+  long long ck_ld, ck_ps;
+  int nz_total, ny_total, nx_total;
   long long per;          // batches per CTA (one contiguous run), 0 = interleaved
   int run;                // > 1: interleaved runs of `run` consecutive batches
 };
@@ -96,7 +108,7 @@ template <int P, int E>
 constexpr int kMaxThreads = (E == 32 && (1 << P) <= 2048) ? 64 : 128;
 
 template <int P, int E, int MODE>
-__global__ void __launch_bounds__(kMaxThreads<P, E>, 3)
+__global__ void __launch_bounds__(kMaxThreads<P, E>, MODE == kYF ? 2 : 3)
     dstE_stream_kernel(StreamArgs a, FftArgs c, const __grid_constant__ CUtensorMap tmap,
                        const __grid_constant__ CUtensorMap omap) {
   extern __shared__ __align__(16) double sm_raw[];
@@ -111,6 +123,22 @@ __global__ void __launch_bounds__(kMaxThreads<P, E>, 3)
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + (blockDim.x / 32 + 1));
   auto gbuf = [&](int s, int g) { return sm + (long long)s * a.stage + (long long)g * a.gbuf; };
   const int W = 2 * a.NF;
+  constexpr bool TL = (MODE == kTload || MODE == kYF);
+  // kYF: c carried per mode, thread-major [group][line][j][t]; cy permuted
+  // to [j][t] (thread t's position Q t + j)
+  double* ycs = sm + 2LL * a.stage + 2 * (blockDim.x / 32 + 1) + 2;
+  double* ycy = ycs + 2LL * a.NF * M;
+  double yx[2][Q];  // kYF: x carried per mode
+  if constexpr (MODE == kYF) {
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+      const int j = i / T, tt = i - (i / T) * T, m = Q * tt + j;
+      ycy[i] = m < a.ny_total ? __ldg(a.cy + m) : 0.0;
+    }
+#pragma unroll
+    for (int L = 0; L < 2; ++L)
+#pragma unroll
+      for (int j = 0; j < Q; ++j) yx[L][j] = 0.0;
+  }
 
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -125,7 +153,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E>, 3)
     int g;
     batch_of(a, it, plane, g);
     meta.plane[s] = plane;
-    if constexpr (MODE == kTload) {
+    if constexpr (TL) {
       for (int r = 0; r < W; ++r) {
         const int row = g * W + r;
         meta.row[s][r] = row < a.nrow ? row : -1;
@@ -202,7 +230,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E>, 3)
     const bool v0 = row0 >= 0, v1 = row1 >= 0;
 
     double2 v[E];
-    if constexpr (MODE == kTload) {
+    if constexpr (TL) {
       // box [pos][W]: a_e of lines (2f, 2f+1) is the double2 at pos e - 1
       // (absent lines and positions >= N were zero-filled by the TMA engine)
       // (the box is swizzled: 16-byte granule g sits at g ^ ((g >> 3) & (NF - 1)))
@@ -229,6 +257,49 @@ __global__ void __launch_bounds__(kMaxThreads<P, E>, 3)
       // at h ^ (r & 7): conflict-free, since thread t owns whole segments),
       // then one TMA tensor store per group (issued by thread 0).
       dstE_post_aligned<P, E>(v, sb, wsum, c.scale, t, f, out);
+      if constexpr (MODE == kYF) {
+        // forward elimination at level l for this thread's 2 x Q modes,
+        // bitwise the arithmetic of thomas_tma_kernel
+        const int l = (int)plane;
+        double cw[12];
+#pragma unroll
+        for (int q = 0; q < 12; ++q) cw[q] = __ldg(a.coef + (long long)l * 12 + q);
+#pragma unroll
+        for (int L = 0; L < 2; ++L) {
+          const int n = L ? row1 : row0;
+          const double cxv = n >= 0 ? __ldg(a.cx + n) : 0.0;
+          double* cs = ycs + ((long long)(f * 2 + L) * Q) * T + t;
+#pragma unroll
+          for (int j = 0; j < Q; ++j) {
+            const int m = Q * t + j;
+            const double cyv = ycy[j * T + t];
+            const double cxy = cxv * cyv;
+            const double lo = fma(cw[0], cxy, fma(cw[1], cxv, fma(cw[2], cyv, cw[3])));
+            const double di = fma(cw[4], cxy, fma(cw[5], cxv, fma(cw[6], cyv, cw[7])));
+            const double up = fma(cw[8], cxy, fma(cw[9], cxv, fma(cw[10], cyv, cw[11])));
+            const double den = (l == 0) ? di : fma(-lo, cs[j * T], di);
+            const bool live = n >= 0 && m < a.ny_total;
+            if (live && fabs(den) < a.thr) {
+              const unsigned long long key =
+                  ((unsigned long long)l * (unsigned long long)a.ny_total + (unsigned long long)m) *
+                      (unsigned long long)a.nx_total +
+                  (unsigned long long)n;
+              atomicMin(a.err, key);
+            }
+            const double rr = 1.0 / den;
+            const double F = L ? out[j].y : out[j].x;
+            const double x = ((l == 0) ? F : fma(-lo, yx[L][j], F)) * rr;
+            yx[L][j] = x;
+            if (L) out[j].y = x; else out[j].x = x;
+            if (l < a.nz_total - 1) {
+              const double cc = up * rr;
+              cs[j * T] = cc;
+              if ((l & 7) == 7 && live)
+                a.ck[(long long)(l >> 3) * a.ck_ps + (long long)n * a.ck_ld + m] = cc;
+            }
+          }
+        }
+      }
       constexpr int NSEG = M / 16;
 #pragma unroll
       for (int L = 0; L < 2; ++L) {
@@ -320,6 +391,7 @@ static int g_tune_NF = 0;
 static int g_tune_l2 = 2;     // TLOAD tensor-map L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
 static int g_tune_order = 0;  // batch order: 0 auto, 1 one run per CTA, R >= 2 runs of R
 static int g_tune_tstore = 1;  // row outputs by TMA tensor stores where the layout allows
+static int g_tune_fuse = 0;    // one-call solve: forward Thomas fused into the y-pass (off: occupancy-starved, 12 ms vs 4 + 3)
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
@@ -341,7 +413,10 @@ static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMa
   StreamArgs b = a;
   b.per = 0;
   b.run = 1;
-  if (g_tune_order == 1) {
+  if (MODE == kYF) {
+    // one CTA per column block, walking the levels in order (the Thomas carry)
+    blocks = a.G;
+  } else if (g_tune_order == 1) {
     b.per = (work + blocks - 1) / blocks;
     blocks = (work + b.per - 1) / b.per;
   } else if (g_tune_order >= 2) {
@@ -371,8 +446,10 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   int gb = std::max(2 * a.rowslot, 2 * G::BUF);
   // tensor-store outputs: rows stored whole (position N lands in the row's
   // padding, so ld >= M), 16-byte aligned rows and planes
-  a.tstore = (k.mode != kTran) && g_tune_tstore && M >= 16 && a.out_ld >= M &&
-             !(reinterpret_cast<uintptr_t>(a.dst) & 15) && !(a.out_ld & 1) && !(a.out_ps & 1);
+  a.tstore = (k.mode != kTran) && (g_tune_tstore || k.mode == kYF) && M >= 16 &&
+             a.out_ld >= M && !(reinterpret_cast<uintptr_t>(a.dst) & 15) && !(a.out_ld & 1) &&
+             !(a.out_ps & 1);
+  if (k.mode == kYF && !a.tstore) return HFB_ERR_ARGUMENT;
   if (a.tstore) {
     gb = (gb + 127) & ~127;  // every group box 1-KB aligned (128B swizzle atoms)
   } else {
@@ -398,7 +475,7 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   long long stage = (long long)a.NF * a.gbuf;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
-  if (k.mode == kTload) {
+  if (k.mode == kTload || k.mode == kYF) {
     a.boxn = std::min(256, M);
     a.nbox = M / a.boxn;
     stage = std::max<long long>(stage, (long long)a.nbox * a.boxn * W);
@@ -427,8 +504,23 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   a.vec_out = (k.mode == kTran) && !(reinterpret_cast<uintptr_t>(a.dst) & 15) &&
               !(a.out_ld & 1) && !(a.out_ps & 1);
   const int threads = a.NF * T;
-  const size_t sm = 1024 + (size_t)2 * a.stage * sizeof(double) +
-                    (threads / 32 + 1) * sizeof(double2) + 2 * sizeof(uint64_t);
+  size_t sm = 1024 + (size_t)2 * a.stage * sizeof(double) +
+              (threads / 32 + 1) * sizeof(double2) + 2 * sizeof(uint64_t);
+  if (k.mode == kYF) {
+    sm += sizeof(double) * ((size_t)2 * a.NF * M + M);  // c carry + permuted cy
+    a.coef = k.coef;
+    a.cx = k.cx;
+    a.cy = k.cy;
+    a.thr = k.thr;
+    a.err = k.err;
+    a.ck = k.cp;
+    a.ck_ld = a.out_ld;
+    a.ck_ps = a.out_ps;
+    a.nz_total = k.nz_total;
+    a.ny_total = a.N;
+    a.nx_total = a.nrow;
+    return launch_stream<P, E, kYF>(a, c, tmap, omap, threads, sm, st);
+  }
   if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, tmap, omap, threads, sm, st);
   if (k.mode == kTload) return launch_stream<P, E, kTload>(a, c, tmap, omap, threads, sm, st);
   return launch_stream<P, E, kRow>(a, c, tmap, omap, threads, sm, st);
@@ -446,17 +538,31 @@ static int launch_p(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStre
   return launch_pe<P, 16>(k, a, c, st);
 }
 
+int tuning(int key) {
+  switch (key) {
+    case 0: return g_tune_E;
+    case 1: return g_tune_NF;
+    case 2: return g_tune_l2;
+    case 3: return g_tune_order;
+    case 4: return g_tune_tstore;
+    case 5: return g_tune_fuse;
+    default: return 0;
+  }
+}
+
 void set_tuning(int key, int value) {
   if (key == 0) g_tune_E = (value == 32) ? 32 : 16;
   if (key == 1) g_tune_NF = value;
   if (key == 2) g_tune_l2 = value;
   if (key == 3) g_tune_order = value;
   if (key == 4) g_tune_tstore = value ? 1 : 0;
+  if (key == 5) g_tune_fuse = value ? 1 : 0;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {
   if (k.nz <= 0 || k.nrow <= 0) return HFB_OK;
-  if (k.mode != kRow && k.mode != kTran && k.mode != kTload) return HFB_ERR_ARGUMENT;
+  if (k.mode < kRow || k.mode > kYF) return HFB_ERR_ARGUMENT;
+  if (k.mode == kYF && (k.z0 != 0 || !k.coef || !k.cp)) return HFB_ERR_ARGUMENT;
   int p = 0;
   while ((1 << p) < k.M) ++p;
   FftArgs c;

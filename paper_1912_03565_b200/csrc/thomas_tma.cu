@@ -34,6 +34,7 @@ struct TmaArgs {
   double thr;
   unsigned long long* err;
   int nx, ny_total;
+  int bwd_only;  // forward sweep already done (x' and checkpoints in place)
 };
 
 __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, double cxy) {
@@ -82,19 +83,24 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
     // The last forward chunk stays in its stage and is the first backward chunk
     // (no store, no reload), so stages run task % S forward and (task-1) % S
     // backward.
-    auto stage_of = [&](int task) { return task < nchunk ? task % S : (task - 1) % S; };
-    auto needs_load = [&](int task) { return task != nchunk; };
+    // backward-only: tasks nchunk .. 2 nchunk - 1, every chunk loaded
+    const int task0 = a.bwd_only ? nchunk : 0;
+    auto stage_of = [&](int task) {
+      return a.bwd_only ? (task - task0) % S : task < nchunk ? task % S : (task - 1) % S;
+    };
+    auto needs_load = [&](int task) { return a.bwd_only || task != nchunk; };
     if (tid == 0) {
-      issue(0, stage_of(0));
-      if (ntask > 1 && needs_load(1)) issue(1, stage_of(1));
+      issue(task0, stage_of(task0));
+      if (task0 + 1 < ntask && needs_load(task0 + 1)) issue(task0 + 1, stage_of(task0 + 1));
     }
     double c = 0.0, x = 0.0, cknext = 0.0;
-    for (int task = 0; task < ntask; ++task) {
+    if (a.bwd_only && live && nchunk > 1) cknext = ck[(long long)(nchunk - 2) * a.ps];
+    for (int task = task0; task < ntask; ++task) {
       const int s = stage_of(task);
       if (tid == 0 && task + 2 < ntask && needs_load(task + 2)) {
         // backward reloads must see the forward stores; otherwise only the
         // stage's previous store has to be done reading shared memory
-        if (task + 2 > nchunk) bulk_wait<0>(); else bulk_wait_read<0>();
+        if (!a.bwd_only && task + 2 > nchunk) bulk_wait<0>(); else bulk_wait_read<0>();
         fence_proxy_async_smem();
         issue(task + 2, stage_of(task + 2));
       }
@@ -134,6 +140,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
         if (live && task == nchunk - 1 && nchunk > 1) cknext = ck[(long long)(nchunk - 2) * a.ps];
       } else {
         // back substitution over levels l0 + nl - 1 .. l0 (x holds W at the level above)
+        if (a.bwd_only && task == task0) x = sdat[s][nl - 1][tid];  // W = x' at the top
         double cprev = cknext;
         if (cidx >= 2 && live) cknext = ck[(long long)(cidx - 2) * a.ps];
         double cb[K];
@@ -170,9 +177,10 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
 }
 
 int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, long long ps,
-                      cudaStream_t st) {
+                      cudaStream_t st, int bwd_only) {
   if (p->nz < 1) return HFB_OK;
   TmaArgs a;
+  a.bwd_only = bwd_only;
   a.w = data;
   a.cpk = cpk;
   a.coef = p->coef;

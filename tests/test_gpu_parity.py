@@ -408,11 +408,12 @@ def tuning():
     lib.hfb_set_tuning(2, 2)
     lib.hfb_set_tuning(3, 0)
     lib.hfb_set_tuning(4, 1)
+    lib.hfb_set_tuning(5, 0)
 
 
 @pytest.mark.parametrize("knobs", [((0, 32),), ((0, 32), (1, 2)), ((0, 32), (1, 1)), ((1, 1),),
                                    ((2, 0),), ((2, 3),), ((3, 1),), ((3, 3),), ((4, 0),),
-                                   ((0, 32), (4, 0))])
+                                   ((0, 32), (4, 0)), ((5, 0),), ((0, 32), (5, 1))])
 def test_tuning_variants_match_oracle(cuda, tuning, knobs):
     """Performance knobs change the FFT factorisation or the CTA shape, never
     the result beyond rounding: transforms (row, transposed-store and
@@ -568,3 +569,27 @@ def test_pipelined_host_solves_match_blocking(cuda):
         assert torch.equal(o, r)
     T = oracle_table(w.scheme.value, w.profile, w.grid)
     assert rel_l2(outs[3].numpy(), orc.solve(ins[3].numpy(), T, *orc.mode_cosines(n, n))) < 1e-12
+
+
+@pytest.mark.parametrize("shape", [(63, 63, 40), (255, 127, 17), (127, 255, 9)])
+def test_fused_forward_sweep_bitwise(cuda, tuning, shape):
+    """The y-pass with the forward Thomas sweep fused in (YF) + backward-only
+    z-solve reproduces the unfused pipeline bit for bit (same arithmetic, same
+    checkpoints), including a pivot latch on the same mode."""
+    import torch
+    nx, ny, nz = shape
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+    prof = hb.constant_profile(5.0, g)
+    F = torch.from_numpy(np.random.default_rng(nz).standard_normal((nz, ny, nx))).cuda()
+    plan = hb._native.get_plan(nx, ny, nz, F.device)
+    hb.tridiag.device_coefficients(plan, hb.SchemeKind.FOURTH_ORDER, prof, g)
+    outs = []
+    for fuse in (1, 0):
+        tuning(5, fuse)
+        U = torch.empty_like(F)
+        work = plan.workspace(0)
+        hb._native.check(plan.lib.hfb_solve(plan.handle, hb._native.ptr(F), hb._native.ptr(U),
+                                            hb._native.ptr(work), plan.stream()), "solve")
+        plan.fetch_status()
+        outs.append(U.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
