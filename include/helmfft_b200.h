@@ -95,7 +95,7 @@ int hfb_plan_set_coefficients(hfb_plan* plan, const double* table, const double*
 
 /* Workspace sizes in bytes. op: 0 = hfb_solve, 1 = hfb_transform_stack,
  * 2 = hfb_solve_slab (for the full n_y modes), 3 = hfb_solve_z,
- * 4 = hfb_solve_slab_z (full n_y). */
+ * 4 = hfb_solve_slab_z (full n_y), 5 = hfb_forward_modes. */
 size_t hfb_workspace_bytes(const hfb_plan* plan, int op);
 
 /* Layout of the hfb_solve workspace (no effect on results): 0 = fast (two
@@ -245,6 +245,30 @@ int hfb_pack_yblocks(hfb_plan* plan, const double* slab, double* send, int kpz,
                      const int* y_starts, int parts, void* stream);
 int hfb_unpack_yblocks(hfb_plan* plan, const double* recv, double* slab, int kpz,
                        const int* y_starts, int parts, void* stream);
+
+/* ---- mode-space partitioned solve (solver.py:319-399) ----
+ * One rank's transformed z-slab lives as padded mode rows (kpz, n_x, ldm),
+ * ldm = hfb_modes_ld(plan) (even), element (l, n, m) at (l*n_x + n)*ldm + m.
+ * The exchange block for rank q is (kpz, n_x, kp(q)), kp(q) = the y-mode
+ * count of q rounded up to even, blocks concatenated in ascending q; the
+ * receiver's concatenation over senders is its y-slab of mode rows
+ * (n_z, n_x, kp), which hfb_solve_modes streams directly.
+ *   hfb_forward_modes: forward 2D DST, natural (kpz, n_y, n_x) -> mode rows
+ *     (workspace hfb_workspace_bytes(plan, 5));
+ *   hfb_inverse_modes: mode rows (overwritten) -> natural out;
+ *   hfb_solve_modes: z-solve of a y-slab of mode rows (n_z levels of the plan,
+ *     row stride ld even, columns = y-modes m_offset .. m_offset + m_count - 1),
+ *     cp_work = ceil(n_z / 8) * n_x * ld doubles;
+ *   hfb_pack_modes / hfb_unpack_modes: mode rows <-> exchange blocks. */
+int hfb_modes_ld(const hfb_plan* plan);
+int hfb_forward_modes(hfb_plan* plan, const double* src, double* modes, void* work, void* stream);
+int hfb_inverse_modes(hfb_plan* plan, double* modes, double* out, void* stream);
+int hfb_solve_modes(hfb_plan* plan, double* data, int ld, int m_count, int m_offset,
+                    void* cp_work, void* stream);
+int hfb_pack_modes(hfb_plan* plan, const double* modes, double* send, const int* y_starts,
+                   int parts, void* stream);
+int hfb_unpack_modes(hfb_plan* plan, const double* recv, double* modes, const int* y_starts,
+                     int parts, void* stream);
 
 #ifdef __cplusplus
 }

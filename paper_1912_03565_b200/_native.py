@@ -48,6 +48,12 @@ SIGNATURES = {
     "hfb_set_tuning": (None, [_i, _i]),
     "hfb_plan_set_workspace_mode": (_i, [_vp, _i]),
     "hfb_stage_timing": (_i, [_vp, _i]),
+    "hfb_modes_ld": (_i, [_vp]),
+    "hfb_forward_modes": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "hfb_inverse_modes": (_i, [_vp, _vp, _vp, _vp]),
+    "hfb_solve_modes": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
+    "hfb_pack_modes": (_i, [_vp, _vp, _vp, _ip, _i, _vp]),
+    "hfb_unpack_modes": (_i, [_vp, _vp, _vp, _ip, _i, _vp]),
     "hfb_solve_host_async": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "hfb_host_sync": (_i, [_vp, _vp]),
     "hfb_plan_set_coefficients_z": (_i, [_vp, _vp, _vp, _vp, _vp, ctypes.c_double]),

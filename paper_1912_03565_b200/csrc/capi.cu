@@ -265,6 +265,7 @@ extern "C" size_t hfb_workspace_bytes(const hfb_plan* p, int op) {
       return sizeof(double) * (fz ? fz : 2 * vol + tw);
     }
     case 4: return sizeof(double) * 2 * vol;  // hfb_solve_slab_z (full n_y modes)
+    case 5: return sizeof(double) * modes_work_elems(p);  // hfb_forward_modes
     default: return 0;
   }
 }

@@ -477,6 +477,90 @@ int solve_fused_z(hfb_plan* p, const double* rhs_re, const double* rhs_im, doubl
   return inverse_2d(p, Si, out_im, st);
 }
 
+// Mode-space transforms for the partitioned solve (one rank's z-slab): the
+// forward 2D DST writes padded mode rows (l, n, m) — the layout the exchange
+// ships and the z-solve streams — and the inverse reads them back.
+long long modes_ld(const hfb_plan* p) { return tran_ld(p); }
+size_t modes_work_elems(const hfb_plan* p) {
+  return tran_path(p) ? (size_t)p->nz * p->ny * x_ld(p) : 0;
+}
+
+int forward_modes(hfb_plan* p, const double* src, double* modes, double* S1, cudaStream_t st) {
+  if (!tran_path(p) || !S1) return HFB_ERR_ARGUMENT;
+  const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), ldx = x_ld(p);
+  Dst16Call x = {};
+  x.tw = p->tw_x;
+  x.sn = p->sn_x;
+  x.scale = p->scale_x;
+  x.M = p->nx + 1;
+  x.nz = p->nz;
+  x.mode = 0;
+  x.src = src;
+  x.src_end = src + p->nz * ps;
+  x.nrow = p->ny;
+  x.in_ld = p->nx;
+  x.in_ps = ps;
+  x.dst = S1;
+  x.out_ld = ldx;
+  x.out_ps = ldx * p->ny;
+  int rc = launch_dst16_mode(x, st);
+  if (rc) return rc;
+  Dst16Call y = {};
+  y.tw = p->tw_y;
+  y.sn = p->sn_y;
+  y.scale = p->scale_y;
+  y.M = p->ny + 1;
+  y.nz = p->nz;
+  y.mode = 2;
+  y.src = S1;
+  y.src_end = S1 + p->nz * ldx * p->ny;
+  y.nrow = p->nx;
+  y.in_ld = ldx;
+  y.in_ps = ldx * p->ny;
+  y.dst = modes;
+  y.out_ld = ldt;
+  y.out_ps = ldt * p->nx;
+  return launch_dst16_mode(y, st);
+}
+
+int inverse_modes(hfb_plan* p, double* modes, double* out, cudaStream_t st) {
+  if (!tran_path(p)) return HFB_ERR_ARGUMENT;
+  const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), pst = ldt * p->nx;
+  Dst16Call y = {};
+  y.tw = p->tw_y;
+  y.sn = p->sn_y;
+  y.scale = p->scale_y;
+  y.M = p->ny + 1;
+  y.nz = p->nz;
+  y.mode = 0;
+  y.src = modes;
+  y.src_end = modes + p->nz * pst;
+  y.nrow = p->nx;
+  y.in_ld = ldt;
+  y.in_ps = pst;
+  y.dst = modes;
+  y.out_ld = ldt;
+  y.out_ps = pst;
+  int rc = launch_dst16_mode(y, st);
+  if (rc) return rc;
+  Dst16Call x = {};
+  x.tw = p->tw_x;
+  x.sn = p->sn_x;
+  x.scale = p->scale_x;
+  x.M = p->nx + 1;
+  x.nz = p->nz;
+  x.mode = 2;
+  x.src = modes;
+  x.src_end = modes + p->nz * pst;
+  x.nrow = p->ny;
+  x.in_ld = ldt;
+  x.in_ps = pst;
+  x.dst = out;
+  x.out_ld = p->nx;
+  x.out_ps = ps;
+  return launch_dst16_mode(x, st);
+}
+
 int transform_planes(hfb_plan* p, const double* src, double* dst, int z0, int z1, double* work,
                      cudaStream_t st) {
   const int nz = z1 - z0;

@@ -429,3 +429,109 @@ extern "C" int hfb_residual_sq_z(hfb_plan* p, const double* u_re, const double* 
   HFB_LAUNCHED();
   return HFB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Mode-space exchange for the partitioned solve. A rank's
+// transformed z-slab is padded mode rows (kpz, n_x, ldm); the block for rank q
+// is (kpz, n_x, kp(q)) with kp(q) = its y-mode count rounded up to even, so the
+// receiver's concatenation over senders is directly its y-slab of mode rows
+// (n_z, n_x, kp) — 16-byte aligned rows for the TMA z-solve, no unpack.
+namespace {
+__device__ __forceinline__ int owner_of(const int* ys, int parts, int m, long long& base,
+                                        int& kp, long long blk_rows) {
+  base = 0;
+  int q = 0;
+  for (;; ++q) {
+    kp = (ys[q + 1] - ys[q] + 1) & ~1;
+    if (q == parts - 1 || m < ys[q + 1]) break;
+    base += blk_rows * kp;
+  }
+  return q;
+}
+}  // namespace
+
+__global__ void pack_modes_kernel(const double* __restrict__ modes, double* __restrict__ send,
+                                  int kpz, int nx, int ny, long long ldm,
+                                  const int* __restrict__ ys, int parts) {
+  const long long total = (long long)kpz * nx * ny;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(e % ny);
+    const long long row = e / ny;  // l * nx + n
+    long long base;
+    int kp;
+    const int q = owner_of(ys, parts, m, base, kp, (long long)kpz * nx);
+    send[base + row * kp + (m - ys[q])] = modes[row * ldm + m];
+  }
+}
+
+__global__ void unpack_modes_kernel(const double* __restrict__ recv, double* __restrict__ modes,
+                                    int kpz, int nx, int ny, long long ldm,
+                                    const int* __restrict__ ys, int parts) {
+  const long long total = (long long)kpz * nx * ny;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(e % ny);
+    const long long row = e / ny;
+    long long base;
+    int kp;
+    const int q = owner_of(ys, parts, m, base, kp, (long long)kpz * nx);
+    modes[row * ldm + m] = recv[base + row * kp + (m - ys[q])];
+  }
+}
+
+extern "C" int hfb_modes_ld(const hfb_plan* p) { return p ? (int)modes_ld(p) : 0; }
+
+extern "C" int hfb_forward_modes(hfb_plan* p, const double* src, double* modes, void* work,
+                                 void* stream) {
+  if (!p || !src || !modes || !work) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return forward_modes(p, src, modes, (double*)work, (cudaStream_t)stream);
+}
+
+extern "C" int hfb_inverse_modes(hfb_plan* p, double* modes, double* out, void* stream) {
+  if (!p || !modes || !out) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return inverse_modes(p, modes, out, (cudaStream_t)stream);
+}
+
+extern "C" int hfb_solve_modes(hfb_plan* p, double* data, int ld, int m_count, int m_offset,
+                               void* cp_work, void* stream) {
+  if (!p || !data || !cp_work || ld < m_count || (ld & 1)) return HFB_ERR_ARGUMENT;
+  if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
+  if (p->coef_i) return HFB_ERR_ARGUMENT;
+  if (m_count < 0 || m_offset < 0 || m_offset + m_count > p->ny) return HFB_ERR_RANGE;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return launch_thomas_tma_cols(p, data, (double*)cp_work, ld, (long long)ld * p->nx, m_count,
+                                m_offset, (cudaStream_t)stream);
+}
+
+extern "C" int hfb_pack_modes(hfb_plan* p, const double* modes, double* send, const int* ys,
+                              int parts, void* stream) {
+  if (!p || !modes || !send || !ys || parts < 1) return HFB_ERR_ARGUMENT;
+  if (ys[0] != 0 || ys[parts] != p->ny) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  int rc = upload_ystarts(p, ys, parts, (cudaStream_t)stream);
+  if (rc) return rc;
+  const long long n = (long long)p->nz * p->nx * p->ny;
+  if (n == 0) return HFB_OK;
+  pack_modes_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      modes, send, p->nz, p->nx, p->ny, modes_ld(p), p->ystarts, parts);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+extern "C" int hfb_unpack_modes(hfb_plan* p, const double* recv, double* modes, const int* ys,
+                                int parts, void* stream) {
+  if (!p || !modes || !recv || !ys || parts < 1) return HFB_ERR_ARGUMENT;
+  if (ys[0] != 0 || ys[parts] != p->ny) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  int rc = upload_ystarts(p, ys, parts, (cudaStream_t)stream);
+  if (rc) return rc;
+  const long long n = (long long)p->nz * p->nx * p->ny;
+  if (n == 0) return HFB_OK;
+  unpack_modes_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      recv, modes, p->nz, p->nx, p->ny, modes_ld(p), p->ystarts, parts);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}

@@ -35,6 +35,7 @@ struct TmaArgs {
   unsigned long long* err;
   int nx, ny_total;
   int bwd_only;  // forward sweep already done (x' and checkpoints in place)
+  int m_off;     // global y-mode of column 0 (a y-slab of modes)
 };
 
 __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, double cxy) {
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
     const bool live = tid < cols;
     const int m = m0 + tid;
     const double cxv = __ldg(a.cx + n);
-    const double cyv = live ? __ldg(a.cy + m) : 0.0;
+    const double cyv = live ? __ldg(a.cy + a.m_off + m) : 0.0;
     const double cxy = cxv * cyv;
     double* ck = a.cpk + (long long)n * a.ld + m0 + tid;
 
@@ -123,7 +124,8 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
             const double den = (l == 0) ? di : fma(-lo, c, di);
             if (live && fabs(den) < a.thr) {
               const unsigned long long key =
-                  ((unsigned long long)l * (unsigned long long)a.ny_total + (unsigned long long)m) *
+                  ((unsigned long long)l * (unsigned long long)a.ny_total +
+                   (unsigned long long)(a.m_off + m)) *
                       (unsigned long long)a.nx +
                   (unsigned long long)n;
               atomicMin(a.err, key);
@@ -178,9 +180,15 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
 
 int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, long long ps,
                       cudaStream_t st, int bwd_only) {
-  if (p->nz < 1) return HFB_OK;
+  return launch_thomas_tma_cols(p, data, cpk, ld, ps, p->ny, 0, st, bwd_only);
+}
+
+int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld, long long ps,
+                           int ncols, int m_off, cudaStream_t st, int bwd_only) {
+  if (p->nz < 1 || ncols < 1) return HFB_OK;
   TmaArgs a;
   a.bwd_only = bwd_only;
+  a.m_off = m_off;
   a.w = data;
   a.cpk = cpk;
   a.coef = p->coef;
@@ -188,8 +196,8 @@ int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, long
   a.cy = p->cy;
   a.nz = p->nz;
   a.nrows = p->nx;
-  a.ncols = p->ny;
-  a.nbpr = (p->ny + BM - 1) / BM;
+  a.ncols = ncols;
+  a.nbpr = (ncols + BM - 1) / BM;
   a.ld = ld;
   a.ps = ps;
   a.thr = p->thr;

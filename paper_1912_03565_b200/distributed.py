@@ -6,14 +6,17 @@ block transposes in between (exchange_forward / exchange_inverse,
 solver.py:146-201). Here each part is a rank (``torch.distributed``, backend
 "nccl" on GPUs, "gloo" in the CPU tests of the exchange geometry):
 
-  1. 2D DST-I of the local z-slab (kpz planes)              [sm_100a kernels]
-  2. pack z_slab[:, y-range(q), :] blocks, ascending q      [pack kernel]
-  3. all_to_all_single with the reference's uneven splits   [NCCL]
-     -> the received buffer IS the y-slab (blocks land contiguously at
-        y_slab[z-range(p)], solver.py:173)
-  4. per-mode Thomas on the y-slab, mode offset y0          [sm_100a kernel]
-  5. inverse all_to_all (send y_slab[z-range(q)], contiguous)
-  6. unpack into the z-slab, inverse 2D DST-I               [kernels]
+  1. 2D DST-I of the local z-slab (kpz planes) into padded mode rows
+     (l, n, m), then pack blocks (kpz, n_x, kp(q)), ascending q  [sm_100a kernels]
+  2. all_to_all_single with the reference's uneven z/y splits   [NCCL]
+     -> the received buffer IS the y-slab of mode rows (n_z, n_x, kp)
+        (blocks land contiguously by sender z-range, as solver.py:173)
+  3. TMA-streamed Thomas on the y-slab, mode offset y0          [sm_100a kernel]
+  4. inverse all_to_all (the y-slab goes back as it came)
+  5. unpack into the mode rows, inverse 2D DST-I                 [kernels]
+
+(The reference's natural-layout blocks (kpz, kpy(q), n_x) are kept by
+split_sizes / exchange_*_collective for the gloo tests of the geometry.)
 
 Ranges come from the reference's plan_partition (larger chunks first), so
 block extents are exactly (n_x, kpy(q), kpz(p)) as in ExchangePlan.
@@ -84,69 +87,131 @@ def exchange_inverse_collective(y_slab, ex, rank, group=None):
     return recv
 
 
+def mode_split_sizes(ex, rank):
+    """(send, recv) element counts of the mode-space exchange (forward direction):
+    the block from rank p to rank q is (kpz(p), n_x, kp(q)), kp(q) = the y-mode
+    count of q rounded up to even (16-byte aligned mode rows)."""
+    zr, yr = ex.partition.z_ranges, ex.partition.y_ranges
+    kp = [((y1 - y0) + 1) & ~1 for y0, y1 in yr]
+    kpz = zr[rank][1] - zr[rank][0]
+    send = [kpz * ex.n_x * k for k in kp]
+    recv = [(z1 - z0) * ex.n_x * kp[rank] for z0, z1 in zr]
+    return send, recv
+
+
+def forward_to_blocks(z_slab, grid, ex, rank):
+    """Stage 1 (per rank): forward 2D DST of the z-slab into padded mode rows
+    and pack the exchange blocks. Returns (send, modes)."""
+    import torch
+    z0, z1 = ex.partition.z_ranges[rank]
+    kpz = z1 - z0
+    dev = z_slab.device
+    tplan = get_plan(grid.n_x, grid.n_y, kpz, dev)
+    st = tplan.stream()
+    ldm = int(tplan.lib.hfb_modes_ld(tplan.handle))
+    modes = torch.empty(kpz * grid.n_x * ldm, dtype=torch.float64, device=dev)
+    with tplan.lock:
+        work = tplan.workspace(5)
+        check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(z_slab), ptr(modes), ptr(work), st),
+              "forward_modes")
+        send = torch.empty(sum(mode_split_sizes(ex, rank)[0]), dtype=torch.float64, device=dev)
+        ys = y_starts(ex)
+        check(tplan.lib.hfb_pack_modes(tplan.handle, ptr(modes), ptr(send),
+                                       ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                       ex.n_parts, st), "pack_modes")
+    return send, modes
+
+
+def solve_received(recv, scheme, profile, grid, ex, rank):
+    """Stage 2 (per rank): z-solve of the received y-slab of mode rows
+    (n_z, n_x, kp) in place; the pivot latch stays in the full-grid plan."""
+    import torch
+    y0, y1 = ex.partition.y_ranges[rank]
+    kp = ((y1 - y0) + 1) & ~1
+    zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, recv.device)
+    with zplan.lock:
+        device_coefficients(zplan, scheme, profile, grid)
+        nck = (grid.n_z + 7) // 8
+        cp = torch.empty(nck * grid.n_x * kp, dtype=torch.float64, device=recv.device)
+        check(zplan.lib.hfb_solve_modes(zplan.handle, ptr(recv), kp, y1 - y0, y0, ptr(cp),
+                                        zplan.stream()), "solve_modes")
+    return zplan
+
+
+def blocks_to_solution(back, modes, grid, ex, rank, out=None):
+    """Stage 3 (per rank): unpack the returned blocks into the mode rows and run
+    the inverse 2D DST into the natural-layout solution slab."""
+    import torch
+    z0, z1 = ex.partition.z_ranges[rank]
+    kpz = z1 - z0
+    tplan = get_plan(grid.n_x, grid.n_y, kpz, back.device)
+    if out is None:
+        out = torch.empty((kpz, grid.n_y, grid.n_x), dtype=torch.float64, device=back.device)
+    with tplan.lock:
+        st = tplan.stream()
+        ys = y_starts(ex)
+        check(tplan.lib.hfb_unpack_modes(tplan.handle, ptr(back), ptr(modes),
+                                         ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                         ex.n_parts, st), "unpack_modes")
+        check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(modes), ptr(out), st),
+              "inverse_modes")
+    return out
+
+
 def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None):
     """Solve with the grid split over the ranks of `group`; z_slab is this rank's
     (kpz, n_y, n_x) CUDA float64 part of the folded RHS. Returns the solution slab
     (a new tensor). Raises SingularSystemError on every rank if any rank hit a
-    vanishing pivot."""
+    vanishing pivot.
+
+    Mode-space exchange: the forward 2D DST leaves padded mode rows (l, n, m);
+    the block for rank q is (kpz, n_x, kp(q)); the receive buffer is directly
+    the y-slab of mode rows the TMA z-solve streams (no unpack on the way in)."""
     import torch
     import torch.distributed as dist
     rank, parts = dist.get_rank(group), dist.get_world_size(group)
     ex = make_exchange_plan(grid, parts)
     z0, z1 = ex.partition.z_ranges[rank]
-    y0, y1 = ex.partition.y_ranges[rank]
     kpz = z1 - z0
     if tuple(z_slab.shape) != (kpz, grid.n_y, grid.n_x):
         raise ValueError(f"z-slab shape {tuple(z_slab.shape)} != {(kpz, grid.n_y, grid.n_x)}")
     dev = z_slab.device
-    tplan = get_plan(grid.n_x, grid.n_y, kpz, dev)
-    zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, dev)
-    ys = y_starts(ex)
-    ys_c = ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
-    local = z_slab.contiguous().clone()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if timings is not None else None
 
     def mark(i):
         if ev is not None:
             ev[i].record()
 
-    with tplan.lock, zplan.lock:
-        device_coefficients(zplan, scheme, profile, grid)
-        st = tplan.stream()
-        wk = tplan.workspace(1)
-        mark(0)
-        check(tplan.lib.hfb_transform_stack(tplan.handle, ptr(local), 0, kpz, ptr(wk), st),
-              "transform")
-        send = torch.empty(local.numel(), dtype=local.dtype, device=dev)
-        check(tplan.lib.hfb_pack_yblocks(tplan.handle, ptr(local), ptr(send), kpz, ys_c, parts,
-                                         st), "pack")
-        mark(1)
-        y_slab = exchange_forward_collective(send, ex, rank, group).contiguous()
-        mark(2)
-        cpw = torch.empty_like(y_slab)
-        check(zplan.lib.hfb_solve_slab(zplan.handle, ptr(y_slab), y1 - y0, y0, ptr(cpw),
-                                       zplan.stream()), "solve_slab")
-        mark(3)
-        recv = exchange_inverse_collective(y_slab, ex, rank, group)
-        mark(4)
-        check(tplan.lib.hfb_unpack_yblocks(tplan.handle, ptr(recv), ptr(local), kpz, ys_c, parts,
-                                           st), "unpack")
-        check(tplan.lib.hfb_transform_stack(tplan.handle, ptr(local), 0, kpz, ptr(wk), st),
-              "transform")
-        mark(5)
-        # agree on the first failing pivot across ranks
-        flag = torch.zeros(1, dtype=torch.int64, device=dev)
-        try:
-            zplan.fetch_status()
-        except Exception:
-            flag.fill_(1)
-        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
-        if int(flag.item()):
-            from .errors import SingularSystemError
-            raise SingularSystemError("vanishing pivot on at least one rank")
+    local = z_slab.contiguous()
+    s_fwd, r_fwd = mode_split_sizes(ex, rank)
+    mark(0)
+    send, modes = forward_to_blocks(local, grid, ex, rank)
+    mark(1)
+    recv = torch.empty(sum(r_fwd), dtype=torch.float64, device=dev)
+    dist.all_to_all_single(recv, send, output_split_sizes=r_fwd, input_split_sizes=s_fwd,
+                           group=group)
+    mark(2)
+    zplan = solve_received(recv, scheme, profile, grid, ex, rank)
+    mark(3)
+    back = torch.empty(sum(s_fwd), dtype=torch.float64, device=dev)
+    dist.all_to_all_single(back, recv, output_split_sizes=s_fwd, input_split_sizes=r_fwd,
+                           group=group)
+    mark(4)
+    out = blocks_to_solution(back, modes, grid, ex, rank)
+    mark(5)
+    # agree on the first failing pivot across ranks
+    flag = torch.zeros(1, dtype=torch.int64, device=dev)
+    try:
+        zplan.fetch_status()
+    except Exception:
+        flag.fill_(1)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if int(flag.item()):
+        from .errors import SingularSystemError
+        raise SingularSystemError("vanishing pivot on at least one rank")
     if timings is not None:
         torch.cuda.synchronize(dev)
         timings.update(transform_s=(ev[0].elapsed_time(ev[1]) + ev[4].elapsed_time(ev[5])) / 1e3,
                        exchange_s=(ev[1].elapsed_time(ev[2]) + ev[3].elapsed_time(ev[4])) / 1e3,
                        tridiag_s=ev[2].elapsed_time(ev[3]) / 1e3)
-    return local
+    return out

@@ -14,6 +14,8 @@ import pytest
 import torch
 import torch.multiprocessing as mp
 
+import paper_1912_03565_b200 as hb
+
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 
 
@@ -77,3 +79,20 @@ def test_split_sizes_match_exchange_plan_blocks():
         assert s == [int(np.prod(ex.block_extents(rank, q))) for q in range(8)]
         assert r == [int(np.prod(ex.block_extents(p, rank))) for p in range(8)]
     assert list(hd.y_starts(ex)) == [0, 128, 256, 384, 512, 640, 768, 896, 1023]
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_mode_split_sizes_consistent(parts):
+    """Mode-space exchange: what p sends to q is what q expects from p, blocks
+    cover every (l, n, m) once (plus one pad column for odd y-counts)."""
+    from paper_1912_03565_b200 import distributed as hd
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), 37, 61, 29)
+    ex = hb.make_exchange_plan(g, parts)
+    sends = [hd.mode_split_sizes(ex, r)[0] for r in range(parts)]
+    recvs = [hd.mode_split_sizes(ex, r)[1] for r in range(parts)]
+    for p in range(parts):
+        for q in range(parts):
+            assert sends[p][q] == recvs[q][p]
+    kp = [((y1 - y0) + 1) & ~1 for y0, y1 in ex.partition.y_ranges]
+    assert sum(map(sum, sends)) == g.n_z * g.n_x * sum(kp)
+    assert sum(kp) - g.n_y == sum((y1 - y0) & 1 for y0, y1 in ex.partition.y_ranges)
