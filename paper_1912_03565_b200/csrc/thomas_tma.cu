@@ -19,7 +19,7 @@
 namespace hfb {
 
 namespace {
-constexpr int BM = 256;  // modes per CTA block = threads
+constexpr int BMAX = 256;  // modes per CTA block = threads (128 for narrow y-slabs)
 constexpr int K = kThomasChunk;  // levels per chunk
 constexpr int S = 3;     // ring stages
 
@@ -43,6 +43,7 @@ __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, 
 }
 }  // namespace
 
+template <int BM>
 __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
   extern __shared__ __align__(16) double dyn[];
   double(*sdat)[K][BM] = reinterpret_cast<double(*)[K][BM]>(dyn);
@@ -197,6 +198,8 @@ int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld,
   a.nz = p->nz;
   a.nrows = p->nx;
   a.ncols = ncols;
+  // narrow y-slabs (multi-GPU, P >= 8) would leave half of a 256-mode block idle
+  const int BM = ncols <= 128 ? 128 : BMAX;
   a.nbpr = (ncols + BM - 1) / BM;
   a.ld = ld;
   a.ps = ps;
@@ -205,15 +208,15 @@ int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld,
   a.nx = p->nx;
   a.ny_total = p->ny;
   const size_t sm = sizeof(double) * (size_t)S * (K * BM + K * 12);
-  HFB_CUDA(cudaFuncSetAttribute(thomas_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sm));
+  auto kern = BM == 128 ? thomas_tma_kernel<128> : thomas_tma_kernel<BMAX>;
+  HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 1, sms = 148, dev = 0;
-  HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, thomas_tma_kernel, BM, sm));
+  HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BM, sm));
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long work = (long long)a.nrows * a.nbpr;
   const long long blocks = std::min<long long>(work, (long long)sms * std::max(per_sm, 1));
-  thomas_tma_kernel<<<(unsigned)blocks, BM, sm, st>>>(a);
+  kern<<<(unsigned)blocks, BM, sm, st>>>(a);
   HFB_LAUNCHED();
   return HFB_OK;
 }

@@ -1,0 +1,55 @@
+"""Per-rank GPU time of the partitioned (multi-GPU) solve, measured on ONE GPU
+by running one rank's stages (no collective), plus the all-to-all volume per
+rank. A projection for P GPUs, not a multi-GPU measurement.
+
+    python tools/partition_estimate.py --cfg 4 --parts 2 4 8
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1912_03565_b200 as hb  # noqa: E402
+from paper_1912_03565_b200 import distributed as hd, workloads as wl  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cfg", type=int, default=4)
+ap.add_argument("--parts", type=int, nargs="+", default=[2, 4, 8])
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+w = wl.workload(a.cfg)
+g = w.grid
+dev = torch.device("cuda", 0)
+res = []
+for P in a.parts:
+    ex = hb.make_exchange_plan(g, P)
+    r = 0
+    z0, z1 = ex.partition.z_ranges[r]
+    F = torch.rand((z1 - z0, g.n_y, g.n_x), dtype=torch.float64, device=dev)
+    s_fwd, r_fwd = hd.mode_split_sizes(ex, r)
+    recv = torch.rand(sum(r_fwd), dtype=torch.float64, device=dev)  # stand-in y-slab
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    best = None
+    for _ in range(a.reps):
+        torch.cuda.synchronize()
+        ev[0].record()
+        send, modes = hd.forward_to_blocks(F, g, ex, r)
+        ev[1].record()
+        hd.solve_received(recv, w.scheme, w.profile, g, ex, r)
+        ev[2].record()
+        hd.blocks_to_solution(send, modes, g, ex, r)
+        ev[3].record()
+        torch.cuda.synchronize()
+        t = [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
+        best = t if best is None or sum(t) < sum(best) else best
+    a2a_bytes = 8 * (sum(s_fwd) - s_fwd[r])  # off-rank bytes each way
+    nvl_ms = 2 * a2a_bytes / 900e9 * 1e3  # both exchanges at 900 GB/s per direction
+    total = sum(best) + nvl_ms
+    res.append({"parts": P, "forward_pack_ms": best[0], "zsolve_ms": best[1],
+                "unpack_inverse_ms": best[2], "alltoall_bytes_each_way": a2a_bytes,
+                "nvlink_ms_at_900GBs": nvl_ms, "projected_ms": total,
+                "projected_pts_per_s": g.n_x * g.n_y * g.n_z / (total / 1e3)})
+print(json.dumps({"cfg": a.cfg, "projection_of_rank0": res}, indent=1))
