@@ -104,11 +104,17 @@ __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long
 
 // E = 16: up to 128 threads (two line pairs of M = 1024), 3 CTAs per SM;
 // E = 32: up to 64 threads (one warp per pair) and the full register budget.
-template <int P, int E>
-constexpr int kMaxThreads = (E == 32 && (1 << P) <= 2048) ? 64 : 128;
+// M = 2048 column/transposing passes: two line pairs per CTA (W = 4 lines,
+// 32-byte box rows and column chunks) at 256 threads, one CTA per SM.
+template <int P, int E, int MODE>
+constexpr int kMaxThreads = (E == 32 && (1 << P) <= 2048)                  ? 64
+                            : (E == 16 && P == 11 && MODE != kRow && MODE != kYF) ? 256
+                                                                                : 128;
+template <int P, int E, int MODE>
+constexpr int kMinBlocks = kMaxThreads<P, E, MODE> == 256 ? 1 : MODE == kYF ? 2 : 3;
 
 template <int P, int E, int MODE>
-__global__ void __launch_bounds__(kMaxThreads<P, E>, MODE == kYF ? 2 : 3)
+__global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MODE>))
     dstE_stream_kernel(StreamArgs a, FftArgs c, const __grid_constant__ CUtensorMap tmap,
                        const __grid_constant__ CUtensorMap omap) {
   extern __shared__ __align__(16) double sm_raw[];
@@ -432,7 +438,11 @@ template <int P, int E>
 static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStream_t st) {
   using G = FE<P, E>;
   constexpr int T = G::T, M = G::M;
-  int nf = std::max(1, std::min(kMaxThreads<P, E> / T, kMaxRows / 2));
+  const int maxt = k.mode == kTran    ? kMaxThreads<P, E, kTran>
+                   : k.mode == kTload ? kMaxThreads<P, E, kTload>
+                   : k.mode == kYF    ? kMaxThreads<P, E, kYF>
+                                      : kMaxThreads<P, E, kRow>;
+  int nf = std::max(1, std::min(maxt / T, kMaxRows / 2));
   if (g_tune_NF > 0) nf = std::max(1, std::min(g_tune_NF, nf));
   a.NF = 1;
   a.logNF = 0;
