@@ -190,9 +190,6 @@ int launch_thomas(hfb_plan* p, double* slab, int mloc, int m_off, double* cpw, c
                               0, st);
 }
 
-int launch_thomas_tran(hfb_plan* p, double* data, double* cpw, long long ld, cudaStream_t st) {
-  return launch_thomas_layout(p, data, cpw, p->nx, p->ny, ld, ld * p->nx, 0, 1, st);
-}
 
 }  // namespace hfb
 
