@@ -227,6 +227,20 @@ int hfb_solve_z(hfb_plan* plan, const double* rhs_re, const double* rhs_im, doub
 int hfb_solve_slab_z(hfb_plan* plan, double* re, double* im, int m_count, int m_offset,
                      void* work, void* stream);
 
+/* Complex right-hand sides (assembly.build_rhs with complex k^2 or complex
+ * gamma, assembly.py:195-224): fields_re / fields_im are arrays of the real and
+ * imaginary parts of the sampled fields, in the order of hfb_rhs_sixth
+ * (f, lap_f, d4_f, f_xxyy, f_xxzz, f_yyzz, f_z) or hfb_rhs_convdiff
+ * (f, f_xx, f_yy, f_z, f_zz); k2 / k2z are the interior-level profiles. */
+int hfb_rhs_sixth_z(hfb_plan* plan, const double* const* fields_re,
+                    const double* const* fields_im, const double* k2_re, const double* k2_im,
+                    const double* k2z_re, const double* k2z_im, double h2, double* F_re,
+                    double* F_im, void* stream);
+int hfb_rhs_convdiff_z(hfb_plan* plan, const double* const* fields_re,
+                       const double* const* fields_im, double hx2, double hy2, double hz2,
+                       double gamma_re, double gamma_im, double* F_re, double* F_im,
+                       void* stream);
+
 /* hfb_apply27 / hfb_residual_sq with the complex table: complex fields as
  * (re, im) pairs, each term w*v added in the reference's order. */
 int hfb_apply27_z(hfb_plan* plan, const double* ext_re, const double* ext_im,

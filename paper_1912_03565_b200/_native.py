@@ -49,6 +49,9 @@ SIGNATURES = {
     "hfb_plan_set_workspace_mode": (_i, [_vp, _i]),
     "hfb_stage_timing": (_i, [_vp, _i]),
     "hfb_modes_ld": (_i, [_vp]),
+    "hfb_rhs_sixth_z": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_double, _vp, _vp,
+                             _vp]),
+    "hfb_rhs_convdiff_z": (_i, [_vp, _vp, _vp] + [ctypes.c_double] * 5 + [_vp, _vp, _vp]),
     "hfb_forward_modes": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "hfb_inverse_modes": (_i, [_vp, _vp, _vp, _vp]),
     "hfb_solve_modes": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),

@@ -14,6 +14,7 @@ complex stays complex) or torch CUDA float64 tensors (device-resident
 pipelines; results stay on the device).
 """
 
+import ctypes
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -204,6 +205,41 @@ def build_rhs(scheme, source: SourceSpec, profile: CoefficientProfile, grid: Gri
         fields = [_sample(getattr(source, n), grid) for n in names]
     else:
         raise ValueError(f"build_rhs has no formula for scheme {scheme!r}")
+    def _imag(a):
+        a = np.asarray(a)
+        return np.iscomplexobj(a) and bool(np.any(a.imag))
+
+    zk = key == "6" and (_imag(profile.k2) or _imag(profile.k2_z))
+    zg = key == "cd4" and complex(profile.gamma).imag != 0
+    if zk or zg:
+        # complex coefficients: one complex combination (both parts at once)
+        with plan.lock:
+            st = plan.stream()
+            up = lambda a: dv.upload(np.ascontiguousarray(a, dtype=np.float64), dev)
+            re = [up(np.real(a)) for a in fields]
+            im = [up(np.imag(a)) if np.iscomplexobj(a) else torch.zeros_like(re[0])
+                  for a in fields]
+            pr = (ctypes.c_void_p * 7)(*[t.data_ptr() for t in re])
+            pi = (ctypes.c_void_p * 7)(*[t.data_ptr() for t in im])
+            outr = torch.empty(grid.shape, dtype=torch.float64, device=dev)
+            outi = torch.empty_like(outr)
+            if zk:
+                k = [np.asarray(profile.k2, complex)[1:-1], np.asarray(profile.k2_z, complex)[1:-1]]
+                kt = [up(k[0].real), up(k[0].imag), up(k[1].real), up(k[1].imag)]
+                check(plan.lib.hfb_rhs_sixth_z(plan.handle, pr, pi, *[ptr(t) for t in kt], hz2,
+                                               ptr(outr), ptr(outi), st), "rhs_sixth_z")
+            else:
+                g = complex(profile.gamma)
+                check(plan.lib.hfb_rhs_convdiff_z(plan.handle, pr, pi, grid.h_x**2, grid.h_y**2,
+                                                  hz2, g.real, g.imag, ptr(outr), ptr(outi), st),
+                      "rhs_convdiff_z")
+            outs = [outr, outi]
+    else:
+        outs = None
+    if outs is not None:
+        if keep_on_device:
+            raise NotImplementedError("complex sources cannot stay on the real device path")
+        return Field3D(dv.download(outs[0]) + 1j * dv.download(outs[1]))
     outs = []
     with plan.lock:
         for part in _split_all(fields):
@@ -223,8 +259,6 @@ def build_rhs(scheme, source: SourceSpec, profile: CoefficientProfile, grid: Gri
                                              ptr(k2z), hz2, ptr(out), st), "rhs_sixth")
             else:
                 gamma = complex(profile.gamma)
-                if gamma.imag:
-                    raise NotImplementedError("complex convection gamma is not supported yet")
                 check(plan.lib.hfb_rhs_convdiff(plan.handle, *[ptr(t) for t in ins],
                                                 grid.h_x**2, grid.h_y**2, hz2, gamma.real,
                                                 ptr(out), st), "rhs_convdiff")

@@ -85,6 +85,71 @@ __global__ void rhs_convdiff_kernel(const double* __restrict__ f, const double* 
   }
 }
 
+// Complex variants (complex k(z) / complex gamma, complex sources): the same
+// formulas in complex arithmetic with the reference's operation order —
+// real coefficients scale both parts, complex products are
+// (ar br - ai bi, ar bi + ai br).
+struct Fields7 {
+  const double* p[7];
+};
+
+__global__ void rhs_sixth_z_kernel(Fields7 fr, Fields7 fi, const double* __restrict__ k2r,
+                                   const double* __restrict__ k2i,
+                                   const double* __restrict__ k2zr,
+                                   const double* __restrict__ k2zi, double h2, long long plane,
+                                   long long n, double* __restrict__ Fr,
+                                   double* __restrict__ Fi) {
+  const double h4 = DMUL(h2, h2);
+  const double c1 = __ddiv_rn(h2, 12.0), c2 = __ddiv_rn(h4, 360.0), c3 = __ddiv_rn(h4, 90.0);
+  const double c4 = __ddiv_rn(h4, 20.0), c5 = __ddiv_rn(DMUL(h2, h4), 60.0);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long l = e / plane;
+    double out[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const Fields7& F = c ? fi : fr;  // f, lap, d4, fxxyy, fxxzz, fyyzz, fz
+      const double mixed = DADD(DADD(F.p[3][e], F.p[4][e]), F.p[5][e]);
+      double in = DADD(F.p[0][e], DMUL(c1, F.p[1][e]));
+      in = DADD(in, DMUL(c2, F.p[2][e]));
+      in = DADD(in, DMUL(c3, mixed));
+      out[c] = DMUL(h2, in);
+    }
+    // rhs -= (c4 k2) f ; rhs += (c5 k2z) fz
+    const double ar = DMUL(c4, k2r[l]), ai = DMUL(c4, k2i[l]);
+    const double f_r = fr.p[0][e], f_i = fi.p[0][e];
+    out[0] = __dsub_rn(out[0], __dsub_rn(DMUL(ar, f_r), DMUL(ai, f_i)));
+    out[1] = __dsub_rn(out[1], DADD(DMUL(ar, f_i), DMUL(ai, f_r)));
+    const double br = DMUL(c5, k2zr[l]), bi = DMUL(c5, k2zi[l]);
+    const double z_r = fr.p[6][e], z_i = fi.p[6][e];
+    out[0] = DADD(out[0], __dsub_rn(DMUL(br, z_r), DMUL(bi, z_i)));
+    out[1] = DADD(out[1], DADD(DMUL(br, z_i), DMUL(bi, z_r)));
+    Fr[e] = out[0];
+    Fi[e] = out[1];
+  }
+}
+
+__global__ void rhs_convdiff_z_kernel(Fields7 fr, Fields7 fi, double hx2, double hy2,
+                                      double hz2, double gr, double gi, long long n,
+                                      double* __restrict__ Fr, double* __restrict__ Fi) {
+  const double a = __ddiv_rn(hx2, 12.0), b = __ddiv_rn(hy2, 12.0), c = __ddiv_rn(hz2, 12.0);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    // fields: f, fxx, fyy, fz, fzz
+    const double zr = fr.p[3][e], zi = fi.p[3][e];
+    const double gzr = DADD(__dsub_rn(DMUL(gr, zr), DMUL(gi, zi)), fr.p[4][e]);
+    const double gzi = DADD(DADD(DMUL(gr, zi), DMUL(gi, zr)), fi.p[4][e]);
+    double inr = DADD(fr.p[0][e], DMUL(a, fr.p[1][e]));
+    double ini = DADD(fi.p[0][e], DMUL(a, fi.p[1][e]));
+    inr = DADD(inr, DMUL(b, fr.p[2][e]));
+    ini = DADD(ini, DMUL(b, fi.p[2][e]));
+    inr = DADD(inr, DMUL(c, gzr));
+    ini = DADD(ini, DMUL(c, gzi));
+    Fr[e] = DMUL(hz2, inr);
+    Fi[e] = DMUL(hz2, ini);
+  }
+}
+
 // 27-point operator on a closed box (assembly.py:229-244). Raw weights
 // (a, b, c, d) per level and offset, in the reference's term order:
 // for dl in (-1, 0, 1): for (di, dj) in _PLANE_OFFSETS (assembly.py:20-25).
@@ -532,6 +597,46 @@ extern "C" int hfb_unpack_modes(hfb_plan* p, const double* recv, double* modes, 
   if (n == 0) return HFB_OK;
   unpack_modes_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
       recv, modes, p->nz, p->nx, p->ny, modes_ld(p), p->ystarts, parts);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+extern "C" int hfb_rhs_sixth_z(hfb_plan* p, const double* const* fields_re,
+                               const double* const* fields_im, const double* k2_re,
+                               const double* k2_im, const double* k2z_re, const double* k2z_im,
+                               double h2, double* F_re, double* F_im, void* stream) {
+  if (!p || !fields_re || !fields_im || !k2_re || !k2_im || !k2z_re || !k2z_im || !F_re ||
+      !F_im)
+    return HFB_ERR_ARGUMENT;
+  Fields7 fr, fi;
+  for (int k = 0; k < 7; ++k) {
+    if (!fields_re[k] || !fields_im[k]) return HFB_ERR_ARGUMENT;
+    fr.p[k] = fields_re[k];
+    fi.p[k] = fields_im[k];
+  }
+  HFB_CUDA(cudaSetDevice(p->device));
+  const long long plane = (long long)p->nx * p->ny, n = plane * p->nz;
+  rhs_sixth_z_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      fr, fi, k2_re, k2_im, k2z_re, k2z_im, h2, plane, n, F_re, F_im);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+extern "C" int hfb_rhs_convdiff_z(hfb_plan* p, const double* const* fields_re,
+                                  const double* const* fields_im, double hx2, double hy2,
+                                  double hz2, double gamma_re, double gamma_im, double* F_re,
+                                  double* F_im, void* stream) {
+  if (!p || !fields_re || !fields_im || !F_re || !F_im) return HFB_ERR_ARGUMENT;
+  Fields7 fr = {}, fi = {};
+  for (int k = 0; k < 5; ++k) {
+    if (!fields_re[k] || !fields_im[k]) return HFB_ERR_ARGUMENT;
+    fr.p[k] = fields_re[k];
+    fi.p[k] = fields_im[k];
+  }
+  HFB_CUDA(cudaSetDevice(p->device));
+  const long long n = (long long)p->nx * p->ny * p->nz;
+  rhs_convdiff_z_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      fr, fi, hx2, hy2, hz2, gamma_re, gamma_im, n, F_re, F_im);
   HFB_LAUNCHED();
   return HFB_OK;
 }

@@ -232,6 +232,15 @@ def main():
         out[f"zd{key}_F"], out[f"zd{key}_B"] = F, B
         out[f"zd{key}_U"] = zsolve(F, B, ref_scheme(key), prof, gd)
 
+    # complex right-hand sides: 6th order with a complex profile, cd4 with a
+    # complex gamma (assembly.py:195-224 in complex arithmetic) — F and the solve
+    zr_src = ref_src
+    out["zr6_F"] = hf.build_rhs(hf.SchemeKind.SIXTH_ORDER, zr_src, pz6, g31).values
+    out["zr6_U"] = zsolve(out["zr6_F"], None, hf.SchemeKind.SIXTH_ORDER, pz6, g31)
+    pcdz = hf.constant_profile(0.0, g15, gamma=-1.5 + 0.5j)
+    out["zrcd_F"] = hf.build_rhs(hf.SchemeKind.CONVECTION_DIFFUSION_4, zr_src, pcdz, g15).values
+    out["zrcd_U"] = zsolve(out["zrcd_F"], None, hf.SchemeKind.CONVECTION_DIFFUSION_4, pcdz, g15)
+
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {os.path.getsize(path) / 1e6:.2f} MB, {len(out)} arrays")

@@ -683,3 +683,24 @@ def test_solve_partitioned_nccl_single_rank(cuda):
     p.join(300)
     assert p.exitcode == 0
     assert q.get(timeout=10) == 0.0
+
+
+def test_complex_rhs_sixth_and_convdiff_vs_reference(golden, cuda):
+    """build_rhs with a complex 6th-order profile and with a complex convection
+    gamma (row f3 with complex coefficients), then the complex solve."""
+    src = wl.manufactured_source()
+    g31 = wl.unit_grid(31)
+    prof6 = hb.CoefficientProfile(k2=golden["z6_k2"], k2_z=golden["z6_k2z"],
+                                  k2_zz=golden["z6_k2zz"])
+    F6 = hb.build_rhs(hb.SchemeKind.SIXTH_ORDER, src, prof6, g31)
+    assert np.iscomplexobj(F6.values)
+    assert np.abs(F6.values - golden["zr6_F"]).max() <= 1e-15 * np.abs(golden["zr6_F"]).max()
+    u6, _ = hb.solve_discrete(F6, hb.BoundaryData.zero(), hb.SchemeKind.SIXTH_ORDER, prof6, g31)
+    assert rel_l2(u6.values, golden["zr6_U"]) < PARITY
+    g15 = wl.unit_grid(15)
+    pcd = hb.constant_profile(0.0, g15, gamma=-1.5 + 0.5j)
+    Fcd = hb.build_rhs(hb.SchemeKind.CONVECTION_DIFFUSION_4, src, pcd, g15)
+    assert np.abs(Fcd.values - golden["zrcd_F"]).max() <= 1e-15 * np.abs(golden["zrcd_F"]).max()
+    ucd, _ = hb.solve_discrete(Fcd, hb.BoundaryData.zero(), hb.SchemeKind.CONVECTION_DIFFUSION_4,
+                               pcd, g15)
+    assert rel_l2(ucd.values, golden["zrcd_U"]) < PARITY
