@@ -72,7 +72,11 @@ uint64_t hfb_launch_count(void);
  * tensor stores where the destination layout allows (1, default) or by
  * thread stores (0); key 5 = fuse the forward Thomas sweep into the one-call
  * solve's y-pass (1) or not (0, default: the carried per-mode state limits the
- * fused kernel to 8 warps per SM, 12 ms against 4 + 3 ms unfused). */
+ * fused kernel to 8 warps per SM, 12 ms against 4 + 3 ms unfused); key 6 =
+ * overlap the z-solve with the y-passes on a second stream, halves of the
+ * x-modes (1) or not (0, default: the CTA caps that make room for both cost
+ * more than the overlap gains, 22.5 vs 21.7 ms at 1023^3), keys 7 / 8 = those
+ * caps (CTAs per SM of the y-passes / of the z-solve). */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.

@@ -101,6 +101,11 @@ extern "C" int hfb_plan_destroy(hfb_plan* p) {
   if (!p) return HFB_OK;
   cudaSetDevice(p->device);
   stage_events_free(p);
+  if (p->ov_stream) {
+    cudaStreamSynchronize(p->ov_stream);
+    cudaStreamDestroy(p->ov_stream);
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(p->ov_ev[i]);
+  }
   cudaFree(p->tw_x);
   cudaFree(p->sn_x);
   cudaFree(p->tw_y);

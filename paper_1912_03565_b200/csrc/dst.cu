@@ -350,18 +350,70 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
     y.cp = CP;
     y.nz_total = p->nz;
   }
-  if ((rc = launch_dst16_mode(y, st))) return rc;
-  mark(2);
-  // 3
-  if ((rc = launch_thomas_tma(p, S2, CP, ldt, pst, st, fuse ? 1 : 0))) return rc;
-  mark(3);
-  // 4
-  y.mode = 0;
-  y.src = S2;
-  y.src_end = S2 + p->nz * pst;
-  y.in_ld = ldt;
-  if ((rc = launch_dst16_mode(y, st))) return rc;
-  mark(4);
+  // Overlapped schedule (fast layout, unfused): halves of the x-modes n.
+  //   st: y-pass n < h | y-pass n >= h (2 CTAs/SM) | . | inverse y n < h (2/SM) | n >= h
+  //   B :              | z-solve n < h (1 CTA/SM)  | z-solve n >= h (1/SM)     |
+  // The HBM-bound z-solve shares the GPU with the L1-bound y-passes.
+  const bool overlap = !p->ws_lean && !fuse && tuning(6) && p->nx >= 64;
+  if (overlap) {
+    if (!p->ov_stream) {
+      HFB_CUDA(cudaStreamCreateWithFlags(&p->ov_stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 4; ++i)
+        HFB_CUDA(cudaEventCreateWithFlags(&p->ov_ev[i], cudaEventDisableTiming));
+    }
+    const int h = (p->nx / 2) & ~7;  // a multiple of every line block (4 lines)
+    const int cap_dst = tuning(7), cap_th = tuning(8);
+    cudaStream_t sb = p->ov_stream;
+    Dst16Call ya = y, yb = y;
+    ya.line0 = 0;
+    ya.line1 = h;
+    yb.line0 = h;
+    yb.line1 = p->nx;
+    yb.max_per_sm = cap_dst;
+    if ((rc = launch_dst16_mode(ya, st))) return rc;
+    HFB_CUDA(cudaEventRecord(p->ov_ev[0], st));
+    if ((rc = launch_dst16_mode(yb, st))) return rc;
+    HFB_CUDA(cudaEventRecord(p->ov_ev[1], st));
+    mark(2);
+    HFB_CUDA(cudaStreamWaitEvent(sb, p->ov_ev[0], 0));
+    if ((rc = launch_thomas_tma_cols(p, S2, CP, ldt, pst, p->ny, 0, sb, 0, 0, h, cap_th)))
+      return rc;
+    HFB_CUDA(cudaEventRecord(p->ov_ev[2], sb));
+    HFB_CUDA(cudaStreamWaitEvent(sb, p->ov_ev[1], 0));
+    if ((rc = launch_thomas_tma_cols(p, S2, CP, ldt, pst, p->ny, 0, sb, 0, h, p->nx, cap_th)))
+      return rc;
+    HFB_CUDA(cudaEventRecord(p->ov_ev[3], sb));
+    y.mode = 0;
+    y.src = S2;
+    y.src_end = S2 + p->nz * pst;
+    y.in_ld = ldt;
+    ya = y;
+    yb = y;
+    ya.line0 = 0;
+    ya.line1 = h;
+    ya.max_per_sm = cap_dst;
+    yb.line0 = h;
+    yb.line1 = p->nx;
+    HFB_CUDA(cudaStreamWaitEvent(st, p->ov_ev[2], 0));
+    if ((rc = launch_dst16_mode(ya, st))) return rc;
+    HFB_CUDA(cudaStreamWaitEvent(st, p->ov_ev[3], 0));
+    mark(3);
+    if ((rc = launch_dst16_mode(yb, st))) return rc;
+    mark(4);
+  } else {
+    if ((rc = launch_dst16_mode(y, st))) return rc;
+    mark(2);
+    // 3
+    if ((rc = launch_thomas_tma(p, S2, CP, ldt, pst, st, fuse ? 1 : 0))) return rc;
+    mark(3);
+    // 4
+    y.mode = 0;
+    y.src = S2;
+    y.src_end = S2 + p->nz * pst;
+    y.in_ld = ldt;
+    if ((rc = launch_dst16_mode(y, st))) return rc;
+    mark(4);
+  }
   // 5
   x.mode = 2;
   x.src = S2;

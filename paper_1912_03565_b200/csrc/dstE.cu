@@ -69,6 +69,8 @@ struct StreamArgs {
   double* ck;             // cp checkpoints (l / 8, n, m) at levels 8q + 7
   long long ck_ld, ck_ps;
   int nz_total, ny_total, nx_total;
+  int g0;                 // first line block of this launch
+  int max_per_sm;         // cap on resident CTAs per SM (0 = occupancy)
   long long per;          // batches per CTA (one contiguous run), 0 = interleaved
   int run;                // > 1: interleaved runs of `run` consecutive batches
 };
@@ -98,7 +100,7 @@ __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long
   }
   if (b >= (long long)a.nz * a.G) return false;
   plane = a.z0 + b / a.G;
-  g = (int)(b % a.G);
+  g = a.g0 + (int)(b % a.G);
   return true;
 }
 
@@ -397,6 +399,9 @@ static int g_tune_NF = 0;
 static int g_tune_l2 = 2;     // TLOAD tensor-map L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
 static int g_tune_order = 0;  // batch order: 0 auto, 1 one run per CTA, R >= 2 runs of R
 static int g_tune_tstore = 1;  // row outputs by TMA tensor stores where the layout allows
+static int g_tune_overlap = 0;  // overlapped z-solve / y-pass schedule (key 6)
+static int g_tune_cap_dst = 2;  // its CTA caps per SM: y-passes (key 7), z-solve (key 8)
+static int g_tune_cap_th = 1;
 static int g_tune_fuse = 0;    // one-call solve: forward Thomas fused into the y-pass (off: occupancy-starved, 12 ms vs 4 + 3)
 
 template <int P, int E, int MODE>
@@ -408,6 +413,7 @@ static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMa
                                 cudaSharedmemCarveoutMaxShared));
   int per_sm = 1;
   HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, sm));
+  if (a.max_per_sm > 0) per_sm = std::min(per_sm, a.max_per_sm);
   if (getenv("HFB_DEBUG"))
     fprintf(stderr, "dstE<P=%d,E=%d,mode=%d>: %d threads, %zu B smem, %d CTAs/SM\n", P, E, MODE,
             threads, sm, per_sm);
@@ -452,6 +458,13 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   }
   const int W = 2 * a.NF;
   a.G = (a.ppp + a.NF - 1) / a.NF;
+  a.g0 = 0;
+  if (k.line1 > k.line0) {  // a sub-range of line blocks
+    if (k.line0 % W || (k.line1 % W && k.line1 != a.nrow)) return HFB_ERR_ARGUMENT;
+    a.g0 = k.line0 / W;
+    a.G = (k.line1 + W - 1) / W - a.g0;
+  }
+  a.max_per_sm = k.max_per_sm;
   a.rowslot = ((a.N + 4) + 1) & ~1;
   int gb = std::max(2 * a.rowslot, 2 * G::BUF);
   // tensor-store outputs: rows stored whole (position N lands in the row's
@@ -556,6 +569,9 @@ int tuning(int key) {
     case 3: return g_tune_order;
     case 4: return g_tune_tstore;
     case 5: return g_tune_fuse;
+    case 6: return g_tune_overlap;
+    case 7: return g_tune_cap_dst;
+    case 8: return g_tune_cap_th;
     default: return 0;
   }
 }
@@ -567,6 +583,9 @@ void set_tuning(int key, int value) {
   if (key == 3) g_tune_order = value;
   if (key == 4) g_tune_tstore = value ? 1 : 0;
   if (key == 5) g_tune_fuse = value ? 1 : 0;
+  if (key == 6) g_tune_overlap = value ? 1 : 0;
+  if (key == 7) g_tune_cap_dst = value;
+  if (key == 8) g_tune_cap_th = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

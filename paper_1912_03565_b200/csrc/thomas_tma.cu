@@ -36,6 +36,7 @@ struct TmaArgs {
   int nx, ny_total;
   int bwd_only;  // forward sweep already done (x' and checkpoints in place)
   int m_off;     // global y-mode of column 0 (a y-slab of modes)
+  int row0;      // first row (x-mode) of this launch
 };
 
 __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, double cxy) {
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
   uint32_t phase = 0;  // bit s: parity of stage s
 
   for (long long blk = blockIdx.x; blk < (long long)a.nrows * a.nbpr; blk += gridDim.x) {
-    const int n = (int)(blk / a.nbpr);
+    const int n = a.row0 + (int)(blk / a.nbpr);
     const int m0 = (int)(blk % a.nbpr) * BM;
     const int cols = min(BM, a.ncols - m0);
     const uint32_t rowbytes = (uint32_t)(((cols + 1) & ~1) * 8);  // ld is even
@@ -185,18 +186,21 @@ int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, long
 }
 
 int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld, long long ps,
-                           int ncols, int m_off, cudaStream_t st, int bwd_only) {
-  if (p->nz < 1 || ncols < 1) return HFB_OK;
+                           int ncols, int m_off, cudaStream_t st, int bwd_only, int row0,
+                           int row1, int max_per_sm) {
+  if (row1 < 0) row1 = p->nx;
+  if (p->nz < 1 || ncols < 1 || row1 <= row0) return HFB_OK;
   TmaArgs a;
   a.bwd_only = bwd_only;
   a.m_off = m_off;
+  a.row0 = row0;
   a.w = data;
   a.cpk = cpk;
   a.coef = p->coef;
   a.cx = p->cx;
   a.cy = p->cy;
   a.nz = p->nz;
-  a.nrows = p->nx;
+  a.nrows = row1 - row0;
   a.ncols = ncols;
   // narrow y-slabs (multi-GPU, P >= 8) would leave half of a 256-mode block idle
   const int BM = ncols <= 128 ? 128 : BMAX;
@@ -212,6 +216,7 @@ int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld,
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 1, sms = 148, dev = 0;
   HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BM, sm));
+  if (max_per_sm > 0) per_sm = std::min(per_sm, max_per_sm);
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long work = (long long)a.nrows * a.nbpr;
