@@ -706,3 +706,26 @@ def test_complex_rhs_sixth_and_convdiff_vs_reference(golden, cuda):
     ucd, _ = hb.solve_discrete(Fcd, hb.BoundaryData.zero(), hb.SchemeKind.CONVECTION_DIFFUSION_4,
                                pcd, g15)
     assert rel_l2(ucd.values, golden["zrcd_U"]) < PARITY
+
+
+@pytest.mark.parametrize("shape", [(15, 15, 1), (15, 31, 2), (31, 15, 9), (4095, 15, 3),
+                                   (15, 4095, 3), (2047, 63, 4), (63, 2047, 17), (127, 127, 65)])
+@pytest.mark.parametrize("lean", [0, 1])
+def test_one_call_edge_shapes_vs_oracle(cuda, shape, lean):
+    """One-call solve (fast and lean layouts) at the edges of the engine: the
+    smallest power-of-two lines (M = 16), M = 4096 (E = 32), M = 2048 (wide CTAs),
+    1 and 2 levels, partial checkpoint chunks."""
+    import torch
+    nx, ny, nz = shape
+    g = hb.make_grid(hb.Domain(0, 1, 0, 2, 0, 0.5), nx, ny, nz)
+    prof = hb.constant_profile(7.0, g)
+    F = np.random.default_rng(nx * 7 + ny + nz).standard_normal((nz, ny, nx))
+    plan = hb._native.get_plan(nx, ny, nz, torch.device("cuda", 0))
+    plan.set_workspace_mode(lean)
+    try:
+        u, _ = hb.solve_discrete(hb.Field3D(F), hb.BoundaryData.zero(), hb.SchemeKind.FOURTH_ORDER,
+                                 prof, g)
+    finally:
+        plan.set_workspace_mode(0)
+    ref = orc.solve(F, oracle_table("4", prof, g), *orc.mode_cosines(nx, ny), workers=4)
+    assert rel_l2(u.values, ref) < PARITY
