@@ -18,6 +18,7 @@ ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--tune", default="", help="key=value,... passed to hfb_set_tuning")
 ap.add_argument("--time", action="store_true", help="print the mean solve time (CUDA events)")
+ap.add_argument("--stages", action="store_true", help="also print the mean per-launch times")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 w = wl.workload(a.cfg, a.n)
@@ -40,6 +41,9 @@ def solve():
 if a.time:
     solve()
     torch.cuda.synchronize()
+    if a.stages:
+        import ctypes
+        _native.check(plan.lib.hfb_stage_timing(plan.handle, a.reps), "stage_timing")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(a.reps):
@@ -47,6 +51,13 @@ if a.time:
     e1.record()
     torch.cuda.synchronize()
     print(f"tune={a.tune} n={n} ms/solve={e0.elapsed_time(e1) / a.reps:.3f}")
+    if a.stages:
+        buf = (ctypes.c_float * (5 * a.reps))()
+        k = ctypes.c_int(0)
+        _native.check(plan.lib.hfb_stage_times(plan.handle, buf, ctypes.byref(k)), "stage_times")
+        ms = [sum(buf[5 * r + i] for r in range(k.value)) / k.value for i in range(5)]
+        print("  stages ms: " + " ".join(f"{v:.3f}" for v in ms))
+        plan.lib.hfb_stage_timing(plan.handle, 0)
 else:
     for _ in range(a.reps):
         solve()
