@@ -256,11 +256,41 @@ __device__ __forceinline__ void pass_regs(double2* v, double2 w1, double2 w4, do
     for (int u = 0; u < R; ++u) w[u] = v[b + u * NB];
     if constexpr (L > 1) {
       static_assert(NB == 1 || FE<P, E>::T * NB == L, "shared twiddle base");
-      double2 wp[R];
-      twiddle_powers<R>(b ? mul_wn_at<E>(w1, b) : w1, b ? mul_wn_at<E>(w4, 4 * b) : w4,
-                        b ? mul_wn_at<E>(w16, 16 * b) : w16, wp);
+      const double2 b1 = b ? mul_wn_at<E>(w1, b) : w1;
+      const double2 b4 = b ? mul_wn_at<E>(w4, 4 * b) : w4;
+      const double2 b16 = b ? mul_wn_at<E>(w16, 16 * b) : w16;
+      if constexpr (R >= 16) {
+        // w^(4a + c) = w^(4a) w^c generated as they are used (the values of
+        // twiddle_powers, without holding all R - 1 powers live); for R = 32
+        // w^(16 + u) = w^16 w^u in the same step
+        const double2 p2 = cmul(b1, b1), p3 = cmul(p2, b1);
+        double2 q = b4;
 #pragma unroll
-      for (int u = 1; u < R; ++u) w[u] = cmul(w[u], wp[u]);
+        for (int a4 = 0; a4 < 4; ++a4) {
+          if (a4 == 2) q = cmul(b4, b4);
+          if (a4 == 3) q = cmul(q, b4);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int u = 4 * a4 + c;
+            double2 f;
+            if (u == 0) {
+              if constexpr (R == 32) w[16] = cmul(w[16], b16);
+              continue;
+            } else if (a4 == 0) {
+              f = c == 1 ? b1 : c == 2 ? p2 : p3;
+            } else {
+              f = c == 0 ? q : cmul(q, c == 1 ? b1 : c == 2 ? p2 : p3);
+            }
+            w[u] = cmul(w[u], f);
+            if constexpr (R == 32) w[u + 16] = cmul(w[u + 16], cmul(b16, f));
+          }
+        }
+      } else {
+        double2 wp[R];
+        twiddle_powers<R>(b1, b4, b16, wp);
+#pragma unroll
+        for (int u = 1; u < R; ++u) w[u] = cmul(w[u], wp[u]);
+      }
     }
     dftR<R>(w);
 #pragma unroll
