@@ -124,13 +124,15 @@ def forward_to_blocks(z_slab, grid, ex, rank):
 
 def solve_received(recv, scheme, profile, grid, ex, rank):
     """Stage 2 (per rank): z-solve of the received y-slab of mode rows
-    (n_z, n_x, kp) in place; the pivot latch stays in the full-grid plan."""
+    (n_z, n_x, kp) in place; the pivot latch stays in the full-grid plan.
+    scheme None: the full-grid plan's current coefficients are used."""
     import torch
     y0, y1 = ex.partition.y_ranges[rank]
     kp = ((y1 - y0) + 1) & ~1
     zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, recv.device)
     with zplan.lock:
-        device_coefficients(zplan, scheme, profile, grid)
+        if scheme is not None:
+            device_coefficients(zplan, scheme, profile, grid)
         nck = (grid.n_z + 7) // 8
         cp = torch.empty(nck * grid.n_x * kp, dtype=torch.float64, device=recv.device)
         check(zplan.lib.hfb_solve_modes(zplan.handle, ptr(recv), kp, y1 - y0, y0, ptr(cp),
@@ -215,3 +217,51 @@ def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None):
                        exchange_s=(ev[1].elapsed_time(ev[2]) + ev[3].elapsed_time(ev[4])) / 1e3,
                        tridiag_s=ev[2].elapsed_time(ev[3]) / 1e3)
     return out
+
+
+def solve_partitioned_local(values, scheme, profile, grid, parts, clock=None):
+    """The Partitioned mode on ONE device: every part runs the per-rank stages of
+    solve_partitioned (mode-row blocks, TMA z-solve on its y-slab) and the
+    all-to-alls are device copies between the parts' buffers. Bit-identical to
+    the one-call solve. Returns (solution, (transform_s, exchange_s, tridiag_s))
+    or None when the mode-space stages do not apply (non power-of-two lines)."""
+    import torch
+    ex = make_exchange_plan(grid, parts)
+    dev = values.device
+    for z0, z1 in ex.partition.z_ranges:
+        tp = get_plan(grid.n_x, grid.n_y, z1 - z0, dev)
+        if not int(tp.lib.hfb_workspace_bytes(tp.handle, 5)):
+            return None
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+    ev[0].record()
+    sends, modes = [], []
+    for r, (z0, z1) in enumerate(ex.partition.z_ranges):
+        s, m = forward_to_blocks(values[z0:z1].contiguous(), grid, ex, r)
+        sends.append(s)
+        modes.append(m)
+    ev[1].record()
+    ssz = [mode_split_sizes(ex, r)[0] for r in range(parts)]
+    rsz = [mode_split_sizes(ex, r)[1] for r in range(parts)]
+
+    def chunk(buf, sizes, q):
+        off = sum(sizes[:q])
+        return buf[off:off + sizes[q]]
+
+    recvs = [torch.cat([chunk(sends[p], ssz[p], q) for p in range(parts)])
+             for q in range(parts)]
+    ev[2].record()
+    zplan = None
+    for r in range(parts):
+        zplan = solve_received(recvs[r], scheme, profile, grid, ex, r)
+    ev[3].record()
+    backs = [torch.cat([chunk(recvs[q], rsz[q], p) for q in range(parts)])
+             for p in range(parts)]
+    ev[4].record()
+    out = torch.empty_like(values)
+    for r, (z0, z1) in enumerate(ex.partition.z_ranges):
+        blocks_to_solution(backs[r], modes[r], grid, ex, r, out=out[z0:z1])
+    ev[5].record()
+    zplan.fetch_status()
+    ev[5].synchronize()
+    sec = lambda a, b: ev[a].elapsed_time(ev[b]) / 1e3
+    return out, (sec(0, 1) + sec(4, 5), sec(1, 2) + sec(3, 4), sec(2, 3))

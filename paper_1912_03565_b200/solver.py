@@ -246,6 +246,13 @@ def _solve_part_device(plan, t, grid, config, clock, part_idx):
     n_z, n_y, n_x = grid.shape
     tag = f"{part_idx}"
     if isinstance(mode, Partitioned):
+        # the multi-GPU per-rank stages, parts exchanging by device copies
+        from .distributed import solve_partitioned_local
+        res = solve_partitioned_local(t, None, None, grid, mode.parts, clock)
+        if res is not None:
+            u, phases = res
+            t.copy_(u)
+            return phases
         ex = make_exchange_plan(grid, mode.parts)
         work_t = plan.workspace(1)
         clock.mark("t0" + tag)

@@ -292,17 +292,19 @@ def test_partitioned_and_shared_modes_bitwise(cuda):
     prof = hb.constant_profile(5.0, g)
     F = np.random.default_rng(59).standard_normal(g.shape)
     # staged = the reference's stage order (x-then-y transform both ways); the
-    # partitioned geometry runs the same per-line arithmetic, so bit-identical
+    # Partitioned mode runs the multi-GPU per-rank stages (mode-row blocks, the
+    # one-call kernels), bit-identical to the one-call solve
     ref, _ = solve(F, hb.SchemeKind.FOURTH_ORDER, prof, g,
                    hb.SolverConfig(mode=hb.Device(staged=True)))
+    one, _ = solve(F, hb.SchemeKind.FOURTH_ORDER, prof, g)
     for cfg in (hb.SolverConfig(), hb.SolverConfig(mode=hb.SharedWorkers(2)),
                 hb.SolverConfig(mode=hb.Partitioned(1)), hb.SolverConfig(mode=hb.Partitioned(3)),
                 hb.SolverConfig(mode=hb.Partitioned(4, 2)), hb.SolverConfig(mode=hb.Device())):
         u, t = solve(F, hb.SchemeKind.FOURTH_ORDER, prof, g, cfg)
         assert np.abs(u - ref).max() <= 1e-13 * np.abs(ref).max(), cfg
         if isinstance(cfg.mode, hb.Partitioned):
-            assert np.array_equal(u, ref)
-            assert t.exchange_s >= 0.0
+            assert np.array_equal(u, one)
+            assert t.exchange_s > 0.0
 
 
 def test_repeat_runs_bitwise_and_input_untouched(cuda):
