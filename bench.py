@@ -374,10 +374,10 @@ def run_ours(args):
             nbytes = points * 8  # every rank copies its slab: the whole volume per step
         e2e = {"value": points / e2e_s, "unit": "pts/s", "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "ms_per_step": e2e_s * 1e3,
-               "path": ("C-ABI hfb_solve_host_async, pinned host buffers, "
-                        f"{args.e2e_steps} pipelined steps + hfb_host_sync") if pipelined
-               else "C-ABI hfb_solve_host, one pinned host volume in place (blocking)"
-               if not multi else "pinned H2D + solve_partitioned + D2H per rank"}
+               "path": "pinned H2D + solve_partitioned + pinned D2H per rank" if multi
+               else ("C-ABI hfb_solve_host_async, pinned host buffers, "
+                     f"{args.e2e_steps} pipelined steps + hfb_host_sync") if pipelined
+               else "C-ABI hfb_solve_host, one pinned host volume in place (blocking)"}
         if not multi:
             e2e["sync_ms_per_step"] = sync_s * 1e3  # one blocking hfb_solve_host call
 
