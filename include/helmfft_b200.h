@@ -283,6 +283,11 @@ int hfb_forward_modes(hfb_plan* plan, const double* src, double* modes, void* wo
 int hfb_inverse_modes(hfb_plan* plan, double* modes, double* out, void* stream);
 int hfb_solve_modes(hfb_plan* plan, double* data, int ld, int m_count, int m_offset,
                     void* cp_work, void* stream);
+/* hfb_solve_modes on a y-slab whose levels are stored out of order (the
+ * chunked exchange lands them chunk by chunk): level l lives at plane
+ * level_plane[l] (host array of n_z ints, copied on `stream`). */
+int hfb_solve_modes_perm(hfb_plan* plan, double* data, int ld, int m_count, int m_offset,
+                         const int* level_plane, void* cp_work, void* stream);
 int hfb_pack_modes(hfb_plan* plan, const double* modes, double* send, const int* y_starts,
                    int parts, void* stream);
 int hfb_unpack_modes(hfb_plan* plan, const double* recv, double* modes, const int* y_starts,

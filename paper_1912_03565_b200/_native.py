@@ -55,6 +55,7 @@ SIGNATURES = {
     "hfb_forward_modes": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "hfb_inverse_modes": (_i, [_vp, _vp, _vp, _vp]),
     "hfb_solve_modes": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
+    "hfb_solve_modes_perm": (_i, [_vp, _vp, _i, _i, _i, _ip, _vp, _vp]),
     "hfb_pack_modes": (_i, [_vp, _vp, _vp, _ip, _i, _vp]),
     "hfb_unpack_modes": (_i, [_vp, _vp, _vp, _ip, _i, _vp]),
     "hfb_solve_host_async": (_i, [_vp, _vp, _vp, _vp, _vp]),

@@ -112,6 +112,7 @@ extern "C" int hfb_plan_destroy(hfb_plan* p) {
   cudaFree(p->sn_y);
   cudaFree(p->dense_x);
   cudaFree(p->dense_y);
+  cudaFree(p->lvlmap);
   cudaFree(p->coef);
   cudaFree(p->coef_i);
   cudaFree(p->cx);

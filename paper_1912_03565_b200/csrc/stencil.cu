@@ -571,6 +571,28 @@ extern "C" int hfb_solve_modes(hfb_plan* p, double* data, int ld, int m_count, i
                                 m_offset, (cudaStream_t)stream);
 }
 
+extern "C" int hfb_solve_modes_perm(hfb_plan* p, double* data, int ld, int m_count,
+                                    int m_offset, const int* level_plane, void* cp_work,
+                                    void* stream) {
+  if (!p || !data || !cp_work || !level_plane || ld < m_count || (ld & 1))
+    return HFB_ERR_ARGUMENT;
+  if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
+  if (p->coef_i) return HFB_ERR_ARGUMENT;
+  if (m_count < 0 || m_offset < 0 || m_offset + m_count > p->ny) return HFB_ERR_RANGE;
+  HFB_CUDA(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->lvlmap_cap < p->nz) {
+    if (p->lvlmap) cudaFree(p->lvlmap);
+    p->lvlmap = nullptr;
+    HFB_CUDA(cudaMalloc(&p->lvlmap, sizeof(int) * p->nz));
+    p->lvlmap_cap = p->nz;
+  }
+  HFB_CUDA(cudaMemcpyAsync(p->lvlmap, level_plane, sizeof(int) * p->nz, cudaMemcpyHostToDevice,
+                           st));
+  return launch_thomas_tma_cols(p, data, (double*)cp_work, ld, (long long)ld * p->nx, m_count,
+                                m_offset, st, 0, 0, -1, 0, p->lvlmap);
+}
+
 extern "C" int hfb_pack_modes(hfb_plan* p, const double* modes, double* send, const int* ys,
                               int parts, void* stream) {
   if (!p || !modes || !send || !ys || parts < 1) return HFB_ERR_ARGUMENT;

@@ -37,6 +37,7 @@ struct TmaArgs {
   int bwd_only;  // forward sweep already done (x' and checkpoints in place)
   int m_off;     // global y-mode of column 0 (a y-slab of modes)
   int row0;      // first row (x-mode) of this launch
+  const int* lvl;  // level -> plane of the data (null: identity), e.g. a chunked y-slab
 };
 
 __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, double cxy) {
@@ -67,13 +68,14 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
     const uint32_t rowbytes = (uint32_t)(((cols + 1) & ~1) * 8);  // ld is even
     double* base = a.w + (long long)n * a.ld + m0;
     auto chunk_of = [&](int task) { return task < nchunk ? task : ntask - 1 - task; };
+    auto plane_of = [&](int l) -> long long { return a.lvl ? __ldg(a.lvl + l) : l; };
     // thread 0: bring chunk `task` into stage s
     auto issue = [&](int task, int s) {
       const int c = chunk_of(task);
       const int l0 = c * K, nl = min(K, a.nz - l0);
       mbar_arrive_expect_tx(&bar[s], nl * rowbytes + (uint32_t)(nl * 12 * 8));
       for (int i = 0; i < nl; ++i)
-        bulk_g2s(&sdat[s][i][0], base + (long long)(l0 + i) * a.ps, rowbytes, &bar[s]);
+        bulk_g2s(&sdat[s][i][0], base + plane_of(l0 + i) * a.ps, rowbytes, &bar[s]);
       bulk_g2s(&scoef[s][0], a.coef + (long long)l0 * 12, (uint32_t)(nl * 12 * 8), &bar[s]);
     };
     const bool live = tid < cols;
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
       if (tid == 0 && task != nchunk - 1) {
         fence_proxy_async_smem();
         for (int i = 0; i < nl; ++i)
-          bulk_s2g(base + (long long)(l0 + i) * a.ps, &sdat[s][i][0], rowbytes);
+          bulk_s2g(base + plane_of(l0 + i) * a.ps, &sdat[s][i][0], rowbytes);
         bulk_commit();
       }
     }
@@ -187,13 +189,14 @@ int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, long
 
 int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld, long long ps,
                            int ncols, int m_off, cudaStream_t st, int bwd_only, int row0,
-                           int row1, int max_per_sm) {
+                           int row1, int max_per_sm, const int* lvl) {
   if (row1 < 0) row1 = p->nx;
   if (p->nz < 1 || ncols < 1 || row1 <= row0) return HFB_OK;
   TmaArgs a;
   a.bwd_only = bwd_only;
   a.m_off = m_off;
   a.row0 = row0;
+  a.lvl = lvl;
   a.w = data;
   a.cpk = cpk;
   a.coef = p->coef;

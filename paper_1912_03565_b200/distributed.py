@@ -160,7 +160,95 @@ def blocks_to_solution(back, modes, grid, ex, rank, out=None):
     return out
 
 
-def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None):
+def chunk_layout(ex, chunks):
+    """Chunked exchange geometry. Every rank's z-range is cut into `chunks` plane
+    ranges (some may be empty); chunk c of all ranks travels in one all-to-all,
+    so the receiver's y-slab holds chunk 0 of every sender, then chunk 1, ...
+    Returns (ranges, level_plane): ranges[r][c] = (c0, c1) local plane range of
+    rank r's chunk c, level_plane[l] = plane of global level l in the y-slab."""
+    zr = ex.partition.z_ranges
+    ranges = []
+    for z0, z1 in zr:
+        n = z1 - z0
+        cuts = [round(c * n / chunks) for c in range(chunks + 1)]
+        ranges.append([(cuts[c], cuts[c + 1]) for c in range(chunks)])
+    level_plane = np.empty(ex.n_z, dtype=np.int32)
+    plane = 0
+    for c in range(chunks):
+        for r, (z0, _) in enumerate(zr):
+            c0, c1 = ranges[r][c]
+            level_plane[z0 + c0:z0 + c1] = np.arange(plane, plane + c1 - c0)
+            plane += c1 - c0
+    return ranges, level_plane
+
+
+def chunk_split_sizes(ex, ranges, rank, c):
+    """(send, recv) element counts of chunk c's all-to-all for `rank`."""
+    yr = ex.partition.y_ranges
+    kp = [((y1 - y0) + 1) & ~1 for y0, y1 in yr]
+    c0, c1 = ranges[rank][c]
+    send = [(c1 - c0) * ex.n_x * k for k in kp]
+    recv = [(ranges[p][c][1] - ranges[p][c][0]) * ex.n_x * kp[rank] for p in range(ex.n_parts)]
+    return send, recv
+
+
+def forward_chunk(z_slab, modes, grid, ex, rank, c0, c1):
+    """Forward 2D DST of local planes [c0, c1) into their mode rows (a slice of
+    `modes`) and pack their exchange blocks; returns the send buffer."""
+    import torch
+    dev = z_slab.device
+    tplan = get_plan(grid.n_x, grid.n_y, c1 - c0, dev)
+    ldm = int(tplan.lib.hfb_modes_ld(tplan.handle))
+    m = modes[c0 * grid.n_x * ldm:c1 * grid.n_x * ldm]
+    with tplan.lock:
+        st = tplan.stream()
+        work = tplan.workspace(5)
+        check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(z_slab[c0:c1]), ptr(m), ptr(work), st),
+              "forward_modes")
+        kp = [((y1 - y0) + 1) & ~1 for y0, y1 in ex.partition.y_ranges]
+        send = torch.empty((c1 - c0) * grid.n_x * sum(kp), dtype=torch.float64, device=dev)
+        ys = y_starts(ex)
+        check(tplan.lib.hfb_pack_modes(tplan.handle, ptr(m), ptr(send),
+                                       ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                       ex.n_parts, st), "pack_modes")
+    return send
+
+
+def inverse_chunk(back, modes, out, grid, ex, c0, c1):
+    """Unpack chunk blocks into the mode rows of local planes [c0, c1) and run
+    their inverse 2D DST into out[c0:c1]."""
+    tplan = get_plan(grid.n_x, grid.n_y, c1 - c0, back.device)
+    ldm = int(tplan.lib.hfb_modes_ld(tplan.handle))
+    m = modes[c0 * grid.n_x * ldm:c1 * grid.n_x * ldm]
+    with tplan.lock:
+        st = tplan.stream()
+        ys = y_starts(ex)
+        check(tplan.lib.hfb_unpack_modes(tplan.handle, ptr(back), ptr(m),
+                                         ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                         ex.n_parts, st), "unpack_modes")
+        check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(m), ptr(out[c0:c1]), st),
+              "inverse_modes")
+
+
+def solve_received_chunked(recv, level_plane, scheme, profile, grid, ex, rank):
+    """solve_received for a y-slab assembled chunk by chunk (levels permuted)."""
+    import torch
+    y0, y1 = ex.partition.y_ranges[rank]
+    kp = ((y1 - y0) + 1) & ~1
+    zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, recv.device)
+    with zplan.lock:
+        if scheme is not None:
+            device_coefficients(zplan, scheme, profile, grid)
+        nck = (grid.n_z + 7) // 8
+        cp = torch.empty(nck * grid.n_x * kp, dtype=torch.float64, device=recv.device)
+        lp = np.ascontiguousarray(level_plane, dtype=np.int32)
+        check(zplan.lib.hfb_solve_modes_perm(zplan.handle, ptr(recv), kp, y1 - y0, y0,
+                                             lp.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                             ptr(cp), zplan.stream()), "solve_modes_perm")
+    return zplan
+
+
+def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None, chunks=4):
     """Solve with the grid split over the ranks of `group`; z_slab is this rank's
     (kpz, n_y, n_x) CUDA float64 part of the folded RHS. Returns the solution slab
     (a new tensor). Raises SingularSystemError on every rank if any rank hit a
@@ -168,7 +256,11 @@ def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None):
 
     Mode-space exchange: the forward 2D DST leaves padded mode rows (l, n, m);
     the block for rank q is (kpz, n_x, kp(q)); the receive buffer is directly
-    the y-slab of mode rows the TMA z-solve streams (no unpack on the way in)."""
+    the y-slab of mode rows the TMA z-solve streams (no unpack on the way in).
+    With chunks > 1 the z-slab goes in `chunks` plane ranges: the all-to-all of
+    chunk c runs (NCCL stream) while chunk c + 1 is transformed, and on the way
+    back chunk c is unpacked and inverse-transformed while chunk c + 1 is in
+    flight; the z-solve reads the chunk-ordered y-slab through a level table."""
     import torch
     import torch.distributed as dist
     rank, parts = dist.get_rank(group), dist.get_world_size(group)
@@ -178,29 +270,54 @@ def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None):
     if tuple(z_slab.shape) != (kpz, grid.n_y, grid.n_x):
         raise ValueError(f"z-slab shape {tuple(z_slab.shape)} != {(kpz, grid.n_y, grid.n_x)}")
     dev = z_slab.device
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if timings is not None else None
+    chunks = max(1, min(chunks, min(z1 - z0 for z0, z1 in ex.partition.z_ranges)))
+    ranges, level_plane = chunk_layout(ex, chunks)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings is not None else None
 
     def mark(i):
         if ev is not None:
             ev[i].record()
 
     local = z_slab.contiguous()
-    s_fwd, r_fwd = mode_split_sizes(ex, rank)
+    ldm = int(get_plan(grid.n_x, grid.n_y, kpz, dev).lib.hfb_modes_ld(
+        get_plan(grid.n_x, grid.n_y, kpz, dev).handle))
+    modes = torch.empty(kpz * grid.n_x * ldm, dtype=torch.float64, device=dev)
+    y0, y1 = ex.partition.y_ranges[rank]
+    kp_me = ((y1 - y0) + 1) & ~1
+    recv = torch.empty(grid.n_z * grid.n_x * kp_me, dtype=torch.float64, device=dev)
+    offs, off = [], 0
+    for c in range(chunks):
+        offs.append(off)
+        off += sum(chunk_split_sizes(ex, ranges, rank, c)[1])
     mark(0)
-    send, modes = forward_to_blocks(local, grid, ex, rank)
+    works, keep = [], []
+    for c in range(chunks):
+        c0, c1 = ranges[rank][c]
+        send = forward_chunk(local, modes, grid, ex, rank, c0, c1)
+        s, r = chunk_split_sizes(ex, ranges, rank, c)
+        keep.append(send)
+        works.append(dist.all_to_all_single(recv[offs[c]:offs[c] + sum(r)], send,
+                                            output_split_sizes=r, input_split_sizes=s,
+                                            group=group, async_op=True))
+    for w in works:
+        w.wait()
     mark(1)
-    recv = torch.empty(sum(r_fwd), dtype=torch.float64, device=dev)
-    dist.all_to_all_single(recv, send, output_split_sizes=r_fwd, input_split_sizes=s_fwd,
-                           group=group)
+    zplan = solve_received_chunked(recv, level_plane, scheme, profile, grid, ex, rank)
     mark(2)
-    zplan = solve_received(recv, scheme, profile, grid, ex, rank)
+    out = torch.empty((kpz, grid.n_y, grid.n_x), dtype=torch.float64, device=dev)
+    backs, works = [], []
+    for c in range(chunks):
+        s, r = chunk_split_sizes(ex, ranges, rank, c)
+        back = torch.empty(sum(s), dtype=torch.float64, device=dev)
+        backs.append(back)
+        works.append(dist.all_to_all_single(back, recv[offs[c]:offs[c] + sum(r)],
+                                            output_split_sizes=s, input_split_sizes=r,
+                                            group=group, async_op=True))
+    for c in range(chunks):
+        works[c].wait()
+        c0, c1 = ranges[rank][c]
+        inverse_chunk(backs[c], modes, out, grid, ex, c0, c1)
     mark(3)
-    back = torch.empty(sum(s_fwd), dtype=torch.float64, device=dev)
-    dist.all_to_all_single(back, recv, output_split_sizes=s_fwd, input_split_sizes=r_fwd,
-                           group=group)
-    mark(4)
-    out = blocks_to_solution(back, modes, grid, ex, rank)
-    mark(5)
     # agree on the first failing pivot across ranks
     flag = torch.zeros(1, dtype=torch.int64, device=dev)
     try:
@@ -213,9 +330,9 @@ def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None):
         raise SingularSystemError("vanishing pivot on at least one rank")
     if timings is not None:
         torch.cuda.synchronize(dev)
-        timings.update(transform_s=(ev[0].elapsed_time(ev[1]) + ev[4].elapsed_time(ev[5])) / 1e3,
-                       exchange_s=(ev[1].elapsed_time(ev[2]) + ev[3].elapsed_time(ev[4])) / 1e3,
-                       tridiag_s=ev[2].elapsed_time(ev[3]) / 1e3)
+        timings.update(forward_exchange_s=ev[0].elapsed_time(ev[1]) / 1e3,
+                       tridiag_s=ev[1].elapsed_time(ev[2]) / 1e3,
+                       exchange_inverse_s=ev[2].elapsed_time(ev[3]) / 1e3)
     return out
 
 

@@ -96,3 +96,24 @@ def test_mode_split_sizes_consistent(parts):
     kp = [((y1 - y0) + 1) & ~1 for y0, y1 in ex.partition.y_ranges]
     assert sum(map(sum, sends)) == g.n_z * g.n_x * sum(kp)
     assert sum(kp) - g.n_y == sum((y1 - y0) & 1 for y0, y1 in ex.partition.y_ranges)
+
+
+@pytest.mark.parametrize("parts,chunks", [(1, 4), (2, 4), (3, 3), (8, 4), (5, 2)])
+def test_chunk_layout_is_a_permutation(parts, chunks):
+    from paper_1912_03565_b200 import distributed as hd
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), 31, 47, 61)
+    ex = hb.make_exchange_plan(g, parts)
+    ranges, lp = hd.chunk_layout(ex, chunks)
+    assert sorted(lp.tolist()) == list(range(g.n_z))
+    for r, (z0, z1) in enumerate(ex.partition.z_ranges):
+        assert ranges[r][0][0] == 0 and ranges[r][-1][1] == z1 - z0
+    # per-chunk splits are consistent across ranks and add up to the unchunked ones
+    for c in range(chunks):
+        for p in range(parts):
+            for q in range(parts):
+                assert hd.chunk_split_sizes(ex, ranges, p, c)[0][q] == \
+                    hd.chunk_split_sizes(ex, ranges, q, c)[1][p]
+    for r in range(parts):
+        tot = [sum(hd.chunk_split_sizes(ex, ranges, r, c)[0][q] for c in range(chunks))
+               for q in range(parts)]
+        assert tot == hd.mode_split_sizes(ex, r)[0]

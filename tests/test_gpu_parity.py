@@ -731,3 +731,70 @@ def test_one_call_edge_shapes_vs_oracle(cuda, shape, lean):
         plan.set_workspace_mode(0)
     ref = orc.solve(F, oracle_table("4", prof, g), *orc.mode_cosines(nx, ny), workers=4)
     assert rel_l2(u.values, ref) < PARITY
+
+
+def _emulated_partitioned_chunked(F, scheme, prof, g, parts, chunks):
+    """solve_partitioned's chunked schedule (per-chunk all-to-alls, the z-solve
+    through the level table), every rank in one process, collectives emulated."""
+    import torch
+    from paper_1912_03565_b200 import distributed as hd
+    ex = hb.make_exchange_plan(g, parts)
+    ranges, level_plane = hd.chunk_layout(ex, chunks)
+    zr = ex.partition.z_ranges
+    slabs = [F[z0:z1].contiguous() for z0, z1 in zr]
+    modes = []
+    for r, (z0, z1) in enumerate(zr):
+        tp = hb._native.get_plan(g.n_x, g.n_y, z1 - z0, F.device)
+        ldm = int(tp.lib.hfb_modes_ld(tp.handle))
+        modes.append(torch.empty((z1 - z0) * g.n_x * ldm, dtype=torch.float64, device=F.device))
+    sends = [[hd.forward_chunk(slabs[r], modes[r], g, ex, r, *ranges[r][c]) for c in range(chunks)]
+             for r in range(parts)]
+
+    def piece(buf, sizes, q):
+        off = sum(sizes[:q])
+        return buf[off:off + sizes[q]]
+
+    recvs = []
+    for q in range(parts):
+        blocks = []
+        for c in range(chunks):
+            for p in range(parts):
+                blocks.append(piece(sends[p][c], hd.chunk_split_sizes(ex, ranges, p, c)[0], q))
+        recvs.append(torch.cat(blocks))
+    for q in range(parts):
+        hd.solve_received_chunked(recvs[q], level_plane, scheme, prof, g, ex, q)
+    outs = [torch.empty_like(s) for s in slabs]
+    for p in range(parts):
+        for c in range(chunks):
+            # rank p's chunk c comes back from every q: the piece of q's y-slab
+            # chunk-c region that p sent
+            parts_back = []
+            for q in range(parts):
+                off_c = sum(sum(hd.chunk_split_sizes(ex, ranges, q, cc)[1]) for cc in range(c))
+                rq = hd.chunk_split_sizes(ex, ranges, q, c)[1]
+                region = recvs[q][off_c:off_c + sum(rq)]
+                parts_back.append(piece(region, rq, p))
+            hd.inverse_chunk(torch.cat(parts_back), modes[p], outs[p], g, ex, *ranges[p][c])
+    return torch.cat(outs)
+
+
+@pytest.mark.parametrize("parts,chunks,shape", [(2, 4, (63, 63, 63)), (3, 3, (127, 63, 50)),
+                                                (8, 4, (255, 255, 40)), (4, 2, (31, 127, 9))])
+def test_partitioned_chunked_stages_bitwise(cuda, parts, chunks, shape):
+    """The overlapped (chunked) multi-GPU schedule reproduces the one-call solve
+    bit for bit: chunk-ordered y-slabs, level table in the z-solve."""
+    import torch
+    nx, ny, nz = shape
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+    prof = hb.constant_profile(-20.0, g)
+    F = torch.from_numpy(np.random.default_rng(parts * 10 + chunks).standard_normal(
+        (nz, ny, nx))).cuda()
+    U = _emulated_partitioned_chunked(F, hb.SchemeKind.FOURTH_ORDER, prof, g, parts, chunks)
+    plan = hb._native.get_plan(nx, ny, nz, F.device)
+    hb.tridiag.device_coefficients(plan, hb.SchemeKind.FOURTH_ORDER, prof, g)
+    ref = torch.empty_like(F)
+    work = plan.workspace(0)
+    hb._native.check(plan.lib.hfb_solve(plan.handle, hb._native.ptr(F), hb._native.ptr(ref),
+                                        hb._native.ptr(work), plan.stream()), "solve")
+    plan.fetch_status()
+    assert torch.equal(U, ref)
