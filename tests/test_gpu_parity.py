@@ -798,3 +798,38 @@ def test_partitioned_chunked_stages_bitwise(cuda, parts, chunks, shape):
                                         hb._native.ptr(work), plan.stream()), "solve")
     plan.fetch_status()
     assert torch.equal(U, ref)
+
+
+def test_capi_argument_validation(cuda):
+    """Error codes of the C-ABI entry points (include/helmfft_b200.h): null
+    pointers, bad ranges, misaligned strides, missing coefficients."""
+    import ctypes
+    import torch
+    from paper_1912_03565_b200 import _native as nv
+    lib = nv.load_library()
+    h = ctypes.c_void_p()
+    assert lib.hfb_plan_create(0, 15, 15, 0, ctypes.byref(h)) == nv.HFB_ERR_ARGUMENT
+    assert lib.hfb_plan_create(15, 15, 7, 0, ctypes.byref(h)) == nv.HFB_OK
+    t = torch.zeros((7, 15, 15), dtype=torch.float64, device="cuda")
+    w = torch.zeros(1 << 22, dtype=torch.float64, device="cuda")
+    P, st = nv.ptr, None
+    # no coefficients yet
+    assert lib.hfb_solve(h, P(t), P(t), P(w), st) == nv.HFB_ERR_NO_COEFFICIENTS
+    assert lib.hfb_solve_z(h, P(t), P(t), P(t), P(t), P(w), st) == nv.HFB_ERR_NO_COEFFICIENTS
+    assert lib.hfb_solve(h, None, P(t), P(w), st) == nv.HFB_ERR_ARGUMENT
+    assert lib.hfb_transform_stack(h, P(t), 3, 2, P(w), st) == nv.HFB_ERR_RANGE
+    assert lib.hfb_transform_stack(h, P(t), 0, 8, P(w), st) == nv.HFB_ERR_RANGE
+    assert lib.hfb_plan_set_workspace_mode(h, 2) == nv.HFB_ERR_ARGUMENT
+    cx = np.cos(np.pi * np.arange(1, 16) / 16)
+    tab = np.zeros(7 * 12)
+    tab[5::12] = -6.0  # diagonal d at offset 0 of every level
+    assert lib.hfb_plan_set_coefficients(h, tab.ctypes.data_as(ctypes.c_void_p),
+                                         cx.ctypes.data_as(ctypes.c_void_p),
+                                         cx.ctypes.data_as(ctypes.c_void_p), 1e-14) == nv.HFB_OK
+    assert lib.hfb_solve_slab(h, P(t), 16, 0, P(w), st) == nv.HFB_ERR_RANGE
+    assert lib.hfb_solve_modes(h, P(t), 15, 15, 0, P(w), st) == nv.HFB_ERR_ARGUMENT  # odd ld
+    assert lib.hfb_solve_modes(h, P(t), 16, 15, 1, P(w), st) == nv.HFB_ERR_RANGE
+    ys = (ctypes.c_int * 3)(0, 7, 14)  # must end at n_y = 15
+    assert lib.hfb_pack_modes(h, P(t), P(w), ys, 2, st) == nv.HFB_ERR_ARGUMENT
+    assert lib.hfb_solve(h, P(t), P(t), P(w), st) == nv.HFB_OK
+    assert lib.hfb_plan_destroy(h) == nv.HFB_OK
