@@ -833,3 +833,43 @@ def test_capi_argument_validation(cuda):
     assert lib.hfb_pack_modes(h, P(t), P(w), ys, 2, st) == nv.HFB_ERR_ARGUMENT
     assert lib.hfb_solve(h, P(t), P(t), P(w), st) == nv.HFB_OK
     assert lib.hfb_plan_destroy(h) == nv.HFB_OK
+
+
+# --------------------------------- the reference's acceptance problems (f2)
+@pytest.fixture(scope="module")
+def acceptance():
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "acceptance.npz")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("key,n", [("2", 125), ("4", 125), ("6", 125), ("2", 250), ("4", 250),
+                                   ("6", 250)])
+def test_acceptance_wave_problems_match_reference(cuda, acceptance, key, n):
+    """Variable-k wave problem on [0, pi]^3 with analytic Dirichlet data, through
+    build_rhs + fold_dirichlet + the one-call solve: the discretisation errors
+    reproduce the reference's own run (tests/golden/make_acceptance_golden.py)."""
+    from acceptance_problems import error_metrics, helmholtz_case
+    scheme = ZSCHEME[key]
+    g, prof, src, bnd, u = helmholtz_case(10.0, 9.0, 10.0, 10.0, 9.0, scheme, n)
+    F = hb.build_rhs(scheme, src, prof, g)
+    sol, _ = hb.solve_discrete(F, bnd, scheme, prof, g)
+    mx, l2 = error_metrics(sol.values, u, g)
+    ref = acceptance[f"wave_{key}_{n}"]
+    assert abs(mx - ref[0]) <= 1e-6 * ref[0] and abs(l2 - ref[1]) <= 1e-6 * ref[1], (mx, l2, ref)
+    folded = hb.fold_dirichlet(F, bnd, scheme, prof, g)
+    assert hb.residual_l2(sol, folded, scheme, prof, g) < 1e-11
+
+
+@pytest.mark.parametrize("n", [64, 128, 256])
+def test_acceptance_convdiff_matches_reference(cuda, acceptance, n):
+    """Convection-diffusion gamma = -100 with analytic Dirichlet data (cd4)."""
+    from acceptance_problems import convdiff_case, error_metrics
+    g, prof, src, bnd, u = convdiff_case(-100.0, n)
+    scheme = hb.SchemeKind.CONVECTION_DIFFUSION_4
+    F = hb.build_rhs(scheme, src, prof, g)
+    sol, _ = hb.solve_discrete(F, bnd, scheme, prof, g)
+    mx, l2 = error_metrics(sol.values, u, g)
+    ref = acceptance[f"cd_{n}"]
+    assert abs(mx - ref[0]) <= 1e-6 * ref[0] and abs(l2 - ref[1]) <= 1e-6 * ref[1], (mx, l2, ref)
