@@ -76,7 +76,9 @@ uint64_t hfb_launch_count(void);
  * overlap the z-solve with the y-passes on a second stream, halves of the
  * x-modes (1) or not (0, default: the CTA caps that make room for both cost
  * more than the overlap gains, 22.5 vs 21.7 ms at 1023^3), keys 7 / 8 = those
- * caps (CTAs per SM of the y-passes / of the z-solve). */
+ * caps (CTAs per SM of the y-passes / of the z-solve); key 9 = write packed
+ * rows (the user's array) by row-pair 1D bulk stores (1) or thread stores (0,
+ * default: the register rotation it needs costs more than it saves). */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.

@@ -60,6 +60,7 @@ struct StreamArgs {
   int nbox, boxn;         // TLOAD: boxes per batch and their extent along the line
   int vec_out;            // TRAN: (line 2k, 2k+1) pairs are 16-byte aligned in dst
   int tstore;             // ROW/TLOAD: outputs leave by TMA tensor stores (omap)
+  int pbulk;              // ROW/TLOAD into packed rows (ld = N): 1D bulk stores of row pairs
   // kYF: forward Thomas sweep (thomas_tma.cu arithmetic) on the y-pass outputs
   const double* coef;     // [l][k][(4a, 2b, 2c, d)]
   const double* cx;       // per line (x-mode)
@@ -106,6 +107,22 @@ __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long
 
 // E = 16: up to 128 threads (two line pairs of M = 1024), 3 CTAs per SM;
 // E = 32: up to 64 threads (one warp per pair) and the full register budget.
+// v'[j] = v[(j + r) mod Q] for a per-thread r: log2(Q) select stages (no
+// dynamic register indexing), so thread t can write its segment's elements in
+// a t-rotated order — distinct banks across the warp in a natural row layout.
+template <int Q>
+__device__ __forceinline__ void rotate_left(double (&v)[Q], int r) {
+#pragma unroll
+  for (int b = 1; b < Q; b <<= 1) {
+    const bool on = (r & b) != 0;
+    double tmp[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) tmp[j] = v[(j + b) % Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) v[j] = on ? tmp[j] : v[j];
+  }
+}
+
 // M = 2048 column/transposing passes: two line pairs per CTA (W = 4 lines,
 // 32-byte box rows and column chunks) at 256 threads, one CTA per SM.
 template <int P, int E, int MODE>
@@ -225,7 +242,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
       long long pl2;
       int g2;
       if (threadIdx.x == 0 && batch_of(a, it + 1, pl2, g2)) {
-        if (a.tstore) bulk_wait_read<0>();  // batch it-1's tensor stores read stage s^1
+        if (a.tstore || a.pbulk) bulk_wait_read<0>();  // batch it-1's stores read stage s^1
         fence_proxy_async_smem();
         issue(it + 1, s ^ 1);
       }
@@ -259,7 +276,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     double2* sb = reinterpret_cast<double2*>(gb);
     fftE_forward<P, E>(v, sb, etw, t, f);
     double2 out[Q];
-    if (MODE != kTran && a.tstore) {
+    if (MODE != kTran && (a.tstore || a.pbulk)) {
       // Segment-aligned outputs staged as the group's tensor box [2 lines]
       // [M/16 segments][16] in the 128B-swizzle layout (granule h of smem row r
       // at h ^ (r & 7): conflict-free, since thread t owns whole segments),
@@ -308,27 +325,74 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
           }
         }
       }
-      constexpr int NSEG = M / 16;
+      if (a.tstore) {
+        constexpr int NSEG = M / 16;
 #pragma unroll
-      for (int L = 0; L < 2; ++L) {
+        for (int L = 0; L < 2; ++L) {
 #pragma unroll
-        for (int h = 0; h < Q / 2; ++h) {
-          const int pos = Q * t + 2 * h;
-          const int row = L * NSEG + (pos >> 4);
-          const int phys = row * 16 + 2 * (((pos >> 1) & 7) ^ (row & 7));
-          const double2 val = L == 0 ? make_double2(out[2 * h].x, out[2 * h + 1].x)
-                                     : make_double2(out[2 * h].y, out[2 * h + 1].y);
-          *reinterpret_cast<double2*>(gb + phys) = val;
+          for (int h = 0; h < Q / 2; ++h) {
+            const int pos = Q * t + 2 * h;
+            const int row = L * NSEG + (pos >> 4);
+            const int phys = row * 16 + 2 * (((pos >> 1) & 7) ^ (row & 7));
+            const double2 val = L == 0 ? make_double2(out[2 * h].x, out[2 * h + 1].x)
+                                       : make_double2(out[2 * h].y, out[2 * h + 1].y);
+            *reinterpret_cast<double2*>(gb + phys) = val;
+          }
         }
-      }
-      fence_proxy_async_smem();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        for (int gg = 0; gg < a.NF; ++gg) {
-          const int r0 = meta.row[s][2 * gg];
-          if (r0 >= 0) tensor_s2g_4d(&omap, 0, 0, r0, (int)plane, gbuf(s, gg));
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          for (int gg = 0; gg < a.NF; ++gg) {
+            const int r0 = meta.row[s][2 * gg];
+            if (r0 >= 0) tensor_s2g_4d(&omap, 0, 0, r0, (int)plane, gbuf(s, gg));
+          }
+          bulk_commit();
         }
-        bulk_commit();
+      } else if constexpr (Q == 16) {
+        // Packed rows (ld = N): the group's two lines are one contiguous run of
+        // 2N doubles. Stage it in natural order, element e at gb[d + e] with d
+        // the run's 16-byte misalignment, writing in a t-rotated order; then
+        // the 16-byte aligned body leaves by one 1D bulk store and the at most
+        // two edge elements by plain stores.
+        double* G = a.dst + plane * a.out_ps + (long long)row0 * a.out_ld;
+        const int d = (int)((reinterpret_cast<uintptr_t>(G) >> 3) & 1);
+        double w0[Q], w1[Q];
+#pragma unroll
+        for (int c = 0; c < Q; ++c) {
+          w0[c] = out[c].x;
+          w1[c] = out[c].y;
+        }
+        rotate_left<Q>(w0, t & (Q - 1));
+        rotate_left<Q>(w1, t & (Q - 1));
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          const int p = Q * t + ((j + t) & (Q - 1));
+          if (p < a.N) {
+            gb[d + p] = w0[j];
+            if (v1) gb[d + a.N + p] = w1[j];
+          }
+        }
+        group_sync<T>(f);
+        const int etot = (v1 ? 2 : 1) * a.N;
+        const int nb = (etot - d) & ~1;
+        if (t == 0 && v0) {
+          if (d) G[0] = gb[d];
+          if (d + nb < etot) G[etot - 1] = gb[d + etot - 1];
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          for (int gg = 0; gg < a.NF; ++gg) {
+            const int r0 = meta.row[s][2 * gg];
+            if (r0 < 0) continue;
+            double* Gg = a.dst + plane * a.out_ps + (long long)r0 * a.out_ld;
+            const int dg = (int)((reinterpret_cast<uintptr_t>(Gg) >> 3) & 1);
+            const int eg = (meta.row[s][2 * gg + 1] >= 0 ? 2 : 1) * a.N;
+            const int nbg = (eg - dg) & ~1;
+            if (nbg > 0) bulk_s2g(Gg + dg, gbuf(s, gg) + 2 * dg, (uint32_t)nbg * 8);
+          }
+          bulk_commit();
+        }
       }
     } else {
       dstE_post<P, E>(v, sb, wsum, c.scale, t, f, out);
@@ -372,7 +436,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     __syncthreads();  // stage s is free for the prefetch issued next iteration
     s ^= 1;
   }
-  if (a.tstore && threadIdx.x == 0) bulk_wait<0>();  // smem stays valid until stored
+  if ((a.tstore || a.pbulk) && threadIdx.x == 0) bulk_wait<0>();  // smem valid until stored
 }
 
 bool dst16_ok(int M) { return M >= 16 && M <= 4096 && (M & (M - 1)) == 0; }
@@ -402,6 +466,7 @@ static int g_tune_tstore = 1;  // row outputs by TMA tensor stores where the lay
 static int g_tune_overlap = 0;  // overlapped z-solve / y-pass schedule (key 6)
 static int g_tune_cap_dst = 2;  // its CTA caps per SM: y-passes (key 7), z-solve (key 8)
 static int g_tune_cap_th = 1;
+static int g_tune_pbulk = 0;    // packed-row outputs by row-pair bulk stores (key 9; off: slower)
 static int g_tune_fuse = 0;    // one-call solve: forward Thomas fused into the y-pass (off: occupancy-starved, 12 ms vs 4 + 3)
 
 template <int P, int E, int MODE>
@@ -473,6 +538,8 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
              a.out_ld >= M && !(reinterpret_cast<uintptr_t>(a.dst) & 15) && !(a.out_ld & 1) &&
              !(a.out_ps & 1);
   if (k.mode == kYF && !a.tstore) return HFB_ERR_ARGUMENT;
+  a.pbulk = !a.tstore && (k.mode == kRow || k.mode == kTload) && E == 16 && g_tune_pbulk &&
+            a.out_ld == a.N && !(reinterpret_cast<uintptr_t>(a.dst) & 7);
   if (a.tstore) {
     gb = (gb + 127) & ~127;  // every group box 1-KB aligned (128B swizzle atoms)
   } else {
@@ -570,6 +637,7 @@ int tuning(int key) {
     case 4: return g_tune_tstore;
     case 5: return g_tune_fuse;
     case 6: return g_tune_overlap;
+    case 9: return g_tune_pbulk;
     case 7: return g_tune_cap_dst;
     case 8: return g_tune_cap_th;
     default: return 0;
@@ -584,6 +652,7 @@ void set_tuning(int key, int value) {
   if (key == 4) g_tune_tstore = value ? 1 : 0;
   if (key == 5) g_tune_fuse = value ? 1 : 0;
   if (key == 6) g_tune_overlap = value ? 1 : 0;
+  if (key == 9) g_tune_pbulk = value ? 1 : 0;
   if (key == 7) g_tune_cap_dst = value;
   if (key == 8) g_tune_cap_th = value;
 }
