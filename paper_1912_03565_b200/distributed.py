@@ -160,6 +160,24 @@ def blocks_to_solution(back, modes, grid, ex, rank, out=None):
     return out
 
 
+def check_status(grid, group=None, device=None):
+    """Agree across ranks on a latched vanishing pivot (synchronises); raises
+    SingularSystemError on every rank if any rank hit one."""
+    import torch
+    import torch.distributed as dist
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, dev)
+    flag = torch.zeros(1, dtype=torch.int64, device=dev)
+    try:
+        zplan.fetch_status()
+    except Exception:
+        flag.fill_(1)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if int(flag.item()):
+        from .errors import SingularSystemError
+        raise SingularSystemError("vanishing pivot on at least one rank")
+
+
 def chunk_layout(ex, chunks):
     """Chunked exchange geometry. Every rank's z-range is cut into `chunks` plane
     ranges (some may be empty); chunk c of all ranks travels in one all-to-all,
@@ -248,7 +266,8 @@ def solve_received_chunked(recv, level_plane, scheme, profile, grid, ex, rank):
     return zplan
 
 
-def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None, chunks=4):
+def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None, chunks=4,
+                      check=True):
     """Solve with the grid split over the ranks of `group`; z_slab is this rank's
     (kpz, n_y, n_x) CUDA float64 part of the folded RHS. Returns the solution slab
     (a new tensor). Raises SingularSystemError on every rank if any rank hit a
@@ -260,7 +279,10 @@ def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None, c
     With chunks > 1 the z-slab goes in `chunks` plane ranges: the all-to-all of
     chunk c runs (NCCL stream) while chunk c + 1 is transformed, and on the way
     back chunk c is unpacked and inverse-transformed while chunk c + 1 is in
-    flight; the z-solve reads the chunk-ordered y-slab through a level table."""
+    flight; the z-solve reads the chunk-ordered y-slab through a level table.
+
+    check=False skips the per-call pivot agreement (a host synchronisation);
+    call check_status(grid, group) after a batch of solves instead."""
     import torch
     import torch.distributed as dist
     rank, parts = dist.get_rank(group), dist.get_world_size(group)
@@ -302,7 +324,7 @@ def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None, c
     for w in works:
         w.wait()
     mark(1)
-    zplan = solve_received_chunked(recv, level_plane, scheme, profile, grid, ex, rank)
+    solve_received_chunked(recv, level_plane, scheme, profile, grid, ex, rank)
     mark(2)
     out = torch.empty((kpz, grid.n_y, grid.n_x), dtype=torch.float64, device=dev)
     backs, works = [], []
@@ -318,16 +340,8 @@ def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None, c
         c0, c1 = ranges[rank][c]
         inverse_chunk(backs[c], modes, out, grid, ex, c0, c1)
     mark(3)
-    # agree on the first failing pivot across ranks
-    flag = torch.zeros(1, dtype=torch.int64, device=dev)
-    try:
-        zplan.fetch_status()
-    except Exception:
-        flag.fill_(1)
-    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
-    if int(flag.item()):
-        from .errors import SingularSystemError
-        raise SingularSystemError("vanishing pivot on at least one rank")
+    if check:
+        check_status(grid, group, dev)
     if timings is not None:
         torch.cuda.synchronize(dev)
         timings.update(forward_exchange_s=ev[0].elapsed_time(ev[1]) / 1e3,
