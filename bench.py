@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", type=int, default=4)
-    ap.add_argument("--e2e-steps", type=int, default=12)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-planes", type=int, default=None,
                     help="z-planes of the oracle CPU sample (default: all n for the "
                          "cpu_baseline, n/4 per step for --impl reference)")
@@ -308,7 +308,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         vol_bytes = F.numel() * 8
-        # the pipelined path keeps two device volumes and four pinned host volumes;
+        # the pipelined path keeps three device volumes and four pinned host volumes;
         # 2047^3 (68.6 GB a volume) only fits the blocking in-place call
         pipelined = 4 * vol_bytes < 0.6 * host_ram_bytes() and args.cfg != 5
         if not multi and not pipelined:

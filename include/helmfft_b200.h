@@ -165,7 +165,8 @@ int hfb_status_fetch(hfb_plan* plan, void* stream, hfb_status* status);
  * stepping): each call enqueues H2D of host_rhs, the solve (on `stream`) and
  * D2H into host_out, and returns without waiting. The H2D of the next call and
  * the D2H of the previous one run on the plan's own copy streams while this
- * one solves; two device volumes alternate. Host buffers must be pinned and
+ * one solves; three device volumes rotate (two when a third does not fit),
+ * so a call's H2D never waits for the previous call's D2H. Host buffers must be pinned and
  * stay untouched until hfb_host_sync, which waits for every pending call and
  * reports a latched pivot failure like hfb_status_fetch. */
 int hfb_solve_host_async(hfb_plan* plan, const double* host_rhs, double* host_out, void* work,

@@ -124,7 +124,7 @@ extern "C" int hfb_plan_destroy(hfb_plan* p) {
     HostPipe* q = p->pipe;
     cudaStreamSynchronize(q->h2d);
     cudaStreamSynchronize(q->d2h);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kPipeMax; ++b) {
       cudaFree(q->buf[b]);
       cudaEventDestroy(q->h2d_done[b]);
       cudaEventDestroy(q->solved[b]);
@@ -416,13 +416,16 @@ static int host_pipe(hfb_plan* p, size_t bytes) {
   if (p->pipe) {
     HFB_CUDA(cudaStreamSynchronize(p->pipe->h2d));
     HFB_CUDA(cudaStreamSynchronize(p->pipe->d2h));
-    for (int b = 0; b < 2; ++b) cudaFree(p->pipe->buf[b]);
+    for (int b = 0; b < kPipeMax; ++b) {
+      cudaFree(p->pipe->buf[b]);
+      p->pipe->buf[b] = nullptr;
+    }
   } else {
     p->pipe = new HostPipe();
     HostPipe* q = p->pipe;
     HFB_CUDA(cudaStreamCreateWithFlags(&q->h2d, cudaStreamNonBlocking));
     HFB_CUDA(cudaStreamCreateWithFlags(&q->d2h, cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kPipeMax; ++b) {
       HFB_CUDA(cudaEventCreateWithFlags(&q->h2d_done[b], cudaEventDisableTiming));
       HFB_CUDA(cudaEventCreateWithFlags(&q->solved[b], cudaEventDisableTiming));
       HFB_CUDA(cudaEventCreateWithFlags(&q->d2h_done[b], cudaEventDisableTiming));
@@ -431,7 +434,16 @@ static int host_pipe(hfb_plan* p, size_t bytes) {
   }
   HostPipe* q = p->pipe;
   q->bytes = 0;
+  q->next = 0;
   for (int b = 0; b < 2; ++b) HFB_CUDA(cudaMalloc(&q->buf[b], bytes));
+  q->nbuf = 2;
+  // a third volume only with room to spare (the solve's workspace is already
+  // allocated by the caller)
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b > bytes + (bytes >> 3) &&
+      cudaMalloc(&q->buf[2], bytes) == cudaSuccess)
+    q->nbuf = 3;
+  cudaGetLastError();  // a refused third volume is not an error
   q->bytes = bytes;
   return HFB_OK;
 }
@@ -446,7 +458,7 @@ extern "C" int hfb_solve_host_async(hfb_plan* p, const double* hin, double* hout
   if (rc) return rc;
   HostPipe* q = p->pipe;
   const int b = q->next;
-  q->next ^= 1;
+  q->next = (b + 1) % q->nbuf;
   HFB_CUDA(cudaStreamWaitEvent(q->h2d, q->d2h_done[b], 0));
   HFB_CUDA(cudaMemcpyAsync(q->buf[b], hin, bytes, cudaMemcpyHostToDevice, q->h2d));
   HFB_CUDA(cudaEventRecord(q->h2d_done[b], q->h2d));

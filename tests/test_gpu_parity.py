@@ -547,8 +547,9 @@ def test_complex_k_large_vs_oracle(cuda, n):
 
 
 def test_pipelined_host_solves_match_blocking(cuda):
-    """hfb_solve_host_async: several right-hand sides in flight (two device
-    volumes, copy streams) give exactly the blocking hfb_solve_host results."""
+    """hfb_solve_host_async: several right-hand sides in flight (three device
+    volumes in rotation, copy streams) give exactly the blocking hfb_solve_host
+    results."""
     import ctypes
     import torch
     w = wl.workload(1)
