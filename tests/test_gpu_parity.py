@@ -875,3 +875,60 @@ def test_acceptance_convdiff_matches_reference(cuda, acceptance, n):
     mx, l2 = error_metrics(sol.values, u, g)
     ref = acceptance[f"cd_{n}"]
     assert abs(mx - ref[0]) <= 1e-6 * ref[0] and abs(l2 - ref[1]) <= 1e-6 * ref[1], (mx, l2, ref)
+
+
+def _random_case(rng):
+    """One seeded random problem: line lengths mixing powers of two (FFT engine)
+    and arbitrary N (dense DST), a scheme, a z-dependent or constant profile
+    and an execution mode."""
+    def extent():
+        return int(rng.choice([1, 3, 7, 15, 31, 63, 127, 255])) if rng.random() < 0.6 \
+            else int(rng.integers(1, 90))
+    nx, ny, nz = extent(), extent(), int(rng.integers(1, 70))
+    scheme = [hb.SchemeKind.SECOND_ORDER, hb.SchemeKind.FOURTH_ORDER, hb.SchemeKind.SIXTH_ORDER,
+              hb.SchemeKind.CONVECTION_DIFFUSION_4][int(rng.integers(0, 4))]
+    if scheme is hb.SchemeKind.SIXTH_ORDER:  # uniform grid (stencil.py:110-114)
+        h = 2.0 ** -int(rng.integers(3, 7))  # dyadic: (h (n + 1)) / (n + 1) == h exactly
+        dom = hb.Domain(0, h * (nx + 1), 0, h * (ny + 1), 0, h * (nz + 1))
+    else:
+        dom = hb.Domain(0, float(rng.uniform(0.5, 3)), 0, float(rng.uniform(0.5, 3)),
+                        0, float(rng.uniform(0.5, 3)))
+    g = hb.make_grid(dom, nx, ny, nz)
+    if scheme is hb.SchemeKind.CONVECTION_DIFFUSION_4:  # k^2 = 0 (stencil.py:143-144)
+        prof = hb.constant_profile(0.0, g, gamma=float(rng.uniform(-20, 20)))
+    elif rng.random() < 0.5:
+        a, b, c = float(rng.uniform(0, 4)), float(rng.uniform(0, 2)), float(rng.uniform(0.5, 3))
+        prof = hb.sample_profile(lambda z: a + b * np.sin(c * z), lambda z: b * c * np.cos(c * z),
+                                 lambda z: -b * c * c * np.sin(c * z), 0.0, g)
+    else:
+        prof = hb.constant_profile(float(rng.uniform(-5, 5)), g)
+    mode = [hb.SolverConfig(), hb.SolverConfig(mode=hb.SharedWorkers(2)),
+            hb.SolverConfig(mode=hb.Partitioned(int(rng.integers(1, 4))))][int(rng.integers(0, 3))]
+    return g, scheme, prof, mode
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_random_problems_vs_oracle(cuda, seed):
+    """Seeded sweep over shapes (1 to 255 points per axis, FFT and dense DST
+    lengths), schemes, constant and z-dependent profiles and execution modes:
+    the device solve matches the oracle to PARITY (relative L2), unless the
+    oracle itself reports a singular pivot, which the device must raise too."""
+    rng = np.random.default_rng(1000 + seed)
+    g, scheme, prof, cfg = _random_case(rng)
+    F = rng.standard_normal(g.shape)
+    T = oracle_table(scheme.value, prof, g)
+    try:
+        ref = orc.solve(F, T, *orc.mode_cosines(g.n_x, g.n_y))
+    except orc.OracleSingular:  # singular system in the oracle: the device raises as well
+        with pytest.raises(hb.SingularSystemError):
+            solve(F, scheme, prof, g, cfg)
+        return
+    from paper_1912_03565_b200.solver import _validate_config
+    try:
+        _validate_config(cfg, g)
+    except (ValueError, hb.InvalidPartitionError) as exc:  # the reference's bounds
+        with pytest.raises(type(exc)):
+            solve(F, scheme, prof, g, cfg)
+        return
+    u, _ = solve(F, scheme, prof, g, cfg)
+    assert rel_l2(u, ref) < PARITY, (g.shape, scheme, cfg)
