@@ -63,7 +63,9 @@ const char* hfb_strerror(int code);
 /* Number of kernels this library has launched in the process (all plans). */
 uint64_t hfb_launch_count(void);
 
-/* Performance knobs (no effect on results): key 0 = DST engine width
+/* Performance knobs (no effect on results). They are process-wide (every plan,
+ * every thread) and read when a kernel is launched: set them before the solves
+ * they should affect, not concurrently with them. key 0 = DST engine width
  * (16 or 32 values per thread), key 1 = transform groups per CTA (0 = auto),
  * key 2 = L2 promotion of the column (tensor-box) loads: 0 none, 1 64 B,
  * 2 128 B (default), 3 256 B; key 3 = batch order: 0 auto (interleaved over
