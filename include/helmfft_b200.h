@@ -80,7 +80,10 @@ uint64_t hfb_launch_count(void);
  * more than the overlap gains, 22.5 vs 21.7 ms at 1023^3), keys 7 / 8 = those
  * caps (CTAs per SM of the y-passes / of the z-solve); key 9 = write packed
  * rows (the user's array) by row-pair 1D bulk stores (1) or thread stores (0,
- * default: the register rotation it needs costs more than it saves). */
+ * default: the register rotation it needs costs more than it saves); key 10 =
+ * cap on resident CTAs per SM for every DST pass (0, default: occupancy);
+ * key 11 = how long the distributed z-solve waits for a neighbour's carry
+ * before latching an exchange error, in ms (0, default: 30000). */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.
@@ -297,6 +300,39 @@ int hfb_pack_modes(hfb_plan* plan, const double* modes, double* send, const int*
                    int parts, void* stream);
 int hfb_unpack_modes(hfb_plan* plan, const double* recv, double* modes, const int* y_starts,
                      int parts, void* stream);
+
+/* ---- transpose-free distributed z-solve ("alternative to
+ * measure next"; replaces the exchange_forward / solve / exchange_inverse
+ * sequence of the reference's Partitioned branch, solver.py:319-399) ----
+ * Every rank keeps its z-slab of mode rows (levels [z0, z0 + nzl) of the
+ * plan's n_z, layout of hfb_forward_modes, row stride ld = hfb_modes_ld) and
+ * the per-mode tridiagonal systems are swept across the ranks: the forward
+ * elimination (dir 0) takes (x', cp) at level z0 - 1 from rank p - 1 and
+ * hands its own last level to rank p + 1; the back substitution (dir 1) takes
+ * W at level z0 + nzl from rank p + 1 and hands W at z0 to rank p - 1. The
+ * carries move per 256-mode block through peer memory: the kernel stores into
+ * the neighbour's carry region and publishes each block by a release store of
+ * `epoch` into the neighbour's flag; the receiving CTA spins on it. One
+ * `epoch` per solve, the same on every rank, increasing (flags start at 0).
+ *   hfb_carry_layout: doubles of one rank's carry region (zero it once) and the
+ *     number of flag blocks;
+ *   hfb_zsolve_carry: `mine` = this rank's region, `peer` = the next rank's
+ *     (dir 0) or the previous rank's (dir 1), NULL exactly when there is none;
+ *     cp_work = ceil(nzl / 8) * n_x * ld doubles, shared by both directions;
+ *     the plan is the full-grid plan (coefficients of all n_z levels);
+ *   hfb_carry_check: synchronises `stream`; HFB_ERR_EXCHANGE when a carry never
+ *     arrived within the timeout (tuning key 11, ms; default 30 s), *code = 1
+ *     (forward carry from rank p - 1) or 2 (backward carry from rank p + 1);
+ *   hfb_ipc_handle / hfb_ipc_open / hfb_ipc_close: CUDA IPC of a device pointer
+ *     inside a larger allocation (64-byte handle + offset), for mapping the
+ *     neighbours' regions in a one-process-per-GPU run. */
+int hfb_carry_layout(hfb_plan* plan, int ld, long long* region_doubles, int* blocks);
+int hfb_zsolve_carry(hfb_plan* plan, int dir, double* modes, int ld, int z0, int nzl,
+                     void* cp_work, double* mine, double* peer, uint32_t epoch, void* stream);
+int hfb_carry_check(hfb_plan* plan, void* stream, int* code);
+int hfb_ipc_handle(const void* ptr, void* handle, long long* offset);
+int hfb_ipc_open(const void* handle, long long offset, void** ptr);
+int hfb_ipc_close(void* ptr, long long offset);
 
 #ifdef __cplusplus
 }

@@ -118,6 +118,7 @@ extern "C" int hfb_plan_destroy(hfb_plan* p) {
   cudaFree(p->cx);
   cudaFree(p->cy);
   cudaFree(p->err);
+  cudaFree(p->xerr);
   cudaFree(p->ystarts);
   cudaFree(p->dev_io);
   if (p->pipe) {

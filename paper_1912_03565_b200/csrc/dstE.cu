@@ -468,6 +468,8 @@ static int g_tune_cap_dst = 2;  // its CTA caps per SM: y-passes (key 7), z-solv
 static int g_tune_cap_th = 1;
 static int g_tune_pbulk = 0;    // packed-row outputs by row-pair bulk stores (key 9; off: slower)
 static int g_tune_fuse = 0;    // one-call solve: forward Thomas fused into the y-pass (off: occupancy-starved, 12 ms vs 4 + 3)
+static int g_tune_cap_all = 0;  // cap on resident CTAs per SM for every DST pass (key 10; 0 = occupancy)
+static int g_tune_carry_ms = 0;  // distributed z-solve: carry wait timeout in ms (key 11; 0 = 30 s)
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
@@ -479,6 +481,7 @@ static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMa
   int per_sm = 1;
   HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, sm));
   if (a.max_per_sm > 0) per_sm = std::min(per_sm, a.max_per_sm);
+  if (g_tune_cap_all > 0) per_sm = std::min(per_sm, g_tune_cap_all);
   if (getenv("HFB_DEBUG"))
     fprintf(stderr, "dstE<P=%d,E=%d,mode=%d>: %d threads, %zu B smem, %d CTAs/SM\n", P, E, MODE,
             threads, sm, per_sm);
@@ -640,6 +643,8 @@ int tuning(int key) {
     case 9: return g_tune_pbulk;
     case 7: return g_tune_cap_dst;
     case 8: return g_tune_cap_th;
+    case 10: return g_tune_cap_all;
+    case 11: return g_tune_carry_ms;
     default: return 0;
   }
 }
@@ -655,6 +660,8 @@ void set_tuning(int key, int value) {
   if (key == 9) g_tune_pbulk = value ? 1 : 0;
   if (key == 7) g_tune_cap_dst = value;
   if (key == 8) g_tune_cap_th = value;
+  if (key == 10) g_tune_cap_all = value;
+  if (key == 11) g_tune_carry_ms = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

@@ -18,6 +18,13 @@ solver.py:146-201). Here each part is a rank (``torch.distributed``, backend
 (The reference's natural-layout blocks (kpz, kpy(q), n_x) are kept by
 split_sizes / exchange_*_collective for the gloo tests of the geometry.)
 
+solve_partitioned_carry is the transpose-free alternative:
+the z-slab stays on its rank for the whole solve and the z-solve itself is
+swept across the ranks, forward then backward, with O(n_x n_y) carries per
+rank boundary moving through peer memory (csrc/thomas_carry.cu). It needs
+no all-to-all, so it is not bound by the 2 (P-1) N^3 8 / P^2 bytes per GPU of
+the exchange.
+
 Ranges come from the reference's plan_partition (larger chunks first), so
 block extents are exactly (n_x, kpy(q), kpz(p)) as in ExchangePlan.
 """
@@ -26,7 +33,8 @@ import ctypes
 
 import numpy as np
 
-from ._native import check, get_plan, ptr
+from ._native import HFB_ERR_EXCHANGE, check, get_plan, ptr
+from .errors import ExchangeError
 from .solver import make_exchange_plan
 from .tridiag import device_coefficients
 
@@ -396,3 +404,238 @@ def solve_partitioned_local(values, scheme, profile, grid, parts, clock=None):
     ev[5].synchronize()
     sec = lambda a, b: ev[a].elapsed_time(ev[b]) / 1e3
     return out, (sec(0, 1) + sec(4, 5), sec(1, 2) + sec(3, 4), sec(2, 3))
+
+
+# ---------------------------------------------------------------------------
+# Transpose-free distributed z-solve (carries through peer memory)
+
+def carry_neighbours(rank, parts):
+    """(previous, next) rank of `rank` in the z-order of the slabs, None at the ends:
+    the forward carry goes rank -> next, the backward carry rank -> previous."""
+    return (rank - 1 if rank > 0 else None, rank + 1 if rank + 1 < parts else None)
+
+
+def carry_layout(plan, ld):
+    """(doubles of one rank's carry region, flag blocks) for the full-grid plan."""
+    size, nb = ctypes.c_longlong(0), ctypes.c_int(0)
+    check(plan.lib.hfb_carry_layout(plan.handle, ld, ctypes.byref(size), ctypes.byref(nb)),
+          "carry_layout")
+    return size.value, nb.value
+
+
+def carry_status_code(plan):
+    """0, or the latched missing-carry direction (1 forward, 2 backward); synchronises."""
+    code = ctypes.c_int(0)
+    rc = plan.lib.hfb_carry_check(plan.handle, plan.stream(), ctypes.byref(code))
+    if rc != HFB_ERR_EXCHANGE:
+        check(rc, "carry_check")
+    return code.value
+
+
+def exchange_error_for(code, rank):
+    """ExchangeError(sender, receiver) of a latched missing carry on `rank`."""
+    sender = rank - 1 if code == 1 else rank + 1
+    return ExchangeError(f"the z-solve carry from rank {sender} to rank {rank} never arrived",
+                         sender=sender, receiver=rank)
+
+
+class CarryLinks:
+    """One rank's carry region (zeroed device memory) and its neighbours'
+    regions mapped by CUDA IPC; the handles travel by all_gather_object on
+    `group` (any backend). `epoch` counts this rank's solves; every rank of the
+    group runs the same solves, so the epochs agree."""
+
+    def __init__(self, grid, group, device):
+        import torch
+        import torch.distributed as dist
+        self.rank, self.parts = dist.get_rank(group), dist.get_world_size(group)
+        self.plan = get_plan(grid.n_x, grid.n_y, grid.n_z, device)
+        lib = self.plan.lib
+        self.ld = int(lib.hfb_modes_ld(self.plan.handle))
+        size, self.blocks = carry_layout(self.plan, self.ld)
+        self.region = torch.zeros(size, dtype=torch.float64, device=device)
+        torch.cuda.synchronize(device)
+        handle, off = (ctypes.c_char * 64)(), ctypes.c_longlong(0)
+        check(lib.hfb_ipc_handle(ptr(self.region), handle, ctypes.byref(off)), "ipc_handle")
+        infos = [None] * self.parts
+        dist.all_gather_object(infos, (bytes(handle), off.value), group=group)
+        self._opened = []
+        prev, nxt = carry_neighbours(self.rank, self.parts)
+        self.prev = self._open(infos[prev]) if prev is not None else None
+        self.next = self._open(infos[nxt]) if nxt is not None else None
+        self.epoch = 0
+
+    def _open(self, info):
+        h, off = info
+        buf = (ctypes.c_char * 64).from_buffer_copy(h)
+        p = ctypes.c_void_p()
+        check(self.plan.lib.hfb_ipc_open(buf, off, ctypes.byref(p)), "ipc_open")
+        self._opened.append((p.value, off))
+        return p.value
+
+    def next_epoch(self):
+        self.epoch = self.epoch % 0xFFFFFFFF + 1  # never 0: the flags start at 0
+        return self.epoch
+
+    def close(self):
+        for p, off in self._opened:
+            self.plan.lib.hfb_ipc_close(p, off)
+        self._opened = []
+
+
+_links = {}
+
+
+def carry_links(grid, group, device):
+    key = (grid.n_x, grid.n_y, grid.n_z, id(group), str(device))
+    if key not in _links:
+        _links[key] = CarryLinks(grid, group, device)
+    return _links[key]
+
+
+def carry_zsolve(plan, modes, ld, z0, kpz, cp, mine, peer_next, peer_prev, epoch):
+    """Forward then backward sweep of one rank's slab of mode rows (both
+    launches on the current stream; the kernels wait for the neighbours)."""
+    st = plan.stream()
+    check(plan.lib.hfb_zsolve_carry(plan.handle, 0, ptr(modes), ld, z0, kpz, ptr(cp), ptr(mine),
+                                    peer_next, epoch, st), "zsolve_carry forward")
+    check(plan.lib.hfb_zsolve_carry(plan.handle, 1, ptr(modes), ld, z0, kpz, ptr(cp), ptr(mine),
+                                    peer_prev, epoch, st), "zsolve_carry backward")
+
+
+def check_status_carry(grid, group=None, device=None):
+    """Agree across ranks on a latched vanishing pivot or a missing carry
+    (synchronises); raises SingularSystemError / ExchangeError on every rank."""
+    import torch
+    import torch.distributed as dist
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    rank = dist.get_rank(group)
+    zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, dev)
+    flags = torch.zeros(3, dtype=torch.int64, device=dev)  # singular, exchange, rank of it
+    code = carry_status_code(zplan)
+    if code:
+        flags[1] = 1
+        flags[2] = rank * 4 + code
+    try:
+        zplan.fetch_status()
+    except Exception:
+        flags[0] = 1
+    dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+    if int(flags[1].item()):
+        r, c = divmod(int(flags[2].item()), 4)
+        raise exchange_error_for(c, r)
+    if int(flags[0].item()):
+        from .errors import SingularSystemError
+        raise SingularSystemError("vanishing pivot on at least one rank")
+
+
+def solve_partitioned_carry(z_slab, scheme, profile, grid, group=None, timings=None,
+                            check=True):
+    """solve_partitioned without the all-to-alls: the 2D DSTs run on the local
+    z-slab (mode rows, as in solve_partitioned) and the z-solve is swept across
+    the ranks with carries through peer memory. Same arguments and result.
+
+    check=False skips the per-call agreement on pivots and carries (a host
+    synchronisation); call check_status_carry(grid, group) after a batch."""
+    import torch
+    import torch.distributed as dist
+    rank, parts = dist.get_rank(group), dist.get_world_size(group)
+    ex = make_exchange_plan(grid, parts)
+    z0, z1 = ex.partition.z_ranges[rank]
+    kpz = z1 - z0
+    if tuple(z_slab.shape) != (kpz, grid.n_y, grid.n_x):
+        raise ValueError(f"z-slab shape {tuple(z_slab.shape)} != {(kpz, grid.n_y, grid.n_x)}")
+    dev = z_slab.device
+    links = carry_links(grid, group, dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timings is not None else None
+
+    def mark(i):
+        if ev is not None:
+            ev[i].record()
+
+    tplan = get_plan(grid.n_x, grid.n_y, kpz, dev)
+    ld = links.ld
+    modes = torch.empty(kpz * grid.n_x * ld, dtype=torch.float64, device=dev)
+    mark(0)
+    with tplan.lock:
+        work = tplan.workspace(5)
+        check_rc = tplan.lib.hfb_forward_modes(tplan.handle, ptr(z_slab.contiguous()), ptr(modes),
+                                               ptr(work), tplan.stream())
+        _check(check_rc, "forward_modes")
+    mark(1)
+    zplan = links.plan
+    with zplan.lock:
+        if scheme is not None:
+            device_coefficients(zplan, scheme, profile, grid)
+        cp = torch.empty(((kpz + 7) // 8) * grid.n_x * ld, dtype=torch.float64, device=dev)
+        carry_zsolve(zplan, modes, ld, z0, kpz, cp, links.region, links.next, links.prev,
+                     links.next_epoch())
+    mark(2)
+    out = torch.empty((kpz, grid.n_y, grid.n_x), dtype=torch.float64, device=dev)
+    with tplan.lock:
+        _check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(modes), ptr(out), tplan.stream()),
+               "inverse_modes")
+    mark(3)
+    if check:
+        check_status_carry(grid, group, dev)
+    if timings is not None:
+        torch.cuda.synchronize(dev)
+        timings.update(transform_s=(ev[0].elapsed_time(ev[1]) + ev[2].elapsed_time(ev[3])) / 1e3,
+                       exchange_s=0.0, tridiag_s=ev[1].elapsed_time(ev[2]) / 1e3)
+    return out
+
+
+_check = check
+
+
+def solve_partitioned_carry_local(values, scheme, profile, grid, parts):
+    """The carry path's per-rank stages for `parts` virtual ranks on ONE device,
+    run rank after rank: forward sweeps in rank order, backward sweeps in
+    reverse order, so every carry a launch waits for was published by an
+    earlier launch on the same stream (nothing waits on a concurrent kernel).
+    The peer regions are the other virtual ranks' device buffers. Bit-identical
+    to the one-call solve. Returns the solution volume."""
+    import torch
+    ex = make_exchange_plan(grid, parts)
+    dev = values.device
+    zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, dev)
+    ld = int(zplan.lib.hfb_modes_ld(zplan.handle))
+    size, _ = carry_layout(zplan, ld)
+    regions = [torch.zeros(size, dtype=torch.float64, device=dev) for _ in range(parts)]
+    modes, cps = [], []
+    for r, (z0, z1) in enumerate(ex.partition.z_ranges):
+        kpz = z1 - z0
+        tplan = get_plan(grid.n_x, grid.n_y, kpz, dev)
+        m = torch.empty(kpz * grid.n_x * ld, dtype=torch.float64, device=dev)
+        with tplan.lock:
+            work = tplan.workspace(5)
+            _check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(values[z0:z1].contiguous()),
+                                               ptr(m), ptr(work), tplan.stream()), "forward_modes")
+        modes.append(m)
+        cps.append(torch.empty(((kpz + 7) // 8) * grid.n_x * ld, dtype=torch.float64, device=dev))
+    with zplan.lock:
+        if scheme is not None:
+            device_coefficients(zplan, scheme, profile, grid)
+        st = zplan.stream()
+        zr = ex.partition.z_ranges
+        for r in range(parts):
+            nxt = ptr(regions[r + 1]) if r + 1 < parts else None
+            _check(zplan.lib.hfb_zsolve_carry(zplan.handle, 0, ptr(modes[r]), ld, zr[r][0],
+                                              zr[r][1] - zr[r][0], ptr(cps[r]), ptr(regions[r]),
+                                              nxt, 1, st), "zsolve_carry forward")
+        for r in reversed(range(parts)):
+            prv = ptr(regions[r - 1]) if r > 0 else None
+            _check(zplan.lib.hfb_zsolve_carry(zplan.handle, 1, ptr(modes[r]), ld, zr[r][0],
+                                              zr[r][1] - zr[r][0], ptr(cps[r]), ptr(regions[r]),
+                                              prv, 1, st), "zsolve_carry backward")
+    out = torch.empty_like(values)
+    for r, (z0, z1) in enumerate(ex.partition.z_ranges):
+        tplan = get_plan(grid.n_x, grid.n_y, z1 - z0, dev)
+        with tplan.lock:
+            _check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(modes[r]), ptr(out[z0:z1]),
+                                               tplan.stream()), "inverse_modes")
+    code = carry_status_code(zplan)
+    if code:
+        raise exchange_error_for(code, 0)
+    zplan.fetch_status()
+    return out

@@ -932,3 +932,158 @@ def test_random_problems_vs_oracle(cuda, seed):
         return
     u, _ = solve(F, scheme, prof, g, cfg)
     assert rel_l2(u, ref) < PARITY, (g.shape, scheme, cfg)
+
+
+# ------------------------------------- transpose-free distributed z-solve
+def _one_call(F, scheme, prof, g):
+    import torch
+    plan = hb._native.get_plan(g.n_x, g.n_y, g.n_z, F.device)
+    hb.tridiag.device_coefficients(plan, scheme, prof, g)
+    ref = torch.empty_like(F)
+    work = plan.workspace(0)
+    hb._native.check(plan.lib.hfb_solve(plan.handle, hb._native.ptr(F), hb._native.ptr(ref),
+                                        hb._native.ptr(work), plan.stream()), "solve")
+    plan.fetch_status()
+    return ref
+
+
+@pytest.mark.parametrize("parts,shape,scheme", [
+    (2, (63, 63, 63), "fourth"), (3, (127, 63, 50), "convdiff"), (8, (255, 255, 40), "fourth"),
+    (5, (31, 127, 23), "sixth"), (4, (63, 31, 9), "fourth"), (7, (127, 127, 64), "convdiff"),
+    (1, (63, 63, 20), "fourth")])
+def test_carry_zsolve_bitwise(cuda, parts, shape, scheme):
+    """The transpose-free distributed z-solve (every rank sweeps its own slab,
+    carries through the neighbours' regions; ranks run one after another on
+    one device) reproduces the one-call solve bit for bit: slabs shorter than
+    a checkpoint chunk (40 levels on 8 ranks), uneven slabs, non-cubic grids,
+    z-dependent k^2 and the nonsymmetric cd4 rows."""
+    import torch
+    from paper_1912_03565_b200 import distributed as hd
+    nx, ny, nz = shape
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+    if scheme == "fourth":
+        sk, prof = hb.SchemeKind.FOURTH_ORDER, hb.constant_profile(-20.0, g)
+    elif scheme == "convdiff":
+        sk, prof = hb.SchemeKind.CONVECTION_DIFFUSION_4, hb.constant_profile(0.0, g, gamma=-3.0)
+    else:
+        g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), 31, 31, 31) if nx != ny else g
+        k2 = 100 * (1 + 0.5 * np.sin(PI * np.linspace(0, 1, g.n_z + 2))) ** 2
+        sk = hb.SchemeKind.SIXTH_ORDER
+        prof = hb.CoefficientProfile(k2=k2, k2_z=np.gradient(k2), k2_zz=np.zeros_like(k2))
+        nx, ny, nz = g.n_x, g.n_y, g.n_z
+    F = torch.from_numpy(np.random.default_rng(parts + nz).standard_normal((nz, ny, nx))).cuda()
+    U = hd.solve_partitioned_carry_local(F, sk, prof, g, parts)
+    assert torch.equal(U, _one_call(F, sk, prof, g))
+
+
+def test_carry_zsolve_repeated_and_ranks_in_any_layout(cuda):
+    """Two solves in a row through fresh carry regions and through the same
+    plan give the same bits (epochs, checkpoints and carries do not leak)."""
+    import torch
+    from paper_1912_03565_b200 import distributed as hd
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), 127, 63, 33)
+    prof = hb.constant_profile(-5.0, g)
+    F = torch.from_numpy(np.random.default_rng(3).standard_normal(g.shape)).cuda()
+    a = hd.solve_partitioned_carry_local(F, hb.SchemeKind.FOURTH_ORDER, prof, g, 3)
+    b = hd.solve_partitioned_carry_local(F, hb.SchemeKind.FOURTH_ORDER, prof, g, 3)
+    c = hd.solve_partitioned_carry_local(F, hb.SchemeKind.FOURTH_ORDER, prof, g, 6)
+    assert torch.equal(a, b) and torch.equal(a, c)
+
+
+def test_carry_zsolve_reports_vanishing_pivot_like_one_call(cuda):
+    """A resonant mode: the carry path latches the same first failing (l, m, n)
+    key as the one-call solve (the pivot check uses the global level)."""
+    import torch
+    from paper_1912_03565_b200 import distributed as hd
+    g = hb.make_grid(hb.Domain(0, PI, 0, PI, 0, PI), 15, 15, 12)
+    sk = hb.SchemeKind.SECOND_ORDER
+    # k^2 that makes the z-system of mode (1, 1) singular: the 2nd-order rows
+    # are (1, di, 1) with di = 2 r_zx cx + 2 r_zy cy - 2 (r_zx + r_zy + 1) + h_z^2 k^2
+    # (stencil.py:70-82), eigenvalues di + 2 cos(pi r / (n_z + 1))
+    r_zx, r_zy = g.h_z**2 / g.h_x**2, g.h_z**2 / g.h_y**2
+    cx, cy, cz = (math.cos(PI / (n + 1)) for n in (g.n_x, g.n_y, g.n_z))
+    k2 = (2 * (r_zx + r_zy + 1) - 2 * r_zx * cx - 2 * r_zy * cy - 2 * cz) / g.h_z**2
+    prof = hb.constant_profile(k2, g)
+    F = torch.ones(g.shape, dtype=torch.float64, device="cuda")
+    with pytest.raises(hb.SingularSystemError) as e1:
+        _one_call(F, sk, prof, g)
+    with pytest.raises(hb.SingularSystemError) as e2:
+        hd.solve_partitioned_carry_local(F, sk, prof, g, 3)
+    assert (e2.value.n, e2.value.m) == (e1.value.n, e1.value.m) == (1, 1)
+
+
+def test_carry_missing_neighbour_latches_exchange_error(cuda):
+    """A rank whose forward carry never arrives gives up after the timeout
+    (tuning key 11) and reports ExchangeError(sender=rank-1, receiver=rank)
+    instead of hanging the GPU; the latch clears after it is read."""
+    import torch
+    from paper_1912_03565_b200 import distributed as hd
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), 63, 63, 16)
+    plan = hb._native.get_plan(63, 63, 16, torch.device("cuda", 0))
+    hb.tridiag.device_coefficients(plan, hb.SchemeKind.FOURTH_ORDER, hb.constant_profile(1.0, g), g)
+    ld = int(plan.lib.hfb_modes_ld(plan.handle))
+    size, _ = hd.carry_layout(plan, ld)
+    mine = torch.zeros(size, dtype=torch.float64, device="cuda")
+    modes = torch.zeros(8 * 63 * ld, dtype=torch.float64, device="cuda")
+    cp = torch.empty(63 * ld, dtype=torch.float64, device="cuda")
+    P = hb._native.ptr
+    lib = plan.lib
+    lib.hfb_set_tuning(11, 300)
+    try:
+        # "rank 1" of two (levels 8..15): nobody publishes its forward carry
+        hb._native.check(lib.hfb_zsolve_carry(plan.handle, 0, P(modes), ld, 8, 8, P(cp), P(mine),
+                                              None, 7, plan.stream()), "carry")
+        code = hd.carry_status_code(plan)
+    finally:
+        lib.hfb_set_tuning(11, 0)
+    assert code == 1
+    err = hd.exchange_error_for(code, 1)
+    assert isinstance(err, hb.ExchangeError) and (err.sender, err.receiver) == (0, 1)
+    assert hd.carry_status_code(plan) == 0
+    # argument checks: a peer is required exactly when a neighbour exists
+    assert lib.hfb_zsolve_carry(plan.handle, 0, P(modes), ld, 0, 8, P(cp), P(mine), None, 1,
+                                plan.stream()) == hb._native.HFB_ERR_ARGUMENT
+    assert lib.hfb_zsolve_carry(plan.handle, 1, P(modes), ld, 8, 8, P(cp), P(mine), P(mine), 1,
+                                plan.stream()) == 0
+    assert lib.hfb_zsolve_carry(plan.handle, 0, P(modes), ld, 10, 8, P(cp), P(mine), None, 1,
+                                plan.stream()) == hb._native.HFB_ERR_RANGE
+    plan.fetch_status()
+    hd.carry_status_code(plan)
+
+
+def _carry_nccl_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    try:
+        from paper_1912_03565_b200 import distributed as hd
+        torch.cuda.set_device(0)
+        g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), 63, 63, 63)
+        prof = hb.constant_profile(-20.0, g)
+        F = torch.from_numpy(np.random.default_rng(1).standard_normal((63, 63, 63))).cuda()
+        U = hd.solve_partitioned_carry(F, hb.SchemeKind.FOURTH_ORDER, prof, g)
+        V = hd.solve_partitioned_carry(F, hb.SchemeKind.FOURTH_ORDER, prof, g)
+        u, _ = hb.solve_discrete(hb.Field3D(F.cpu().numpy()), hb.BoundaryData.zero(),
+                                 hb.SchemeKind.FOURTH_ORDER, prof, g)
+        q.put((float(np.abs(U.cpu().numpy() - u.values).max()), bool(torch.equal(U, V))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_solve_partitioned_carry_nccl_single_rank(cuda):
+    """solve_partitioned_carry through a real NCCL process group (one rank: the
+    IPC handle of the carry region is taken and gathered; no neighbour to map)."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_carry_nccl_worker, args=(0, 1, port, q))
+    p.start()
+    p.join(300)
+    assert p.exitcode == 0
+    assert q.get(timeout=10) == (0.0, True)
