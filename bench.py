@@ -57,7 +57,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--partitioned-path", action="store_true",
-                    help="use the multi-GPU (partitioned, NCCL) path even at N = 1")
+                    help="use the multi-GPU (partitioned) path even at N = 1")
+    ap.add_argument("--exchange", default="carry", choices=["carry", "alltoall"],
+                    help="multi-GPU z-solve: transpose-free carries through peer memory "
+                         "(default) or the reference's slab<->pencil all-to-all over NCCL")
     return ap.parse_args()
 
 
@@ -78,11 +81,12 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
-def workload_config(w, n_gpus):
+def workload_config(w, n_gpus, exchange="carry"):
+    multi = ("zslab{}+peer_carry" if exchange == "carry" else "zslab{}+nccl_alltoall").format(n_gpus)
     return {"workload": f"cfg{w.cfg}: {WORKLOAD_TEXT[w.cfg]}", "n": w.n,
             "points": w.n ** 3, "scheme": getattr(w.scheme, "value", "table"),
             "rhs": w.rhs_kind, "seed": w.seed,
-            "parallelism": "single" if n_gpus == 1 else f"zslab{n_gpus}+nccl_alltoall",
+            "parallelism": "single" if n_gpus == 1 else multi,
             "l2_flush": f"inputs {w.n ** 3 * 8 / 1e9:.1f} GB >> 126 MB L2 (no flush needed)"}
 
 
@@ -260,9 +264,13 @@ def run_ours(args):
         F = torch.rand((z1 - z0, n, n), generator=g, device=dev, dtype=torch.float64)
         F.mul_(2.0).sub_(1.0)
 
+        solve_part = (hd.solve_partitioned_carry if args.exchange == "carry"
+                      else hd.solve_partitioned)
+        check_part = hd.check_status_carry if args.exchange == "carry" else hd.check_status
+
         def step():
-            # pivot agreement once after the timed loop (it synchronises the host)
-            hd.solve_partitioned(F, w.scheme, w.profile, w.grid, check=False)
+            # pivot (and carry) agreement once after the timed loop (it synchronises the host)
+            solve_part(F, w.scheme, w.profile, w.grid, check=False)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -287,7 +295,7 @@ def run_ours(args):
     launches = int(lib.hfb_launch_count() - l0)
     clocks = sampler.stop()
     if multi:
-        hd.check_status(w.grid, None, dev)
+        check_part(w.grid, None, dev)
     stage_ms = None
     if not multi:
         buf = (ctypes.c_float * (5 * args.steps))()
@@ -366,7 +374,7 @@ def run_ours(args):
             t0 = time.perf_counter()
             for _ in range(steps):
                 d = hin.to(dev, non_blocking=True)
-                u = hd.solve_partitioned(d, w.scheme, w.profile, w.grid)
+                u = solve_part(d, w.scheme, w.profile, w.grid)
                 hout.copy_(u, non_blocking=True)
                 torch.cuda.synchronize(dev)
             barrier()
@@ -377,7 +385,7 @@ def run_ours(args):
             nbytes = points * 8  # every rank copies its slab: the whole volume per step
         e2e = {"value": points / e2e_s, "unit": "pts/s", "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "ms_per_step": e2e_s * 1e3,
-               "path": "pinned H2D + solve_partitioned + pinned D2H per rank" if multi
+               "path": f"pinned H2D + {solve_part.__name__} + pinned D2H per rank" if multi
                else ("C-ABI hfb_solve_host_async, pinned host buffers, "
                      f"{args.e2e_steps} pipelined steps + hfb_host_sync") if pipelined
                else "C-ABI hfb_solve_host, one pinned host volume in place (blocking)"}
@@ -434,7 +442,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded, generated on device)",
-            "config": workload_config(w, world), "roofline": roofline, "cpu_baseline": cpu,
+            "config": workload_config(w, world, args.exchange), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "device": torch.cuda.get_device_name(dev)}
     print(json.dumps(line), flush=True)

@@ -470,6 +470,7 @@ static int g_tune_pbulk = 0;    // packed-row outputs by row-pair bulk stores (k
 static int g_tune_fuse = 0;    // one-call solve: forward Thomas fused into the y-pass (off: occupancy-starved, 12 ms vs 4 + 3)
 static int g_tune_cap_all = 0;  // cap on resident CTAs per SM for every DST pass (key 10; 0 = occupancy)
 static int g_tune_carry_ms = 0;  // distributed z-solve: carry wait timeout in ms (key 11; 0 = 30 s)
+static int g_tune_carry_cap = 0;  // distributed z-solve: CTAs per SM (key 12; 0 = occupancy)
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
@@ -645,6 +646,7 @@ int tuning(int key) {
     case 8: return g_tune_cap_th;
     case 10: return g_tune_cap_all;
     case 11: return g_tune_carry_ms;
+    case 12: return g_tune_carry_cap;
     default: return 0;
   }
 }
@@ -662,6 +664,7 @@ void set_tuning(int key, int value) {
   if (key == 8) g_tune_cap_th = value;
   if (key == 10) g_tune_cap_all = value;
   if (key == 11) g_tune_carry_ms = value;
+  if (key == 12) g_tune_carry_cap = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

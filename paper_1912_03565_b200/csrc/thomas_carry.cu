@@ -43,7 +43,7 @@ namespace hfb {
 namespace {
 constexpr int BM = 256;
 constexpr int K = kThomasChunk;
-constexpr int S = 3;
+constexpr int SMAX = 6;  // ring stages: 3 at full occupancy, 6 with one or two CTAs per SM
 
 struct CarryArgs {
   double* w;            // local slab: local level l at w + l * ps
@@ -101,6 +101,7 @@ __device__ void wait_block(const unsigned* flag, unsigned epoch, unsigned long l
 }
 
 // thread 0: bring local chunk c (levels c*K ..) and its weights into stage s
+template <int S>
 __device__ __forceinline__ void issue_chunk(const CarryArgs& a, double (*sdat)[K][BM],
                                             double (*scoef)[K * 12], uint64_t* bar,
                                             const double* base, uint32_t rowbytes, int c, int s) {
@@ -113,8 +114,8 @@ __device__ __forceinline__ void issue_chunk(const CarryArgs& a, double (*sdat)[K
 
 // DIR 0: forward elimination (chunks ascending), DIR 1: back substitution
 // (chunks descending); one launch per direction and rank.
-template <int DIR>
-__global__ void __launch_bounds__(BM) thomas_carry_kernel(CarryArgs a) {
+template <int DIR, int S>
+__global__ void __launch_bounds__(BM, 4) thomas_carry_kernel(CarryArgs a) {
   extern __shared__ __align__(16) double dyn[];
   double(*sdat)[K][BM] = reinterpret_cast<double(*)[K][BM]>(dyn);
   double(*scoef)[K * 12] = reinterpret_cast<double(*)[K * 12]>(dyn + S * K * BM);
@@ -149,8 +150,8 @@ __global__ void __launch_bounds__(BM) thomas_carry_kernel(CarryArgs a) {
     const double cxy = cxv * cyv;
     double* ck = a.cpk + (long long)n * a.ld + m0 + tid;
     if (tid == 0) {
-      issue_chunk(a, sdat, scoef, bar, base, rowbytes, chunk_of(0), 0);
-      if (nchunk > 1) issue_chunk(a, sdat, scoef, bar, base, rowbytes, chunk_of(1), 1);
+      for (int t = 0; t < S - 1 && t < nchunk; ++t)
+        issue_chunk<S>(a, sdat, scoef, bar, base, rowbytes, chunk_of(t), t);
     }
     // the carry in: forward (x', cp) at z0 - 1, backward W at z1
     double c = 0.0, x = 0.0;
@@ -177,10 +178,11 @@ __global__ void __launch_bounds__(BM) thomas_carry_kernel(CarryArgs a) {
     double cbelow = DIR ? cp_below(chunk_of(0)) : 0.0;
     for (int task = 0; task < nchunk; ++task) {
       const int s = task % S;
-      if (tid == 0 && task + 2 < nchunk) {
+      if (tid == 0 && task + S - 1 < nchunk) {
         bulk_wait_read<0>();  // stage s' was stored from at task - 1
         fence_proxy_async_smem();
-        issue_chunk(a, sdat, scoef, bar, base, rowbytes, chunk_of(task + 2), (task + 2) % S);
+        issue_chunk<S>(a, sdat, scoef, bar, base, rowbytes, chunk_of(task + S - 1),
+                       (task + S - 1) % S);
       }
       mbar_wait(&bar[s], (phase >> s) & 1u);
       phase ^= 1u << s;
@@ -302,11 +304,19 @@ int launch_thomas_carry(hfb_plan* p, int dir, double* data, long long ld, int z0
   const int ms = tuning(11);
   a.timeout_ns = (unsigned long long)(ms > 0 ? ms : 30000) * 1000000ULL;
   a.xerr = p->xerr;
+  // tuning key 12: CTAs per SM (0 = occupancy, 3-stage ring). Capped at one or
+  // two, the ring deepens to 6 stages (the HBM-bound sweep keeps its bytes in
+  // flight) and the blocks come in more, shorter waves: the pipeline bubble of
+  // a rank boundary is one wave per direction.
+  const int cap = tuning(12);
+  const int S = (cap == 1 || cap == 2) ? SMAX : 3;
   const size_t sm = sizeof(double) * (size_t)S * (K * BM + K * 12);
-  auto kern = dir ? thomas_carry_kernel<1> : thomas_carry_kernel<0>;
+  auto kern = dir ? (S == 3 ? thomas_carry_kernel<1, 3> : thomas_carry_kernel<1, SMAX>)
+                  : (S == 3 ? thomas_carry_kernel<0, 3> : thomas_carry_kernel<0, SMAX>);
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 1, sms = 148, dev = 0;
   HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BM, sm));
+  if (cap > 0) per_sm = std::min(per_sm, cap);
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long work = (long long)a.nrows * a.nbpr;
