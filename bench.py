@@ -152,10 +152,21 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def dist_setup(n_gpus):
+def dist_setup(n_gpus, force=False):
     import torch
     import torch.distributed as dist
+    if force and "RANK" not in os.environ:  # a one-rank group for --partitioned-path
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.update(RANK="0", LOCAL_RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(port))
     if n_gpus > 1 or "RANK" in os.environ:
+        # keep rank 0's stdout to the one JSON line (NCCL prints its version banner
+        # there at NCCL_DEBUG=VERSION)
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
         if not dist.is_initialized():
             local = int(os.environ.get("LOCAL_RANK", 0))
             torch.cuda.set_device(local)
@@ -229,7 +240,7 @@ def run_ours(args):
     from paper_1912_03565_b200 import _native, workloads as wl
     from paper_1912_03565_b200.tridiag import device_coefficients
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup(args.gpus, force=args.partitioned_path)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     w = wl.workload(args.cfg)
