@@ -83,7 +83,11 @@ uint64_t hfb_launch_count(void);
  * default: the register rotation it needs costs more than it saves); key 10 =
  * cap on resident CTAs per SM for every DST pass (0, default: occupancy);
  * key 11 = how long the distributed z-solve waits for a neighbour's carry
- * before latching an exchange error, in ms (0, default: 30000). */
+ * before latching an exchange error, in ms (0, default: 30000); key 12 = CTAs
+ * per SM of the distributed z-solve (0, default: occupancy; 1 or 2 deepen its
+ * copy ring); key 13 = write packed rows (the user's odd-pitch array) by 2D
+ * tensor stores of the destination viewed as flat 128-byte rows, head and tail
+ * by plain stores (1, default) or by thread stores (0). */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.

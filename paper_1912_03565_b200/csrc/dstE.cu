@@ -61,6 +61,10 @@ struct StreamArgs {
   int vec_out;            // TRAN: (line 2k, 2k+1) pairs are 16-byte aligned in dst
   int tstore;             // ROW/TLOAD: outputs leave by TMA tensor stores (omap)
   int pbulk;              // ROW/TLOAD into packed rows (ld = N): 1D bulk stores of row pairs
+  int ustore;             // ROW/TLOAD into packed rows (ld = N): a line pair is one run of 2N
+                          // doubles; its full 128-byte rows leave by a 2D tensor store of the
+                          // destination viewed as flat rows of 16 (umap: 127-row box, omap:
+                          // 126), the <= 15-element head and tail by thread stores
   // kYF: forward Thomas sweep (thomas_tma.cu arithmetic) on the y-pass outputs
   const double* coef;     // [l][k][(4a, 2b, 2c, d)]
   const double* cx;       // per line (x-mode)
@@ -135,7 +139,8 @@ constexpr int kMinBlocks = kMaxThreads<P, E, MODE> == 256 ? 1 : MODE == kYF ? 2 
 template <int P, int E, int MODE>
 __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MODE>))
     dstE_stream_kernel(StreamArgs a, FftArgs c, const __grid_constant__ CUtensorMap tmap,
-                       const __grid_constant__ CUtensorMap omap) {
+                       const __grid_constant__ CUtensorMap omap,
+                       const __grid_constant__ CUtensorMap umap) {
   extern __shared__ __align__(16) double sm_raw[];
   __shared__ BatchMeta meta;
   constexpr int M = FE<P, E>::M, T = FE<P, E>::T, SEG = FE<P, E>::SEG, Q = 2 * SEG;
@@ -242,7 +247,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
       long long pl2;
       int g2;
       if (threadIdx.x == 0 && batch_of(a, it + 1, pl2, g2)) {
-        if (a.tstore || a.pbulk) bulk_wait_read<0>();  // batch it-1's stores read stage s^1
+        if (a.tstore || a.pbulk || a.ustore) bulk_wait_read<0>();  // batch it-1's stores read stage s^1
         fence_proxy_async_smem();
         issue(it + 1, s ^ 1);
       }
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     double2* sb = reinterpret_cast<double2*>(gb);
     fftE_forward<P, E>(v, sb, etw, t, f);
     double2 out[Q];
-    if (MODE != kTran && (a.tstore || a.pbulk)) {
+    if (MODE != kTran && (a.tstore || a.pbulk || a.ustore)) {
       // Segment-aligned outputs staged as the group's tensor box [2 lines]
       // [M/16 segments][16] in the 128B-swizzle layout (granule h of smem row r
       // at h ^ (r & 7): conflict-free, since thread t owns whole segments),
@@ -347,6 +352,77 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
             if (r0 >= 0) tensor_s2g_4d(&omap, 0, 0, r0, (int)plane, gbuf(s, gg));
           }
           bulk_commit();
+        }
+      } else if (a.ustore) {
+        if constexpr (Q == 16) {
+          // The group's two lines are one run of 2N doubles at flat offset o of the
+          // destination; run element e sits at u = e - ha in the box of the flat
+          // 128-byte rows that start at o + ha (the first 16-aligned offset). Every
+          // element is staged at box row u >> 4 (128B-swizzled), head elements
+          // (u < 0) in the spare row -1 and tail elements past the full rows: the
+          // staging code is branch-free, and a thread's granule-aligned pairs are
+          // 16-byte stores on 8 distinct bank groups per 8 lanes. The full rows leave
+          // by one 2D tensor store (thread 0); the <= 15 head and tail elements by
+          // plain stores from shared memory.
+          const long long o = plane * a.out_ps + (long long)row0 * a.out_ld;
+          const int ha = (int)((16 - (o & 15)) & 15);
+          double* ub = gb + 128;  // box row 0: 1-KB aligned, row -1 below it
+#pragma unroll
+          for (int L = 0; L < 2; ++L) {
+            const int u0 = L * a.N + Q * t - ha;
+            auto at = [&](int u) { const int q = u >> 4, cc = u & 15;
+                                   return ub + q * 16 + 2 * ((cc >> 1) ^ (q & 7)) + (cc & 1); };
+            auto val = [&](int jj) { return L ? out[jj].y : out[jj].x; };
+            const bool last = Q * t + Q > a.N;  // the segment holding the padding position
+            if (!(u0 & 1)) {
+#pragma unroll
+              for (int jj = 0; jj < Q; jj += 2) {
+                double* d = at(u0 + jj);
+                if (jj < Q - 2 || !last)
+                  *reinterpret_cast<double2*>(d) = make_double2(val(jj), val(jj + 1));
+                else
+                  *d = val(jj);
+              }
+            } else {
+              *at(u0) = val(0);
+#pragma unroll
+              for (int jj = 1; jj < Q - 1; jj += 2)
+                *reinterpret_cast<double2*>(at(u0 + jj)) = make_double2(val(jj), val(jj + 1));
+              if (!last) *at(u0 + Q - 1) = val(Q - 1);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncthreads();
+          const int len = (v1 ? 2 : 1) * a.N;
+          const int nrows = (len - ha) >> 4;
+          const bool tma = v1 && (nrows == 126 || nrows == 127);
+          if (threadIdx.x == 0) {
+            for (int gg = 0; gg < a.NF; ++gg) {
+              const int r0 = meta.row[s][2 * gg];
+              if (r0 < 0 || meta.row[s][2 * gg + 1] < 0) continue;
+              const long long og = plane * a.out_ps + (long long)r0 * a.out_ld;
+              const int hg = (int)((16 - (og & 15)) & 15);
+              const int ng = (2 * a.N - hg) >> 4;
+              const int frow = (int)((og + hg) >> 4);
+              if (ng == 127) tensor_s2g_2d(&umap, 0, frow, gbuf(s, gg) + 128);
+              else if (ng == 126) tensor_s2g_2d(&omap, 0, frow, gbuf(s, gg) + 128);
+            }
+            bulk_commit();
+          }
+          if (v0) {
+            double* G = a.dst + o;
+            auto ld_u = [&](int u) {
+              const int q = u >> 4, cc = u & 15;
+              return ub[q * 16 + 2 * ((cc >> 1) ^ (q & 7)) + (cc & 1)];
+            };
+            if (tma) {
+              if (t < ha) G[t] = ld_u(t - ha);
+              const int e = ha + 16 * nrows + t;
+              if (e < len) G[e] = ld_u(e - ha);
+            } else {
+              for (int e = t; e < len; e += T) G[e] = ld_u(e - ha);
+            }
+          }
         }
       } else if constexpr (Q == 16) {
         // Packed rows (ld = N): the group's two lines are one contiguous run of
@@ -436,7 +512,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     __syncthreads();  // stage s is free for the prefetch issued next iteration
     s ^= 1;
   }
-  if ((a.tstore || a.pbulk) && threadIdx.x == 0) bulk_wait<0>();  // smem valid until stored
+  if ((a.tstore || a.pbulk || a.ustore) && threadIdx.x == 0) bulk_wait<0>();  // smem valid until stored
 }
 
 bool dst16_ok(int M) { return M >= 16 && M <= 4096 && (M & (M - 1)) == 0; }
@@ -471,10 +547,12 @@ static int g_tune_fuse = 0;    // one-call solve: forward Thomas fused into the 
 static int g_tune_cap_all = 0;  // cap on resident CTAs per SM for every DST pass (key 10; 0 = occupancy)
 static int g_tune_carry_ms = 0;  // distributed z-solve: carry wait timeout in ms (key 11; 0 = 30 s)
 static int g_tune_carry_cap = 0;  // distributed z-solve: CTAs per SM (key 12; 0 = occupancy)
+static int g_tune_ustore = 1;  // packed-row outputs by flat-row tensor stores (key 13)
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
-                         const CUtensorMap& omap, int threads, size_t sm, cudaStream_t st) {
+                         const CUtensorMap& omap, const CUtensorMap& umap, int threads, size_t sm,
+                         cudaStream_t st) {
   auto kern = dstE_stream_kernel<P, E, MODE>;
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -505,7 +583,7 @@ static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMa
   } else if (MODE == kTload) {
     b.run = 2;  // pairs of neighbouring column blocks (measured best at W = 4)
   }
-  kern<<<(unsigned)blocks, threads, sm, st>>>(b, c, tmap, omap);
+  kern<<<(unsigned)blocks, threads, sm, st>>>(b, c, tmap, omap, umap);
   return HFB_OK;
 }
 
@@ -544,7 +622,11 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   if (k.mode == kYF && !a.tstore) return HFB_ERR_ARGUMENT;
   a.pbulk = !a.tstore && (k.mode == kRow || k.mode == kTload) && E == 16 && g_tune_pbulk &&
             a.out_ld == a.N && !(reinterpret_cast<uintptr_t>(a.dst) & 7);
-  if (a.tstore) {
+  a.ustore = !a.tstore && !a.pbulk && (k.mode == kRow || k.mode == kTload) && E == 16 &&
+             g_tune_ustore && M == 1024 && a.out_ld == a.N &&
+             !(reinterpret_cast<uintptr_t>(a.dst) & 15);
+  if (a.ustore) gb = std::max(gb, 128 + 130 * 16);  // spare KB + rows -1 .. 128 of the flat box
+  if (a.tstore || a.ustore) {
     gb = (gb + 127) & ~127;  // every group box 1-KB aligned (128B swizzle atoms)
   } else {
     const int want = 16 / a.NF;  // group offsets spread over the 8 16-byte bank groups
@@ -565,6 +647,24 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return HFB_ERR_ARGUMENT;
+  }
+  CUtensorMap umap;
+  memset(&umap, 0, sizeof(umap));
+  if (a.ustore) {
+    // the destination as flat 128-byte rows: [16 doubles][rows], boxes of 127 / 126 rows
+    auto enc = tensor_encoder();
+    if (!enc) return HFB_ERR_CUDA;
+    const long long total = (long long)(a.z0 + a.nz) * a.out_ps;  // doubles from dst
+    cuuint64_t dims[2] = {16, (cuuint64_t)(total / 16)};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t estr[2] = {1, 1};
+    for (int h = 0; h < 2; ++h) {
+      cuuint32_t box[2] = {16, (cuuint32_t)(h ? 126 : 127)};
+      CUresult r = enc(h ? &omap : &umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a.dst, dims, strides,
+                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return HFB_ERR_ARGUMENT;
+    }
   }
   long long stage = (long long)a.NF * a.gbuf;
   CUtensorMap tmap;
@@ -613,11 +713,11 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
     a.nz_total = k.nz_total;
     a.ny_total = a.N;
     a.nx_total = a.nrow;
-    return launch_stream<P, E, kYF>(a, c, tmap, omap, threads, sm, st);
+    return launch_stream<P, E, kYF>(a, c, tmap, omap, umap, threads, sm, st);
   }
-  if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, tmap, omap, threads, sm, st);
-  if (k.mode == kTload) return launch_stream<P, E, kTload>(a, c, tmap, omap, threads, sm, st);
-  return launch_stream<P, E, kRow>(a, c, tmap, omap, threads, sm, st);
+  if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, tmap, omap, umap, threads, sm, st);
+  if (k.mode == kTload) return launch_stream<P, E, kTload>(a, c, tmap, omap, umap, threads, sm, st);
+  return launch_stream<P, E, kRow>(a, c, tmap, omap, umap, threads, sm, st);
 }
 
 template <int P>
@@ -647,6 +747,7 @@ int tuning(int key) {
     case 10: return g_tune_cap_all;
     case 11: return g_tune_carry_ms;
     case 12: return g_tune_carry_cap;
+    case 13: return g_tune_ustore;
     default: return 0;
   }
 }
@@ -665,6 +766,7 @@ void set_tuning(int key, int value) {
   if (key == 10) g_tune_cap_all = value;
   if (key == 11) g_tune_carry_ms = value;
   if (key == 12) g_tune_carry_cap = value;
+  if (key == 13) g_tune_ustore = value ? 1 : 0;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

@@ -60,6 +60,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// 2D tiled tensor store of a shared-memory box (bulk-group completion).
+__device__ __forceinline__ void tensor_s2g_2d(const void* tmap, int c0, int c1, const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+}
 }  // namespace hfb
 
 namespace hfb {
