@@ -1087,3 +1087,29 @@ def test_solve_partitioned_carry_nccl_single_rank(cuda):
     p.join(300)
     assert p.exitcode == 0
     assert q.get(timeout=10) == (0.0, True)
+
+
+@pytest.mark.parametrize("shape", [(1023, 15, 6), (1023, 31, 5), (2047, 15, 3), (1023, 1023, 2)])
+def test_flat_row_final_pass_bitwise(cuda, shape):
+    """The final inverse x-pass writing the user's odd-pitch rows by flat-128B-row
+    tensor stores (tuning key 13, on at M = 1024 / 2048) equals the thread-store
+    path bit for bit, odd and even planes, and against the oracle."""
+    import torch
+    nx, ny, nz = shape
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+    prof = hb.constant_profile(-7.0, g)
+    F = torch.from_numpy(np.random.default_rng(nx + nz).standard_normal((nz, ny, nx))).cuda()
+    plan = hb._native.get_plan(nx, ny, nz, F.device)
+    lib = plan.lib
+    outs = []
+    for key in (1, 0):
+        lib.hfb_set_tuning(13, key)
+        try:
+            outs.append(_one_call(F, hb.SchemeKind.FOURTH_ORDER, prof, g))
+        finally:
+            lib.hfb_set_tuning(13, 1)
+    assert torch.equal(outs[0], outs[1])
+    if nx * ny * nz <= 2e5:
+        ref = orc.solve(F.cpu().numpy(), oracle_table("4", prof, g),
+                        *orc.mode_cosines(nx, ny), workers=4)
+        assert rel_l2(outs[0].cpu().numpy(), ref) < PARITY
