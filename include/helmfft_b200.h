@@ -87,7 +87,9 @@ uint64_t hfb_launch_count(void);
  * per SM of the distributed z-solve (0, default: occupancy; 1 or 2 deepen its
  * copy ring); key 13 = write packed rows (the user's odd-pitch array) by 2D
  * tensor stores of the destination viewed as flat 128-byte rows, head and tail
- * by plain stores (1, default) or by thread stores (0). */
+ * by plain stores (1, default) or by thread stores (0); key 14 = row passes
+ * with tensor stores run the transform groups of a CTA decoupled (own prefetch,
+ * mbarrier and store; 1, default) or in CTA lockstep (0). */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.

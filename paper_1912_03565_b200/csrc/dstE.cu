@@ -61,6 +61,8 @@ struct StreamArgs {
   int vec_out;            // TRAN: (line 2k, 2k+1) pairs are 16-byte aligned in dst
   int tstore;             // ROW/TLOAD: outputs leave by TMA tensor stores (omap)
   int pbulk;              // ROW/TLOAD into packed rows (ld = N): 1D bulk stores of row pairs
+  int indep;              // ROW with tensor stores: the groups of a CTA run decoupled (own
+                          // prefetch, mbarrier and tensor store; named-barrier syncs only)
   int ustore;             // ROW/TLOAD into packed rows (ld = N): a line pair is one run of 2N
                           // doubles; its full 128-byte rows leave by a 2D tensor store of the
                           // destination viewed as flat rows of 16 (umap: 2N/16-row box,
@@ -171,9 +173,16 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
       for (int j = 0; j < Q; ++j) yx[L][j] = 0.0;
   }
 
+  __shared__ uint64_t gbar[2][kMaxRows / 2];  // indep: per stage and group
+  const bool indep = MODE == kRow && a.indep;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    if (indep)
+      for (int gg = 0; gg < a.NF; ++gg) {
+        mbar_init(&gbar[0][gg], 1);
+        mbar_init(&gbar[1][gg], 1);
+      }
     mbar_fence_init();
   }
   __syncthreads();
@@ -231,6 +240,47 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     }
   };
 
+  // indep (ROW): the leader of group f brings the group's two rows of batch `it`
+  // into its own buffer of stage s, completing on gbar[s][f]
+  auto issue_rows = [&](long long it, int s) {
+    long long plane;
+    int g;
+    batch_of(a, it, plane, g);
+    uint32_t total = 0;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1) mbar_arrive_expect_tx(&gbar[s][f], total);
+#pragma unroll 1
+      for (int r = 2 * f; r < 2 * f + 2; ++r) {
+        const int k = g * a.NF + (r >> 1);
+        const int row = 2 * k + (r & 1);
+        if (k >= a.ppp || row >= a.nrow) {
+          if (pass == 0) {
+            meta.row[s][r] = -1;
+            meta.delta[s][r] = 2;
+          }
+          continue;
+        }
+        const double* A = a.src + plane * a.in_ps + (long long)row * a.in_ld;
+        const double* A16 =
+            reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(A) & ~uintptr_t(15));
+        const int d = (int)(A - A16);
+        uint32_t S = (uint32_t)((8 * (a.N + d) + 15) & ~15);
+        const bool cut = A16 + S / 8 > a.src_end;
+        if (cut) S -= 16;
+        double* dstrow = gbuf(s, f) + (r & 1) * a.rowslot + 2;
+        if (pass == 0) {
+          total += S;
+          meta.row[s][r] = row;
+          meta.delta[s][r] = 2 + d;
+          if (cut) dstrow[d + a.N - 1] = __ldg(A + a.N - 1);  // not covered by the copy
+        } else {
+          bulk_g2s(dstrow, A16, S, &gbar[s][f]);
+        }
+      }
+    }
+  };
+
   EngineTw<P, E> etw;
   engine_tw<P, E>(c.tw, c.sn, t, etw);
   int s = 0;
@@ -238,7 +288,11 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
   {
     long long pl;
     int g;
-    if (threadIdx.x == 0 && batch_of(a, 0, pl, g)) issue(0, 0);
+    if (indep) {
+      if (t == 0 && batch_of(a, 0, pl, g)) issue_rows(0, 0);
+    } else if (threadIdx.x == 0 && batch_of(a, 0, pl, g)) {
+      issue(0, 0);
+    }
   }
   for (long long it = 0;; ++it) {
     long long plane;
@@ -247,13 +301,19 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     {
       long long pl2;
       int g2;
-      if (threadIdx.x == 0 && batch_of(a, it + 1, pl2, g2)) {
+      if (indep) {
+        if (t == 0 && batch_of(a, it + 1, pl2, g2)) {
+          bulk_wait_read<0>();  // this group's batch it-1 store read its buffer of stage s^1
+          fence_proxy_async_smem();
+          issue_rows(it + 1, s ^ 1);
+        }
+      } else if (threadIdx.x == 0 && batch_of(a, it + 1, pl2, g2)) {
         if (a.tstore || a.pbulk || a.ustore) bulk_wait_read<0>();  // batch it-1's stores read stage s^1
         fence_proxy_async_smem();
         issue(it + 1, s ^ 1);
       }
     }
-    mbar_wait(&bar[s], s == 0 ? phase0 : phase1);
+    mbar_wait(indep ? &gbar[s][f] : &bar[s], s == 0 ? phase0 : phase1);
     if (s == 0) phase0 ^= 1; else phase1 ^= 1;
 
     double* gb = gbuf(s, f);
@@ -346,13 +406,21 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
           }
         }
         fence_proxy_async_smem();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          for (int gg = 0; gg < a.NF; ++gg) {
-            const int r0 = meta.row[s][2 * gg];
-            if (r0 >= 0) tensor_s2g_4d(&omap, 0, 0, r0, (int)plane, gbuf(s, gg));
+        if (indep) {
+          group_sync<T>(f);
+          if (t == 0) {
+            if (row0 >= 0) tensor_s2g_4d(&omap, 0, 0, row0, (int)plane, gb);
+            bulk_commit();
           }
-          bulk_commit();
+        } else {
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            for (int gg = 0; gg < a.NF; ++gg) {
+              const int r0 = meta.row[s][2 * gg];
+              if (r0 >= 0) tensor_s2g_4d(&omap, 0, 0, r0, (int)plane, gbuf(s, gg));
+            }
+            bulk_commit();
+          }
         }
       } else if (a.ustore) {
         if constexpr (Q == 16) {
@@ -511,10 +579,14 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         }
       }
     }
-    __syncthreads();  // stage s is free for the prefetch issued next iteration
+    if (indep)
+      group_sync<T>(f);  // the group's buffer of stage s is free for its next prefetch
+    else
+      __syncthreads();  // stage s is free for the prefetch issued next iteration
     s ^= 1;
   }
-  if ((a.tstore || a.pbulk || a.ustore) && threadIdx.x == 0) bulk_wait<0>();  // smem valid until stored
+  if ((a.tstore || a.pbulk || a.ustore) && (indep ? t == 0 : threadIdx.x == 0))
+    bulk_wait<0>();  // smem valid until stored
 }
 
 bool dst16_ok(int M) { return M >= 16 && M <= 4096 && (M & (M - 1)) == 0; }
@@ -550,6 +622,7 @@ static int g_tune_cap_all = 0;  // cap on resident CTAs per SM for every DST pas
 static int g_tune_carry_ms = 0;  // distributed z-solve: carry wait timeout in ms (key 11; 0 = 30 s)
 static int g_tune_carry_cap = 0;  // distributed z-solve: CTAs per SM (key 12; 0 = occupancy)
 static int g_tune_ustore = 1;  // packed-row outputs by flat-row tensor stores (key 13)
+static int g_tune_indep = 1;   // ROW passes with tensor stores: decoupled groups (key 14)
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
@@ -652,6 +725,7 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return HFB_ERR_ARGUMENT;
   }
+  a.indep = k.mode == kRow && a.tstore && g_tune_indep && T >= 32;
   CUtensorMap umap;
   memset(&umap, 0, sizeof(umap));
   if (a.ustore) {
@@ -753,6 +827,7 @@ int tuning(int key) {
     case 11: return g_tune_carry_ms;
     case 12: return g_tune_carry_cap;
     case 13: return g_tune_ustore;
+    case 14: return g_tune_indep;
     default: return 0;
   }
 }
@@ -772,6 +847,7 @@ void set_tuning(int key, int value) {
   if (key == 11) g_tune_carry_ms = value;
   if (key == 12) g_tune_carry_cap = value;
   if (key == 13) g_tune_ustore = value ? 1 : 0;
+  if (key == 14) g_tune_indep = value ? 1 : 0;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

@@ -413,12 +413,17 @@ def tuning():
     lib.hfb_set_tuning(5, 0)
     lib.hfb_set_tuning(6, 0)
     lib.hfb_set_tuning(9, 0)
+    lib.hfb_set_tuning(10, 0)
+    lib.hfb_set_tuning(13, 1)
+    lib.hfb_set_tuning(14, 1)
 
 
 @pytest.mark.parametrize("knobs", [((0, 32),), ((0, 32), (1, 2)), ((0, 32), (1, 1)), ((1, 1),),
                                    ((2, 0),), ((2, 3),), ((3, 1),), ((3, 3),), ((4, 0),),
                                    ((0, 32), (4, 0)), ((5, 0),), ((0, 32), (5, 1)),
-                                   ((6, 1),), ((6, 1), (7, 1), (8, 2)), ((9, 1),)])
+                                   ((6, 1),), ((6, 1), (7, 1), (8, 2)), ((9, 1),),
+                                   ((14, 0),), ((14, 0), (13, 0)), ((1, 1), (14, 1)),
+                                   ((10, 2),)])
 def test_tuning_variants_match_oracle(cuda, tuning, knobs):
     """Performance knobs change the FFT factorisation or the CTA shape, never
     the result beyond rounding: transforms (row, transposed-store and
