@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
   }
 
   __shared__ uint64_t gbar[2][kMaxRows / 2];  // indep: per stage and group
-  const bool indep = MODE == kRow && a.indep;
+  const bool indep = (MODE == kRow || MODE == kTload) && a.indep;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -281,6 +281,22 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     }
   };
 
+  // indep (TLOAD): the leader of group f brings the group's two columns of batch
+  // `it` as unswizzled [pos][2 lines] boxes into its own buffer of stage s
+  auto issue_box = [&](long long it, int s) {
+    long long plane;
+    int g;
+    batch_of(a, it, plane, g);
+    for (int r = 2 * f; r < 2 * f + 2; ++r) {
+      const int row = g * W + r;
+      meta.row[s][r] = row < a.nrow ? row : -1;
+    }
+    mbar_arrive_expect_tx(&gbar[s][f], (uint32_t)(a.nbox * a.boxn * 2 * 8));
+    for (int b = 0; b < a.nbox; ++b)
+      tensor_g2s_3d(gbuf(s, f) + (long long)b * a.boxn * 2, &tmap, g * W + 2 * f, b * a.boxn,
+                    (int)plane, &gbar[s][f]);
+  };
+
   EngineTw<P, E> etw;
   engine_tw<P, E>(c.tw, c.sn, t, etw);
   int s = 0;
@@ -289,7 +305,9 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     long long pl;
     int g;
     if (indep) {
-      if (t == 0 && batch_of(a, 0, pl, g)) issue_rows(0, 0);
+      if (t == 0 && batch_of(a, 0, pl, g)) {
+        if constexpr (TL) issue_box(0, 0); else issue_rows(0, 0);
+      }
     } else if (threadIdx.x == 0 && batch_of(a, 0, pl, g)) {
       issue(0, 0);
     }
@@ -305,7 +323,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         if (t == 0 && batch_of(a, it + 1, pl2, g2)) {
           bulk_wait_read<0>();  // this group's batch it-1 store read its buffer of stage s^1
           fence_proxy_async_smem();
-          issue_rows(it + 1, s ^ 1);
+          if constexpr (TL) issue_box(it + 1, s ^ 1); else issue_rows(it + 1, s ^ 1);
         }
       } else if (threadIdx.x == 0 && batch_of(a, it + 1, pl2, g2)) {
         if (a.tstore || a.pbulk || a.ustore) bulk_wait_read<0>();  // batch it-1's stores read stage s^1
@@ -325,12 +343,19 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
       // box [pos][W]: a_e of lines (2f, 2f+1) is the double2 at pos e - 1
       // (absent lines and positions >= N were zero-filled by the TMA engine)
       // (the box is swizzled: 16-byte granule g sits at g ^ ((g >> 3) & (NF - 1)))
-      const double2* bx = reinterpret_cast<const double2*>(gbuf(s, 0));
-      dstE_pre<P, E>(v, c.sn, etw, t, [&](int e) -> double2 {
-        const int gr = ((e + M - 1) & (M - 1)) * a.NF + f;
-        return bx[gr ^ ((gr >> 3) & (a.NF - 1))];
-      });
-      __syncthreads();  // the box interleaves all groups' lines
+      if (indep) {  // the group's own [pos][2 lines] box, unswizzled
+        const double2* bx = reinterpret_cast<const double2*>(gb);
+        dstE_pre<P, E>(v, c.sn, etw, t,
+                       [&](int e) -> double2 { return bx[(e + M - 1) & (M - 1)]; });
+        group_sync<T>(f);
+      } else {
+        const double2* bx = reinterpret_cast<const double2*>(gbuf(s, 0));
+        dstE_pre<P, E>(v, c.sn, etw, t, [&](int e) -> double2 {
+          const int gr = ((e + M - 1) & (M - 1)) * a.NF + f;
+          return bx[gr ^ ((gr >> 3) & (a.NF - 1))];
+        });
+        __syncthreads();  // the box interleaves all groups' lines
+      }
     } else {
       const double* r0 = gb + meta.delta[s][2 * f] - 1;  // a_e at r0[e]
       const double* r1 = gb + a.rowslot + meta.delta[s][2 * f + 1] - 1;
@@ -461,12 +486,20 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
             }
           }
           fence_proxy_async_smem();
-          __syncthreads();
           const int len = (v1 ? 2 : 1) * a.N;
           const int nrows = (len - ha) >> 4;
           const int hi = (2 * a.N) >> 4;  // full rows of a pair run: hi or hi - 1
           const bool tma = v1 && (nrows == hi || nrows == hi - 1);
-          if (threadIdx.x == 0) {
+          if (indep) {
+            group_sync<T>(f);
+            if (t == 0) {
+              if (tma) tensor_s2g_2d(nrows == hi ? &umap : &omap, 0, (int)((o + ha) >> 4), ub);
+              bulk_commit();
+            }
+          } else {
+            __syncthreads();
+          }
+          if (!indep && threadIdx.x == 0) {
             for (int gg = 0; gg < a.NF; ++gg) {
               const int r0 = meta.row[s][2 * gg];
               if (r0 < 0 || meta.row[s][2 * gg + 1] < 0) continue;
@@ -725,7 +758,11 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return HFB_ERR_ARGUMENT;
   }
-  a.indep = k.mode == kRow && a.tstore && g_tune_indep && T >= 32;
+  // decoupled groups: row passes, and column passes at M = 2048 (measured: x 3.90 -> 3.78,
+  // inverse y 3.92 -> 3.82 ms at 1023^3; final x-pass 46.3 -> 42.3 ms at 2047^3; the
+  // column passes at M = 1024 got slower with per-group boxes, 4.28 -> 4.57 ms)
+  a.indep = (k.mode == kRow || (k.mode == kTload && M == 2048)) && (a.tstore || a.ustore) &&
+            g_tune_indep && T >= 32;
   CUtensorMap umap;
   memset(&umap, 0, sizeof(umap));
   if (a.ustore) {
@@ -758,11 +795,13 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
       return HFB_ERR_ARGUMENT;
     cuuint64_t dims[3] = {(cuuint64_t)a.nrow, (cuuint64_t)a.N, (cuuint64_t)(a.z0 + a.nz)};
     cuuint64_t strides[2] = {(cuuint64_t)a.in_ld * 8, (cuuint64_t)a.in_ps * 8};
-    cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)a.boxn, 1};
+    // indep: one unswizzled [pos][2 lines] box per group
+    cuuint32_t box[3] = {(cuuint32_t)(a.indep ? 2 : W), (cuuint32_t)a.boxn, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(a.src), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     a.NF == 8   ? CU_TENSOR_MAP_SWIZZLE_128B
+                     a.indep     ? CU_TENSOR_MAP_SWIZZLE_NONE
+                     : a.NF == 8 ? CU_TENSOR_MAP_SWIZZLE_128B
                      : a.NF == 4 ? CU_TENSOR_MAP_SWIZZLE_64B
                      : a.NF == 2 ? CU_TENSOR_MAP_SWIZZLE_32B
                                  : CU_TENSOR_MAP_SWIZZLE_NONE,
