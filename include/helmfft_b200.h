@@ -335,6 +335,15 @@ int hfb_unpack_modes(hfb_plan* plan, const double* recv, double* modes, const in
 int hfb_carry_layout(hfb_plan* plan, int ld, long long* region_doubles, int* blocks);
 int hfb_zsolve_carry(hfb_plan* plan, int dir, double* modes, int ld, int z0, int nzl,
                      void* cp_work, double* mine, double* peer, uint32_t epoch, void* stream);
+/* The same for a complex table (complex k(z), hfb_plan_set_coefficients_z): the
+ * slab travels as real and imaginary mode-row volumes (each from
+ * hfb_forward_modes), cp_work = 2 * ceil(nzl / 8) * n_x * ld doubles, and the
+ * carry region holds complex carries (hfb_carry_layout_z). Same arithmetic as
+ * hfb_solve_z's z-solve, bit for bit. */
+int hfb_carry_layout_z(hfb_plan* plan, int ld, long long* region_doubles, int* blocks);
+int hfb_zsolve_carry_z(hfb_plan* plan, int dir, double* modes_re, double* modes_im, int ld,
+                       int z0, int nzl, void* cp_work, double* mine, double* peer,
+                       uint32_t epoch, void* stream);
 int hfb_carry_check(hfb_plan* plan, void* stream, int* code);
 int hfb_ipc_handle(const void* ptr, void* handle, long long* offset);
 int hfb_ipc_open(const void* handle, long long offset, void** ptr);

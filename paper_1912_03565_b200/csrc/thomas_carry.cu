@@ -269,6 +269,282 @@ __global__ void __launch_bounds__(BM, 4) thomas_carry_kernel(CarryArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Complex coefficients (complex k(z)) across ranks: the same
+// pipeline on two real volumes (re, im) with thomas_tma_z.cu's complex
+// arithmetic, expression for expression. Carry region (doubles, A = n_x ld):
+//   [0, 2A)  x' re, im at z0 - 1;  [2A, 4A) cp re, im at z0 - 1;
+//   [4A, 6A) W re, im at z1;       then nblk forward + nblk backward flags.
+namespace {
+struct cz2 {
+  double r, i;
+};
+__device__ __forceinline__ cz2 zmul2(cz2 a, cz2 b) {
+  return {fma(a.r, b.r, -a.i * b.i), fma(a.r, b.i, a.i * b.r)};
+}
+__device__ __forceinline__ cz2 zfms2(cz2 a, cz2 b, cz2 c) {  // a - b * c
+  return {fma(-b.r, c.r, fma(b.i, c.i, a.r)), fma(-b.r, c.i, fma(-b.i, c.r, a.i))};
+}
+__device__ __forceinline__ cz2 zrcp2(cz2 d, double& n2) {
+  n2 = fma(d.r, d.r, d.i * d.i);
+  const double inv = 1.0 / n2;
+  return {d.r * inv, -d.i * inv};
+}
+
+struct CarryZArgs {
+  double* wr;
+  double* wi;
+  double* cpk;  // chunk q: re at plane 2q, im at 2q + 1
+  const double* coefr;
+  const double* coefi;
+  const double* cx;
+  const double* cy;
+  int nzl, z0, nz;
+  int nrows, ncols, nbpr;
+  long long ld, ps;
+  double thr2;
+  unsigned long long* err;
+  double* mine;
+  double* peer;
+  unsigned epoch;
+  unsigned long long timeout_ns;
+  unsigned* xerr;
+};
+}  // namespace
+
+template <int DIR>
+__global__ void __launch_bounds__(BM) thomas_carry_z_kernel(CarryZArgs a) {
+  constexpr int S = 3;
+  extern __shared__ __align__(16) double dyn[];
+  double(*sdat)[2][K][BM] = reinterpret_cast<double(*)[2][K][BM]>(dyn);
+  double(*scoef)[2][K * 12] = reinterpret_cast<double(*)[2][K * 12]>(dyn + S * 2 * K * BM);
+  __shared__ uint64_t bar[S];
+  const int tid = threadIdx.x;
+  const int nchunk = (a.nzl + K - 1) / K;
+  const long long A = (long long)a.nrows * a.ld;
+  const long long nblk = (long long)a.nrows * a.nbpr;
+  const bool has_prev = a.z0 > 0, has_next = a.z0 + a.nzl < a.nz;
+  unsigned* flags_mine = reinterpret_cast<unsigned*>(a.mine + 6 * A) + (DIR ? nblk : 0);
+  unsigned* flags_peer =
+      a.peer ? reinterpret_cast<unsigned*>(a.peer + 6 * A) + (DIR ? nblk : 0) : nullptr;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+
+  for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int n = (int)(blk / a.nbpr);
+    const int m0 = (int)(blk % a.nbpr) * BM;
+    const int cols = min(BM, a.ncols - m0);
+    const uint32_t rowbytes = (uint32_t)(((cols + 1) & ~1) * 8);
+    const long long boff = (long long)n * a.ld + m0;
+    auto chunk_of = [&](int task) { return DIR ? nchunk - 1 - task : task; };
+    auto issue = [&](int c, int s) {
+      const int l0 = c * K, nl = min(K, a.nzl - l0);
+      mbar_arrive_expect_tx(&bar[s], 2 * nl * rowbytes + (uint32_t)(2 * nl * 12 * 8));
+      for (int i = 0; i < nl; ++i) {
+        const long long off = boff + (long long)(l0 + i) * a.ps;
+        bulk_g2s(&sdat[s][0][i][0], a.wr + off, rowbytes, &bar[s]);
+        bulk_g2s(&sdat[s][1][i][0], a.wi + off, rowbytes, &bar[s]);
+      }
+      bulk_g2s(&scoef[s][0][0], a.coefr + (long long)(a.z0 + l0) * 12, (uint32_t)(nl * 12 * 8),
+               &bar[s]);
+      bulk_g2s(&scoef[s][1][0], a.coefi + (long long)(a.z0 + l0) * 12, (uint32_t)(nl * 12 * 8),
+               &bar[s]);
+    };
+    const bool live = tid < cols;
+    const int m = m0 + tid;
+    const long long idx = (long long)n * a.ld + m;
+    const double cxv = __ldg(a.cx + n);
+    const double cyv = live ? __ldg(a.cy + m) : 0.0;
+    const double cxy = cxv * cyv;
+    double* ck = a.cpk + boff + tid;
+    auto lam = [&](int s, int i, int k) -> cz2 {
+      return {eig_c(&scoef[s][0][i * 12 + 4 * k], cxv, cyv, cxy),
+              eig_c(&scoef[s][1][i * 12 + 4 * k], cxv, cyv, cxy)};
+    };
+    if (tid == 0) {
+      issue(chunk_of(0), 0);
+      if (nchunk > 1) issue(chunk_of(1), 1);
+    }
+    cz2 c = {0.0, 0.0}, x = {0.0, 0.0};
+    const bool wait_in = DIR ? has_next : has_prev;
+    if (wait_in) {
+      if (tid == 0) wait_block(flags_mine + blk, a.epoch, a.timeout_ns, a.xerr, DIR ? 2u : 1u);
+      __syncthreads();
+      if (live) {
+        if (DIR) {
+          x = {__ldcg(a.mine + 4 * A + idx), __ldcg(a.mine + 5 * A + idx)};
+        } else {
+          x = {__ldcg(a.mine + idx), __ldcg(a.mine + A + idx)};
+          c = {__ldcg(a.mine + 2 * A + idx), __ldcg(a.mine + 3 * A + idx)};
+        }
+      }
+    }
+    auto cp_below = [&](int cidx) -> cz2 {
+      if (!live) return {0.0, 0.0};
+      if (cidx > 0)
+        return {ck[(long long)(2 * (cidx - 1)) * a.ps], ck[(long long)(2 * (cidx - 1) + 1) * a.ps]};
+      if (has_prev) return {__ldcg(a.mine + 2 * A + idx), __ldcg(a.mine + 3 * A + idx)};
+      return {0.0, 0.0};
+    };
+    cz2 cbelow = DIR ? cp_below(chunk_of(0)) : cz2{0.0, 0.0};
+    for (int task = 0; task < nchunk; ++task) {
+      const int s = task % S;
+      if (tid == 0 && task + 2 < nchunk) {
+        bulk_wait_read<0>();
+        fence_proxy_async_smem();
+        issue(chunk_of(task + 2), (task + 2) % S);
+      }
+      mbar_wait(&bar[s], (phase >> s) & 1u);
+      phase ^= 1u << s;
+      const int cidx = chunk_of(task);
+      const int l0 = cidx * K, nl = min(K, a.nzl - l0);
+      if (DIR == 0) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          if (i < nl) {
+            const int l = a.z0 + l0 + i;
+            const cz2 lo = lam(s, i, 0), di = lam(s, i, 1), up = lam(s, i, 2);
+            const cz2 den = (l == 0) ? di : zfms2(di, lo, c);
+            double n2;
+            const cz2 rr = zrcp2(den, n2);
+            if (live && !(n2 >= a.thr2)) {
+              const unsigned long long key =
+                  ((unsigned long long)l * (unsigned long long)a.ncols + (unsigned long long)m) *
+                      (unsigned long long)a.nrows +
+                  (unsigned long long)n;
+              atomicMin(a.err, key);
+            }
+            const cz2 f = {sdat[s][0][i][tid], sdat[s][1][i][tid]};
+            x = zmul2((l == 0) ? f : zfms2(f, lo, x), rr);
+            sdat[s][0][i][tid] = x.r;
+            sdat[s][1][i][tid] = x.i;
+            if (l < a.nz - 1) {
+              c = zmul2(up, rr);
+              if (i == K - 1 && live) {
+                ck[(long long)(2 * cidx) * a.ps] = c.r;
+                ck[(long long)(2 * cidx + 1) * a.ps] = c.i;
+              }
+            }
+          }
+        }
+      } else {
+        cz2 cprev = cbelow;
+        if (task + 1 < nchunk) cbelow = cp_below(chunk_of(task + 1));
+        cz2 cb[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          const int l = a.z0 + l0 + i;
+          if (i < nl && l < a.nz - 1) {
+            const cz2 di = lam(s, i, 1);
+            const cz2 dl = (l == 0) ? di : zfms2(di, lam(s, i, 0), cprev);
+            double n2;
+            cprev = zmul2(lam(s, i, 2), zrcp2(dl, n2));
+            cb[i] = cprev;
+          }
+        }
+#pragma unroll
+        for (int i = K - 1; i >= 0; --i) {
+          const int l = a.z0 + l0 + i;
+          if (i < nl) {
+            const cz2 f = {sdat[s][0][i][tid], sdat[s][1][i][tid]};
+            if (l < a.nz - 1) {
+              x = zfms2(f, cb[i], x);
+              sdat[s][0][i][tid] = x.r;
+              sdat[s][1][i][tid] = x.i;
+            } else {
+              x = f;  // top of the system: W = x'
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        for (int i = 0; i < nl; ++i) {
+          const long long off = boff + (long long)(l0 + i) * a.ps;
+          bulk_s2g(a.wr + off, &sdat[s][0][i][0], rowbytes);
+          bulk_s2g(a.wi + off, &sdat[s][1][i][0], rowbytes);
+        }
+        bulk_commit();
+      }
+    }
+    const bool send = DIR ? has_prev : has_next;
+    if (send) {
+      if (live) {
+        if (DIR) {
+          a.peer[4 * A + idx] = x.r;
+          a.peer[5 * A + idx] = x.i;
+        } else {
+          a.peer[idx] = x.r;
+          a.peer[A + idx] = x.i;
+          a.peer[2 * A + idx] = c.r;
+          a.peer[3 * A + idx] = c.i;
+        }
+      }
+      __threadfence_system();
+      __syncthreads();
+      if (tid == 0) st_release_sys(flags_peer + blk, a.epoch);
+    }
+    if (tid == 0) bulk_wait<0>();
+    __syncthreads();
+  }
+}
+
+long long carry_region_doubles_z(const hfb_plan* p, long long ld, long long* nblk) {
+  const long long nb = (long long)p->nx * ((p->ny + BM - 1) / BM);
+  if (nblk) *nblk = nb;
+  return 6LL * p->nx * ld + (2 * nb + 1) / 2;
+}
+
+int launch_thomas_carry_z(hfb_plan* p, int dir, double* re, double* im, long long ld, int z0,
+                          int nzl, double* cpk, double* mine, double* peer, unsigned epoch,
+                          cudaStream_t st) {
+  if (!p->xerr) {
+    HFB_CUDA(cudaMalloc(&p->xerr, sizeof(unsigned)));
+    HFB_CUDA(cudaMemset(p->xerr, 0, sizeof(unsigned)));
+  }
+  CarryZArgs a;
+  a.wr = re;
+  a.wi = im;
+  a.cpk = cpk;
+  a.coefr = p->coef;
+  a.coefi = p->coef_i;
+  a.cx = p->cx;
+  a.cy = p->cy;
+  a.nzl = nzl;
+  a.z0 = z0;
+  a.nz = p->nz;
+  a.nrows = p->nx;
+  a.ncols = p->ny;
+  a.nbpr = (p->ny + BM - 1) / BM;
+  a.ld = ld;
+  a.ps = ld * p->nx;
+  a.thr2 = p->thr * p->thr;
+  a.err = p->err;
+  a.mine = mine;
+  a.peer = peer;
+  a.epoch = epoch;
+  const int ms = tuning(11);
+  a.timeout_ns = (unsigned long long)(ms > 0 ? ms : 30000) * 1000000ULL;
+  a.xerr = p->xerr;
+  const size_t sm = sizeof(double) * (size_t)3 * 2 * (K * BM + K * 12);
+  auto kern = dir ? thomas_carry_z_kernel<1> : thomas_carry_z_kernel<0>;
+  HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per_sm = 1, sms = 148, dev = 0;
+  HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BM, sm));
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long work = (long long)a.nrows * a.nbpr;
+  const long long blocks = std::min<long long>(work, (long long)sms * std::max(per_sm, 1));
+  kern<<<(unsigned)blocks, BM, sm, st>>>(a);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
 long long carry_region_doubles(const hfb_plan* p, long long ld, long long* nblk) {
   const long long nb = (long long)p->nx * ((p->ny + BM - 1) / BM);
   if (nblk) *nblk = nb;
@@ -353,6 +629,31 @@ extern "C" int hfb_zsolve_carry(hfb_plan* p, int dir, double* modes, int ld, int
   HFB_CUDA(cudaSetDevice(p->device));
   return launch_thomas_carry(p, dir, modes, ld, z0, nzl, (double*)cp_work, mine, peer, epoch,
                              (cudaStream_t)stream);
+}
+
+extern "C" int hfb_carry_layout_z(hfb_plan* p, int ld, long long* region_doubles, int* blocks) {
+  if (!p || ld < p->ny || (ld & 1)) return HFB_ERR_ARGUMENT;
+  long long nb = 0;
+  const long long r = carry_region_doubles_z(p, ld, &nb);
+  if (region_doubles) *region_doubles = r;
+  if (blocks) *blocks = (int)nb;
+  return HFB_OK;
+}
+
+extern "C" int hfb_zsolve_carry_z(hfb_plan* p, int dir, double* modes_re, double* modes_im,
+                                  int ld, int z0, int nzl, void* cp_work, double* mine,
+                                  double* peer, uint32_t epoch, void* stream) {
+  if (!p || !modes_re || !modes_im || !cp_work || !mine || ld < p->ny || (ld & 1) ||
+      (dir != 0 && dir != 1))
+    return HFB_ERR_ARGUMENT;
+  if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
+  if (!p->coef_i) return HFB_ERR_ARGUMENT;  // a real table: hfb_zsolve_carry
+  if (z0 < 0 || nzl < 1 || z0 + nzl > p->nz) return HFB_ERR_RANGE;
+  const bool needs_peer = dir == 0 ? z0 + nzl < p->nz : z0 > 0;
+  if (needs_peer != (peer != nullptr)) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return launch_thomas_carry_z(p, dir, modes_re, modes_im, ld, z0, nzl, (double*)cp_work, mine,
+                               peer, epoch, (cudaStream_t)stream);
 }
 
 extern "C" int hfb_carry_check(hfb_plan* p, void* stream, int* code) {

@@ -423,6 +423,14 @@ def carry_layout(plan, ld):
     return size.value, nb.value
 
 
+def carry_layout_z(plan, ld):
+    """carry_layout for a complex table (complex carries)."""
+    size, nb = ctypes.c_longlong(0), ctypes.c_int(0)
+    check(plan.lib.hfb_carry_layout_z(plan.handle, ld, ctypes.byref(size), ctypes.byref(nb)),
+          "carry_layout_z")
+    return size.value, nb.value
+
+
 def carry_status_code(plan):
     """0, or the latched missing-carry direction (1 forward, 2 backward); synchronises."""
     code = ctypes.c_int(0)
@@ -452,7 +460,8 @@ class CarryLinks:
         self.plan = get_plan(grid.n_x, grid.n_y, grid.n_z, device)
         lib = self.plan.lib
         self.ld = int(lib.hfb_modes_ld(self.plan.handle))
-        size, self.blocks = carry_layout(self.plan, self.ld)
+        # sized for complex carries (the larger layout): one region serves both tables
+        size, self.blocks = carry_layout_z(self.plan, self.ld)
         self.region = torch.zeros(size, dtype=torch.float64, device=device)
         torch.cuda.synchronize(device)
         handle, off = (ctypes.c_char * 64)(), ctypes.c_longlong(0)
@@ -503,6 +512,17 @@ def carry_zsolve(plan, modes, ld, z0, kpz, cp, mine, peer_next, peer_prev, epoch
                                     peer_prev, epoch, st), "zsolve_carry backward")
 
 
+def carry_zsolve_z(plan, modes_re, modes_im, ld, z0, kpz, cp, mine, peer_next, peer_prev,
+                   epoch):
+    """carry_zsolve for a complex table: (re, im) mode-row volumes, cp with two
+    planes per checkpoint."""
+    st = plan.stream()
+    for d, peer in ((0, peer_next), (1, peer_prev)):
+        check(plan.lib.hfb_zsolve_carry_z(plan.handle, d, ptr(modes_re), ptr(modes_im), ld, z0,
+                                          kpz, ptr(cp), ptr(mine), peer, epoch, st),
+              f"zsolve_carry_z dir {d}")
+
+
 def check_status_carry(grid, group=None, device=None):
     """Agree across ranks on a latched vanishing pivot or a missing carry
     (synchronises); raises SingularSystemError / ExchangeError on every rank."""
@@ -534,6 +554,8 @@ def solve_partitioned_carry(z_slab, scheme, profile, grid, group=None, timings=N
     """solve_partitioned without the all-to-alls: the 2D DSTs run on the local
     z-slab (mode rows, as in solve_partitioned) and the z-solve is swept across
     the ranks with carries through peer memory. Same arguments and result.
+    A complex table (complex k(z)) takes a complex128 (or real) slab and returns
+    a complex128 slab; its real and imaginary parts are transformed separately.
 
     check=False skips the per-call agreement on pivots and carries (a host
     synchronisation); call check_status_carry(grid, group) after a batch."""
@@ -555,26 +577,42 @@ def solve_partitioned_carry(z_slab, scheme, profile, grid, group=None, timings=N
 
     tplan = get_plan(grid.n_x, grid.n_y, kpz, dev)
     ld = links.ld
-    modes = torch.empty(kpz * grid.n_x * ld, dtype=torch.float64, device=dev)
-    mark(0)
-    with tplan.lock:
-        work = tplan.workspace(5)
-        check_rc = tplan.lib.hfb_forward_modes(tplan.handle, ptr(z_slab.contiguous()), ptr(modes),
-                                               ptr(work), tplan.stream())
-        _check(check_rc, "forward_modes")
-    mark(1)
     zplan = links.plan
     with zplan.lock:
         if scheme is not None:
             device_coefficients(zplan, scheme, profile, grid)
-        cp = torch.empty(((kpz + 7) // 8) * grid.n_x * ld, dtype=torch.float64, device=dev)
-        carry_zsolve(zplan, modes, ld, z0, kpz, cp, links.region, links.next, links.prev,
-                     links.next_epoch())
-    mark(2)
-    out = torch.empty((kpz, grid.n_y, grid.n_x), dtype=torch.float64, device=dev)
+        cplx = zplan.complex_coef
+    if torch.is_complex(z_slab) and not cplx:
+        raise ValueError("complex right-hand side with a real table: solve re and im separately")
+    parts_in = ((z_slab.real.contiguous(), z_slab.imag.contiguous()) if torch.is_complex(z_slab)
+                else (z_slab.contiguous(), torch.zeros_like(z_slab)) if cplx
+                else (z_slab.contiguous(),))
+    modes = [torch.empty(kpz * grid.n_x * ld, dtype=torch.float64, device=dev) for _ in parts_in]
+    mark(0)
     with tplan.lock:
-        _check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(modes), ptr(out), tplan.stream()),
-               "inverse_modes")
+        work = tplan.workspace(5)
+        for src, m in zip(parts_in, modes):
+            _check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(src), ptr(m), ptr(work),
+                                               tplan.stream()), "forward_modes")
+    mark(1)
+    with zplan.lock:
+        nck = (kpz + 7) // 8
+        if cplx:
+            cp = torch.empty(2 * nck * grid.n_x * ld, dtype=torch.float64, device=dev)
+            carry_zsolve_z(zplan, modes[0], modes[1], ld, z0, kpz, cp, links.region, links.next,
+                           links.prev, links.next_epoch())
+        else:
+            cp = torch.empty(nck * grid.n_x * ld, dtype=torch.float64, device=dev)
+            carry_zsolve(zplan, modes[0], ld, z0, kpz, cp, links.region, links.next,
+                         links.prev, links.next_epoch())
+    mark(2)
+    outs = [torch.empty((kpz, grid.n_y, grid.n_x), dtype=torch.float64, device=dev)
+            for _ in modes]
+    with tplan.lock:
+        for m, o in zip(modes, outs):
+            _check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(m), ptr(o), tplan.stream()),
+                   "inverse_modes")
+    out = torch.complex(outs[0], outs[1]) if cplx else outs[0]
     mark(3)
     if check:
         check_status_carry(grid, group, dev)
@@ -600,40 +638,57 @@ def solve_partitioned_carry_local(values, scheme, profile, grid, parts):
     dev = values.device
     zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, dev)
     ld = int(zplan.lib.hfb_modes_ld(zplan.handle))
-    size, _ = carry_layout(zplan, ld)
-    regions = [torch.zeros(size, dtype=torch.float64, device=dev) for _ in range(parts)]
-    modes, cps = [], []
-    for r, (z0, z1) in enumerate(ex.partition.z_ranges):
-        kpz = z1 - z0
-        tplan = get_plan(grid.n_x, grid.n_y, kpz, dev)
-        m = torch.empty(kpz * grid.n_x * ld, dtype=torch.float64, device=dev)
-        with tplan.lock:
-            work = tplan.workspace(5)
-            _check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(values[z0:z1].contiguous()),
-                                               ptr(m), ptr(work), tplan.stream()), "forward_modes")
-        modes.append(m)
-        cps.append(torch.empty(((kpz + 7) // 8) * grid.n_x * ld, dtype=torch.float64, device=dev))
     with zplan.lock:
         if scheme is not None:
             device_coefficients(zplan, scheme, profile, grid)
-        st = zplan.stream()
-        zr = ex.partition.z_ranges
+        cplx = zplan.complex_coef
+    if torch.is_complex(values) and not cplx:
+        raise ValueError("complex right-hand side with a real table: solve re and im separately")
+    vols = ((values.real.contiguous(), values.imag.contiguous()) if torch.is_complex(values)
+            else (values.contiguous(), torch.zeros_like(values)) if cplx else (values,))
+    size, _ = (carry_layout_z if cplx else carry_layout)(zplan, ld)
+    regions = [torch.zeros(size, dtype=torch.float64, device=dev) for _ in range(parts)]
+    zr = ex.partition.z_ranges
+    modes, cps = [], []
+    for r, (z0, z1) in enumerate(zr):
+        kpz = z1 - z0
+        tplan = get_plan(grid.n_x, grid.n_y, kpz, dev)
+        ms = []
+        with tplan.lock:
+            work = tplan.workspace(5)
+            for v in vols:
+                m = torch.empty(kpz * grid.n_x * ld, dtype=torch.float64, device=dev)
+                _check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(v[z0:z1].contiguous()),
+                                                   ptr(m), ptr(work), tplan.stream()),
+                       "forward_modes")
+                ms.append(m)
+        modes.append(ms)
+        cps.append(torch.empty(len(vols) * ((kpz + 7) // 8) * grid.n_x * ld,
+                               dtype=torch.float64, device=dev))
+
+    def sweep(r, d, peer):
+        if cplx:
+            return zplan.lib.hfb_zsolve_carry_z(zplan.handle, d, ptr(modes[r][0]), ptr(modes[r][1]),
+                                                ld, zr[r][0], zr[r][1] - zr[r][0], ptr(cps[r]),
+                                                ptr(regions[r]), peer, 1, zplan.stream())
+        return zplan.lib.hfb_zsolve_carry(zplan.handle, d, ptr(modes[r][0]), ld, zr[r][0],
+                                          zr[r][1] - zr[r][0], ptr(cps[r]), ptr(regions[r]), peer,
+                                          1, zplan.stream())
+
+    with zplan.lock:
         for r in range(parts):
-            nxt = ptr(regions[r + 1]) if r + 1 < parts else None
-            _check(zplan.lib.hfb_zsolve_carry(zplan.handle, 0, ptr(modes[r]), ld, zr[r][0],
-                                              zr[r][1] - zr[r][0], ptr(cps[r]), ptr(regions[r]),
-                                              nxt, 1, st), "zsolve_carry forward")
+            _check(sweep(r, 0, ptr(regions[r + 1]) if r + 1 < parts else None),
+                   "zsolve_carry forward")
         for r in reversed(range(parts)):
-            prv = ptr(regions[r - 1]) if r > 0 else None
-            _check(zplan.lib.hfb_zsolve_carry(zplan.handle, 1, ptr(modes[r]), ld, zr[r][0],
-                                              zr[r][1] - zr[r][0], ptr(cps[r]), ptr(regions[r]),
-                                              prv, 1, st), "zsolve_carry backward")
-    out = torch.empty_like(values)
-    for r, (z0, z1) in enumerate(ex.partition.z_ranges):
+            _check(sweep(r, 1, ptr(regions[r - 1]) if r > 0 else None), "zsolve_carry backward")
+    outs = [torch.empty(values.shape, dtype=torch.float64, device=dev) for _ in vols]
+    for r, (z0, z1) in enumerate(zr):
         tplan = get_plan(grid.n_x, grid.n_y, z1 - z0, dev)
         with tplan.lock:
-            _check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(modes[r]), ptr(out[z0:z1]),
-                                               tplan.stream()), "inverse_modes")
+            for m, o in zip(modes[r], outs):
+                _check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(m), ptr(o[z0:z1]),
+                                                   tplan.stream()), "inverse_modes")
+    out = torch.complex(outs[0], outs[1]) if cplx else outs[0]
     code = carry_status_code(zplan)
     if code:
         raise exchange_error_for(code, 0)

@@ -1072,7 +1072,13 @@ def _carry_nccl_worker(rank, world, port, q):
         V = hd.solve_partitioned_carry(F, hb.SchemeKind.FOURTH_ORDER, prof, g)
         u, _ = hb.solve_discrete(hb.Field3D(F.cpu().numpy()), hb.BoundaryData.zero(),
                                  hb.SchemeKind.FOURTH_ORDER, prof, g)
-        q.put((float(np.abs(U.cpu().numpy() - u.values).max()), bool(torch.equal(U, V))))
+        # complex k(z) through the same links (the region is sized for complex carries)
+        k2 = np.full(g.n_z + 2, -20.0 + 5.0j)
+        profz = hb.CoefficientProfile(k2=k2, k2_z=np.zeros_like(k2), k2_zz=np.zeros_like(k2))
+        Fz = torch.complex(F, 0.5 * F)
+        W = hd.solve_partitioned_carry(Fz, hb.SchemeKind.FOURTH_ORDER, profz, g)
+        ok_z = bool(torch.equal(W, _one_call_z(Fz, hb.SchemeKind.FOURTH_ORDER, profz, g)))
+        q.put((float(np.abs(U.cpu().numpy() - u.values).max()), bool(torch.equal(U, V)), ok_z))
     finally:
         dist.destroy_process_group()
 
@@ -1091,7 +1097,7 @@ def test_solve_partitioned_carry_nccl_single_rank(cuda):
     p.start()
     p.join(300)
     assert p.exitcode == 0
-    assert q.get(timeout=10) == (0.0, True)
+    assert q.get(timeout=10) == (0.0, True, True)
 
 
 @pytest.mark.parametrize("shape", [(1023, 15, 6), (1023, 31, 5), (2047, 15, 3), (1023, 1023, 2)])
@@ -1118,3 +1124,38 @@ def test_flat_row_final_pass_bitwise(cuda, shape):
         ref = orc.solve(F.cpu().numpy(), oracle_table("4", prof, g),
                         *orc.mode_cosines(nx, ny), workers=4)
         assert rel_l2(outs[0].cpu().numpy(), ref) < PARITY
+
+
+def _one_call_z(F, scheme, prof, g):
+    import torch
+    plan = hb._native.get_plan(g.n_x, g.n_y, g.n_z, F.device)
+    hb.tridiag.device_coefficients(plan, scheme, prof, g)
+    assert plan.complex_coef
+    tr, ti = F.real.contiguous(), F.imag.contiguous()
+    work = plan.workspace(3)
+    P = hb._native.ptr
+    hb._native.check(plan.lib.hfb_solve_z(plan.handle, P(tr), P(ti), P(tr), P(ti), P(work),
+                                          plan.stream()), "solve_z")
+    plan.fetch_status()
+    return torch.complex(tr, ti)
+
+
+@pytest.mark.parametrize("parts,shape,scheme", [(2, (63, 63, 40), "fourth"), (3, (127, 31, 25), "fourth"),
+                                                (8, (63, 63, 29), "sixth"), (5, (31, 31, 31), "sixth")])
+def test_carry_zsolve_complex_k_bitwise(cuda, parts, shape, scheme):
+    """Complex k(z) (row f1) through the transpose-free distributed z-solve:
+    complex carries, equal bit for bit to the one-call complex solve."""
+    import torch
+    from paper_1912_03565_b200 import distributed as hd
+    nx, ny, nz = shape
+    if scheme == "sixth":
+        nx = ny = nz = shape[0]
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+    z = np.linspace(0.0, 1.0, g.n_z + 2)
+    k2 = (30.0 + 10.0j) * (1 + 0.5 * np.sin(PI * z)) ** 2
+    prof = hb.CoefficientProfile(k2=k2, k2_z=np.gradient(k2, z), k2_zz=np.zeros_like(k2))
+    sk = hb.SchemeKind.SIXTH_ORDER if scheme == "sixth" else hb.SchemeKind.FOURTH_ORDER
+    rng = np.random.default_rng(parts + nz)
+    F = torch.from_numpy(rng.standard_normal(g.shape) + 1j * rng.standard_normal(g.shape)).cuda()
+    U = hd.solve_partitioned_carry_local(F, sk, prof, g, parts)
+    assert torch.equal(U, _one_call_z(F, sk, prof, g))
