@@ -955,7 +955,8 @@ def _one_call(F, scheme, prof, g):
 @pytest.mark.parametrize("parts,shape,scheme", [
     (2, (63, 63, 63), "fourth"), (3, (127, 63, 50), "convdiff"), (8, (255, 255, 40), "fourth"),
     (5, (31, 127, 23), "sixth"), (4, (63, 31, 9), "fourth"), (7, (127, 127, 64), "convdiff"),
-    (1, (63, 63, 20), "fourth")])
+    (1, (63, 63, 20), "fourth"), (6, (15, 15, 6), "fourth"), (3, (31, 1023, 9), "convdiff"),
+    (4, (1023, 15, 11), "fourth")])
 def test_carry_zsolve_bitwise(cuda, parts, shape, scheme):
     """The transpose-free distributed z-solve (every rank sweeps its own slab,
     carries through the neighbours' regions; ranks run one after another on
