@@ -460,18 +460,33 @@ class CarryLinks:
         self.plan = get_plan(grid.n_x, grid.n_y, grid.n_z, device)
         lib = self.plan.lib
         self.ld = int(lib.hfb_modes_ld(self.plan.handle))
-        # sized for complex carries (the larger layout): one region serves both tables
-        size, self.blocks = carry_layout_z(self.plan, self.ld)
-        self.region = torch.zeros(size, dtype=torch.float64, device=device)
+        # one region per carry layout (real and complex tables): their flags sit at
+        # different offsets, so a rank that alternates the two never reads one
+        # layout's carries as the other's flags. Both live in ONE allocation
+        # (one IPC handle to open per neighbour): real at 0, complex at `zoff`.
+        size, self.blocks = carry_layout(self.plan, self.ld)
+        size_z, _ = carry_layout_z(self.plan, self.ld)
+        zoff = (size + 63) // 64 * 64
+        self._buf = torch.zeros(zoff + size_z, dtype=torch.float64, device=device)
+        self.region, self.region_z = self._buf[:size], self._buf[zoff:zoff + size_z]
         torch.cuda.synchronize(device)
         handle, off = (ctypes.c_char * 64)(), ctypes.c_longlong(0)
-        check(lib.hfb_ipc_handle(ptr(self.region), handle, ctypes.byref(off)), "ipc_handle")
+        check(lib.hfb_ipc_handle(ptr(self._buf), handle, ctypes.byref(off)), "ipc_handle")
         infos = [None] * self.parts
         dist.all_gather_object(infos, (bytes(handle), off.value), group=group)
         self._opened = []
         prev, nxt = carry_neighbours(self.rank, self.parts)
-        self.prev = self._open(infos[prev]) if prev is not None else None
-        self.next = self._open(infos[nxt]) if nxt is not None else None
+        zb = 8 * zoff
+        if prev is not None:
+            base = self._open(infos[prev])
+            self.prev, self.prev_z = base, base + zb
+        else:
+            self.prev = self.prev_z = None
+        if nxt is not None:
+            base = self._open(infos[nxt])
+            self.next, self.next_z = base, base + zb
+        else:
+            self.next = self.next_z = None
         self.epoch = 0
 
     def _open(self, info):
@@ -599,8 +614,8 @@ def solve_partitioned_carry(z_slab, scheme, profile, grid, group=None, timings=N
         nck = (kpz + 7) // 8
         if cplx:
             cp = torch.empty(2 * nck * grid.n_x * ld, dtype=torch.float64, device=dev)
-            carry_zsolve_z(zplan, modes[0], modes[1], ld, z0, kpz, cp, links.region, links.next,
-                           links.prev, links.next_epoch())
+            carry_zsolve_z(zplan, modes[0], modes[1], ld, z0, kpz, cp, links.region_z,
+                           links.next_z, links.prev_z, links.next_epoch())
         else:
             cp = torch.empty(nck * grid.n_x * ld, dtype=torch.float64, device=dev)
             carry_zsolve(zplan, modes[0], ld, z0, kpz, cp, links.region, links.next,
