@@ -546,7 +546,9 @@ def check_status_carry(grid, group=None, device=None):
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     rank = dist.get_rank(group)
     zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, dev)
-    flags = torch.zeros(3, dtype=torch.int64, device=dev)  # singular, exchange, rank of it
+    links = _links.get((grid.n_x, grid.n_y, grid.n_z, id(group), str(dev)))
+    # singular, exchange, rank*4+code of it, solve epoch
+    flags = torch.zeros(4, dtype=torch.int64, device=dev)
     code = carry_status_code(zplan)
     if code:
         flags[1] = 1
@@ -555,7 +557,13 @@ def check_status_carry(grid, group=None, device=None):
         zplan.fetch_status()
     except Exception:
         flags[0] = 1
+    if links is not None:
+        flags[3] = links.epoch
     dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+    if links is not None:
+        # a rank that skipped a solve (an error before its launches) rejoins the
+        # others' epoch, so the next solve's flags agree again
+        links.epoch = int(flags[3].item())
     if int(flags[1].item()):
         r, c = divmod(int(flags[2].item()), 4)
         raise exchange_error_for(c, r)
