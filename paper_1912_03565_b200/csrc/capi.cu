@@ -73,6 +73,19 @@ static int build_dense(int n, double** out) {
   return HFB_OK;
 }
 
+namespace hfb {
+// dense DST-I matrices on demand (tuning key 17 forces the dense path for
+// power-of-two lengths, whose plans have none)
+int ensure_dense(hfb_plan* p) {
+  if (!p->dense_x) {
+    int rc = build_dense(p->nx, &p->dense_x);
+    if (rc) return rc;
+  }
+  if (!p->dense_y) return build_dense(p->ny, &p->dense_y);
+  return HFB_OK;
+}
+}  // namespace hfb
+
 extern "C" const char* hfb_version(void) { return "helmfft_b200 0.1.0 (sm_100a)"; }
 
 extern "C" const char* hfb_strerror(int code) {

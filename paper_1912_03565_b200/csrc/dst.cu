@@ -60,28 +60,32 @@ __global__ void __launch_bounds__(512) dst_x_fft_kernel(const double* __restrict
 __global__ void __launch_bounds__(512) dst_y_fft_kernel(const double* __restrict__ src,
                                                          double* __restrict__ dst, int z0,
                                                          int x0, int x1, long long ld,
-                                                         long long ps, int N, FftCtx c, int B) {
+                                                         long long ps, int N, FftCtx c, int B,
+                                                         int nplanes) {
   extern __shared__ double2 smem[];
   const int f = threadIdx.x / c.G, g = threadIdx.x % c.G;
   const int W = 2 * B;
   double2* wsum = smem + B * (c.M + 1);
   double* sb = reinterpret_cast<double*>(smem);
-  const long long plane = z0 + blockIdx.y;
   const int col0 = x0 + blockIdx.x * W;
   const int ncols = min(W, x1 - col0);
-  const double* P = src + plane * ps + col0;
-  double* Q = dst + plane * ps + col0;
   const int total = N * W;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    const int row = e / W, col = e - row * W;
-    const double v = col < ncols ? P[row * ld + col] : 0.0;
-    sb[2 * ((col >> 1) * (c.M + 1) + row + 1) + (col & 1)] = v;
-  }
-  __syncthreads();
-  dst_core(smem + f * (c.M + 1), c, g, wsum);
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    const int row = e / W, col = e - row * W;
-    if (col < ncols) Q[row * ld + col] = sb[2 * ((col >> 1) * (c.M + 1) + row) + (col & 1)];
+  // planes z0 + blockIdx.y + k gridDim.y (gridDim.y <= 65535)
+  for (long long plane = z0 + blockIdx.y; plane < z0 + nplanes; plane += gridDim.y) {
+    const double* P = src + plane * ps + col0;
+    double* Q = dst + plane * ps + col0;
+    __syncthreads();  // the previous plane's stores have read shared memory
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int row = e / W, col = e - row * W;
+      const double v = col < ncols ? P[row * ld + col] : 0.0;
+      sb[2 * ((col >> 1) * (c.M + 1) + row + 1) + (col & 1)] = v;
+    }
+    __syncthreads();
+    dst_core(smem + f * (c.M + 1), c, g, wsum);
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int row = e / W, col = e - row * W;
+      if (col < ncols) Q[row * ld + col] = sb[2 * ((col >> 1) * (c.M + 1) + row) + (col & 1)];
+    }
   }
 }
 
@@ -134,17 +138,232 @@ __global__ void __launch_bounds__(256) dgemm_batched_kernel(
     }
 }
 
+// The same product on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64): 64x64
+// CTA tiles, 4 warps of 32x32 (4 x 4 m8n8 accumulators each), k in blocks of 16
+// staged through shared memory as in dgemm_batched_kernel. Fragments (PTX
+// m8n8k4 .f64): A[r = lane/4][k = lane%4], B[k = lane%4][c = lane/4],
+// C[r = lane/4][c = 2 (lane%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) dmma_batched_kernel(
+    int Mr, int Nc, int Kd, const double* __restrict__ A, long long lda, long long sA,
+    const double* __restrict__ Bm, long long ldb, long long sB, double* __restrict__ C,
+    long long ldc, long long sC) {
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int b = blockIdx.z;
+  A += b * sA;
+  Bm += b * sB;
+  C += b * sC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+  const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc[4][4][2] = {};
+  for (int k0 = 0; k0 < Kd; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 128) {
+      const int kk = e % 16, r = e / 16;  // A tile: 64 rows x 16 k
+      const int gr = row0 + r, gk = k0 + kk;
+      As[kk][r] = (gr < Mr && gk < Kd) ? A[gr * lda + gk] : 0.0;
+      const int cc = e % 64, kb = e / 64;  // B tile: 16 k x 64 cols
+      const int gk2 = k0 + kb, gc = col0 + cc;
+      Bs[kb][cc] = (gk2 < Kd && gc < Nc) ? Bm[gk2 * ldb + gc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < 16; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[ks + fk][wr + 8 * i + fr];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[ks + fk][wc + 8 * j + fr];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = row0 + wr + 8 * i + fr, cc = col0 + wc + 8 * j + 2 * fk + h;
+        if (r < Mr && cc < Nc) C[r * ldc + cc] = acc[i][j][h];
+      }
+}
+
+// Small-N 2D DST-I of whole planes on the FP64 tensor cores: Y = S_y X S_x
+// (S symmetric, orthonormal scale included) with X, the intermediate T = X S_x,
+// and both S in shared memory, zero-padded to NP x NP (NP = 32 or 64). One
+// plane per CTA iteration, persistent over planes: 16 B/point of HBM traffic
+// for the whole 2D transform (one read, one write of a contiguous plane) and
+// 4 NP flops per point on DMMA (mma.sync.m8n8k4.f64). Warp w owns output rows
+// [8w, 8w + 8) of each product, all NP/8 column tiles.
+// Layouts: natural planes (row j = y position, ld = row stride, x fastest) or
+// mode rows (row n = x mode, y modes m fastest — the one-call solve's and the
+// partitioned path's (l, n, m) layout). tin: the input is mode rows (read
+// transposed, W[n][m] -> X[m][n]); tout: write Y[m][n] as mode rows (n, m).
+struct D2Layout {
+  long long ld_in, ps_in, ld_out, ps_out;
+  int tin, tout;
+};
+
+template <int NP>
+__global__ void __launch_bounds__(4 * NP) dmma_dst2d_kernel(const double* src, double* dst,
+                                                            int z0, int nz, int nx, int ny,
+                                                            const double* __restrict__ Sx,
+                                                            const double* __restrict__ Sy,
+                                                            D2Layout lay) {
+  constexpr int LD = NP + 1, NT = NP / 8;
+  extern __shared__ double sm2[];
+  double* xs = sm2;              // X, then Y
+  double* ts = xs + NP * LD;     // T = X S_x
+  double* sx = ts + NP * LD;
+  double* sy = sx + NP * LD;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int nth = blockDim.x;
+  for (int e = threadIdx.x; e < NP * NP; e += nth) {
+    const int r = e / NP, c = e % NP;
+    sx[r * LD + c] = (r < nx && c < nx) ? __ldg(Sx + r * nx + c) : 0.0;
+    sy[r * LD + c] = (r < ny && c < ny) ? __ldg(Sy + r * ny + c) : 0.0;
+  }
+  for (int pl = blockIdx.x; pl < nz; pl += gridDim.x) {
+    const double* X = src + (long long)(z0 + pl) * lay.ps_in;
+    __syncthreads();  // the previous plane's Y has been stored
+    if (!lay.tin) {
+      for (int e = threadIdx.x; e < NP * NP; e += nth) {
+        const int r = e / NP, c = e % NP;
+        xs[r * LD + c] = (r < ny && c < nx) ? X[r * lay.ld_in + c] : 0.0;
+      }
+    } else {  // mode rows: element (n, m) at X[n ld + m] -> xs[m][n]
+      for (int e = threadIdx.x; e < NP * NP; e += nth) {
+        const int n = e / NP, m = e % NP;
+        xs[m * LD + n] = (n < nx && m < ny) ? X[n * lay.ld_in + m] : 0.0;
+      }
+    }
+    __syncthreads();
+    // T = X S_x (rows of X: y positions j, columns: x modes n)
+    double acc[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < NP; ks += 4) {
+      const double a = xs[(8 * warp + fr) * LD + ks + fk];
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+        dmma884(acc[j][0], acc[j][1], a, sx[(ks + fk) * LD + 8 * j + fr]);
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      ts[(8 * warp + fr) * LD + 8 * j + 2 * fk] = acc[j][0];
+      ts[(8 * warp + fr) * LD + 8 * j + 2 * fk + 1] = acc[j][1];
+    }
+    __syncthreads();
+    // Y = S_y T (rows: y modes m)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < NP; ks += 4) {
+      const double a = sy[(8 * warp + fr) * LD + ks + fk];
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+        dmma884(acc[j][0], acc[j][1], a, ts[(ks + fk) * LD + 8 * j + fr]);
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      xs[(8 * warp + fr) * LD + 8 * j + 2 * fk] = acc[j][0];
+      xs[(8 * warp + fr) * LD + 8 * j + 2 * fk + 1] = acc[j][1];
+    }
+    __syncthreads();
+    double* Y = dst + (long long)(z0 + pl) * lay.ps_out;
+    if (!lay.tout) {
+      for (int e = threadIdx.x; e < nx * ny; e += nth) {
+        const int r = e / nx, c = e - r * nx;
+        Y[r * lay.ld_out + c] = xs[r * LD + c];
+      }
+    } else {  // mode rows (n, m): Y[n ld + m] = xs[m][n]
+      for (int e = threadIdx.x; e < nx * ny; e += nth) {
+        const int n = e / ny, m = e - n * ny;
+        Y[n * lay.ld_out + m] = xs[m * LD + n];
+      }
+    }
+  }
+}
+
+// Where the whole-plane DMMA transform is used (tools/dense_bench.py on a B200,
+// ~32 MB stacks, 2D transform): N = 31 0.43 ms against 0.74 for the FFT engine;
+// N = 15 1.56 vs 1.46 (FFT); N = 63 (64-padded tiles) 0.82 vs 0.53 (FFT); N = 40
+// 1.79 vs 1.45 for the two-pass dense GEMM. So: lines of at most 32 (tuning key
+// 18, default 32; 0 = never), and at least 16 where the FFT engine applies.
+static int dmma2d_np(const hfb_plan* p) {
+  const int lim = tuning(18);
+  const int n = std::max(p->nx, p->ny);
+  if (lim <= 0 || n > lim || n > 64) return 0;
+  if (n < 16 && dst16_ok(p->nx + 1) && dst16_ok(p->ny + 1)) return 0;
+  return n <= 32 ? 32 : 64;
+}
+
+static int launch_dmma2d(hfb_plan* p, const double* src, double* dst, int z0, int z1,
+                         cudaStream_t st, const D2Layout* layout = nullptr) {
+  const int np = dmma2d_np(p);
+  int rc = ensure_dense(p);
+  if (rc) return rc;
+  const size_t sm = sizeof(double) * 4 * (size_t)np * (np + 1);
+  auto kern = np == 32 ? dmma_dst2d_kernel<32> : dmma_dst2d_kernel<64>;
+  HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per_sm = 1, sms = 148, dev = 0;
+  HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 4 * np, sm));
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nz = z1 - z0;
+  const int blocks = std::max(1, std::min(nz, sms * std::max(per_sm, 1)));
+  D2Layout nat = {p->nx, (long long)p->nx * p->ny, p->nx, (long long)p->nx * p->ny, 0, 0};
+  kern<<<blocks, 4 * np, sm, st>>>(src, dst, z0, nz, p->nx, p->ny, p->dense_x, p->dense_y,
+                                   layout ? *layout : nat);
+  HFB_LAUNCHED();
+  return HFB_OK;
+}
+
+// batched dense product: the DMMA kernel (tuning key 16 = 1, default) or the
+// CUDA-core one (0)
+static int launch_dense_gemm(int Mr, int Nc, int Kd, const double* A, long long lda, long long sA,
+                             const double* Bm, long long ldb, long long sB, double* C,
+                             long long ldc, long long sC, int batch, cudaStream_t st) {
+  // gridDim.z is at most 65535: long stacks of small planes go in chunks
+  for (int b0 = 0; b0 < batch; b0 += 65535) {
+    const int nb = std::min(batch - b0, 65535);
+    dim3 grid((Nc + 63) / 64, (Mr + 63) / 64, nb);
+    const double* Ab = A + (long long)b0 * sA;
+    const double* Bb = Bm + (long long)b0 * sB;
+    double* Cb = C + (long long)b0 * sC;
+    if (tuning(16))
+      dmma_batched_kernel<<<grid, 128, 0, st>>>(Mr, Nc, Kd, Ab, lda, sA, Bb, ldb, sB, Cb, ldc, sC);
+    else
+      dgemm_batched_kernel<<<grid, 256, 0, st>>>(Mr, Nc, Kd, Ab, lda, sA, Bb, ldb, sB, Cb, ldc, sC);
+    HFB_LAUNCHED();
+  }
+  return HFB_OK;
+}
+
 // Copy a (planes x rows x cols) region between two arrays of equal strides.
 __global__ void copy_region_kernel(const double* __restrict__ src, double* __restrict__ dst,
                                    int rows, int cols, long long ld, long long ps,
-                                   long long off) {
-  const long long pl = blockIdx.y;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)rows * cols;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long r = e / cols, cc = e % cols;
-    const long long o = off + pl * ps + r * ld + cc;
-    dst[o] = src[o];
-  }
+                                   long long off, int nplanes) {
+  for (long long pl = blockIdx.y; pl < nplanes; pl += gridDim.y)
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+         e < (long long)rows * cols; e += (long long)gridDim.x * blockDim.x) {
+      const long long r = e / cols, cc = e % cols;
+      const long long o = off + pl * ps + r * ld + cc;
+      dst[o] = src[o];
+    }
 }
 
 size_t dense_tmp_elems(const hfb_plan* p, int nplanes) {
@@ -163,18 +382,30 @@ static FftCtx make_ctx(int M, int logM, const double2* tw, const double* sn, dou
   return c;
 }
 
+// tuning key 17: lines of length <= key use the dense product even when N + 1
+// is a power of two (the FFT / DMMA crossover measurement)
+static bool force_dense(const hfb_plan* p) {
+  const int lim = tuning(17);
+  return lim > 0 && p->nx <= lim && p->ny <= lim;
+}
+
 int launch_dst_x(hfb_plan* p, const double* src, double* dst, int z0, int z1, int y0, int y1,
                  double* tmp, cudaStream_t st) {
   const int nz = z1 - z0, nr = y1 - y0;
   if (nz <= 0 || nr <= 0) return HFB_OK;
   const long long ld = p->nx, ps = (long long)p->ny * p->nx;
-  if (dst16_ok(p->nx + 1)) {
+  const bool dense = force_dense(p);
+  if (dense) {
+    int rc = ensure_dense(p);
+    if (rc) return rc;
+  }
+  if (!dense && dst16_ok(p->nx + 1)) {
     const long long off = (long long)y0 * ld;
     return launch_dst16(p->tw_x, p->sn_x, p->scale_x, p->nx + 1, src + off,
                         src + (long long)p->nz * ps, dst + off, z0, nz, nr, ld, ps, ld, ps, false,
                         st);
   }
-  if (p->logMx >= 0) {
+  if (!dense && p->logMx >= 0) {
     const int M = p->nx + 1;
     FftCtx c = make_ctx(M, p->logMx, p->tw_x, p->sn_x, p->scale_x);
     const int B = std::max(1, 256 / c.G);
@@ -200,13 +431,11 @@ int launch_dst_x(hfb_plan* p, const double* src, double* dst, int z0, int z1, in
   if (!tmp) return HFB_ERR_ARGUMENT;
   const double* A = src + (long long)z0 * ps + (long long)y0 * ld;
   double* C = tmp + (long long)z0 * ps + (long long)y0 * ld;
-  dim3 grid((p->nx + 63) / 64, (nr + 63) / 64, nz);
-  dgemm_batched_kernel<<<grid, 256, 0, st>>>(nr, p->nx, p->nx, A, ld, ps, p->dense_x, p->nx, 0, C,
-                                             ld, ps);
-  HFB_LAUNCHED();
-  dim3 cg(std::max(1, std::min(1024, (nr * p->nx + 255) / 256)), nz);
+  int rc = launch_dense_gemm(nr, p->nx, p->nx, A, ld, ps, p->dense_x, p->nx, 0, C, ld, ps, nz, st);
+  if (rc) return rc;
+  dim3 cg(std::max(1, std::min(1024, (nr * p->nx + 255) / 256)), std::min(nz, 65535));
   copy_region_kernel<<<cg, 256, 0, st>>>(tmp, dst, nr, p->nx, ld, ps,
-                                         (long long)z0 * ps + (long long)y0 * ld);
+                                         (long long)z0 * ps + (long long)y0 * ld, nz);
   HFB_LAUNCHED();
   return HFB_OK;
 }
@@ -216,7 +445,12 @@ int launch_dst_y(hfb_plan* p, const double* src, double* dst, int z0, int z1, in
   const int nz = z1 - z0, ncol = x1 - x0;
   if (nz <= 0 || ncol <= 0) return HFB_OK;
   const long long ld = p->nx, ps = (long long)p->ny * p->nx;
-  if (p->logMy >= 0) {
+  const bool dense = force_dense(p);
+  if (dense) {
+    int rc = ensure_dense(p);
+    if (rc) return rc;
+  }
+  if (!dense && p->logMy >= 0) {
     const int M = p->ny + 1;
     FftCtx c = make_ctx(M, p->logMy, p->tw_y, p->sn_y, p->scale_y);
     int B = std::max(1, 512 / c.G);
@@ -228,20 +462,20 @@ int launch_dst_y(hfb_plan* p, const double* src, double* dst, int z0, int z1, in
     if (sm > 48 * 1024)
       HFB_CUDA(cudaFuncSetAttribute(dst_y_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sm));
-    dim3 grid((ncol + 2 * B - 1) / (2 * B), nz);
-    dst_y_fft_kernel<<<grid, threads, sm, st>>>(src, dst, z0, x0, x1, ld, ps, p->ny, c, B);
+    dim3 grid((ncol + 2 * B - 1) / (2 * B), std::min(nz, 65535));
+    dst_y_fft_kernel<<<grid, threads, sm, st>>>(src, dst, z0, x0, x1, ld, ps, p->ny, c, B, nz);
     HFB_LAUNCHED();
     return HFB_OK;
   }
   if (!tmp) return HFB_ERR_ARGUMENT;
   const double* Bp = src + (long long)z0 * ps + x0;
   double* C = tmp + (long long)z0 * ps + x0;
-  dim3 grid((ncol + 63) / 64, (p->ny + 63) / 64, nz);
-  dgemm_batched_kernel<<<grid, 256, 0, st>>>(p->ny, ncol, p->ny, p->dense_y, p->ny, 0, Bp, ld, ps,
-                                             C, ld, ps);
-  HFB_LAUNCHED();
-  dim3 cg(std::max(1, std::min(1024, (p->ny * ncol + 255) / 256)), nz);
-  copy_region_kernel<<<cg, 256, 0, st>>>(tmp, dst, p->ny, ncol, ld, ps, (long long)z0 * ps + x0);
+  int rc = launch_dense_gemm(p->ny, ncol, p->ny, p->dense_y, p->ny, 0, Bp, ld, ps, C, ld, ps, nz,
+                             st);
+  if (rc) return rc;
+  dim3 cg(std::max(1, std::min(1024, (p->ny * ncol + 255) / 256)), std::min(nz, 65535));
+  copy_region_kernel<<<cg, 256, 0, st>>>(tmp, dst, p->ny, ncol, ld, ps, (long long)z0 * ps + x0,
+                                         nz);
   HFB_LAUNCHED();
   return HFB_OK;
 }
@@ -305,6 +539,22 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
     if (p->stage_ring) cudaEventRecord(p->stage_ev[slot * 6 + i], st);
   };
   mark(0);
+  if (dmma2d_np(p)) {
+    // small N: forward 2D DST of whole planes on DMMA straight into the mode
+    // rows, the TMA z-solve, the inverse 2D DST back to natural planes (3
+    // launches; the stage slots of the two y-passes stay empty)
+    int rc;
+    D2Layout fw = {p->nx, ps, ldt, pst, 0, 1}, iv = {ldt, pst, p->nx, ps, 1, 0};
+    if ((rc = launch_dmma2d(p, rhs, S2, 0, p->nz, st, &fw))) return rc;
+    mark(1);
+    mark(2);
+    if ((rc = launch_thomas_tma(p, S2, CP, ldt, pst, st, 0))) return rc;
+    mark(3);
+    mark(4);
+    if ((rc = launch_dmma2d(p, S2, out, 0, p->nz, st, &iv))) return rc;
+    mark(5);
+    return HFB_OK;
+  }
   // 1
   x.src = rhs;
   x.src_end = rhs + p->nz * ps;
@@ -443,6 +693,10 @@ size_t fused_work_elems_z(const hfb_plan* p) {
 static int forward_2d(hfb_plan* p, const double* rhs, double* S1, double* S2, cudaStream_t st) {
   const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), ldx = x_ld(p);
   const long long pst = fused_plane(p);
+  if (dmma2d_np(p)) {  // small N: the DMMA whole-plane transform, as in solve_fused
+    D2Layout fw = {p->nx, ps, ldt, pst, 0, 1};
+    return launch_dmma2d(p, rhs, S2, 0, p->nz, st, &fw);
+  }
   Dst16Call x = {};
   x.tw = p->tw_x;
   x.sn = p->sn_x;
@@ -480,6 +734,10 @@ static int forward_2d(hfb_plan* p, const double* rhs, double* S1, double* S2, cu
 static int inverse_2d(hfb_plan* p, double* S2, double* out, cudaStream_t st) {
   const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p);
   const long long pst = fused_plane(p);
+  if (dmma2d_np(p)) {
+    D2Layout iv = {ldt, pst, p->nx, ps, 1, 0};
+    return launch_dmma2d(p, S2, out, 0, p->nz, st, &iv);
+  }
   Dst16Call y = {};
   y.tw = p->tw_y;
   y.sn = p->sn_y;
@@ -540,6 +798,10 @@ size_t modes_work_elems(const hfb_plan* p) {
 int forward_modes(hfb_plan* p, const double* src, double* modes, double* S1, cudaStream_t st) {
   if (!tran_path(p) || !S1) return HFB_ERR_ARGUMENT;
   const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), ldx = x_ld(p);
+  if (dmma2d_np(p)) {  // small N: the one-call solve's DMMA transform (bitwise the same)
+    D2Layout fw = {p->nx, ps, ldt, ldt * p->nx, 0, 1};
+    return launch_dmma2d(p, src, modes, 0, p->nz, st, &fw);
+  }
   Dst16Call x = {};
   x.tw = p->tw_x;
   x.sn = p->sn_x;
@@ -578,6 +840,10 @@ int forward_modes(hfb_plan* p, const double* src, double* modes, double* S1, cud
 int inverse_modes(hfb_plan* p, double* modes, double* out, cudaStream_t st) {
   if (!tran_path(p)) return HFB_ERR_ARGUMENT;
   const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), pst = ldt * p->nx;
+  if (dmma2d_np(p)) {
+    D2Layout iv = {ldt, pst, p->nx, ps, 1, 0};
+    return launch_dmma2d(p, modes, out, 0, p->nz, st, &iv);
+  }
   Dst16Call y = {};
   y.tw = p->tw_y;
   y.sn = p->sn_y;
@@ -617,7 +883,8 @@ int transform_planes(hfb_plan* p, const double* src, double* dst, int z0, int z1
                      cudaStream_t st) {
   const int nz = z1 - z0;
   if (nz <= 0) return HFB_OK;
-  if (!tran_path(p)) {
+  if (dmma2d_np(p)) return launch_dmma2d(p, src, dst, z0, z1, st);
+  if (!tran_path(p) || force_dense(p)) {
     int rc = launch_dst_x(p, src, dst, z0, z1, 0, p->ny, work, st);
     if (rc) return rc;
     return launch_dst_y(p, dst, dst, z0, z1, 0, p->nx, work, st);

@@ -656,6 +656,9 @@ static int g_tune_carry_ms = 0;  // distributed z-solve: carry wait timeout in m
 static int g_tune_carry_cap = 0;  // distributed z-solve: CTAs per SM (key 12; 0 = occupancy)
 static int g_tune_ustore = 1;  // packed-row outputs by flat-row tensor stores (key 13)
 static int g_tune_indep = 1;   // ROW passes with tensor stores: decoupled groups (key 14)
+static int g_tune_dmma = 1;    // dense DST-I products on the FP64 tensor cores (key 16)
+static int g_tune_dense_max = 0;  // force the dense path for lines up to this length (key 17)
+static int g_tune_dmma2d = 32;  // whole-plane DMMA 2D DST-I for lines up to this length (key 18)
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
@@ -867,6 +870,9 @@ int tuning(int key) {
     case 12: return g_tune_carry_cap;
     case 13: return g_tune_ustore;
     case 14: return g_tune_indep;
+    case 16: return g_tune_dmma;
+    case 17: return g_tune_dense_max;
+    case 18: return g_tune_dmma2d;
     default: return 0;
   }
 }
@@ -887,6 +893,9 @@ void set_tuning(int key, int value) {
   if (key == 12) g_tune_carry_cap = value;
   if (key == 13) g_tune_ustore = value ? 1 : 0;
   if (key == 14) g_tune_indep = value ? 1 : 0;
+  if (key == 16) g_tune_dmma = value ? 1 : 0;
+  if (key == 17) g_tune_dense_max = value;
+  if (key == 18) g_tune_dmma2d = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

@@ -1160,3 +1160,37 @@ def test_carry_zsolve_complex_k_bitwise(cuda, parts, shape, scheme):
     F = torch.from_numpy(rng.standard_normal(g.shape) + 1j * rng.standard_normal(g.shape)).cuda()
     U = hd.solve_partitioned_carry_local(F, sk, prof, g, parts)
     assert torch.equal(U, _one_call_z(F, sk, prof, g))
+
+
+@pytest.mark.parametrize("nx,ny,nz", [(7, 7, 70000), (10, 9, 70000), (15, 15, 66000)])
+def test_transform_stack_more_planes_than_grid_limit(cuda, nx, ny, nz):
+    """Stacks of more than 65535 small planes (the CUDA grid's y/z limit) on the
+    generic FFT, dense and engine paths."""
+    rng = np.random.default_rng(nx * ny)
+    data = rng.standard_normal((nz, ny, nx))
+    f = hb.Field3D(data.copy())
+    hb.transform_stack(hb.make_plan(nx, ny), f)
+    ref = orc.dst_stack(data, workers=8)
+    assert np.abs(f.values - ref).max() < 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("nx,ny,nz", [(31, 31, 40), (15, 31, 9), (63, 63, 5), (40, 23, 7),
+                                      (1, 5, 3), (64, 64, 2)])
+def test_dmma_dst2d_vs_scipy(cuda, nx, ny, nz):
+    """The whole-plane 2D DST-I on the FP64 tensor cores (tuning key 18) against
+    scipy's DST (the reference's kernel), and the dense DMMA GEMM path (key 17)."""
+    lib = hb._native.load_library()
+    rng = np.random.default_rng(nx + 7 * ny)
+    data = rng.standard_normal((nz, ny, nx))
+    ref = orc.dst_stack(data, workers=4)
+    for knobs in (((18, 64),), ((17, 64),), ((17, 64), (16, 0))):
+        for k, v in knobs:
+            lib.hfb_set_tuning(k, v)
+        try:
+            f = hb.Field3D(data.copy())
+            hb.transform_stack(hb.make_plan(nx, ny), f)
+        finally:
+            lib.hfb_set_tuning(16, 1)
+            lib.hfb_set_tuning(17, 0)
+            lib.hfb_set_tuning(18, 0)
+        assert np.abs(f.values - ref).max() < 1e-13 * np.abs(ref).max(), knobs
