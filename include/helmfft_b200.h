@@ -89,7 +89,12 @@ uint64_t hfb_launch_count(void);
  * tensor stores of the destination viewed as flat 128-byte rows, head and tail
  * by plain stores (1, default) or by thread stores (0); key 14 = row passes
  * with tensor stores run the transform groups of a CTA decoupled (own prefetch,
- * mbarrier and store; 1, default) or in CTA lockstep (0). */
+ * mbarrier and store; 1, default) or in CTA lockstep (0); key 16 = dense DST-I
+ * products (lengths without an FFT) on the FP64 tensor cores (1, default) or
+ * CUDA cores (0); key 17 = force the dense product for lines up to this length
+ * (0, default: never; a measurement knob); key 18 = whole-plane 2D DST-I on the
+ * FP64 tensor cores for lines up to this length (32, default; lines of 16 and
+ * more where the FFT engine applies; 0 = never). */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.

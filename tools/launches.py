@@ -16,7 +16,11 @@ for r in rows:
     if hdr and len(r) == len(hdr):
         d = dict(zip(hdr, r))
         key = (int(d["ID"]), d["Kernel Name"].split("(")[0][:44])
-        k.setdefault(key, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+        try:
+            val = float(d["Metric Value"].replace(",", ""))
+        except ValueError:  # "n/a" for a metric this kernel does not have
+            continue
+        k.setdefault(key, {})[d["Metric Name"]] = val
 short = {"gpu__time_duration.sum": "ms", "dram__bytes_read.sum": "rd_GB",
          "dram__bytes_write.sum": "wr_GB"}
 for (i, name), m in k.items():
