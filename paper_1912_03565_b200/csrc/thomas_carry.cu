@@ -101,7 +101,6 @@ __device__ void wait_block(const unsigned* flag, unsigned epoch, unsigned long l
 }
 
 // thread 0: bring local chunk c (levels c*K ..) and its weights into stage s
-template <int S>
 __device__ __forceinline__ void issue_chunk(const CarryArgs& a, double (*sdat)[K][BM],
                                             double (*scoef)[K * 12], uint64_t* bar,
                                             const double* base, uint32_t rowbytes, int c, int s) {
@@ -151,7 +150,7 @@ __global__ void __launch_bounds__(BM, 4) thomas_carry_kernel(CarryArgs a) {
     double* ck = a.cpk + (long long)n * a.ld + m0 + tid;
     if (tid == 0) {
       for (int t = 0; t < S - 1 && t < nchunk; ++t)
-        issue_chunk<S>(a, sdat, scoef, bar, base, rowbytes, chunk_of(t), t);
+        issue_chunk(a, sdat, scoef, bar, base, rowbytes, chunk_of(t), t);
     }
     // the carry in: forward (x', cp) at z0 - 1, backward W at z1
     double c = 0.0, x = 0.0;
@@ -181,7 +180,7 @@ __global__ void __launch_bounds__(BM, 4) thomas_carry_kernel(CarryArgs a) {
       if (tid == 0 && task + S - 1 < nchunk) {
         bulk_wait_read<0>();  // stage s' was stored from at task - 1
         fence_proxy_async_smem();
-        issue_chunk<S>(a, sdat, scoef, bar, base, rowbytes, chunk_of(task + S - 1),
+        issue_chunk(a, sdat, scoef, bar, base, rowbytes, chunk_of(task + S - 1),
                        (task + S - 1) % S);
       }
       mbar_wait(&bar[s], (phase >> s) & 1u);
