@@ -1,0 +1,46 @@
+"""HBM rate of the compact RHS operator (K1, hfb_rhs_fourth) at n^3.
+
+    python tools/stencil_rate.py [--n 1023]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1912_03565_b200 import _native, workloads as wl  # noqa: E402
+from paper_1912_03565_b200.tridiag import device_coefficients  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=1023)
+ap.add_argument("--reps", type=int, default=5)
+a = ap.parse_args()
+n = a.n
+dev = torch.device("cuda", 0)
+P = _native.ptr
+w = wl.workload(4, n)
+plan = _native.get_plan(n, n, n, dev)
+device_coefficients(plan, w.scheme, w.profile, w.grid)
+lib = plan.lib
+f = torch.rand((n + 2, n + 2, n + 2), dtype=torch.float64, device=dev)
+F = torch.empty((n, n, n), dtype=torch.float64, device=dev)
+st = plan.stream()
+
+
+def timed(fn, nbytes, name):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.reps
+    print(f"{name}: {ms:.3f} ms, {nbytes / ms / 1e6:.0f} GB/s (algorithmic {nbytes / 1e9:.2f} GB)")
+
+
+timed(lambda: _native.check(lib.hfb_rhs_fourth(plan.handle, P(f), P(F), 1e-6, st), "rhs4"),
+      8 * ((n + 2) ** 3 + n ** 3), "rhs_fourth (K1)")
