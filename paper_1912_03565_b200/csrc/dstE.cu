@@ -659,6 +659,7 @@ static int g_tune_indep = 1;   // ROW passes with tensor stores: decoupled group
 static int g_tune_dmma = 1;    // dense DST-I products on the FP64 tensor cores (key 16)
 static int g_tune_dense_max = 0;  // force the dense path for lines up to this length (key 17)
 static int g_tune_dmma2d = 32;  // whole-plane DMMA 2D DST-I for lines up to this length (key 18)
+static int g_tune_rhs_march = 32;  // 4th-order RHS operator: levels per marching CTA (key 20; 0 = gathers)
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
@@ -873,6 +874,7 @@ int tuning(int key) {
     case 16: return g_tune_dmma;
     case 17: return g_tune_dense_max;
     case 18: return g_tune_dmma2d;
+    case 20: return g_tune_rhs_march;
     default: return 0;
   }
 }
@@ -896,6 +898,7 @@ void set_tuning(int key, int value) {
   if (key == 16) g_tune_dmma = value ? 1 : 0;
   if (key == 17) g_tune_dense_max = value;
   if (key == 18) g_tune_dmma2d = value;
+  if (key == 20) g_tune_rhs_march = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

@@ -42,5 +42,13 @@ def timed(fn, nbytes, name):
     print(f"{name}: {ms:.3f} ms, {nbytes / ms / 1e6:.0f} GB/s (algorithmic {nbytes / 1e9:.2f} GB)")
 
 
-timed(lambda: _native.check(lib.hfb_rhs_fourth(plan.handle, P(f), P(F), 1e-6, st), "rhs4"),
-      8 * ((n + 2) ** 3 + n ** 3), "rhs_fourth (K1)")
+ref = None
+for v in (0, 16, 32, 64):
+    lib.hfb_set_tuning(20, v)
+    timed(lambda: _native.check(lib.hfb_rhs_fourth(plan.handle, P(f), P(F), 1e-6, st), "rhs4"),
+          8 * ((n + 2) ** 3 + n ** 3), f"rhs_fourth (K1), tuning 20 = {v}")
+    if ref is None:
+        ref = F.clone()
+    else:
+        assert torch.equal(F, ref), v
+lib.hfb_set_tuning(20, 32)
