@@ -222,6 +222,52 @@ __global__ void apply27_kernel(const double* __restrict__ ext, const double* __r
   out[o] = mode == 0 ? v : __dsub_rn(rhs[o], v);
 }
 
+// The 27-point operator marching up the levels (tuning key 20 > 0): a thread owns
+// column (i, j) and keeps the three 3 x 3 planes around it in registers, so each
+// level costs the nine values of one new plane instead of 27 gathers; the sum
+// runs in apply27_point's order (k, then the offsets), bit for bit.
+template <int TX, int TY>
+__global__ void __launch_bounds__(TX * TY) apply27_march_kernel(
+    const double* __restrict__ ext, const double* __restrict__ rhs, double* __restrict__ out,
+    const double* __restrict__ raw, int nx, int ny, int nz, uint32_t mask, int mode, int lz) {
+  const int i = blockIdx.x * TX + threadIdx.x % TX, j = blockIdx.y * TY + threadIdx.x / TX;
+  if (i >= nx || j >= ny) return;
+  const int l0 = blockIdx.z * lz, l1 = min(nz, l0 + lz);
+  const long long X = nx + 2, XY = X * (ny + 2);
+  const long long col = (long long)(j + 1) * X + (i + 1);
+  // the offset tables as compile-time constants (registers, no constant-bank loads)
+  constexpr int DI[9] = {-1, 1, -1, 1, -1, 1, 0, 0, 0};
+  constexpr int DJ[9] = {-1, -1, 1, 1, 0, 0, -1, 1, 0};
+  constexpr int WI[9] = {0, 0, 0, 0, 1, 1, 2, 2, 3};
+  double pl[3][9];
+  auto load_plane = [&](int L, double* d) {  // closed plane L around the column
+    const long long b = (long long)L * XY + col;
+#pragma unroll
+    for (int o = 0; o < 9; ++o) d[o] = __ldg(&ext[b + (long long)DJ[o] * X + DI[o]]);
+  };
+  load_plane(l0, pl[0]);
+  load_plane(l0 + 1, pl[1]);
+  for (int l = l0; l < l1; ++l) {
+    load_plane(l + 2, pl[2]);
+    double w[12];  // this level's weights (the same for every thread: broadcast loads)
+#pragma unroll
+    for (int q = 0; q < 12; ++q) w[q] = __ldg(&raw[(long long)l * 12 + q]);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int o = 0; o < 9; ++o)
+        if (mask & (1u << (k * 9 + o))) acc = DADD(acc, DMUL(w[k * 4 + WI[o]], pl[k][o]));
+    const long long oo = ((long long)l * ny + j) * nx + i;
+    out[oo] = mode == 0 ? acc : __dsub_rn(rhs[oo], acc);
+#pragma unroll
+    for (int o = 0; o < 9; ++o) {
+      pl[0][o] = pl[1][o];
+      pl[1][o] = pl[2][o];
+    }
+  }
+}
+
 // Residual sum of squares with a zero boundary: u is interior-only, so the
 // neighbour fetch is bounds-checked instead of padded (assembly.py:277-289).
 __global__ void residual_sq_kernel(const double* __restrict__ u, const double* __restrict__ F,
@@ -445,9 +491,17 @@ extern "C" int hfb_apply27(hfb_plan* p, const double* ext, const double* rhs, do
   if (!p || !ext || !out || (mode == 1 && !rhs)) return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
   HFB_CUDA(cudaSetDevice(p->device));
-  dim3 grid((p->nx + 127) / 128, p->ny, p->nz);
-  apply27_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(ext, rhs, out, p->coef + 12LL * p->nz,
-                                                         p->nx, p->ny, p->nz, mask, mode);
+  const int lz = tuning(20);
+  if (lz > 0) {
+    constexpr int TX = 64, TY = 4;
+    dim3 grid((p->nx + TX - 1) / TX, (p->ny + TY - 1) / TY, (p->nz + lz - 1) / lz);
+    apply27_march_kernel<TX, TY><<<grid, TX * TY, 0, (cudaStream_t)stream>>>(
+        ext, rhs, out, p->coef + 12LL * p->nz, p->nx, p->ny, p->nz, mask, mode, lz);
+  } else {
+    dim3 grid((p->nx + 127) / 128, p->ny, p->nz);
+    apply27_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(ext, rhs, out, p->coef + 12LL * p->nz,
+                                                           p->nx, p->ny, p->nz, mask, mode);
+  }
   HFB_LAUNCHED();
   return HFB_OK;
 }

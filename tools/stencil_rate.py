@@ -52,3 +52,21 @@ for v in (0, 16, 32, 64):
     else:
         assert torch.equal(F, ref), v
 lib.hfb_set_tuning(20, 32)
+
+# the 27-point apply (fold mode 1 and plain mode 0), all 27 terms
+ext = f
+rhs = torch.rand((n, n, n), dtype=torch.float64, device=dev)
+refs = {}
+for v in (0, 32):
+    lib.hfb_set_tuning(20, v)
+    for mode in (0, 1):
+        timed(lambda: _native.check(lib.hfb_apply27(plan.handle, P(ext), P(rhs), P(F), 0x7FFFFFF,
+                                                    mode, st), "apply27"),
+              8 * ((n + 2) ** 3 + (2 if mode else 1) * n ** 3),
+              f"apply27 mode {mode}, tuning 20 = {v}")
+        if v == 0:
+            refs[mode] = F.clone()
+        else:
+            assert torch.equal(F, refs[mode]), mode
+lib.hfb_set_tuning(20, 32)
+print("apply27 bitwise equal across variants")
