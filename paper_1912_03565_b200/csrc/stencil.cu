@@ -306,6 +306,71 @@ __global__ void residual_sq_kernel(const double* __restrict__ u, const double* _
   }
 }
 
+// The residual, marching: 148 x 8 persistent CTAs (the partial-sum count of
+// hfb_residual_partials) walk 64 x 4 column tiles of lz levels; a thread keeps
+// the three 3 x 3 planes of u around its column in registers (zero outside the
+// interior) and the level's weights, and sums the terms in residual_sq_kernel's
+// order. Only the order of the final sum of squares differs.
+template <int TX, int TY>
+__global__ void __launch_bounds__(TX * TY) residual_sq_march_kernel(
+    const double* __restrict__ u, const double* __restrict__ F, const double* __restrict__ raw,
+    int nx, int ny, int nz, uint32_t mask, double* __restrict__ partial, int lz) {
+  constexpr int DI[9] = {-1, 1, -1, 1, -1, 1, 0, 0, 0};
+  constexpr int DJ[9] = {-1, -1, 1, 1, 0, 0, -1, 1, 0};
+  constexpr int WI[9] = {0, 0, 0, 0, 1, 1, 2, 2, 3};
+  __shared__ double red[TX * TY / 32];
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const int gx = (nx + TX - 1) / TX, gy = (ny + TY - 1) / TY, gz = (nz + lz - 1) / lz;
+  const long long items = (long long)gx * gy * gz;
+  const long long XY = (long long)nx * ny;
+  double s = 0.0;
+  for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+    const int bx = (int)(it % gx), by = (int)((it / gx) % gy), bz = (int)(it / ((long long)gx * gy));
+    const int i = bx * TX + tx, j = by * TY + ty;
+    if (i >= nx || j >= ny) continue;
+    const int l0 = bz * lz, l1 = min(nz, l0 + lz);
+    auto load_plane = [&](int L, double* d) {
+#pragma unroll
+      for (int o = 0; o < 9; ++o) {
+        const int ii = i + DI[o], jj = j + DJ[o];
+        d[o] = (L >= 0 && L < nz && ii >= 0 && ii < nx && jj >= 0 && jj < ny)
+                   ? __ldg(&u[(long long)L * XY + (long long)jj * nx + ii])
+                   : 0.0;
+      }
+    };
+    double pl[3][9];
+    load_plane(l0 - 1, pl[0]);
+    load_plane(l0, pl[1]);
+    for (int l = l0; l < l1; ++l) {
+      load_plane(l + 1, pl[2]);
+      double w[12];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) w[q] = __ldg(&raw[(long long)l * 12 + q]);
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int o = 0; o < 9; ++o)
+          if (mask & (1u << (k * 9 + o))) acc = DADD(acc, DMUL(w[k * 4 + WI[o]], pl[k][o]));
+      const double r = acc - F[(long long)l * XY + (long long)j * nx + i];
+      s = fma(r, r, s);
+#pragma unroll
+      for (int o = 0; o < 9; ++o) {
+        pl[0][o] = pl[1][o];
+        pl[1][o] = pl[2][o];
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < TX * TY / 32; ++w) t += red[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
 // Complex weights (complex k(z)): out = A ext or rhs - A ext with complex
 // arithmetic, each term w * v = (wr vr - wi vi, wr vi + wi vr) added in the
 // reference's order (assembly.py:229-244 on complex128).
@@ -516,8 +581,13 @@ extern "C" int hfb_residual_sq(hfb_plan* p, const double* u, const double* F, do
   if (!p || !u || !F || !partial) return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
   HFB_CUDA(cudaSetDevice(p->device));
-  residual_sq_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
-      u, F, p->coef + 12LL * p->nz, p->nx, p->ny, p->nz, mask, partial);
+  const int lz = tuning(20);
+  if (lz > 0)
+    residual_sq_march_kernel<64, 4><<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+        u, F, p->coef + 12LL * p->nz, p->nx, p->ny, p->nz, mask, partial, lz);
+  else
+    residual_sq_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+        u, F, p->coef + 12LL * p->nz, p->nx, p->ny, p->nz, mask, partial);
   HFB_LAUNCHED();
   return HFB_OK;
 }

@@ -70,3 +70,17 @@ for v in (0, 32):
             assert torch.equal(F, refs[mode]), mode
 lib.hfb_set_tuning(20, 32)
 print("apply27 bitwise equal across variants")
+
+# the residual sum of squares (zero boundary, interior u)
+u = torch.rand((n, n, n), dtype=torch.float64, device=dev)
+npart = int(lib.hfb_residual_partials(plan.handle))
+part = torch.empty(npart, dtype=torch.float64, device=dev)
+vals = {}
+for v in (0, 32):
+    lib.hfb_set_tuning(20, v)
+    timed(lambda: _native.check(lib.hfb_residual_sq(plan.handle, P(u), P(rhs), P(part), 0x7FFFFFF,
+                                                    st), "residual"),
+          8 * 2 * n ** 3, f"residual_sq, tuning 20 = {v}")
+    vals[v] = float(part.sum())
+lib.hfb_set_tuning(20, 32)
+print("residual sums", vals)
