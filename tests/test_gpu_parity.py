@@ -1194,3 +1194,46 @@ def test_dmma_dst2d_vs_scipy(cuda, nx, ny, nz):
             lib.hfb_set_tuning(17, 0)
             lib.hfb_set_tuning(18, 0)
         assert np.abs(f.values - ref).max() < 1e-13 * np.abs(ref).max(), knobs
+
+
+@pytest.mark.parametrize("shape", [(37, 23, 19), (64, 4, 33), (5, 130, 7), (129, 9, 65)])
+def test_marching_stencils_match_gather_kernels(cuda, shape):
+    """The level-marching RHS operator, 27-point apply and residual (tuning key
+    20 > 0, default 32) against the per-point gather kernels (key 20 = 0) on
+    shapes that do not fill the 64 x 4 x 32 tiles: bitwise for the operators,
+    1e-14 for the (reordered) sum of squares."""
+    import torch
+    nx, ny, nz = shape
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+    plan = hb._native.get_plan(nx, ny, nz, torch.device("cuda", 0))
+    hb.tridiag.device_coefficients(plan, hb.SchemeKind.FOURTH_ORDER,
+                                   hb.constant_profile(-3.0, g), g)
+    lib, P, st = plan.lib, hb._native.ptr, plan.stream()
+    rng = np.random.default_rng(nx * ny + nz)
+    f = torch.from_numpy(rng.standard_normal((nz + 2, ny + 2, nx + 2))).cuda()
+    rhs = torch.from_numpy(rng.standard_normal((nz, ny, nx))).cuda()
+    u = torch.from_numpy(rng.standard_normal((nz, ny, nx))).cuda()
+    part = torch.empty(int(lib.hfb_residual_partials(plan.handle)), dtype=torch.float64,
+                       device="cuda")
+    outs = []
+    try:
+        for v in (0, 32, 5):
+            lib.hfb_set_tuning(20, v)
+            F = torch.empty((nz, ny, nx), dtype=torch.float64, device="cuda")
+            hb._native.check(lib.hfb_rhs_fourth(plan.handle, P(f), P(F), 0.37, st), "rhs4")
+            A0 = torch.empty_like(F)
+            hb._native.check(lib.hfb_apply27(plan.handle, P(f), P(rhs), P(A0), 0x7FFFFFF, 0, st),
+                             "apply27")
+            A1 = torch.empty_like(F)
+            hb._native.check(lib.hfb_apply27(plan.handle, P(f), P(rhs), P(A1), 0x5A5A5A5, 1, st),
+                             "fold")
+            hb._native.check(lib.hfb_residual_sq(plan.handle, P(u), P(rhs), P(part), 0x7FFFFFF,
+                                                 st), "residual")
+            outs.append((F, A0, A1, float(part.sum())))
+    finally:
+        lib.hfb_set_tuning(20, 32)
+    ref = outs[0]
+    for o in outs[1:]:
+        for a, b in zip(o[:3], ref[:3]):
+            assert torch.equal(a, b)
+        assert abs(o[3] - ref[3]) <= 1e-14 * ref[3]
