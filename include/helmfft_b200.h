@@ -94,7 +94,9 @@ uint64_t hfb_launch_count(void);
  * CUDA cores (0); key 17 = force the dense product for lines up to this length
  * (0, default: never; a measurement knob); key 18 = whole-plane 2D DST-I on the
  * FP64 tensor cores for lines up to this length (32, default; lines of 16 and
- * more where the FFT engine applies; 0 = never); key 20 = levels per CTA of the
+ * more where the FFT engine applies; 0 = never); key 19 = one-call z-solve with
+ * whole columns in shared memory when n_z <= 256 and the modes fit in four
+ * waves (1, default) or always the TMA copy ring (0); key 20 = levels per CTA of the
  * marching 4th-order RHS operator (32, default; 0 = one CTA per row, per-point
  * gathers). */
 void hfb_set_tuning(int key, int value);

@@ -660,6 +660,7 @@ static int g_tune_dmma = 1;    // dense DST-I products on the FP64 tensor cores 
 static int g_tune_dense_max = 0;  // force the dense path for lines up to this length (key 17)
 static int g_tune_dmma2d = 32;  // whole-plane DMMA 2D DST-I for lines up to this length (key 18)
 static int g_tune_rhs_march = 32;  // 4th-order RHS operator: levels per marching CTA (key 20; 0 = gathers)
+static int g_tune_thomas_smem = 1;  // one-call z-solve with whole columns in shared memory, n_z <= 256 (key 19)
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
@@ -874,6 +875,7 @@ int tuning(int key) {
     case 16: return g_tune_dmma;
     case 17: return g_tune_dense_max;
     case 18: return g_tune_dmma2d;
+    case 19: return g_tune_thomas_smem;
     case 20: return g_tune_rhs_march;
     default: return 0;
   }
@@ -898,6 +900,7 @@ void set_tuning(int key, int value) {
   if (key == 16) g_tune_dmma = value ? 1 : 0;
   if (key == 17) g_tune_dense_max = value;
   if (key == 18) g_tune_dmma2d = value;
+  if (key == 19) g_tune_thomas_smem = value ? 1 : 0;
   if (key == 20) g_tune_rhs_march = value;
 }
 

@@ -182,8 +182,108 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
   }
 }
 
+// Small systems (n_z <= 256, e.g. cfg1 / cfg2): one warp owns 32 modes of a row
+// and holds all their levels in shared memory (data and cp, 512 n_z bytes), so
+// the sweeps run without a copy ring or per-chunk barriers: load every level,
+// eliminate up, substitute down, store every level. Latency-bound problems
+// (a few thousand modes, a 2 n_z-step recurrence each) are what it is for. The
+// arithmetic is thomas_tma_kernel's expression for expression (cp is kept
+// instead of recomputed: the same values), so results are bitwise the same.
+__global__ void __launch_bounds__(32) thomas_smem_kernel(TmaArgs a) {
+  extern __shared__ __align__(16) double smq[];
+  double* sd = smq;                    // [nz][32] data
+  double* sc = sd + (long long)a.nz * 32;   // [nz][32] cp
+  double* co = sc + (long long)a.nz * 32;   // [nz][12] weights
+  const int t = threadIdx.x;
+  for (int e = t; e < a.nz * 12; e += 32) co[e] = __ldg(a.coef + e);
+  const long long blk = blockIdx.x;
+  const int n = a.row0 + (int)(blk / a.nbpr);
+  const int m0 = (int)(blk % a.nbpr) * 32;
+  const int cols = min(32, a.ncols - m0);
+  const bool live = t < cols;
+  const int m = m0 + t;
+  double* base = a.w + (long long)n * a.ld + m0 + t;
+  if (live) {  // 16 independent loads in flight per thread
+    int l = 0;
+    for (; l + 16 <= a.nz; l += 16) {
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = base[(long long)(l + q) * a.ps];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) sd[(l + q) * 32 + t] = v[q];
+    }
+    for (; l < a.nz; ++l) sd[l * 32 + t] = base[(long long)l * a.ps];
+  }
+  __syncwarp();
+  const double cxv = __ldg(a.cx + n);
+  const double cyv = live ? __ldg(a.cy + a.m_off + m) : 0.0;
+  const double cxy = cxv * cyv;
+  double c = 0.0, x = 0.0;
+  for (int l = 0; l < a.nz; ++l) {
+    const double* cl = co + l * 12;
+    const double lo = eig_s(cl, cxv, cyv, cxy);
+    const double di = eig_s(cl + 4, cxv, cyv, cxy);
+    const double up = eig_s(cl + 8, cxv, cyv, cxy);
+    const double den = (l == 0) ? di : fma(-lo, c, di);
+    if (live && fabs(den) < a.thr) {
+      const unsigned long long key =
+          ((unsigned long long)l * (unsigned long long)a.ny_total +
+           (unsigned long long)(a.m_off + m)) *
+              (unsigned long long)a.nx +
+          (unsigned long long)n;
+      atomicMin(a.err, key);
+    }
+    const double rr = 1.0 / den;
+    x = ((l == 0) ? sd[l * 32 + t] : fma(-lo, x, sd[l * 32 + t])) * rr;
+    sd[l * 32 + t] = x;
+    if (l < a.nz - 1) {
+      c = up * rr;
+      sc[l * 32 + t] = c;
+    }
+  }
+  for (int l = a.nz - 2; l >= 0; --l) {
+    x = fma(-sc[l * 32 + t], x, sd[l * 32 + t]);
+    sd[l * 32 + t] = x;
+  }
+  if (live)
+    for (int l = 0; l < a.nz; ++l) base[(long long)l * a.ps] = sd[l * 32 + t];
+}
+
 int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, long long ps,
                       cudaStream_t st, int bwd_only) {
+  // the whole column on chip (tuning key 19, default on) when the modes fit in
+  // a few waves of it; many modes keep the bandwidth-bound copy ring
+  const size_t sm_small = sizeof(double) * ((size_t)p->nz * 64 + (size_t)p->nz * 12);
+  int per_sm_small = 0, sms_small = 148, dev_small = 0;
+  if (!bwd_only && p->nz <= 256 && tuning(19)) {
+    HFB_CUDA(cudaFuncSetAttribute(thomas_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sm_small));
+    HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_small, thomas_smem_kernel, 32,
+                                                           sm_small));
+    if (cudaGetDevice(&dev_small) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms_small, cudaDevAttrMultiProcessorCount, dev_small);
+  }
+  const long long blocks_small = (long long)p->nx * ((p->ny + 31) / 32);
+  if (per_sm_small > 0 && blocks_small <= 4LL * sms_small * per_sm_small) {
+    TmaArgs a = {};
+    a.w = data;
+    a.coef = p->coef;
+    a.cx = p->cx;
+    a.cy = p->cy;
+    a.nz = p->nz;
+    a.nrows = p->nx;
+    a.ncols = p->ny;
+    a.nbpr = (p->ny + 31) / 32;
+    a.ld = ld;
+    a.ps = ps;
+    a.thr = p->thr;
+    a.err = p->err;
+    a.nx = p->nx;
+    a.ny_total = p->ny;
+    thomas_smem_kernel<<<(unsigned)blocks_small, 32, sm_small, st>>>(a);
+    HFB_LAUNCHED();
+    return HFB_OK;
+  }
   return launch_thomas_tma_cols(p, data, cpk, ld, ps, p->ny, 0, st, bwd_only);
 }
 
