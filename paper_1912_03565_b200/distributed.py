@@ -34,6 +34,7 @@ import ctypes
 import numpy as np
 
 from ._native import HFB_ERR_EXCHANGE, check, get_plan, ptr
+from ._native import check as _check  # for functions whose `check` argument shadows it
 from .errors import ExchangeError
 from .solver import make_exchange_plan
 from .tridiag import device_coefficients
@@ -644,9 +645,6 @@ def solve_partitioned_carry(z_slab, scheme, profile, grid, group=None, timings=N
         timings.update(transform_s=(ev[0].elapsed_time(ev[1]) + ev[2].elapsed_time(ev[3])) / 1e3,
                        exchange_s=0.0, tridiag_s=ev[1].elapsed_time(ev[2]) / 1e3)
     return out
-
-
-_check = check
 
 
 def solve_partitioned_carry_local(values, scheme, profile, grid, parts):
