@@ -228,7 +228,7 @@ def run_reference(args):
                              "sample": sample},
             "e2e": {"value": value, "unit": "pts/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args):
@@ -456,13 +456,31 @@ def run_ours(args):
             "config": workload_config(w, world, args.exchange), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "device": torch.cuda.get_device_name(dev)}
-    print(json.dumps(line), flush=True)
-    if multi:
+    emit(line)
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
+_STDOUT_FD = None
+
+
+def emit(line):
+    """Print the one JSON result line on the real stdout. Everything else that
+    reaches file descriptor 1 during the run (library banners such as NCCL's
+    version line) was redirected to stderr by main()."""
+    sys.stdout.flush()
+    if _STDOUT_FD is not None:
+        os.write(_STDOUT_FD, (json.dumps(line) + "\n").encode())
+    else:
+        emit(line)
+
+
 def main():
+    global _STDOUT_FD
     args = parse()
+    sys.stdout.flush()
+    _STDOUT_FD = os.dup(1)
+    os.dup2(2, 1)  # stdout -> stderr until the result line
     if args.impl == "reference":
         run_reference(args)
     else:
