@@ -445,7 +445,8 @@ def test_tuning_variants_match_oracle(cuda, tuning, knobs):
     assert rel_l2(u, ref) < PARITY
 
 
-@pytest.mark.parametrize("shape", [(31, 31, 31), (127, 63, 33), (255, 15, 9)])
+@pytest.mark.parametrize("shape", [(31, 31, 31), (127, 63, 33), (255, 15, 9), (2047, 15, 4),
+                                   (2047, 31, 3)])
 def test_lean_workspace_bitwise_equal_fast(cuda, shape):
     """The lean one-volume workspace (transposing x-pass stores) and the fast
     two-volume one (row/tensor-box passes) run the same per-line arithmetic."""
@@ -468,7 +469,9 @@ def test_lean_workspace_bitwise_equal_fast(cuda, shape):
     plan.set_workspace_mode(0)
     assert np.array_equal(outs[0], outs[1])
     ref = orc.solve(F.cpu().numpy(), oracle_table("4", prof, g), *orc.mode_cosines(nx, ny))
-    assert rel_l2(outs[0], ref) < PARITY
+    # the 2047-wide shapes are very anisotropic (h_z / h_x ~ 400): conditioning
+    # amplifies rounding to ~1.5e-11, inside the north star's 1e-10
+    assert rel_l2(outs[0], ref) < (PARITY if nx < 2047 else TOL)
 
 
 # ------------------------------------------------------ complex k(z) (f1)
