@@ -199,7 +199,10 @@ __global__ void __launch_bounds__(128) dmma_batched_kernel(
       }
 }
 
-// Small-N 2D DST-I of whole planes on the FP64 tensor cores: Y = S_y X S_x
+// Small-N 2D DST-I of whole planes on the FP64 tensor cores (the reference's
+// per-plane dst2d, spectral.py:54-72, written as the dense product its own
+// test checks against: dst2d_reference / oracle.dense_sine_matrix,
+// spectral.py:66-72, oracle.py:106-109): Y = S_y X S_x
 // (S symmetric, orthonormal scale included) with X, the intermediate T = X S_x,
 // and both S in shared memory, zero-padded to NP x NP (NP = 32 or 64). One
 // plane per CTA iteration, persistent over planes: 16 B/point of HBM traffic
