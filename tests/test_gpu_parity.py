@@ -1240,3 +1240,91 @@ def test_marching_stencils_match_gather_kernels(cuda, shape):
         for a, b in zip(o[:3], ref[:3]):
             assert torch.equal(a, b)
         assert abs(o[3] - ref[3]) <= 1e-14 * ref[3]
+
+
+def _ipc_carry_worker(rank, world, port, q):
+    """One rank of a two-process carry solve on ONE GPU, sequenced by host
+    barriers (rank 0 forward | rank 1 forward + backward | rank 0 backward), so
+    every carry a kernel reads was published by a kernel that already finished:
+    nothing waits on a concurrently running kernel. Exercises the real CUDA IPC
+    path (handles gathered over gloo, the neighbour's region opened in another
+    process, carries and flags stored into it)."""
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1912_03565_b200 import distributed as hd
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        nx, ny, nz = 63, 63, 40
+        g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+        prof = hb.constant_profile(-20.0, g)
+        F = torch.from_numpy(np.random.default_rng(11).standard_normal((nz, ny, nx))).cuda()
+        ex = hb.make_exchange_plan(g, world)
+        z0, z1 = ex.partition.z_ranges[rank]
+        kpz = z1 - z0
+        links = hd.carry_links(g, None, dev)
+        zplan = links.plan
+        hb.tridiag.device_coefficients(zplan, hb.SchemeKind.FOURTH_ORDER, prof, g)
+        tplan = hb._native.get_plan(nx, ny, kpz, dev)
+        ld, P, st = links.ld, hb._native.ptr, tplan.stream()
+        modes = torch.empty(kpz * nx * ld, dtype=torch.float64, device=dev)
+        work = tplan.workspace(5)
+        hb._native.check(tplan.lib.hfb_forward_modes(tplan.handle, P(F[z0:z1].contiguous()),
+                                                     P(modes), P(work), st), "fwd")
+        cp = torch.empty(((kpz + 7) // 8) * nx * ld, dtype=torch.float64, device=dev)
+        epoch = links.next_epoch()
+
+        def sweep(d):
+            peer = links.next if d == 0 else links.prev
+            hb._native.check(zplan.lib.hfb_zsolve_carry(zplan.handle, d, P(modes), ld, z0, kpz,
+                                                        P(cp), P(links.region), peer, epoch,
+                                                        zplan.stream()), f"sweep {d}")
+            torch.cuda.synchronize()
+
+        if rank == 0:
+            sweep(0)
+            dist.barrier()
+            dist.barrier()
+            sweep(1)
+        else:
+            dist.barrier()
+            sweep(0)
+            sweep(1)
+            dist.barrier()
+        out = torch.empty((kpz, ny, nx), dtype=torch.float64, device=dev)
+        hb._native.check(tplan.lib.hfb_inverse_modes(tplan.handle, P(modes), P(out), st), "inv")
+        torch.cuda.synchronize()
+        q.put((rank, out.cpu().numpy(), hd.carry_status_code(zplan)))
+        dist.barrier()  # keep both regions mapped until both ranks are done
+        links.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_carry_ipc_two_processes_one_gpu(cuda):
+    """The transpose-free solve across two processes: bitwise equal to the
+    one-call solve, no missing carry."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_carry_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in range(2)), key=lambda x: x[0])
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(code == 0 for _, _, code in res)
+    U = np.concatenate([r[1] for r in res])
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), 63, 63, 40)
+    F = torch.from_numpy(np.random.default_rng(11).standard_normal((40, 63, 63))).cuda()
+    ref = _one_call(F, hb.SchemeKind.FOURTH_ORDER, hb.constant_profile(-20.0, g), g)
+    assert np.array_equal(U, ref.cpu().numpy())
