@@ -1243,8 +1243,8 @@ def test_marching_stencils_match_gather_kernels(cuda, shape):
 
 
 def _ipc_carry_worker(rank, world, port, q):
-    """One rank of a two-process carry solve on ONE GPU, sequenced by host
-    barriers (rank 0 forward | rank 1 forward + backward | rank 0 backward), so
+    """One rank of a multi-process carry solve on ONE GPU, sequenced by host
+    barriers (forward sweeps rank by rank up, back substitutions down), so
     every carry a kernel reads was published by a kernel that already finished:
     nothing waits on a concurrently running kernel. Exercises the real CUDA IPC
     path (handles gathered over gloo, the neighbour's region opened in another
@@ -1284,15 +1284,13 @@ def _ipc_carry_worker(rank, world, port, q):
                                                         zplan.stream()), f"sweep {d}")
             torch.cuda.synchronize()
 
-        if rank == 0:
-            sweep(0)
-            dist.barrier()
-            dist.barrier()
-            sweep(1)
-        else:
-            dist.barrier()
-            sweep(0)
-            sweep(1)
+        # one rank at a time: forward sweeps up the ranks, then back substitutions
+        # down (the last rank does both in its phase)
+        for phase in range(2 * world - 1):
+            if phase == rank:
+                sweep(0)
+            if phase == 2 * world - 2 - rank:
+                sweep(1)
             dist.barrier()
         out = torch.empty((kpz, ny, nx), dtype=torch.float64, device=dev)
         hb._native.check(tplan.lib.hfb_inverse_modes(tplan.handle, P(modes), P(out), st), "inv")
@@ -1304,9 +1302,11 @@ def _ipc_carry_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_carry_ipc_two_processes_one_gpu(cuda):
-    """The transpose-free solve across two processes: bitwise equal to the
-    one-call solve, no missing carry."""
+@pytest.mark.parametrize("world", [2, 3])
+def test_carry_ipc_two_processes_one_gpu(cuda, world):
+    """The transpose-free solve across two or three processes (three: a middle
+    rank with a neighbour on each side): bitwise equal to the one-call solve, no
+    missing carry."""
     import socket
     import torch
     import torch.multiprocessing as mp
@@ -1315,10 +1315,11 @@ def test_carry_ipc_two_processes_one_gpu(cuda):
         port = sk.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ipc_carry_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_carry_worker, args=(r, world, port, q))
+             for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted((q.get(timeout=300) for _ in range(2)), key=lambda x: x[0])
+    res = sorted((q.get(timeout=300) for _ in range(world)), key=lambda x: x[0])
     for p in procs:
         p.join(120)
     assert all(p.exitcode == 0 for p in procs)
