@@ -1242,7 +1242,7 @@ def test_marching_stencils_match_gather_kernels(cuda, shape):
         assert abs(o[3] - ref[3]) <= 1e-14 * ref[3]
 
 
-def _ipc_carry_worker(rank, world, port, q):
+def _ipc_carry_worker(rank, world, port, q, cplx=False):
     """One rank of a multi-process carry solve on ONE GPU, sequenced by host
     barriers (forward sweeps rank by rank up, back substitutions down), so
     every carry a kernel reads was published by a kernel that already finished:
@@ -1260,8 +1260,8 @@ def _ipc_carry_worker(rank, world, port, q):
         dev = torch.device("cuda", 0)
         nx, ny, nz = 63, 63, 40
         g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
-        prof = hb.constant_profile(-20.0, g)
-        F = torch.from_numpy(np.random.default_rng(11).standard_normal((nz, ny, nx))).cuda()
+        prof = _ipc_profile(g, cplx)
+        F = _ipc_rhs(cplx)
         ex = hb.make_exchange_plan(g, world)
         z0, z1 = ex.partition.z_ranges[rank]
         kpz = z1 - z0
@@ -1270,18 +1270,28 @@ def _ipc_carry_worker(rank, world, port, q):
         hb.tridiag.device_coefficients(zplan, hb.SchemeKind.FOURTH_ORDER, prof, g)
         tplan = hb._native.get_plan(nx, ny, kpz, dev)
         ld, P, st = links.ld, hb._native.ptr, tplan.stream()
-        modes = torch.empty(kpz * nx * ld, dtype=torch.float64, device=dev)
+        parts = [F.real, F.imag] if cplx else [F]
+        modes = [torch.empty(kpz * nx * ld, dtype=torch.float64, device=dev) for _ in parts]
         work = tplan.workspace(5)
-        hb._native.check(tplan.lib.hfb_forward_modes(tplan.handle, P(F[z0:z1].contiguous()),
-                                                     P(modes), P(work), st), "fwd")
-        cp = torch.empty(((kpz + 7) // 8) * nx * ld, dtype=torch.float64, device=dev)
+        for v, m in zip(parts, modes):
+            hb._native.check(tplan.lib.hfb_forward_modes(tplan.handle, P(v[z0:z1].contiguous()),
+                                                         P(m), P(work), st), "fwd")
+        cp = torch.empty(len(parts) * ((kpz + 7) // 8) * nx * ld, dtype=torch.float64,
+                         device=dev)
         epoch = links.next_epoch()
 
         def sweep(d):
-            peer = links.next if d == 0 else links.prev
-            hb._native.check(zplan.lib.hfb_zsolve_carry(zplan.handle, d, P(modes), ld, z0, kpz,
-                                                        P(cp), P(links.region), peer, epoch,
-                                                        zplan.stream()), f"sweep {d}")
+            if cplx:
+                peer = links.next_z if d == 0 else links.prev_z
+                rc = zplan.lib.hfb_zsolve_carry_z(zplan.handle, d, P(modes[0]), P(modes[1]), ld,
+                                                  z0, kpz, P(cp), P(links.region_z), peer, epoch,
+                                                  zplan.stream())
+            else:
+                peer = links.next if d == 0 else links.prev
+                rc = zplan.lib.hfb_zsolve_carry(zplan.handle, d, P(modes[0]), ld, z0, kpz,
+                                                P(cp), P(links.region), peer, epoch,
+                                                zplan.stream())
+            hb._native.check(rc, f"sweep {d}")
             torch.cuda.synchronize()
 
         # one rank at a time: forward sweeps up the ranks, then back substitutions
@@ -1292,18 +1302,38 @@ def _ipc_carry_worker(rank, world, port, q):
             if phase == 2 * world - 2 - rank:
                 sweep(1)
             dist.barrier()
-        out = torch.empty((kpz, ny, nx), dtype=torch.float64, device=dev)
-        hb._native.check(tplan.lib.hfb_inverse_modes(tplan.handle, P(modes), P(out), st), "inv")
+        outs = []
+        for m in modes:
+            out = torch.empty((kpz, ny, nx), dtype=torch.float64, device=dev)
+            hb._native.check(tplan.lib.hfb_inverse_modes(tplan.handle, P(m), P(out), st), "inv")
+            outs.append(out)
         torch.cuda.synchronize()
-        q.put((rank, out.cpu().numpy(), hd.carry_status_code(zplan)))
+        res = torch.complex(outs[0], outs[1]) if cplx else outs[0]
+        q.put((rank, res.cpu().numpy(), hd.carry_status_code(zplan)))
         dist.barrier()  # keep both regions mapped until both ranks are done
         links.close()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_carry_ipc_two_processes_one_gpu(cuda, world):
+def _ipc_profile(g, cplx):
+    if not cplx:
+        return hb.constant_profile(-20.0, g)
+    k2 = np.full(g.n_z + 2, -20.0 + 4.0j)
+    return hb.CoefficientProfile(k2=k2, k2_z=np.zeros_like(k2), k2_zz=np.zeros_like(k2))
+
+
+def _ipc_rhs(cplx):
+    import torch
+    rng = np.random.default_rng(11)
+    F = rng.standard_normal((40, 63, 63))
+    if cplx:
+        F = F + 1j * rng.standard_normal((40, 63, 63))
+    return torch.from_numpy(F).cuda()
+
+
+@pytest.mark.parametrize("world,cplx", [(2, False), (3, False), (3, True)])
+def test_carry_ipc_two_processes_one_gpu(cuda, world, cplx):
     """The transpose-free solve across two or three processes (three: a middle
     rank with a neighbour on each side): bitwise equal to the one-call solve, no
     missing carry."""
@@ -1315,7 +1345,7 @@ def test_carry_ipc_two_processes_one_gpu(cuda, world):
         port = sk.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ipc_carry_worker, args=(r, world, port, q))
+    procs = [ctx.Process(target=_ipc_carry_worker, args=(r, world, port, q, cplx))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -1326,6 +1356,7 @@ def test_carry_ipc_two_processes_one_gpu(cuda, world):
     assert all(code == 0 for _, _, code in res)
     U = np.concatenate([r[1] for r in res])
     g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), 63, 63, 40)
-    F = torch.from_numpy(np.random.default_rng(11).standard_normal((40, 63, 63))).cuda()
-    ref = _one_call(F, hb.SchemeKind.FOURTH_ORDER, hb.constant_profile(-20.0, g), g)
+    F = _ipc_rhs(cplx)
+    solve1 = _one_call_z if cplx else _one_call
+    ref = solve1(F, hb.SchemeKind.FOURTH_ORDER, _ipc_profile(g, cplx), g)
     assert np.array_equal(U, ref.cpu().numpy())
