@@ -14,7 +14,10 @@ def run_bench(*args, env=None):
                          capture_output=True, text=True, timeout=600, cwd=ROOT,
                          env=dict(os.environ, **(env or {})))
     assert out.returncode == 0, out.stderr[-2000:]
-    return [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    lines = out.stdout.splitlines()
+    # stdout carries the JSON result line and nothing else (banners go to stderr)
+    assert all(ln.startswith("{") for ln in lines), lines
+    return lines
 
 
 def test_reference_arm_json_line():
