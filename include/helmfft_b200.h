@@ -63,8 +63,9 @@ const char* hfb_strerror(int code);
 /* Number of kernels this library has launched in the process (all plans). */
 uint64_t hfb_launch_count(void);
 
-/* Performance knobs (no effect on results, bit for bit, except where noted below).
- * They are process-wide (every plan,
+/* Performance knobs (no effect on results beyond rounding: keys 0, 17 and 18
+ * change the transform's factorisation; every other knob keeps the bits, except
+ * key 20's reordered residual sum). They are process-wide (every plan,
  * every thread) and read when a kernel is launched: set them before the solves
  * they should affect, not concurrently with them. key 0 = DST engine width
  * (16 or 32 values per thread), key 1 = transform groups per CTA (0 = auto),
@@ -100,9 +101,7 @@ uint64_t hfb_launch_count(void);
  * waves (1, default) or always the TMA copy ring (0); key 20 = levels per CTA of
  * the marching stencil kernels: the 4th-order RHS operator, the 27-point apply
  * and the residual (32, default; 0 = the per-point gather kernels). Keys 5, 6 and
- * 9 keep measured-slower variants for A/B runs; key 17 is a measurement knob. The
- * residual's sum of squares is the only result whose rounding depends on a knob
- * (key 20 reorders its final sum). */
+ * 9 keep measured-slower variants for A/B runs; key 17 is a measurement knob. */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.
