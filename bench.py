@@ -11,10 +11,11 @@ strong scaling of the same grid. Rank 0 prints ONE JSON line.
 
 `value` times device-resident data with CUDA events (inputs, 8.6 GB, are far
 larger than L2). `e2e` goes through the C-ABI host-buffer entry
-(hfb_solve_host: pinned H2D, solve, D2H). `cpu_baseline` times the oracle
-port (numpy/scipy, all host threads) on a bounded slab of the same planes.
-`--impl reference` times that CPU port alone (the reference is Python: there
-is no compiled oracle/_ref).
+(hfb_solve_host: pinned H2D, solve, D2H). `cpu_baseline` times the stock
+reference the same way (one sample).
+`--impl reference` times the UNMODIFIED reference (helmfft, installed into
+oracle/_ref by oracle/build_ref.sh) on the host cores: stock solve_discrete
+with SharedWorkers on a bounded z-slab sample of the same workload.
 """
 
 import argparse
@@ -61,6 +62,9 @@ def parse():
     ap.add_argument("--exchange", default="carry", choices=["carry", "alltoall"],
                     help="multi-GPU z-solve: transpose-free carries through peer memory "
                          "(default) or the reference's slab<->pencil all-to-all over NCCL")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="CPU test of the launcher: every rank joins a gloo group and rank 0 "
+                         "prints the world size seen by an all-reduce")
     return ap.parse_args()
 
 
@@ -163,10 +167,10 @@ def dist_setup(n_gpus, force=False):
         os.environ.update(RANK="0", LOCAL_RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
                           MASTER_PORT=str(port))
     if n_gpus > 1 or "RANK" in os.environ:
-        # keep rank 0's stdout to the one JSON line (NCCL prints its version banner
-        # there at NCCL_DEBUG=VERSION)
-        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-            os.environ["NCCL_DEBUG"] = "WARN"
+        # NCCL's INFO lines (communicator init: rank / nranks) go to stderr: main()
+        # points fd 1 at stderr until the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if not dist.is_initialized():
             local = int(os.environ.get("LOCAL_RANK", 0))
             torch.cuda.set_device(local)
@@ -199,33 +203,84 @@ def oracle_baseline(w, planes, workers):
     return planes * w.n * w.n / dt, dt
 
 
+def reference_sample(w, planes, workers):
+    """The UNMODIFIED reference (oracle/_ref, installed by oracle/build_ref.sh) on
+    the first `planes` z-levels of the workload (full n x n planes, same step h,
+    the same seeded host F as complex128): stock helmfft.solve_discrete with
+    SharedWorkers(min(workers, planes)) (Sequential() for workers = 1), the call
+    BASELINE.md §2 names. Returns (pts/s by total_s, pts/s by transform +
+    exchange + tridiag, PhaseTimings) or None without the reference."""
+    from oracle import ref_bridge as rb
+    hf = rb.load()
+    if hf is None:
+        return None
+    F, sch, prof, g = rb.reference_case(hf, w, planes)
+    _, t = rb.solve_reference(hf, F, sch, prof, g, workers)
+    pts = planes * w.n * w.n
+    return pts / t.total_s, pts / (t.transform_s + t.exchange_s + t.tridiag_s), t
+
+
+def default_ref_planes(w):
+    # about 64 Mi points per sample: a few seconds of the reference on 8-32 cores
+    return max(2, min(w.n, (64 << 20) // (w.n * w.n)))
+
+
 def run_reference(args):
-    rank, world, _ = (0, 1, 0)
+    """CPU reference arm: the stock reference (kind "reference"), each step one
+    bounded sample of the workload; the oracle port when the reference is not
+    installed (kind "port")."""
     if args.gpus > 1 or "RANK" in os.environ:
-        rank = int(os.environ.get("RANK", 0))
-        if rank != 0:
+        if int(os.environ.get("RANK", 0)) != 0:
             return
     from paper_1912_03565_b200 import workloads as wl
     w = wl.workload(args.cfg)
     cores = os.cpu_count() or 1
-    if args.cpu_planes is None:
-        args.cpu_planes = max(2, w.n // 4)
-    for _ in range(args.warmup):
-        oracle_baseline(w, max(2, args.cpu_planes // 4), cores)
-    vals = []
-    for _ in range(args.steps):
-        v, dt = oracle_baseline(w, args.cpu_planes, cores)
-        vals.append(v)
+    planes = args.cpu_planes or default_ref_planes(w)
+    kind = "reference"
+    if reference_sample(w, 2, cores) is None:  # warms the FFT plans too
+        kind = "port"
+    vals, stage_vals, parts = [], [], []
+    if kind == "reference":
+        for _ in range(args.warmup):
+            reference_sample(w, max(2, planes // 4), cores)
+        for _ in range(args.steps):
+            v, vs, t = reference_sample(w, planes, cores)
+            vals.append(v)
+            stage_vals.append(vs)
+            parts.append(t)
+        seq_planes = max(2, planes // 8)
+        seq = reference_sample(w, seq_planes, 1)
+        port_v, _ = oracle_baseline(w, planes, cores)
+        tmed = parts[len(parts) // 2]
+        sample = (f"stock helmfft.solve_discrete (oracle/_ref) with SharedWorkers({min(cores, planes)}) "
+                  f"on the first {planes} of {w.n} z-planes (full {w.n}x{w.n} planes, same h, "
+                  f"same seeded F as complex128) per step; value = points / PhaseTimings.total_s")
+        extra = {"stages_value": statistics.median(stage_vals),
+                 "stages_definition": "points / (transform_s + exchange_s + tridiag_s)",
+                 "phase_timings_s": {"setup": tmed.setup_s, "transform": tmed.transform_s,
+                                     "exchange": tmed.exchange_s, "tridiag": tmed.tridiag_s,
+                                     "total": tmed.total_s},
+                 "sequential": {"value": seq[0], "stages_value": seq[1], "cores": 1,
+                                "sample": f"Sequential() on the first {seq_planes} z-planes"},
+                 "port": {"value": port_v, "cores": cores,
+                          "sample": f"oracle port (numpy/scipy, batched DUCC0) on the same "
+                                    f"{planes} planes"}}
+    else:
+        for _ in range(args.warmup):
+            oracle_baseline(w, max(2, planes // 4), cores)
+        for _ in range(args.steps):
+            vals.append(oracle_baseline(w, planes, cores)[0])
+        sample = (f"{planes} of {w.n} z-planes (full {w.n}x{w.n} planes) per step, "
+                  f"oracle port numpy/scipy DUCC0, {cores} threads (reference not installed)")
+        extra = {}
     value = statistics.median(vals)
-    sample = (f"{args.cpu_planes} of {w.n} z-planes (full {w.n}x{w.n} planes) per step, "
-              f"oracle port numpy/scipy DUCC0, {cores} threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "pts/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": args.cpu_planes * w.n * w.n / value * 1e3,
+            "ms_per_step": planes * w.n * w.n / value * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": workload_config(w, args.gpus),
-            "cpu_baseline": {"value": value, "unit": "pts/s", "cores": cores, "kind": "port",
-                             "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "pts/s", "cores": cores, "kind": kind,
+                             "sample": sample, **extra},
             "e2e": {"value": value, "unit": "pts/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     emit(line)
@@ -270,10 +325,8 @@ def run_ours(args):
         from paper_1912_03565_b200 import distributed as hd
         ex = hb.make_exchange_plan(w.grid, world)
         z0, z1 = ex.partition.z_ranges[rank]
-        g = torch.Generator(device=dev)
-        g.manual_seed(w.seed * 1000 + rank)
-        F = torch.rand((z1 - z0, n, n), generator=g, device=dev, dtype=torch.float64)
-        F.mul_(2.0).sub_(1.0)
+        # this rank's planes of the one-GPU volume (same values at every N)
+        F = wl.device_rhs(w, dev, planes=z1 - z0, z0=z0)
 
         solve_part = (hd.solve_partitioned_carry if args.exchange == "carry"
                       else hd.solve_partitioned)
@@ -443,12 +496,20 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu and not multi:
         cores = os.cpu_count() or 1
-        if args.cpu_planes is None:
-            args.cpu_planes = n if args.cfg <= 4 else 128
-        v, dt = oracle_baseline(w, args.cpu_planes, cores)
-        cpu = {"value": v, "unit": "pts/s", "cores": cores, "kind": "port",
-               "sample": f"{args.cpu_planes} of {n} z-planes (full {n}x{n} planes), "
-                         f"{dt:.1f} s, numpy/scipy oracle"}
+        planes = args.cpu_planes or default_ref_planes(w)
+        t0 = time.perf_counter()
+        ref = reference_sample(w, planes, cores)
+        if ref is not None:
+            cpu = {"value": ref[0], "unit": "pts/s", "cores": cores, "kind": "reference",
+                   "sample": f"stock helmfft.solve_discrete (oracle/_ref), SharedWorkers("
+                             f"{min(cores, planes)}), first {planes} of {n} z-planes (full "
+                             f"{n}x{n} planes), {time.perf_counter() - t0:.1f} s; value = "
+                             f"points / total_s", "stages_value": ref[1]}
+        else:
+            v, dt = oracle_baseline(w, planes, cores)
+            cpu = {"value": v, "unit": "pts/s", "cores": cores, "kind": "port",
+                   "sample": f"{planes} of {n} z-planes (full {n}x{n} planes), "
+                             f"{dt:.1f} s, numpy/scipy oracle"}
     line = {"metric": METRIC, "value": value, "unit": "pts/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -475,13 +536,46 @@ def emit(line):
         emit(line)
 
 
+def self_launch(args):
+    """`python bench.py --gpus N` with N > 1 outside a launcher: start N local
+    ranks under torch.distributed.run (one process per GPU, rendezvous on
+    127.0.0.1) with the same arguments; rank 0's JSON line passes through on
+    stdout, everything else (NCCL INFO included) on stderr. Returns the exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, BENCH_SELF_LAUNCHED="1")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def launch_check(args):
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    if dist.get_rank() == 0:
+        emit({"launch_check": True, "world": dist.get_world_size(), "sum": int(t.item()),
+              "n_gpus": args.gpus, "self_launched": os.environ.get("BENCH_SELF_LAUNCHED") == "1"})
+    dist.destroy_process_group()
+
+
 def main():
     global _STDOUT_FD
     args = parse()
+    if args.gpus > 1 and "RANK" not in os.environ and "LOCAL_RANK" not in os.environ:
+        sys.exit(self_launch(args))
     sys.stdout.flush()
     _STDOUT_FD = os.dup(1)
     os.dup2(2, 1)  # stdout -> stderr until the result line
-    if args.impl == "reference":
+    if args.launch_check:
+        launch_check(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -339,11 +339,19 @@ extern "C" int hfb_solve(hfb_plan* p, const double* rhs, double* out, void* work
   const size_t vol = (size_t)p->nx * p->ny * p->nz;
   double* cpw = (double*)work;
   double* tmp = transform_work_elems(p, p->nz) ? cpw + vol : nullptr;
+  const StageMarks mark(p, st);
+  mark(0);
   int rc = transform_range(p, rhs, out, 0, p->nz, tmp, st);
   if (rc) return rc;
+  mark(1);
+  mark(2);
   rc = launch_thomas(p, out, p->ny, 0, cpw, st);
   if (rc) return rc;
-  return transform_range(p, out, out, 0, p->nz, tmp, st);
+  mark(3);
+  mark(4);
+  rc = transform_range(p, out, out, 0, p->nz, tmp, st);
+  mark(5);
+  return rc;
 }
 
 extern "C" int hfb_solve_slab_z(hfb_plan* p, double* re, double* im, int m_count, int m_offset,
@@ -366,11 +374,18 @@ extern "C" int hfb_solve_z(hfb_plan* p, const double* rhs_re, const double* rhs_
   const size_t vol = (size_t)p->nx * p->ny * p->nz;
   double* cpw = (double*)work;
   double* tmp = transform_work_elems(p, p->nz) ? cpw + 2 * vol : nullptr;
+  const StageMarks mark(p, st);
+  mark(0);
   int rc = transform_range(p, rhs_re, out_re, 0, p->nz, tmp, st);
   if (!rc) rc = transform_range(p, rhs_im, out_im, 0, p->nz, tmp, st);
+  mark(1);
+  mark(2);
   if (!rc) rc = launch_thomas_slab_z(p, out_re, out_im, p->ny, 0, cpw, st);
+  mark(3);
+  mark(4);
   if (!rc) rc = transform_range(p, out_re, out_re, 0, p->nz, tmp, st);
   if (!rc) rc = transform_range(p, out_im, out_im, 0, p->nz, tmp, st);
+  mark(5);
   return rc;
 }
 

@@ -537,10 +537,7 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
   y.scale = p->scale_y;
   y.M = p->ny + 1;
   int rc;
-  const int slot = p->stage_ring ? (int)(p->stage_count++ % p->stage_ring) : 0;
-  auto mark = [&](int i) {
-    if (p->stage_ring) cudaEventRecord(p->stage_ev[slot * 6 + i], st);
-  };
+  const StageMarks mark(p, st);
   mark(0);
   if (dmma2d_np(p)) {
     // small N: forward 2D DST of whole planes on DMMA straight into the mode
@@ -783,11 +780,19 @@ int solve_fused_z(hfb_plan* p, const double* rhs_re, const double* rhs_im, doubl
   double* Si = Sr + pst * p->nz;
   double* CP = Si + pst * p->nz;
   int rc;
+  const StageMarks mark(p, st);
+  mark(0);
   if ((rc = forward_2d(p, rhs_re, S1, Sr, st))) return rc;
   if ((rc = forward_2d(p, rhs_im, S1, Si, st))) return rc;
+  mark(1);
+  mark(2);
   if ((rc = launch_thomas_tma_z(p, Sr, Si, CP, ldt, pst, st))) return rc;
+  mark(3);
+  mark(4);
   if ((rc = inverse_2d(p, Sr, out_re, st))) return rc;
-  return inverse_2d(p, Si, out_im, st);
+  if ((rc = inverse_2d(p, Si, out_im, st))) return rc;
+  mark(5);
+  return HFB_OK;
 }
 
 // Mode-space transforms for the partitioned solve (one rank's z-slab): the

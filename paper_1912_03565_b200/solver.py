@@ -9,9 +9,11 @@ Every mode runs on the GPU — there is no CPU path:
 
 - ``Sequential()`` / ``SharedWorkers(w)`` / ``Device()``: the single-GPU
   pipeline (forward 2D DST-I -> per-mode Thomas -> inverse 2D DST-I) of the
-  sm_100a library in one call (hfb_solve); its phase timings report the whole
-  device time as transform_s. ``Device(staged=True)`` runs the three stages
-  as separate calls (transform_s / tridiag_s measured separately). Host
+  sm_100a library in one call (hfb_solve); its phase timings split the
+  device time into transform_s (the four DST launches) and tridiag_s (the
+  z-solve) from the library's per-launch CUDA events, as the reference
+  reports them. ``Device(staged=True)`` runs the three stages as separate
+  calls. Host
   worker counts are validated like the reference and otherwise irrelevant:
   parallelism is the GPU's.
 - ``Partitioned(p, t)``: the reference's slab <-> pencil geometry on one
@@ -25,6 +27,8 @@ Every mode runs on the GPU — there is no CPU path:
 Phase timings come from CUDA events on the solve's stream.
 """
 
+import ctypes
+import threading
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Union
@@ -77,7 +81,9 @@ Mode = Union[Sequential, SharedWorkers, Partitioned, Device]
 class SolverConfig:
     mode: Mode = field(default_factory=Sequential)
     transform_parallelism: str = PER_PLANE
-    # accepted for signature compatibility; the device path moves blocks itself
+    # factory(n_parts) -> list of transports, one per part (the reference's plugin
+    # hook, solver.py:65-66): Partitioned mode then routes its blocks through
+    # them (_solve_transport); None = the device moves the blocks itself
     transport_factory: Optional[Callable] = None
 
 
@@ -186,6 +192,30 @@ def exchange_inverse(plan: ExchangePlan, transport, part: int, y_slab):
     return z_slab
 
 
+def _coerce_config(config):
+    """Accept the reference's own SolverConfig / mode objects (helmfft.solver) as
+    well as this package's: callers written against the reference (its harness,
+    its tests) pass those. Matched by class name and fields."""
+    if isinstance(config, SolverConfig) and isinstance(
+            config.mode, (Sequential, SharedWorkers, Partitioned, Device)):
+        return config
+    mode = getattr(config, "mode", None)
+    kind = type(mode).__name__
+    if kind == "Sequential":
+        mode = Sequential()
+    elif kind == "SharedWorkers":
+        mode = SharedWorkers(mode.workers)
+    elif kind == "Partitioned":
+        mode = Partitioned(mode.parts, getattr(mode, "workers_per_part", 1))
+    elif kind == "Device":
+        mode = Device(getattr(mode, "staged", False))
+    else:
+        raise ValueError(f"unknown mode {mode!r}")
+    return SolverConfig(mode=mode,
+                        transform_parallelism=getattr(config, "transform_parallelism", PER_PLANE),
+                        transport_factory=getattr(config, "transport_factory", None))
+
+
 def _validate_config(config: SolverConfig, grid: Grid3D):
     """Worker / part bounds exactly as the reference enforces them (solver.py:204-238)."""
     if config.transform_parallelism not in (PER_PLANE, PER_LINE_BATCH):
@@ -288,10 +318,38 @@ def _solve_part_device(plan, t, grid, config, clock, part_idx):
         return (clock.seconds("t0" + tag, "t1" + tag) + clock.seconds("t2" + tag, "t3" + tag),
                 0.0, clock.seconds("t1" + tag, "t2" + tag))
     work = plan.workspace(0)
-    clock.mark("t0" + tag)
-    check(lib.hfb_solve(h, ptr(t), ptr(t), ptr(work), st), "solve")
-    clock.mark("t1" + tag)
-    return (clock.seconds("t0" + tag, "t1" + tag), 0.0, 0.0)
+    with _StageSplit(plan) as split:
+        check(lib.hfb_solve(h, ptr(t), ptr(t), ptr(work), st), "solve")
+    return split.phases
+
+
+class _StageSplit:
+    """Phase split of one one-call solve (hfb_solve / hfb_solve_z) from the
+    library's per-launch CUDA events (hfb_stage_timing): transform_s = the
+    forward and inverse 2D DST launches, tridiag_s = the z-solve — the
+    reference's PhaseTimings breakdown (solver.py:310-316)."""
+
+    def __init__(self, plan):
+        self.plan = plan
+        self.phases = (0.0, 0.0, 0.0)
+
+    def __enter__(self):
+        check(self.plan.lib.hfb_stage_timing(self.plan.handle, 1), "stage_timing")
+        return self
+
+    def __exit__(self, exc_type, *exc):
+        lib, h = self.plan.lib, self.plan.handle
+        try:
+            if exc_type is None:
+                ms = (ctypes.c_float * 5)()
+                nslots = ctypes.c_int(0)
+                check(lib.hfb_stage_times(h, ms, ctypes.byref(nslots)), "stage_times")
+                if nslots.value != 1:
+                    raise RuntimeError("the solve recorded no stage events")
+                self.phases = ((ms[0] + ms[1] + ms[3] + ms[4]) / 1e3, 0.0, ms[2] / 1e3)
+        finally:
+            lib.hfb_stage_timing(h, 0)
+        return False
 
 
 def _solve_z_device(plan, tr, ti, grid, config, clock):
@@ -333,10 +391,126 @@ def _solve_z_device(plan, tr, ti, grid, config, clock):
                 clock.seconds("z1", "z2") + clock.seconds("z3", "z4"),
                 clock.seconds("z2", "z3"))
     work = plan.workspace(3)
-    clock.mark("z0")
-    check(lib.hfb_solve_z(h, ptr(tr), ptr(ti), ptr(tr), ptr(ti), ptr(work), st), "solve_z")
-    clock.mark("z1")
-    return (clock.seconds("z0", "z1"), 0.0, 0.0)
+    with _StageSplit(plan) as split:
+        check(lib.hfb_solve_z(h, ptr(tr), ptr(ti), ptr(tr), ptr(ti), ptr(work), st), "solve_z")
+    return split.phases
+
+
+def _solve_transport(plan, parts, grid, config):
+    """Partitioned(p, t) with a caller-supplied ``transport_factory``: the
+    reference's part-thread structure (solver.py:319-399) with its blocks routed
+    through the caller's transports (its plugin hook, solver.py:323-327).
+
+    One host thread per part, barrier-separated stages like the reference:
+    the part transforms its z-slab on the device, downloads it, sends and
+    receives the (kpz, kpy(q), n_x) blocks through ``transports[part]``
+    (exchange_forward, ascending destination order), uploads its y-slab and
+    runs the per-mode z-solves there with mode offset y0, and the mirror image
+    back. A transport failure raises the transport's own exception (e.g.
+    ExchangeError) exactly as the reference propagates it. The blocks hold the
+    reference's dtype: complex128 when the field or the table is complex.
+    Device calls are serialised by a lock (one device, one workspace); every
+    arithmetic step is the same kernel as the in-device Partitioned mode."""
+    torch = dv._torch()
+    mode = config.mode
+    nparts = mode.parts
+    lib, h = plan.lib, plan.handle
+    ex = make_exchange_plan(grid, nparts)
+    transports = config.transport_factory(nparts)
+    work_t = plan.workspace(1)
+    dev_lock = threading.Lock()
+    barrier = threading.Barrier(nparts)
+    cplx = len(parts) == 2
+    times = [None] * nparts
+    errors = []
+
+    def dev_call(fn):
+        with dev_lock:
+            with torch.cuda.device(plan.device):
+                out = fn(plan.stream())
+                torch.cuda.current_stream(plan.device).synchronize()
+                return out
+
+    def transform(z0, z1):
+        def go(st):
+            for t in parts:
+                check(lib.hfb_transform_stack(h, ptr(t), z0, z1, ptr(work_t), st), "transform")
+        dev_call(go)
+
+    def host_slab(z0, z1):
+        hs = [t[z0:z1].cpu().numpy() for t in parts]
+        return hs[0] + 1j * hs[1] if cplx else hs[0]
+
+    def run_part(part):
+        try:
+            tr = exs = tri = 0.0
+            z0, z1 = ex.partition.z_ranges[part]
+            y0, y1 = ex.partition.y_ranges[part]
+            barrier.wait()
+            t0 = time.perf_counter()
+            transform(z0, z1)
+            local = dev_call(lambda st: host_slab(z0, z1))
+            tr += time.perf_counter() - t0
+            barrier.wait()
+            t0 = time.perf_counter()
+            y_slab = exchange_forward(ex, transports[part], part, local)
+            exs += time.perf_counter() - t0
+            barrier.wait()
+            t0 = time.perf_counter()
+
+            def solve(st):
+                re = dv.upload(np.ascontiguousarray(y_slab.real if cplx else y_slab), plan.device)
+                if cplx:
+                    im = dv.upload(np.ascontiguousarray(y_slab.imag), plan.device)
+                    cpw = torch.empty((2,) + tuple(re.shape), dtype=torch.float64,
+                                      device=plan.device)
+                    if plan.complex_coef:
+                        check(lib.hfb_solve_slab_z(h, ptr(re), ptr(im), y1 - y0, y0, ptr(cpw),
+                                                   st), "solve_slab_z")
+                    else:
+                        for t in (re, im):
+                            check(lib.hfb_solve_slab(h, ptr(t), y1 - y0, y0, ptr(cpw), st),
+                                  "solve_slab")
+                    return re.cpu().numpy() + 1j * im.cpu().numpy()
+                cpw = torch.empty_like(re)
+                check(lib.hfb_solve_slab(h, ptr(re), y1 - y0, y0, ptr(cpw), st), "solve_slab")
+                return re.cpu().numpy()
+
+            y_slab = dev_call(solve)
+            tri += time.perf_counter() - t0
+            barrier.wait()
+            t0 = time.perf_counter()
+            local = exchange_inverse(ex, transports[part], part, y_slab)
+            exs += time.perf_counter() - t0
+            barrier.wait()
+            t0 = time.perf_counter()
+
+            def put_back(st):
+                for k, t in enumerate(parts):
+                    src = (local.imag if k else local.real) if cplx else local
+                    t[z0:z1].copy_(torch.from_numpy(np.ascontiguousarray(src)))
+
+            dev_call(put_back)
+            transform(z0, z1)
+            tr += time.perf_counter() - t0
+            times[part] = (tr, exs, tri)
+        except BaseException as exc:  # propagate to the caller, release the peers
+            errors.append(exc)
+            barrier.abort()
+
+    threads = [threading.Thread(target=run_part, args=(q,)) for q in range(nparts)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for tp in transports:
+        tp.close()
+    if errors:
+        for exc in errors:  # the root cause rather than broken-barrier fallout
+            if not isinstance(exc, threading.BrokenBarrierError):
+                raise exc
+        raise errors[0]
+    return tuple(max(t[i] for t in times) for i in range(3))
 
 
 def solve_discrete(rhs: Field3D, boundary: BoundaryData, scheme, profile: CoefficientProfile,
@@ -348,6 +522,7 @@ def solve_discrete(rhs: Field3D, boundary: BoundaryData, scheme, profile: Coeffi
     """
     torch = dv._torch()
     t_start = time.perf_counter()
+    config = _coerce_config(config)
     _validate_config(config, grid)
     make_plan(grid.n_x, grid.n_y)
     scheme_key(scheme)
@@ -368,7 +543,14 @@ def solve_discrete(rhs: Field3D, boundary: BoundaryData, scheme, profile: Coeffi
         setup_s = time.perf_counter() - t_start
         clock = _EventClock(torch, device)
         transform_s = exchange_s = tridiag_s = 0.0
-        if plan.complex_coef:
+        if isinstance(config.mode, Partitioned) and config.transport_factory is not None:
+            if on_device and plan.complex_coef:
+                raise NotImplementedError("complex k(z) needs numpy (complex) fields")
+            if plan.complex_coef:
+                while len(parts) < 2:
+                    parts.append(torch.zeros_like(parts[0]))
+            transform_s, exchange_s, tridiag_s = _solve_transport(plan, parts, grid, config)
+        elif plan.complex_coef:
             if on_device:
                 raise NotImplementedError("complex k(z) needs numpy (complex) fields")
             while len(parts) < 2:

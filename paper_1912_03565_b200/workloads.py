@@ -126,17 +126,35 @@ def host_rhs(w: Workload, planes=None):
     return rng.uniform(-1.0, 1.0, shape)
 
 
-def device_rhs(w: Workload, device, planes=None):
-    """Seeded F generated directly on the device (large configs; torch Philox)."""
+RHS_CHUNK = 8  # device_rhs draws planes in seeded chunks of this many planes
+
+
+def device_rhs(w: Workload, device, planes=None, z0=0):
+    """Seeded F generated directly on the device (large configs; torch Philox).
+
+    Planes [z0, z0 + planes) of the workload's volume (all n by default). The
+    volume is drawn in chunks of RHS_CHUNK planes, chunk c from its own
+    generator seeded (seed, c), so any z-slab (one rank's part of a
+    multi-GPU run) equals the same planes of the one-GPU volume bit for bit."""
     import torch
-    nz = w.n if planes is None else planes
+    nz = w.n - z0 if planes is None else planes
+    out = torch.empty((nz, w.n, w.n), device=device, dtype=torch.float64)
     g = torch.Generator(device=device)
-    g.manual_seed(w.seed)
-    shape = (nz, w.n, w.n)
-    if w.rhs_kind == "normal":
-        return torch.randn(shape, generator=g, device=device, dtype=torch.float64)
-    t = torch.rand(shape, generator=g, device=device, dtype=torch.float64)
-    return t.mul_(2.0).sub_(1.0)
+    c = z0 // RHS_CHUNK
+    while c * RHS_CHUNK < z0 + nz:
+        a, b = c * RHS_CHUNK, min((c + 1) * RHS_CHUNK, w.n)
+        g.manual_seed(w.seed * 1_000_003 + c)
+        shape = (b - a, w.n, w.n)
+        if w.rhs_kind == "normal":
+            blk = torch.randn(shape, generator=g, device=device, dtype=torch.float64)
+        else:
+            blk = torch.rand(shape, generator=g, device=device, dtype=torch.float64)
+            blk.mul_(2.0).sub_(1.0)
+        lo, hi = max(a, z0), min(b, z0 + nz)
+        out[lo - z0:hi - z0].copy_(blk[lo - a:hi - a])
+        del blk
+        c += 1
+    return out
 
 
 # --------------------------------------------- manufactured solution (cfg1/2)

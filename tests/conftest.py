@@ -21,6 +21,13 @@ def golden():
 
 
 @pytest.fixture(scope="session")
+def golden_r2():
+    path = os.path.join(ROOT, "tests", "golden", "golden_r2.npz")
+    with np.load(path) as g:
+        return {k: g[k] for k in g.files}
+
+
+@pytest.fixture(scope="session")
 def cuda():
     import torch
     if not torch.cuda.is_available():

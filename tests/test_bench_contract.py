@@ -27,7 +27,8 @@ def test_reference_arm_json_line():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["unit"] == "pts/s" and d["value"] > 0
     assert d["higher_is_better"] is True and d["steps"] == 2
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    # the stock reference when oracle/_ref is installed (oracle/build_ref.sh), else the port
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("cfg1")
 
@@ -36,3 +37,20 @@ def test_reference_arm_non_zero_rank_is_silent():
     lines = run_bench("--impl", "reference", "--cfg", "1", "--steps", "1", "--warmup", "1",
                       "--cpu-planes", "2", "--gpus", "2", env={"RANK": "1", "WORLD_SIZE": "2"})
     assert lines == []
+
+
+def test_self_launch_gloo_ranks():
+    """`python bench.py --gpus 2` outside a launcher spawns 2 local ranks itself
+    (torch.distributed.run, rendezvous on 127.0.0.1); they meet in a gloo group."""
+    lines = run_bench("--launch-check", "--gpus", "2")
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d == {"launch_check": True, "world": 2, "sum": 2, "n_gpus": 2, "self_launched": True}
+
+
+def test_self_launch_reference_arm_prints_one_line():
+    lines = run_bench("--impl", "reference", "--gpus", "2", "--cfg", "1", "--steps", "1",
+                      "--warmup", "0", "--cpu-planes", "4")
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2

@@ -1,0 +1,137 @@
+"""Parity of the benchmarked configurations (round 2): cfg4 at its full 1023^3
+through the bench's exact call, cfg5 on 2047^2 planes through the lean in-place
+layout, and the general admissible table against the real reference.
+
+All device work goes through the C-ABI. Tolerances: the north star's 1e-10
+relative L2 against the oracle; against the reference's own summaries
+(tests/golden/golden_r2.npz, make_golden_r2.py) the measured agreement is
+~1e-14, asserted at 1e-11 (PARITY of test_gpu_parity.py).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import _r2cases as r2
+import paper_1912_03565_b200 as hb
+from oracle import helm_oracle as orc
+from paper_1912_03565_b200 import _native, workloads as wl
+from paper_1912_03565_b200.tridiag import device_coefficients
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+PARITY = 1e-11
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def host_ram_gb():
+    return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
+
+
+def test_cfg4_full_1023_bench_call(cuda):
+    """cfg4 at its FULL 1023^3, exactly as bench.py times it: device-generated
+    F (torch Philox, seed 4), hfb_solve into a separate U with the fast
+    workspace, against the oracle on the same F (all host threads)."""
+    import torch
+    if host_ram_gb() < 80:
+        pytest.fail(f"the 1023^3 oracle needs ~60 GB of host RAM; box has {host_ram_gb():.0f}")
+    w = wl.workload(4)
+    n = w.n
+    lib = _native.load_library()
+    plan = _native.get_plan(n, n, n, cuda)
+    device_coefficients(plan, w.scheme, w.profile, w.grid)
+    plan.set_workspace_mode(False)
+    F = wl.device_rhs(w, cuda)
+    U = torch.empty_like(F)
+    work = plan.workspace(0)
+    _native.check(lib.hfb_solve(plan.handle, _native.ptr(F), _native.ptr(U),
+                                _native.ptr(work), plan.stream()), "solve")
+    plan.fetch_status()
+    del work
+    Fh = F.cpu().numpy()
+    Uh = U.cpu().numpy()
+    del F, U
+    torch.cuda.empty_cache()
+    g = w.grid
+    z = np.zeros(n + 2)
+    T = orc.weight_table("cd4", z, z, z, -1.5, (g.h_x, g.h_y, g.h_z), n)
+    ref = orc.solve(Fh, T, *orc.mode_cosines(n, n), workers=orc.default_workers())
+    del Fh
+    err = rel_l2(Uh, ref)
+    print(f"cfg4 1023^3 full, bench call: rel L2 vs oracle {err:.3e}")
+    assert err < TOL
+
+
+def test_cfg5_slab_2047_lean_in_place(cuda, golden_r2):
+    """cfg5 (general table, 2047^2 planes) on its first 16 planes through the
+    layout the 2047^3 bench runs: lean workspace (hfb_plan_set_workspace_mode 1),
+    in place (U = F). Against the oracle and the reference's summaries."""
+    import torch
+    F, T, (nx, ny, nz), scheme, prof, g = r2.case("cfg5s")
+    lib = _native.load_library()
+    plan = _native.get_plan(nx, ny, nz, cuda)
+    device_coefficients(plan, scheme, prof, g)
+    plan.set_workspace_mode(True)
+    try:
+        X = torch.from_numpy(F).to(cuda)
+        work = plan.workspace(0)
+        _native.check(lib.hfb_solve(plan.handle, _native.ptr(X), _native.ptr(X),
+                                    _native.ptr(work), plan.stream()), "solve")
+        plan.fetch_status()
+        U = X.cpu().numpy()
+    finally:
+        plan.set_workspace_mode(False)
+    ref = orc.solve(F, T, *orc.mode_cosines(nx, ny), workers=orc.default_workers())
+    err = rel_l2(U, ref)
+    errs = r2.summary_errors("cfg5s", U, golden_r2)
+    print(f"cfg5 2047^2 x 16 lean in place: rel L2 vs oracle {err:.3e}; "
+          f"vs reference summaries {errs}")
+    assert err < TOL
+    assert max(errs) < PARITY
+
+
+def test_cfg5_slab_fast_layout_equals_lean(cuda):
+    """The fast (two-volume) layout gives the same bits as the lean one at 2047^2."""
+    import torch
+    F, T, (nx, ny, nz), scheme, prof, g = r2.case("cfg5s")
+    F = F[:9]
+    g = r2.slab_grid(2047, 9)
+    scheme = hb.StencilTable(*(t[:9] for t in T))
+    out = []
+    for lean in (False, True):
+        plan = _native.get_plan(nx, ny, 9, cuda)
+        device_coefficients(plan, scheme, r2.zero_profile(9), g)
+        plan.set_workspace_mode(lean)
+        X = torch.from_numpy(F.copy()).to(cuda)
+        Y = torch.empty_like(X)
+        work = plan.workspace(0)
+        lib = _native.load_library()
+        _native.check(lib.hfb_solve(plan.handle, _native.ptr(X), _native.ptr(Y),
+                                    _native.ptr(work), plan.stream()), "solve")
+        plan.fetch_status()
+        plan.set_workspace_mode(False)
+        out.append(Y.cpu().numpy())
+    assert np.array_equal(out[0], out[1])
+
+
+def test_general_table_63_full_vs_reference(cuda, golden_r2):
+    F, T, _, scheme, prof, g = r2.case("gen63")
+    u, _ = hb.solve_discrete(hb.Field3D(F), hb.BoundaryData.zero(), scheme, prof, g)
+    err = rel_l2(u.values, golden_r2["gen63_U"])
+    print(f"general table 63^3 vs reference: {err:.3e}")
+    assert err < PARITY
+
+
+@pytest.mark.parametrize("name", ["gen127", "cd4n127", "cfg4s"])
+def test_benchmarked_schemes_vs_reference_summaries(cuda, golden_r2, name):
+    F, T, (nx, ny, nz), scheme, prof, g = r2.case(name)
+    u, _ = hb.solve_discrete(hb.Field3D(F), hb.BoundaryData.zero(), scheme, prof, g)
+    errs = r2.summary_errors(name, u.values, golden_r2)
+    ref = orc.solve(F, T, *orc.mode_cosines(nx, ny), workers=orc.default_workers())
+    err = rel_l2(u.values, ref)
+    print(f"{name}: vs oracle {err:.3e}, vs reference summaries {errs}")
+    assert err < TOL
+    assert max(errs) < PARITY

@@ -168,3 +168,25 @@ def test_complex_solves_match_reference(golden, name, key):
     F, B, T, cs = z_case(golden, name, key)
     U = orc.solve(oracle_fold(F, B, T), T, *cs)
     assert rel_l2(U, golden[f"{name}_U"]) < 1e-12
+
+
+# ------------------------------------ round 2: the benchmarked configurations
+import _r2cases as r2  # noqa: E402
+
+
+def test_oracle_general_table_63_full(golden_r2):
+    """cfg5 class (general admissible table) at 63^3 against the reference."""
+    F, T, (nx, ny, nz), *_ = r2.case("gen63")
+    U = orc.solve(F, T, *orc.mode_cosines(nx, ny), workers=4)
+    assert rel_l2(U, golden_r2["gen63_U"]) < 1e-13
+
+
+@pytest.mark.parametrize("name", ["gen127", "cd4n127", "cfg4s", "cfg5s"])
+def test_oracle_benchmarked_configs_summaries(golden_r2, name):
+    """The cfg4 workload (first 8 of its 1023^2 planes), the cfg5 workload (first
+    16 of its 2047^2 planes) and 127^3 cubes of both schemes, against summaries
+    of the reference's solutions."""
+    F, T, (nx, ny, nz), *_ = r2.case(name)
+    U = orc.solve(F, T, *orc.mode_cosines(nx, ny), workers=orc.default_workers())
+    errs = r2.summary_errors(name, U, golden_r2)
+    assert max(errs) < 1e-13, errs
