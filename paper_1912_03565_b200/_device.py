@@ -21,7 +21,10 @@ def is_tensor(x):
 
 
 def unwrap(field):
-    """Field3D-like (anything with .values) or raw array -> raw array."""
+    """Field3D-like (anything with .values) or raw array / tensor -> raw array.
+    (A torch tensor has a .values() method of its own: it is returned as is.)"""
+    if is_tensor(field) or isinstance(field, np.ndarray):
+        return field
     return field.values if hasattr(field, "values") else field
 
 
