@@ -39,6 +39,13 @@ ALG_BYTES_PER_PT = 48  # 3 stages x (8 B read + 8 B write)
 STAGE_ALG_BYTES = 16
 STAGES_FAST = ["dstE x rows F->S1", "dstE y columns S1->S2 (tensor boxes)",
                "thomas_tma z-solve S2", "dstE inverse y rows S2", "dstE inverse x columns S2->U"]
+STAGES_WAVE = ["dstE x rows F->S1", "dstE y columns + forward elimination S1->S2 x', CP cp",
+               "(z-solve fused into the y-passes)",
+               "back substitution + dstE inverse y rows S2 (planes descending)",
+               "dstE inverse x columns S2->U"]
+# bytes each launch must move in the wavefront-fused schedule: the y-pass reads
+# the x-pass output and writes x' and cp; the inverse y-pass reads both back
+STAGE_BYTES_WAVE = [16, 24, 0, 24, 16]
 STAGES_LEAN = ["dstE x rows->columns F->S", "dstE y rows S", "thomas_tma z-solve S",
                "dstE inverse y rows S", "dstE inverse x columns S->U"]
 FALLBACK_HBM = 6650.0
@@ -484,16 +491,18 @@ def run_ours(args):
                               "over the whole step"}
     if stage_ms is not None:
         lean = bool(getattr(plan, "lean", False))
-        names = STAGES_LEAN if lean else STAGES_FAST
-        stages = [{"kernel": nm, "ms": t, "alg_bytes_per_point": STAGE_ALG_BYTES,
-                   "achieved_GBs": STAGE_ALG_BYTES * points / (t / 1e3) / 1e9,
+        wave = stage_ms[2] <= 1e-3 < stage_ms[1]
+        names = STAGES_WAVE if wave else STAGES_LEAN if lean else STAGES_FAST
+        nbytes = STAGE_BYTES_WAVE if wave else [STAGE_ALG_BYTES] * 5
+        stages = [{"kernel": nm, "ms": t, "alg_bytes_per_point": b,
+                   "achieved_GBs": b * points / (t / 1e3) / 1e9 if t > 1e-3 else 0.0,
                    "traffic_bytes": traffic_tab.get(nm)}
-                  for nm, t in zip(names, stage_ms)]
+                  for nm, t, b in zip(names, stage_ms, nbytes)]
         dom = max(stages, key=lambda e: e["ms"])
         roofline = {"bound": "hbm", "achieved": dom["achieved_GBs"], "peak": peak, "unit": "GB/s",
                     "frac": dom["achieved_GBs"] / peak, "traffic": dom["traffic_bytes"],
                     "kernel": dom["kernel"], "kernel_ms": dom["ms"],
-                    "alg_bytes_per_launch": STAGE_ALG_BYTES * points,
+                    "alg_bytes_per_launch": dom["alg_bytes_per_point"] * points,
                     "share_of_step": dom["ms"] / ms, "peak_source": peak_src,
                     "stages": stages, "pipeline": pipeline}
     else:

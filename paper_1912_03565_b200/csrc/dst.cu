@@ -504,11 +504,108 @@ static long long fused_plane(const hfb_plan* p) {
   return std::max(x_ld(p) * p->ny, tran_ld(p) * p->nx);
 }
 
+// Wavefront-fused z-solve (tuning key 21, default on): fast layout, y-lines of
+// 511 or 1023 (the fused passes run the M <= 1024 engine with decoupled
+// 64-thread groups). Workspace: S1 + S2 + the full cp volume + the W carry
+// plane + the level counters.
+static bool wave_path(const hfb_plan* p) {
+  return tran_path(p) && !p->ws_lean && tuning(21) && (p->ny + 1 == 512 || p->ny + 1 == 1024) &&
+         p->nx + 1 <= 4096;
+}
+static size_t wave_flag_elems(const hfb_plan* p) { return (2 * (size_t)p->nx + 16 + 1) / 2; }
+
 size_t fused_work_elems(const hfb_plan* p) {
   if (!tran_path(p)) return 0;
+  if (wave_path(p))
+    return (size_t)fused_plane(p) * (3 * (size_t)p->nz + 1) + wave_flag_elems(p);
   const size_t nck = (p->nz + kThomasChunk - 1) / kThomasChunk;
   const size_t arrays = p->ws_lean ? 1 : 2;
   return (size_t)fused_plane(p) * (arrays * p->nz + nck);
+}
+
+// The wavefront-fused one-call solve (4 launches):
+//   1. x-DST                 F (l, j, i) -> S1 (l, j, n)          [ROW]
+//   2. y-DST + forward elim. S1 columns -> S2 x' (l, n, m), CP cp [kYF2]
+//   3. back subst. + inv y   S2 x', CP -> S2 (l, n, j)            [kYB, planes descending]
+//   4. x-DST                 S2 columns j -> out (l, j, i)        [TLOAD]
+// The z-solve's x' round trip of launch 3 of the five-launch schedule is gone:
+// x' and cp cross HBM once each way inside the y-passes.
+static int solve_wave(hfb_plan* p, const double* rhs, double* out, double* work,
+                      cudaStream_t st) {
+  const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), ldx = x_ld(p);
+  const long long pst = fused_plane(p);
+  double* S1 = work;
+  double* S2 = S1 + pst * p->nz;
+  double* CP = S2 + pst * p->nz;
+  double* WC = CP + pst * p->nz;
+  unsigned* flags = reinterpret_cast<unsigned*>(WC + pst);
+  HFB_CUDA(cudaMemsetAsync(flags, 0, wave_flag_elems(p) * sizeof(double), st));
+  Dst16Call x = {};
+  x.tw = p->tw_x;
+  x.sn = p->sn_x;
+  x.scale = p->scale_x;
+  x.M = p->nx + 1;
+  x.nz = p->nz;
+  Dst16Call y = x;
+  y.tw = p->tw_y;
+  y.sn = p->sn_y;
+  y.scale = p->scale_y;
+  y.M = p->ny + 1;
+  int rc;
+  const StageMarks mark(p, st);
+  mark(0);
+  x.mode = 0;  // ROW: F rows -> S1 (l, j, n)
+  x.src = rhs;
+  x.src_end = rhs + p->nz * ps;
+  x.nrow = p->ny;
+  x.in_ld = p->nx;
+  x.in_ps = ps;
+  x.dst = S1;
+  x.out_ld = ldx;
+  x.out_ps = pst;
+  if ((rc = launch_dst16_mode(x, st))) return rc;
+  mark(1);
+  y.mode = 4;  // kYF2: S1 columns -> S2 x', CP
+  y.src = S1;
+  y.src_end = S1 + p->nz * pst;
+  y.nrow = p->nx;
+  y.in_ld = ldx;
+  y.in_ps = pst;
+  y.dst = S2;
+  y.out_ld = ldt;
+  y.out_ps = pst;
+  y.coef = p->coef;
+  y.cx = p->cx;
+  y.cy = p->cy;
+  y.thr = p->thr;
+  y.err = p->err;
+  y.cp = CP;
+  y.nz_total = p->nz;
+  y.flags = flags;
+  if ((rc = launch_dst16_mode(y, st))) return rc;
+  mark(2);
+  mark(3);  // the z-solve rides in launches 2 and 3
+  y.mode = 5;  // kYB: S2 x' rows (descending planes) -> S2 (l, n, j)
+  y.src = S2;
+  y.src_end = S2 + p->nz * pst;
+  y.in_ld = ldt;
+  y.in_ps = pst;
+  y.wc = WC;
+  y.flags = flags + p->nx + 8;
+  if ((rc = launch_dst16_mode(y, st))) return rc;
+  mark(4);
+  x.mode = 2;  // TLOAD: S2 columns j -> out (l, j, i)
+  x.src = S2;
+  x.src_end = S2 + p->nz * pst;
+  x.nrow = p->ny;
+  x.in_ld = ldt;
+  x.in_ps = pst;
+  x.dst = out;
+  x.out_ld = p->nx;
+  x.out_ps = ps;
+  if ((rc = launch_dst16_mode(x, st))) return rc;
+  mark(5);
+  return HFB_OK;
 }
 
 // Five launches. Fast layout:
@@ -537,6 +634,7 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
   y.scale = p->scale_y;
   y.M = p->ny + 1;
   int rc;
+  if (wave_path(p) && !dmma2d_np(p)) return solve_wave(p, rhs, out, work, st);
   const StageMarks mark(p, st);
   mark(0);
   if (dmma2d_np(p)) {

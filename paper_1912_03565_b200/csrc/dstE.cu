@@ -38,7 +38,22 @@ namespace hfb {
 // Dst16Call::mode. kYF = the y-pass of the one-call solve fused with the
 // forward Thomas sweep: TLOAD input, then per mode x' = (F - lo x)/den, c =
 // up/den carried across levels, x' out by tensor store, c checkpointed.
-enum { kRow = 0, kTran = 1, kTload = 2, kYF = 3 };
+//
+// kYF2 / kYB = the wavefront-fused z-solve of the one-call solve:
+//   kYF2: TLOAD y-pass of (plane l, column block g), then the forward
+//         elimination of its modes with the carries (x', cp at level l - 1) read
+//         from the previous level's outputs in L2 (written by item (l - 1, g),
+//         published by flags[g] = l); x' and cp leave by plain stores into the
+//         (l, n, m) volumes S2 and CP, then flags[g] = l + 1.
+//   kYB : ROW inverse y-pass over planes in DESCENDING order; before the
+//         transform the staged x' rows of line pair k become W = x' - cp W(l+1)
+//         with W(l+1) from the carry plane wc (item (l + 1, k), published by
+//         flags[k] = n_z - 1 - l); W(l) goes back to wc, then flags[k] = n_z - l.
+// Items are interleaved over persistent, co-resident CTAs in increasing order,
+// and an item waits only for an item G (the items per plane) before it, so the
+// wait always ends (the smallest unfinished item never waits on a later one).
+// The arithmetic is thomas_tma_kernel's expression for expression: bitwise equal.
+enum { kRow = 0, kTran = 1, kTload = 2, kYF = 3, kYF2 = 4, kYB = 5 };
 
 struct FftArgs {
   const double2* __restrict__ tw;  // tw[k] = exp(-2 pi i k/M)
@@ -79,6 +94,12 @@ struct StreamArgs {
   int nz_total, ny_total, nx_total;
   int g0;                 // first line block of this launch
   int max_per_sm;         // cap on resident CTAs per SM (0 = occupancy)
+  // kYF2 / kYB: per column block (kYF2) or line pair (kYB) level counters, the
+  // back substitution's W carry plane (n, m) of row stride ck_ld, and the
+  // descending plane order of kYB
+  unsigned* flags;
+  double* wc;
+  int desc;
   long long per;          // batches per CTA (one contiguous run), 0 = interleaved
   int run;                // > 1: interleaved runs of `run` consecutive batches
 };
@@ -107,9 +128,36 @@ __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long
     b = blockIdx.x + it * gridDim.x;
   }
   if (b >= (long long)a.nz * a.G) return false;
-  plane = a.z0 + b / a.G;
+  plane = a.desc ? a.z0 + a.nz - 1 - b / a.G : a.z0 + b / a.G;
   g = a.g0 + (int)(b % a.G);
   return true;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// spin until *p >= v (acquire); the caller then barriers its threads. The wait
+// always ends by construction (see kYF2 / kYB); a broken invariant traps after
+// 20 s (a launch failure) instead of spinning forever.
+__device__ __forceinline__ void wait_level(const unsigned* p, unsigned v) {
+  if (ld_acquire_gpu(p) < v) {
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_gpu(p) < v) {
+      __nanosleep(64);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > 20000000000ull) __trap();
+    }
+  }
+  __threadfence();
+}
+__device__ __forceinline__ double2 ldcg2(const double* p) {
+  return __ldcg(reinterpret_cast<const double2*>(p));
 }
 
 // E = 16: up to 128 threads (two line pairs of M = 1024), 3 CTAs per SM;
@@ -134,7 +182,7 @@ __device__ __forceinline__ void rotate_left(double (&v)[Q], int r) {
 // 32-byte box rows and column chunks) at 256 threads, one CTA per SM.
 template <int P, int E, int MODE>
 constexpr int kMaxThreads = (E == 32 && (1 << P) <= 2048)                  ? 64
-                            : (E == 16 && P == 11 && MODE != kRow && MODE != kYF) ? 256
+                            : (E == 16 && P == 11 && (MODE == kTran || MODE == kTload)) ? 256
                                                                                 : 128;
 template <int P, int E, int MODE>
 constexpr int kMinBlocks = kMaxThreads<P, E, MODE> == 256 ? 1 : MODE == kYF ? 2 : 3;
@@ -156,7 +204,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
   uint64_t* bar = reinterpret_cast<uint64_t*>(wsum + (blockDim.x / 32 + 1));
   auto gbuf = [&](int s, int g) { return sm + (long long)s * a.stage + (long long)g * a.gbuf; };
   const int W = 2 * a.NF;
-  constexpr bool TL = (MODE == kTload || MODE == kYF);
+  constexpr bool TL = (MODE == kTload || MODE == kYF || MODE == kYF2);
   // kYF: c carried per mode, thread-major [group][line][j][t]; cy permuted
   // to [j][t] (thread t's position Q t + j)
   double* ycs = sm + 2LL * a.stage + 2 * (blockDim.x / 32 + 1) + 2;
@@ -174,7 +222,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
   }
 
   __shared__ uint64_t gbar[2][kMaxRows / 2];  // indep: per stage and group
-  const bool indep = (MODE == kRow || MODE == kTload) && a.indep;
+  const bool indep = (MODE == kRow || MODE == kTload || MODE == kYB) && a.indep;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -357,6 +405,42 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         __syncthreads();  // the box interleaves all groups' lines
       }
     } else {
+      if constexpr (MODE == kYB) {
+        // back substitution on the staged x' rows of this group's line pair:
+        // W(l) = x'(l) - cp(l) W(l+1) (thomas_tma_kernel's fma), W(l) -> wc
+        const int l = (int)plane, nzt = a.nz_total;
+        const int pair = g * a.NF + f;
+        if (l < nzt - 1) {
+          if (t == 0) wait_level(a.flags + pair, (unsigned)(nzt - 1 - l));
+          group_sync<T>(f);
+        }
+#pragma unroll
+        for (int L = 0; L < 2; ++L) {
+          const int n = L ? row1 : row0;
+          if (n < 0) continue;
+          double* row = gb + L * a.rowslot + meta.delta[s][2 * f + L];  // position m at row[m]
+          double* wr = a.wc + (long long)n * a.ck_ld;
+          const double* cr = a.ck + (long long)l * a.ck_ps + (long long)n * a.ck_ld;
+#pragma unroll 4
+          for (int u = t; 2 * u < a.N; u += T) {
+            const int m = 2 * u;
+            double2 x = *reinterpret_cast<const double2*>(row + m);
+            if (l < nzt - 1) {
+              const double2 c2 = __ldg(reinterpret_cast<const double2*>(cr + m));
+              const double2 w2 = ldcg2(wr + m);
+              x.x = fma(-c2.x, w2.x, x.x);
+              x.y = fma(-c2.y, w2.y, x.y);
+            }
+            *reinterpret_cast<double2*>(wr + m) = x;
+            *reinterpret_cast<double2*>(row + m) = x;
+          }
+        }
+        group_sync<T>(f);
+        if (t == 0) {
+          __threadfence();
+          st_release_gpu(a.flags + pair, (unsigned)(nzt - l));
+        }
+      }
       const double* r0 = gb + meta.delta[s][2 * f] - 1;  // a_e at r0[e]
       const double* r1 = gb + a.rowslot + meta.delta[s][2 * f + 1] - 1;
       dstE_pre<P, E>(v, c.sn, etw, t, [&](int e) -> double2 {
@@ -367,7 +451,89 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     double2* sb = reinterpret_cast<double2*>(gb);
     fftE_forward<P, E>(v, sb, etw, t, f);
     double2 out[Q];
-    if (MODE != kTran && (a.tstore || a.pbulk || a.ustore)) {
+    if constexpr (MODE == kYF2) {
+      dstE_post_aligned<P, E>(v, sb, wsum, c.scale, t, f, out);
+      // the outputs wait in the group's scratch ([line][j][t]: conflict-free, each
+      // thread reads back only its own) so the elimination runs with the
+      // registers of the transform free for the carries
+      double* fo = gb;
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        fo[j * T + t] = out[j].x;
+        fo[(Q + j) * T + t] = out[j].y;
+      }
+      // forward elimination at level l for this thread's 2 x Q modes; the
+      // carries are level l - 1's outputs of the same column block
+      const int l = (int)plane, nzt = a.nz_total;
+      if (l > 0) {
+        if (threadIdx.x == 0) wait_level(a.flags + g, (unsigned)l);
+        __syncthreads();
+      }
+      const double* cwp = a.coef + (long long)l * 12;
+#pragma unroll 1
+      for (int L = 0; L < 2; ++L) {
+        const int n = L ? row1 : row0;
+        if (n < 0) continue;
+        const double cxv = __ldg(a.cx + n);
+        const long long o = (long long)n * a.out_ld + Q * t;
+        double* xo = a.dst + (long long)l * a.out_ps + o;
+        double* co = a.ck + (long long)l * a.ck_ps + o;
+        double cw[12];
+#pragma unroll
+        for (int q = 0; q < 12; ++q) cw[q] = __ldg(cwp + q);
+        constexpr int H = 8;  // modes per carry batch (registers)
+#pragma unroll 1
+        for (int h = 0; h < Q; h += H) {
+          double xin[H], cin[H];
+          if (l > 0) {
+            const double* xp = xo - a.out_ps + h;
+            const double* cq = co - a.ck_ps + h;
+#pragma unroll
+            for (int j = 0; j < H; j += 2) {
+              const double2 x2 = ldcg2(xp + j), c2 = ldcg2(cq + j);
+              xin[j] = x2.x;
+              xin[j + 1] = x2.y;
+              cin[j] = c2.x;
+              cin[j + 1] = c2.y;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < H; j += 2) {
+            double xr[2], cr[2];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              const int m = Q * t + h + j + jj;
+              const double cyv = m < a.ny_total ? __ldg(a.cy + m) : 0.0;
+              const double cxy = cxv * cyv;
+              const double lo = fma(cw[0], cxy, fma(cw[1], cxv, fma(cw[2], cyv, cw[3])));
+              const double di = fma(cw[4], cxy, fma(cw[5], cxv, fma(cw[6], cyv, cw[7])));
+              const double up = fma(cw[8], cxy, fma(cw[9], cxv, fma(cw[10], cyv, cw[11])));
+              const double den = (l == 0) ? di : fma(-lo, cin[j + jj], di);
+              if (m < a.ny_total && fabs(den) < a.thr) {
+                const unsigned long long key =
+                    ((unsigned long long)l * (unsigned long long)a.ny_total +
+                     (unsigned long long)m) *
+                        (unsigned long long)a.nx_total +
+                    (unsigned long long)n;
+                atomicMin(a.err, key);
+              }
+              const double rr = 1.0 / den;
+              const double F = fo[(L * Q + h + j + jj) * T + t];
+              xr[jj] = ((l == 0) ? F : fma(-lo, xin[j + jj], F)) * rr;
+              cr[jj] = up * rr;
+            }
+            *reinterpret_cast<double2*>(xo + h + j) = make_double2(xr[0], xr[1]);
+            if (l < nzt - 1)
+              *reinterpret_cast<double2*>(co + h + j) = make_double2(cr[0], cr[1]);
+          }
+        }
+      }
+      __syncthreads();  // every thread's x' and cp of level l are stored
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_gpu(a.flags + g, (unsigned)(l + 1));
+      }
+    } else if (MODE != kTran && (a.tstore || a.pbulk || a.ustore)) {
       // Segment-aligned outputs staged as the group's tensor box [2 lines]
       // [M/16 segments][16] in the 128B-swizzle layout (granule h of smem row r
       // at h ^ (r & 7): conflict-free, since thread t owns whole segments),
@@ -661,6 +827,7 @@ static int g_tune_dense_max = 0;  // force the dense path for lines up to this l
 static int g_tune_dmma2d = 32;  // whole-plane DMMA 2D DST-I for lines up to this length (key 18)
 static int g_tune_rhs_march = 32;  // 4th-order RHS operator: levels per marching CTA (key 20; 0 = gathers)
 static int g_tune_thomas_smem = 1;  // one-call z-solve with whole columns in shared memory, n_z <= 256 (key 19)
+static int g_tune_wave = 1;  // one-call solve: wavefront-fused z-solve in the y-passes (key 21)
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
@@ -688,6 +855,10 @@ static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMa
   if (MODE == kYF) {
     // one CTA per column block, walking the levels in order (the Thomas carry)
     blocks = a.G;
+  } else if (MODE == kYF2 || MODE == kYB) {
+    // wavefront-fused z-solve: interleaved items over co-resident CTAs (the
+    // flag waits need every CTA resident), column blocks in runs of two
+    b.run = MODE == kYF2 ? 2 : 1;
   } else if (g_tune_order == 1) {
     b.per = (work + blocks - 1) / blocks;
     blocks = (work + b.per - 1) / b.per;
@@ -707,7 +878,12 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   const int maxt = k.mode == kTran    ? kMaxThreads<P, E, kTran>
                    : k.mode == kTload ? kMaxThreads<P, E, kTload>
                    : k.mode == kYF    ? kMaxThreads<P, E, kYF>
+                   : k.mode == kYF2   ? kMaxThreads<P, E, kYF2>
+                   : k.mode == kYB    ? kMaxThreads<P, E, kYB>
                                       : kMaxThreads<P, E, kRow>;
+  if ((k.mode == kYF2 || k.mode == kYB) && (P > 10 || E != 16 || !k.flags || !k.cp ||
+                                            !k.coef || (k.mode == kYB && !k.wc)))
+    return HFB_ERR_ARGUMENT;
   int nf = std::max(1, std::min(maxt / T, kMaxRows / 2));
   if (g_tune_NF > 0) nf = std::max(1, std::min(g_tune_NF, nf));
   a.NF = 1;
@@ -729,10 +905,14 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   int gb = std::max(2 * a.rowslot, 2 * G::BUF);
   // tensor-store outputs: rows stored whole (position N lands in the row's
   // padding, so ld >= M), 16-byte aligned rows and planes
-  a.tstore = (k.mode != kTran) && (g_tune_tstore || k.mode == kYF) && M >= 16 &&
+  a.flags = k.flags;
+  a.wc = k.wc;
+  a.desc = k.mode == kYB;
+  a.tstore = (k.mode != kTran && k.mode != kYF2) &&
+             (g_tune_tstore || k.mode == kYF || k.mode == kYB) && M >= 16 &&
              a.out_ld >= M && !(reinterpret_cast<uintptr_t>(a.dst) & 15) && !(a.out_ld & 1) &&
              !(a.out_ps & 1);
-  if (k.mode == kYF && !a.tstore) return HFB_ERR_ARGUMENT;
+  if ((k.mode == kYF || k.mode == kYB) && !a.tstore) return HFB_ERR_ARGUMENT;
   a.pbulk = !a.tstore && (k.mode == kRow || k.mode == kTload) && E == 16 && g_tune_pbulk &&
             a.out_ld == a.N && !(reinterpret_cast<uintptr_t>(a.dst) & 7);
   // (measured: 4.47 -> 4.22 ms at M = 1024, 46.3 -> 45.3 ms at M = 2048, slower at 512)
@@ -766,8 +946,9 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   // decoupled groups: row passes, and column passes at M = 2048 (measured: x 3.90 -> 3.78,
   // inverse y 3.92 -> 3.82 ms at 1023^3; final x-pass 46.3 -> 42.3 ms at 2047^3; the
   // column passes at M = 1024 got slower with per-group boxes, 4.28 -> 4.57 ms)
-  a.indep = (k.mode == kRow || (k.mode == kTload && M == 2048)) && (a.tstore || a.ustore) &&
-            g_tune_indep && T >= 32;
+  a.indep = (k.mode == kRow || k.mode == kYB || (k.mode == kTload && M == 2048)) &&
+            (a.tstore || a.ustore) && (g_tune_indep || k.mode == kYB) && T >= 32;
+  if (k.mode == kYB && !a.indep) return HFB_ERR_ARGUMENT;
   CUtensorMap umap;
   memset(&umap, 0, sizeof(umap));
   if (a.ustore) {
@@ -790,7 +971,7 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   long long stage = (long long)a.NF * a.gbuf;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
-  if (k.mode == kTload || k.mode == kYF) {
+  if (k.mode == kTload || k.mode == kYF || k.mode == kYF2) {
     a.boxn = std::min(256, M);
     a.nbox = M / a.boxn;
     stage = std::max<long long>(stage, (long long)a.nbox * a.boxn * W);
@@ -838,6 +1019,25 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
     a.nx_total = a.nrow;
     return launch_stream<P, E, kYF>(a, c, tmap, omap, umap, threads, sm, st);
   }
+  if (k.mode == kYF2 || k.mode == kYB) {
+    a.coef = k.coef;
+    a.cx = k.cx;
+    a.cy = k.cy;
+    a.thr = k.thr;
+    a.err = k.err;
+    a.ck = k.cp;  // the full cp volume, layout of the y-pass output rows
+    // (n, m) rows of the mode volume: the kYF2 output / the kYB input layout
+    a.ck_ld = k.mode == kYF2 ? a.out_ld : a.in_ld;
+    a.ck_ps = k.mode == kYF2 ? a.out_ps : a.in_ps;
+    a.nz_total = k.nz_total;
+    a.ny_total = a.N;
+    a.nx_total = a.nrow;
+    if constexpr (P <= 10 && E == 16) {
+      if (k.mode == kYF2) return launch_stream<P, E, kYF2>(a, c, tmap, omap, umap, threads, sm, st);
+      return launch_stream<P, E, kYB>(a, c, tmap, omap, umap, threads, sm, st);
+    }
+    return HFB_ERR_ARGUMENT;
+  }
   if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, tmap, omap, umap, threads, sm, st);
   if (k.mode == kTload) return launch_stream<P, E, kTload>(a, c, tmap, omap, umap, threads, sm, st);
   return launch_stream<P, E, kRow>(a, c, tmap, omap, umap, threads, sm, st);
@@ -877,6 +1077,7 @@ int tuning(int key) {
     case 18: return g_tune_dmma2d;
     case 19: return g_tune_thomas_smem;
     case 20: return g_tune_rhs_march;
+    case 21: return g_tune_wave;
     default: return 0;
   }
 }
@@ -902,11 +1103,12 @@ void set_tuning(int key, int value) {
   if (key == 18) g_tune_dmma2d = value;
   if (key == 19) g_tune_thomas_smem = value ? 1 : 0;
   if (key == 20) g_tune_rhs_march = value;
+  if (key == 21) g_tune_wave = value ? 1 : 0;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {
   if (k.nz <= 0 || k.nrow <= 0) return HFB_OK;
-  if (k.mode < kRow || k.mode > kYF) return HFB_ERR_ARGUMENT;
+  if (k.mode < kRow || k.mode > kYB) return HFB_ERR_ARGUMENT;
   if (k.mode == kYF && (k.z0 != 0 || !k.coef || !k.cp)) return HFB_ERR_ARGUMENT;
   int p = 0;
   while ((1 << p) < k.M) ++p;

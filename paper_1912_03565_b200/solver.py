@@ -346,7 +346,12 @@ class _StageSplit:
                 check(lib.hfb_stage_times(h, ms, ctypes.byref(nslots)), "stage_times")
                 if nslots.value != 1:
                     raise RuntimeError("the solve recorded no stage events")
-                self.phases = ((ms[0] + ms[1] + ms[3] + ms[4]) / 1e3, 0.0, ms[2] / 1e3)
+                if ms[2] <= 1e-3 < ms[1]:
+                    # wavefront-fused schedule: the z-solve sweeps ride in the two
+                    # y-pass launches (forward elimination / back substitution)
+                    self.phases = ((ms[0] + ms[4]) / 1e3, 0.0, (ms[1] + ms[3]) / 1e3)
+                else:
+                    self.phases = ((ms[0] + ms[1] + ms[3] + ms[4]) / 1e3, 0.0, ms[2] / 1e3)
         finally:
             lib.hfb_stage_timing(h, 0)
         return False
