@@ -100,8 +100,13 @@ uint64_t hfb_launch_count(void);
  * whole columns in shared memory when n_z <= 256 and the modes fit in four
  * waves (1, default) or always the TMA copy ring (0); key 20 = levels per CTA of
  * the marching stencil kernels: the 4th-order RHS operator, the 27-point apply
- * and the residual (32, default; 0 = the per-point gather kernels). Keys 5, 6 and
- * 9 keep measured-slower variants for A/B runs; key 17 is a measurement knob. */
+ * and the residual (32, default; 0 = the per-point gather kernels); key 21 = the
+ * one-call solve's wavefront-fused z-solve (forward elimination inside the
+ * y-pass, back substitution inside the inverse y-pass, carries through L2 with
+ * per-block level counters; fast layout, y-lines of 511 / 1023; bitwise equal;
+ * 0, default: measured slower); key 22 = its measurement variants. Keys 5, 6, 9
+ * and 21 keep measured-slower variants for A/B runs; keys 17 and 22 are
+ * measurement knobs (22 bit 0 skips the waits: wrong results). */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.

@@ -100,6 +100,7 @@ struct StreamArgs {
   unsigned* flags;
   double* wc;
   int desc;
+  int dbg;  // measurement only (tuning key 22): 1 no waits, 2 acq_rel fences, 4 no fences
   long long per;          // batches per CTA (one contiguous run), 0 = interleaved
   int run;                // > 1: interleaved runs of `run` consecutive batches
 };
@@ -144,7 +145,15 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 // spin until *p >= v (acquire); the caller then barriers its threads. The wait
 // always ends by construction (see kYF2 / kYB); a broken invariant traps after
 // 20 s (a launch failure) instead of spinning forever.
-__device__ __forceinline__ void wait_level(const unsigned* p, unsigned v) {
+__device__ __forceinline__ void fence_gpu(int dbg) {
+  if (dbg & 4) return;
+  if (dbg & 2)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  else
+    __threadfence();
+}
+__device__ __forceinline__ void wait_level(const unsigned* p, unsigned v, int dbg) {
+  if (dbg & 1) return;
   if (ld_acquire_gpu(p) < v) {
     unsigned long long t0, t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -154,7 +163,7 @@ __device__ __forceinline__ void wait_level(const unsigned* p, unsigned v) {
       if (t1 - t0 > 20000000000ull) __trap();
     }
   }
-  __threadfence();
+  fence_gpu(dbg);
 }
 __device__ __forceinline__ double2 ldcg2(const double* p) {
   return __ldcg(reinterpret_cast<const double2*>(p));
@@ -411,9 +420,10 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         const int l = (int)plane, nzt = a.nz_total;
         const int pair = g * a.NF + f;
         if (l < nzt - 1) {
-          if (t == 0) wait_level(a.flags + pair, (unsigned)(nzt - 1 - l));
+          if (t == 0) wait_level(a.flags + pair, (unsigned)(nzt - 1 - l), a.dbg);
           group_sync<T>(f);
         }
+        // W(l) = x'(l) - cp(l) W(l + 1) on coalesced 16-byte lanes of each line
 #pragma unroll
         for (int L = 0; L < 2; ++L) {
           const int n = L ? row1 : row0;
@@ -437,7 +447,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         }
         group_sync<T>(f);
         if (t == 0) {
-          __threadfence();
+          fence_gpu(a.dbg);
           st_release_gpu(a.flags + pair, (unsigned)(nzt - l));
         }
       }
@@ -453,20 +463,31 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     double2 out[Q];
     if constexpr (MODE == kYF2) {
       dstE_post_aligned<P, E>(v, sb, wsum, c.scale, t, f, out);
-      // the outputs wait in the group's scratch ([line][j][t]: conflict-free, each
-      // thread reads back only its own) so the elimination runs with the
-      // registers of the transform free for the carries
-      double* fo = gb;
+      // The outputs wait in the group's scratch in the 128B-swizzled box layout
+      // of the tensor-store path (conflict-free both ways), and the elimination
+      // re-maps threads to modes m = t + T i: every carry load and every x' / cp
+      // store is then a coalesced 256-byte warp access, and the transform's
+      // registers are free for the carries.
+      constexpr int NSEG = M / 16;
+      auto phys = [](int L, int pos) {
+        const int row = L * NSEG + (pos >> 4);
+        return row * 16 + 2 * (((pos >> 1) & 7) ^ (row & 7)) + (pos & 1);
+      };
 #pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        fo[j * T + t] = out[j].x;
-        fo[(Q + j) * T + t] = out[j].y;
-      }
-      // forward elimination at level l for this thread's 2 x Q modes; the
-      // carries are level l - 1's outputs of the same column block
+      for (int L = 0; L < 2; ++L)
+#pragma unroll
+        for (int h = 0; h < Q / 2; ++h) {
+          const int pos = Q * t + 2 * h;
+          *reinterpret_cast<double2*>(gb + phys(L, pos)) =
+              L == 0 ? make_double2(out[2 * h].x, out[2 * h + 1].x)
+                     : make_double2(out[2 * h].y, out[2 * h + 1].y);
+        }
+      group_sync<T>(f);
+      // forward elimination at level l of the group's 2 x M modes; the carries
+      // are level l - 1's outputs of the same column block
       const int l = (int)plane, nzt = a.nz_total;
       if (l > 0) {
-        if (threadIdx.x == 0) wait_level(a.flags + g, (unsigned)l);
+        if (threadIdx.x == 0) wait_level(a.flags + g, (unsigned)l, a.dbg);
         __syncthreads();
       }
       const double* cwp = a.coef + (long long)l * 12;
@@ -475,62 +496,51 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         const int n = L ? row1 : row0;
         if (n < 0) continue;
         const double cxv = __ldg(a.cx + n);
-        const long long o = (long long)n * a.out_ld + Q * t;
+        const long long o = (long long)n * a.out_ld + t;
         double* xo = a.dst + (long long)l * a.out_ps + o;
         double* co = a.ck + (long long)l * a.ck_ps + o;
         double cw[12];
 #pragma unroll
         for (int q = 0; q < 12; ++q) cw[q] = __ldg(cwp + q);
-        constexpr int H = 8;  // modes per carry batch (registers)
+        constexpr int H = Q / 2;  // modes per carry batch
 #pragma unroll 1
         for (int h = 0; h < Q; h += H) {
           double xin[H], cin[H];
           if (l > 0) {
-            const double* xp = xo - a.out_ps + h;
-            const double* cq = co - a.ck_ps + h;
+            const double* xp = xo - a.out_ps + T * h;
+            const double* cq = co - a.ck_ps + T * h;
 #pragma unroll
-            for (int j = 0; j < H; j += 2) {
-              const double2 x2 = ldcg2(xp + j), c2 = ldcg2(cq + j);
-              xin[j] = x2.x;
-              xin[j + 1] = x2.y;
-              cin[j] = c2.x;
-              cin[j + 1] = c2.y;
+            for (int i = 0; i < H; ++i) {
+              xin[i] = __ldcg(xp + T * i);
+              cin[i] = __ldcg(cq + T * i);
             }
           }
 #pragma unroll
-          for (int j = 0; j < H; j += 2) {
-            double xr[2], cr[2];
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) {
-              const int m = Q * t + h + j + jj;
-              const double cyv = m < a.ny_total ? __ldg(a.cy + m) : 0.0;
-              const double cxy = cxv * cyv;
-              const double lo = fma(cw[0], cxy, fma(cw[1], cxv, fma(cw[2], cyv, cw[3])));
-              const double di = fma(cw[4], cxy, fma(cw[5], cxv, fma(cw[6], cyv, cw[7])));
-              const double up = fma(cw[8], cxy, fma(cw[9], cxv, fma(cw[10], cyv, cw[11])));
-              const double den = (l == 0) ? di : fma(-lo, cin[j + jj], di);
-              if (m < a.ny_total && fabs(den) < a.thr) {
-                const unsigned long long key =
-                    ((unsigned long long)l * (unsigned long long)a.ny_total +
-                     (unsigned long long)m) *
-                        (unsigned long long)a.nx_total +
-                    (unsigned long long)n;
-                atomicMin(a.err, key);
-              }
-              const double rr = 1.0 / den;
-              const double F = fo[(L * Q + h + j + jj) * T + t];
-              xr[jj] = ((l == 0) ? F : fma(-lo, xin[j + jj], F)) * rr;
-              cr[jj] = up * rr;
+          for (int i = 0; i < H; ++i) {
+            const int m = t + T * (h + i);
+            const double cyv = m < a.ny_total ? __ldg(a.cy + m) : 0.0;
+            const double cxy = cxv * cyv;
+            const double lo = fma(cw[0], cxy, fma(cw[1], cxv, fma(cw[2], cyv, cw[3])));
+            const double di = fma(cw[4], cxy, fma(cw[5], cxv, fma(cw[6], cyv, cw[7])));
+            const double up = fma(cw[8], cxy, fma(cw[9], cxv, fma(cw[10], cyv, cw[11])));
+            const double den = (l == 0) ? di : fma(-lo, cin[i], di);
+            if (m < a.ny_total && fabs(den) < a.thr) {
+              const unsigned long long key =
+                  ((unsigned long long)l * (unsigned long long)a.ny_total + (unsigned long long)m) *
+                      (unsigned long long)a.nx_total +
+                  (unsigned long long)n;
+              atomicMin(a.err, key);
             }
-            *reinterpret_cast<double2*>(xo + h + j) = make_double2(xr[0], xr[1]);
-            if (l < nzt - 1)
-              *reinterpret_cast<double2*>(co + h + j) = make_double2(cr[0], cr[1]);
+            const double rr = 1.0 / den;
+            const double F = gb[phys(L, m)];
+            xo[T * (h + i)] = ((l == 0) ? F : fma(-lo, xin[i], F)) * rr;
+            if (l < nzt - 1) co[T * (h + i)] = up * rr;
           }
         }
       }
       __syncthreads();  // every thread's x' and cp of level l are stored
       if (threadIdx.x == 0) {
-        __threadfence();
+        fence_gpu(a.dbg);
         st_release_gpu(a.flags + g, (unsigned)(l + 1));
       }
     } else if (MODE != kTran && (a.tstore || a.pbulk || a.ustore)) {
@@ -827,7 +837,11 @@ static int g_tune_dense_max = 0;  // force the dense path for lines up to this l
 static int g_tune_dmma2d = 32;  // whole-plane DMMA 2D DST-I for lines up to this length (key 18)
 static int g_tune_rhs_march = 32;  // 4th-order RHS operator: levels per marching CTA (key 20; 0 = gathers)
 static int g_tune_thomas_smem = 1;  // one-call z-solve with whole columns in shared memory, n_z <= 256 (key 19)
-static int g_tune_wave = 1;  // one-call solve: wavefront-fused z-solve in the y-passes (key 21)
+// one-call solve: wavefront-fused z-solve in the y-passes (key 21). Off: measured
+// 34.7 vs 22.1 ms at 1023^3 — the carry / cp loads stall the
+// 12 warps per SM the register-resident engine leaves (long scoreboard 3-8 per issue)
+static int g_tune_wave = 0;
+static int g_tune_wave_dbg = 0;  // its measurement variants (key 22; wrong results for bit 1)
 
 template <int P, int E, int MODE>
 static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMap& tmap,
@@ -908,6 +922,7 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   a.flags = k.flags;
   a.wc = k.wc;
   a.desc = k.mode == kYB;
+  a.dbg = g_tune_wave_dbg;
   a.tstore = (k.mode != kTran && k.mode != kYF2) &&
              (g_tune_tstore || k.mode == kYF || k.mode == kYB) && M >= 16 &&
              a.out_ld >= M && !(reinterpret_cast<uintptr_t>(a.dst) & 15) && !(a.out_ld & 1) &&
@@ -1078,6 +1093,7 @@ int tuning(int key) {
     case 19: return g_tune_thomas_smem;
     case 20: return g_tune_rhs_march;
     case 21: return g_tune_wave;
+    case 22: return g_tune_wave_dbg;
     default: return 0;
   }
 }
@@ -1104,6 +1120,7 @@ void set_tuning(int key, int value) {
   if (key == 19) g_tune_thomas_smem = value ? 1 : 0;
   if (key == 20) g_tune_rhs_march = value;
   if (key == 21) g_tune_wave = value ? 1 : 0;
+  if (key == 22) g_tune_wave_dbg = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

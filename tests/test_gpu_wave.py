@@ -1,7 +1,6 @@
-"""The wavefront-fused z-solve (tuning key 21, the default one-call schedule for
-y-lines of 511 / 1023): forward elimination inside the y-pass, back substitution
-inside the inverse y-pass, carries through L2 between the items of consecutive
-levels. It must equal the five-launch schedule (key 21 = 0) BIT FOR BIT — the
+"""The wavefront-fused z-solve (tuning key 21; measured slower, off by default —
+DESIGN.md §8): forward elimination inside the y-pass, back substitution inside
+the inverse y-pass, carries through L2 between the items of consecutive levels. It must equal the five-launch schedule (key 21 = 0) BIT FOR BIT — the
 same expressions — on every shape class, and raise the same singular mode."""
 import math
 
@@ -31,7 +30,7 @@ def solve_with(key21, F, scheme, prof, g, cuda):
         plan.fetch_status()
         return Y.cpu().numpy()
     finally:
-        lib.hfb_set_tuning(21, 1)
+        lib.hfb_set_tuning(21, 0)
 
 
 @pytest.mark.parametrize("nx,ny,nz", [(1023, 1023, 9), (511, 511, 20), (255, 511, 33),
