@@ -352,6 +352,19 @@ int hfb_unpack_modes(hfb_plan* plan, const double* recv, double* modes, const in
 int hfb_carry_layout(hfb_plan* plan, int ld, long long* region_doubles, int* blocks);
 int hfb_zsolve_carry(hfb_plan* plan, int dir, double* modes, int ld, int z0, int nzl,
                      void* cp_work, double* mine, double* peer, uint32_t epoch, void* stream);
+/* Verification of the cross-rank carry protocol on ONE device (no peer GPUs):
+ * the direction-`dir` sweeps of `nranks` virtual ranks run in ONE cooperative
+ * launch, so every rank's CTAs spin on flags that the neighbouring rank's CTAs
+ * publish while running concurrently (the live release/acquire path of
+ * hfb_zsolve_carry across GPUs). Rank r owns levels [z0s[r], z0s[r] + nzls[r])
+ * (consecutive, covering the plan's n_z), its mode rows modes[r], checkpoints
+ * cp_works[r] and carry region regions[r] (hfb_carry_layout, zeroed); the peer
+ * of rank r is regions[r + 1] (dir 0) or regions[r - 1] (dir 1). Synchronises
+ * `stream`. Replaces nothing in the reference: it stands in for the P-GPU run
+ * of solver.py:319-399 where only one GPU is available. */
+int hfb_zsolve_carry_vranks(hfb_plan* plan, int dir, int nranks, double* const* modes, int ld,
+                            const int* z0s, const int* nzls, void* const* cp_works,
+                            double* const* regions, uint32_t epoch, void* stream);
 /* The same for a complex table (complex k(z), hfb_plan_set_coefficients_z): the
  * slab travels as real and imaginary mode-row volumes (each from
  * hfb_forward_modes), cp_work = 2 * ceil(nzl / 8) * n_x * ld doubles, and the

@@ -89,6 +89,7 @@ SIGNATURES = {
     "hfb_carry_layout": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_longlong), _ip]),
     "hfb_zsolve_carry": (_i, [_vp, _i, _vp, _i, _i, _i, _vp, _vp, _vp, _u32, _vp]),
     "hfb_carry_check": (_i, [_vp, _vp, _ip]),
+    "hfb_zsolve_carry_vranks": (_i, [_vp, _i, _i, _vp, _i, _ip, _ip, _vp, _vp, _u32, _vp]),
     "hfb_carry_layout_z": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_longlong), _ip]),
     "hfb_zsolve_carry_z": (_i, [_vp, _i, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _u32, _vp]),
     "hfb_ipc_handle": (_i, [_vp, _vp, ctypes.POINTER(ctypes.c_longlong)]),

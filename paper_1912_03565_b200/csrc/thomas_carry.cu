@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "hfb_internal.cuh"
 #include "tma.cuh"
@@ -112,9 +113,11 @@ __device__ __forceinline__ void issue_chunk(const CarryArgs& a, double (*sdat)[K
 }  // namespace
 
 // DIR 0: forward elimination (chunks ascending), DIR 1: back substitution
-// (chunks descending); one launch per direction and rank.
+// (chunks descending); one launch per direction and rank. The CTA walks the
+// mode blocks cta, cta + ncta, ... (ascending: a block waits only on the same
+// block of the neighbour, which that rank's CTA reaches no later).
 template <int DIR, int S>
-__global__ void __launch_bounds__(BM, 4) thomas_carry_kernel(CarryArgs a) {
+__device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, long long ncta) {
   extern __shared__ __align__(16) double dyn[];
   double(*sdat)[K][BM] = reinterpret_cast<double(*)[K][BM]>(dyn);
   double(*scoef)[K * 12] = reinterpret_cast<double(*)[K * 12]>(dyn + S * K * BM);
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(BM, 4) thomas_carry_kernel(CarryArgs a) {
   __syncthreads();
   uint32_t phase = 0;
 
-  for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  for (long long blk = cta; blk < nblk; blk += ncta) {
     const int n = (int)(blk / a.nbpr);
     const int m0 = (int)(blk % a.nbpr) * BM;
     const int cols = min(BM, a.ncols - m0);
@@ -266,6 +269,23 @@ __global__ void __launch_bounds__(BM, 4) thomas_carry_kernel(CarryArgs a) {
     if (tid == 0) bulk_wait<0>();  // stores done before the stages are refilled
     __syncthreads();
   }
+}
+
+template <int DIR, int S>
+__global__ void __launch_bounds__(BM, 4) thomas_carry_kernel(CarryArgs a) {
+  carry_body<DIR, S>(a, blockIdx.x, gridDim.x);
+}
+
+// Verification of the cross-rank protocol on ONE device: every virtual rank's
+// sweep in ONE cooperative launch (all CTAs co-resident), CTA group r serving
+// rank r. Rank r's CTAs really spin on flags that rank r -/+ 1's CTAs release
+// while running concurrently — the live acquire/release path of the
+// multi-GPU run, without separate launches waiting on one another.
+template <int DIR, int S>
+__global__ void __launch_bounds__(BM, 4) thomas_carry_vranks_kernel(const CarryArgs* va, int per) {
+  const int r = blockIdx.x / per;
+  const CarryArgs a = va[r];
+  carry_body<DIR, S>(a, blockIdx.x - (long long)r * per, per);
 }
 
 // ---------------------------------------------------------------------------
@@ -601,6 +621,65 @@ int launch_thomas_carry(hfb_plan* p, int dir, double* data, long long ld, int z0
   return HFB_OK;
 }
 
+int launch_thomas_carry_vranks(hfb_plan* p, int dir, int nranks, double* const* data,
+                               long long ld, const int* z0s, const int* nzls,
+                               double* const* cpks, double* const* regions, unsigned epoch,
+                               cudaStream_t st) {
+  if (!p->xerr) {
+    HFB_CUDA(cudaMalloc(&p->xerr, sizeof(unsigned)));
+    HFB_CUDA(cudaMemset(p->xerr, 0, sizeof(unsigned)));
+  }
+  std::vector<CarryArgs> host(nranks);
+  const int ms = tuning(11);
+  for (int r = 0; r < nranks; ++r) {
+    CarryArgs& a = host[r];
+    memset(&a, 0, sizeof(a));
+    a.w = data[r];
+    a.cpk = cpks[r];
+    a.coef = p->coef;
+    a.cx = p->cx;
+    a.cy = p->cy;
+    a.nzl = nzls[r];
+    a.z0 = z0s[r];
+    a.nz = p->nz;
+    a.nrows = p->nx;
+    a.ncols = p->ny;
+    a.nbpr = (p->ny + BM - 1) / BM;
+    a.ld = ld;
+    a.ps = ld * p->nx;
+    a.thr = p->thr;
+    a.err = p->err;
+    a.mine = regions[r];
+    a.peer = dir == 0 ? (r + 1 < nranks ? regions[r + 1] : nullptr)
+                      : (r > 0 ? regions[r - 1] : nullptr);
+    a.epoch = epoch;
+    a.timeout_ns = (unsigned long long)(ms > 0 ? ms : 30000) * 1000000ULL;
+    a.xerr = p->xerr;
+  }
+  constexpr int S = 3;
+  const size_t sm = sizeof(double) * (size_t)S * (K * BM + K * 12);
+  auto kern = dir ? thomas_carry_vranks_kernel<1, S> : thomas_carry_vranks_kernel<0, S>;
+  HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int per_sm = 1, sms = 148, dev = 0;
+  HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BM, sm));
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long work = (long long)p->nx * ((p->ny + BM - 1) / BM);
+  int per = (int)std::min<long long>(work, (long long)sms * per_sm / nranks);
+  if (per < 1) return HFB_ERR_ARGUMENT;  // more ranks than co-resident CTAs
+  CarryArgs* dargs = nullptr;
+  HFB_CUDA(cudaMalloc(&dargs, sizeof(CarryArgs) * nranks));
+  HFB_CUDA(cudaMemcpy(dargs, host.data(), sizeof(CarryArgs) * nranks, cudaMemcpyHostToDevice));
+  void* args[] = {&dargs, &per};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(nranks * per),
+                                                    dim3(BM), args, sm, st);
+  HFB_LAUNCHED();
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  cudaFree(dargs);
+  if (e != cudaSuccess || e2 != cudaSuccess) return HFB_ERR_CUDA;
+  return HFB_OK;
+}
+
 }  // namespace hfb
 
 // ------------------------------------------------------------------ C-ABI
@@ -628,6 +707,28 @@ extern "C" int hfb_zsolve_carry(hfb_plan* p, int dir, double* modes, int ld, int
   HFB_CUDA(cudaSetDevice(p->device));
   return launch_thomas_carry(p, dir, modes, ld, z0, nzl, (double*)cp_work, mine, peer, epoch,
                              (cudaStream_t)stream);
+}
+
+extern "C" int hfb_zsolve_carry_vranks(hfb_plan* p, int dir, int nranks, double* const* modes,
+                                       int ld, const int* z0s, const int* nzls,
+                                       void* const* cp_works, double* const* regions,
+                                       uint32_t epoch, void* stream) {
+  if (!p || !modes || !z0s || !nzls || !cp_works || !regions || nranks < 1 || ld < p->ny ||
+      (ld & 1) || (dir != 0 && dir != 1))
+    return HFB_ERR_ARGUMENT;
+  if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
+  if (p->coef_i) return HFB_ERR_ARGUMENT;
+  int next = 0;
+  for (int r = 0; r < nranks; ++r) {  // consecutive slabs covering the plan's levels
+    if (!modes[r] || !cp_works[r] || !regions[r] || z0s[r] != next || nzls[r] < 1)
+      return HFB_ERR_RANGE;
+    next += nzls[r];
+  }
+  if (next != p->nz) return HFB_ERR_RANGE;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return launch_thomas_carry_vranks(p, dir, nranks, modes, ld, z0s, nzls,
+                                    reinterpret_cast<double* const*>(cp_works), regions, epoch,
+                                    (cudaStream_t)stream);
 }
 
 extern "C" int hfb_carry_layout_z(hfb_plan* p, int ld, long long* region_doubles, int* blocks) {

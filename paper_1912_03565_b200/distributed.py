@@ -647,6 +647,65 @@ def solve_partitioned_carry(z_slab, scheme, profile, grid, group=None, timings=N
     return out
 
 
+def solve_partitioned_carry_coop(values, scheme, profile, grid, parts):
+    """The carry path with `parts` virtual ranks on ONE device, each direction's
+    sweeps of ALL ranks in one cooperative launch (hfb_zsolve_carry_vranks):
+    rank r's CTAs spin on flags rank r -/+ 1's CTAs publish while both run —
+    the live cross-rank protocol, not a sequenced emulation. The transforms are
+    the per-rank stages of solve_partitioned_carry. Real tables. Returns the
+    solution volume (bit-identical to the one-call solve)."""
+    import ctypes
+    import torch
+    ex = make_exchange_plan(grid, parts)
+    dev = values.device
+    zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, dev)
+    ld = int(zplan.lib.hfb_modes_ld(zplan.handle))
+    with zplan.lock:
+        if scheme is not None:
+            device_coefficients(zplan, scheme, profile, grid)
+        if zplan.complex_coef:
+            raise ValueError("solve_partitioned_carry_coop takes a real table")
+    size, _ = carry_layout(zplan, ld)
+    zr = ex.partition.z_ranges
+    regions = [torch.zeros(size, dtype=torch.float64, device=dev) for _ in range(parts)]
+    modes, cps = [], []
+    for z0, z1 in zr:
+        kpz = z1 - z0
+        tplan = get_plan(grid.n_x, grid.n_y, kpz, dev)
+        m = torch.empty(kpz * grid.n_x * ld, dtype=torch.float64, device=dev)
+        with tplan.lock:
+            work = tplan.workspace(5)
+            _check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(values[z0:z1].contiguous()),
+                                               ptr(m), ptr(work), tplan.stream()),
+                   "forward_modes")
+        modes.append(m)
+        cps.append(torch.empty(((kpz + 7) // 8) * grid.n_x * ld, dtype=torch.float64,
+                               device=dev))
+    P = ctypes.c_void_p * parts
+    I = ctypes.c_int * parts
+    mp = P(*[t.data_ptr() for t in modes])
+    cpp = P(*[t.data_ptr() for t in cps])
+    rp = P(*[t.data_ptr() for t in regions])
+    z0s = I(*[a for a, _ in zr])
+    nzs = I(*[b - a for a, b in zr])
+    with zplan.lock:
+        for d in (0, 1):
+            _check(zplan.lib.hfb_zsolve_carry_vranks(zplan.handle, d, parts, mp, ld, z0s, nzs,
+                                                     cpp, rp, 1, zplan.stream()),
+                   "zsolve_carry_vranks")
+    out = torch.empty(values.shape, dtype=torch.float64, device=dev)
+    for r, (z0, z1) in enumerate(zr):
+        tplan = get_plan(grid.n_x, grid.n_y, z1 - z0, dev)
+        with tplan.lock:
+            _check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(modes[r]), ptr(out[z0:z1]),
+                                               tplan.stream()), "inverse_modes")
+    code = carry_status_code(zplan)
+    if code:
+        raise exchange_error_for(code, 0)
+    zplan.fetch_status()
+    return out
+
+
 def solve_partitioned_carry_local(values, scheme, profile, grid, parts):
     """The carry path's per-rank stages for `parts` virtual ranks on ONE device,
     run rank after rank: forward sweeps in rank order, backward sweeps in
