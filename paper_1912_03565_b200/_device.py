@@ -7,6 +7,9 @@ real solves (the operators are real and linear, so real and imaginary parts
 never mix when the coefficients are real).
 """
 
+import threading
+import warnings
+
 import numpy as np
 
 from ._native import NativeUnavailableError, _torch
@@ -78,3 +81,155 @@ def write_back(dst, parts):
         dst.imag[...] = parts[1] if len(parts) > 1 else 0.0
     else:
         dst[...] = parts[0]
+
+
+# ------------------------------------------------- pipelined host <-> device copies
+# Host arrays travel through two reusable pinned staging buffers per device on a
+# dedicated copy stream: the (multi-threaded) host copy of chunk k overlaps the
+# DMA of chunk k - 1 (or k + 1 on the way back), so a solve_discrete on numpy
+# arrays moves at close to the PCIe rate instead of a pageable synchronous copy.
+# Strided host views (the real / imaginary part of a complex128 array) are
+# gathered / scattered by the host copy itself: no temporary host arrays.
+_CHUNK = 8 << 20  # doubles per staging buffer (64 MB)
+_staging = {}
+_staging_lock = threading.Lock()
+
+
+class _Staging:
+    def __init__(self, device, n):
+        torch = _torch()
+        self.device = device
+        self.n = n
+        self.bufs = [torch.empty(n, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        self.stream = torch.cuda.Stream(device)
+        self.events = [torch.cuda.Event() for _ in range(2)]
+        self.lock = threading.Lock()
+
+
+def _stage(device, plane):
+    torch = _torch()
+    dev = torch.device(device)
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    need = max(_CHUNK, plane)
+    with _staging_lock:
+        st = _staging.get(key)
+        if st is None or st.n < need:
+            st = _staging[key] = _Staging(torch.device("cuda", key), need)
+        return st
+
+
+def _chunks(shape, n):
+    rows = shape[0] if shape else 1
+    plane = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+    step = max(1, n // max(plane, 1))
+    for a in range(0, rows, step):
+        yield a, min(rows, a + step)
+
+
+def _host_tensor(view):
+    torch = _torch()
+    with warnings.catch_warnings():  # read-only inputs are only read
+        warnings.simplefilter("ignore")
+        return torch.from_numpy(view)
+
+
+def h2d(src, dst):
+    """Copy the float64 host view `src` (any positive strides) into the
+    contiguous device tensor `dst` of the same shape."""
+    torch = _torch()
+    src = np.asarray(src)
+    if src.ndim == 0 or src.size == 0:
+        dst.copy_(_host_tensor(np.ascontiguousarray(src)))
+        return
+    plane = src.size // src.shape[0]
+    st = _stage(dst.device, plane)
+    with st.lock:
+        cur = torch.cuda.current_stream(dst.device)
+        st.stream.wait_stream(cur)
+        for k, (a, b) in enumerate(_chunks(src.shape, st.n)):
+            i = k & 1
+            st.events[i].synchronize()  # the DMA that last read buffer i is done
+            hb = st.bufs[i][:(b - a) * plane].view((b - a,) + src.shape[1:])
+            hb.copy_(_host_tensor(src[a:b]))
+            with torch.cuda.stream(st.stream):
+                dst[a:b].copy_(hb, non_blocking=True)
+                st.events[i].record(st.stream)
+        cur.wait_stream(st.stream)
+        for e in st.events:
+            e.synchronize()  # the buffers are free for the next caller
+
+
+def d2h(src, dst):
+    """Copy the contiguous device tensor `src` into the writeable float64 host
+    view `dst` (any positive strides) of the same shape; synchronous."""
+    torch = _torch()
+    if dst.ndim == 0 or dst.size == 0:
+        dst[...] = src.cpu().numpy()
+        return
+    plane = dst.size // dst.shape[0]
+    st = _stage(src.device, plane)
+    with st.lock:
+        st.stream.wait_stream(torch.cuda.current_stream(src.device))
+        pending = None
+        for k, (a, b) in enumerate(_chunks(dst.shape, st.n)):
+            i = k & 1
+            hb = st.bufs[i][:(b - a) * plane].view((b - a,) + dst.shape[1:])
+            with torch.cuda.stream(st.stream):
+                hb.copy_(src[a:b], non_blocking=True)
+                st.events[i].record(st.stream)
+            if pending is not None:
+                j, pa, pb, phb = pending
+                st.events[j].synchronize()
+                _host_tensor(dst[pa:pb]).copy_(phb)
+            pending = (i, a, b, hb)
+        j, pa, pb, phb = pending
+        st.events[j].synchronize()
+        _host_tensor(dst[pa:pb]).copy_(phb)
+
+
+def _any_nonzero(view):
+    torch = _torch()
+    for a, b in _chunks(view.shape, _CHUNK):
+        if bool(_host_tensor(view[a:b]).ne(0).any()):
+            return True
+    return False
+
+
+def upload_parts(arr, device):
+    """Host array -> [re] or [re, im] contiguous float64 device tensors (the
+    imaginary part only when it is not zero), by pipelined pinned copies."""
+    torch = _torch()
+    a = np.asarray(arr)
+    if np.iscomplexobj(a):
+        if a.dtype != np.complex128:
+            a = a.astype(np.complex128)
+        views = [a.real]
+        if _any_nonzero(a.imag):
+            views.append(a.imag)
+    else:
+        views = [a if a.dtype == np.float64 else a.astype(np.float64)]
+    out = []
+    for v in views:
+        t = torch.empty(v.shape, dtype=torch.float64, device=device)
+        h2d(v, t)
+        out.append(t)
+    return out
+
+
+def download_parts(parts, like):
+    """[re] or [re, im] device tensors -> a new host array: complex128 when `like`
+    is complex or there is an imaginary part, else float64."""
+    torch = _torch()
+    cplx = len(parts) > 1 or np.iscomplexobj(like)
+    shape = tuple(parts[0].shape)
+    if not cplx:
+        out = np.empty(shape, dtype=np.float64)
+        d2h(parts[0], out)
+        return out
+    out = np.empty(shape, dtype=np.complex128)
+    d2h(parts[0], out.real)
+    if len(parts) > 1:
+        d2h(parts[1], out.imag)
+    else:
+        _host_tensor(out.imag).zero_()
+    return out

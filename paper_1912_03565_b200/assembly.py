@@ -311,7 +311,7 @@ def _apply_parts(ext_parts, rhs_parts, scheme, profile, grid, mode, device):
 def _parts_of(values, device):
     if dv.is_tensor(values):
         return [dv.device_tensor(values)]
-    return [dv.upload(p, device) for p in dv.real_parts(values)]
+    return dv.upload_parts(values, device)
 
 
 def _result(outs, like):
@@ -319,7 +319,7 @@ def _result(outs, like):
         if len(outs) > 1:
             raise NotImplementedError("complex results (complex k(z)) need numpy fields")
         return Field3D(outs[0])
-    return Field3D(dv.join_parts([dv.download(o) for o in outs], like))
+    return Field3D(dv.download_parts(outs, like))
 
 
 def apply_stencil(u: Field3D, boundary: BoundaryData, scheme, profile: CoefficientProfile,
@@ -354,6 +354,20 @@ def fold_dirichlet(rhs: Field3D, boundary: BoundaryData, scheme, profile: Coeffi
     if dv.is_tensor(values) and len(outs) > 1:
         raise NotImplementedError("complex boundary data on a real device field")
     return _result(outs, values)
+
+
+def fold_device_parts(rhs_parts, boundary: BoundaryData, scheme, profile: CoefficientProfile,
+                      grid: Grid3D, device):
+    """fold_dirichlet on right-hand sides already on the device ([re] or [re, im]
+    float64 tensors; the result may gain an imaginary part from complex boundary
+    data). A zero boundary returns the parts themselves."""
+    if boundary.known_zero:
+        return list(rhs_parts)
+    box = boundary.closed_box(grid)
+    if not np.any(box):
+        return list(rhs_parts)
+    return _apply_parts(_parts_of(box, device), list(rhs_parts), scheme, profile, grid, 1,
+                        device)
 
 
 def residual_l2(u: Field3D, rhs_folded: Field3D, scheme, profile: CoefficientProfile,

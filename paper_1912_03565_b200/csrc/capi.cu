@@ -217,6 +217,10 @@ extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const
                                          const double* cy, double thr) {
   if (!p || !table || !cx || !cy) return HFB_ERR_ARGUMENT;
   HFB_CUDA(cudaSetDevice(p->device));
+  if (p->have_coef) HFB_CUDA(cudaDeviceSynchronize());  // see hfb_plan_set_coefficients
+  // kernels queued on any stream (torch side streams do not order against the
+  // synchronous copies below) may still read the old table: let them finish
+  if (p->have_coef) HFB_CUDA(cudaDeviceSynchronize());
   const size_t nlev = (size_t)p->nz * 12;
   std::vector<double> buf(2 * nlev);
   scaled_table(table, nlev, buf.data());

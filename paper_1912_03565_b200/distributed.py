@@ -275,6 +275,18 @@ def solve_received_chunked(recv, level_plane, scheme, profile, grid, ex, rank):
     return zplan
 
 
+def require_mode_space(grid):
+    """The multi-GPU paths run the mode-row transforms (hfb_forward_modes), which
+    need n_x + 1 and n_y + 1 powers of two in [16, 4096] (the FFT engine). Any
+    other extent raises here, clearly, instead of deep inside the library; the
+    one-device Partitioned mode and the one-call solve take every size."""
+    ok = lambda n: 16 <= n + 1 <= 4096 and (n + 1) & n == 0
+    if not (ok(grid.n_x) and ok(grid.n_y)):
+        raise ValueError(
+            f"multi-GPU solve needs n_x + 1 and n_y + 1 powers of two in [16, 4096], got "
+            f"n_x = {grid.n_x}, n_y = {grid.n_y} (use the one-device solve for this grid)")
+
+
 def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None, chunks=4,
                       check=True):
     """Solve with the grid split over the ranks of `group`; z_slab is this rank's
@@ -294,6 +306,7 @@ def solve_partitioned(z_slab, scheme, profile, grid, group=None, timings=None, c
     call check_status(grid, group) after a batch of solves instead."""
     import torch
     import torch.distributed as dist
+    require_mode_space(grid)
     rank, parts = dist.get_rank(group), dist.get_world_size(group)
     ex = make_exchange_plan(grid, parts)
     z0, z1 = ex.partition.z_ranges[rank]
@@ -491,10 +504,13 @@ class CarryLinks:
         self.epoch = 0
 
     def _open(self, info):
+        import torch
         h, off = info
         buf = (ctypes.c_char * 64).from_buffer_copy(h)
         p = ctypes.c_void_p()
-        check(self.plan.lib.hfb_ipc_open(buf, off, ctypes.byref(p)), "ipc_open")
+        # the mapping is made on the current device: the slab's, not the caller's
+        with torch.cuda.device(self.plan.device):
+            check(self.plan.lib.hfb_ipc_open(buf, off, ctypes.byref(p)), "ipc_open")
         self._opened.append((p.value, off))
         return p.value
 
@@ -511,11 +527,39 @@ class CarryLinks:
 _links = {}
 
 
+def _links_key(grid, group, device):
+    """Cache key of a group's carry links: the group's member ranks (stable,
+    unlike id(group), which a recreated group can reuse)."""
+    import torch.distributed as dist
+    try:
+        members = tuple(dist.get_process_group_ranks(group)) if group is not None \
+            else ("world", dist.get_world_size())
+    except Exception:
+        members = (id(group),)
+    return (grid.n_x, grid.n_y, grid.n_z, members, str(device))
+
+
 def carry_links(grid, group, device):
-    key = (grid.n_x, grid.n_y, grid.n_z, id(group), str(device))
-    if key not in _links:
-        _links[key] = CarryLinks(grid, group, device)
-    return _links[key]
+    key = _links_key(grid, group, device)
+    links = _links.get(key)
+    if links is not None and links.parts != _group_size(group):
+        links.close()
+        links = None
+    if links is None:
+        links = _links[key] = CarryLinks(grid, group, device)
+    return links
+
+
+def _group_size(group):
+    import torch.distributed as dist
+    return dist.get_world_size(group)
+
+
+def close_carry_links():
+    """Unmap every neighbour's carry region (call before destroying the groups)."""
+    for links in _links.values():
+        links.close()
+    _links.clear()
 
 
 def carry_zsolve(plan, modes, ld, z0, kpz, cp, mine, peer_next, peer_prev, epoch):
@@ -547,7 +591,7 @@ def check_status_carry(grid, group=None, device=None):
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     rank = dist.get_rank(group)
     zplan = get_plan(grid.n_x, grid.n_y, grid.n_z, dev)
-    links = _links.get((grid.n_x, grid.n_y, grid.n_z, id(group), str(dev)))
+    links = _links.get(_links_key(grid, group, dev))
     # singular, exchange, rank*4+code of it, solve epoch
     flags = torch.zeros(4, dtype=torch.int64, device=dev)
     code = carry_status_code(zplan)
@@ -585,6 +629,7 @@ def solve_partitioned_carry(z_slab, scheme, profile, grid, group=None, timings=N
     synchronisation); call check_status_carry(grid, group) after a batch."""
     import torch
     import torch.distributed as dist
+    require_mode_space(grid)
     rank, parts = dist.get_rank(group), dist.get_world_size(group)
     ex = make_exchange_plan(grid, parts)
     z0, z1 = ex.partition.z_ranges[rank]

@@ -37,7 +37,7 @@ import numpy as np
 
 from . import _device as dv
 from ._native import check, get_plan, ptr
-from .assembly import BoundaryData, Field3D, build_rhs, fold_dirichlet
+from .assembly import BoundaryData, Field3D, build_rhs, fold_device_parts, fold_dirichlet
 from .errors import InvalidPartitionError
 from .grid import CoefficientProfile, Grid3D
 from .spectral import make_plan
@@ -539,9 +539,14 @@ def solve_discrete(rhs: Field3D, boundary: BoundaryData, scheme, profile: Coeffi
     plan = get_plan(grid.n_x, grid.n_y, grid.n_z, device)
     with plan.lock:
         device_coefficients(plan, scheme, profile, grid)
-        work = fold_dirichlet(Field3D(values), boundary, scheme, profile, grid).values
-        parts = [dv.device_tensor(work)] if on_device else \
-            [dv.upload(p, device) for p in dv.real_parts(work)]
+        if on_device:
+            work = fold_dirichlet(Field3D(values), boundary, scheme, profile, grid).values
+            parts = [dv.device_tensor(work)]
+        else:
+            # host arrays: pipelined pinned upload of the caller's array (never
+            # modified), then the Dirichlet fold on the device (assembly.py:258-274)
+            parts = fold_device_parts(dv.upload_parts(values, device), boundary, scheme,
+                                      profile, grid, device)
         # the fold may have switched the plan's coefficients back and forth
         device_coefficients(plan, scheme, profile, grid)
         torch.cuda.current_stream(device).synchronize()
@@ -572,8 +577,7 @@ def solve_discrete(rhs: Field3D, boundary: BoundaryData, scheme, profile: Coeffi
     if on_device:
         out = Field3D(parts[0])
     else:
-        like = work if np.iscomplexobj(work) else np.empty(0)
-        out = Field3D(dv.join_parts([dv.download(t) for t in parts], like))
+        out = Field3D(dv.download_parts(parts, values))
     timings = PhaseTimings(setup_s=setup_s, transform_s=transform_s, exchange_s=exchange_s,
                            tridiag_s=tridiag_s, total_s=time.perf_counter() - t_start)
     return out, timings
