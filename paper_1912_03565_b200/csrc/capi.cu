@@ -301,6 +301,7 @@ static int transform_range(hfb_plan* p, const double* src, double* dst, int z0, 
 
 extern "C" int hfb_transform_stack(hfb_plan* p, double* data, int z0, int z1, void* work,
                                    void* stream) {
+  const NvtxRange nvtx_("hfb_transform_stack");
   if (!p || !data) return HFB_ERR_ARGUMENT;
   if (z0 < 0 || z0 > z1 || z1 > p->nz) return HFB_ERR_RANGE;
   HFB_CUDA(cudaSetDevice(p->device));
@@ -309,6 +310,7 @@ extern "C" int hfb_transform_stack(hfb_plan* p, double* data, int z0, int z1, vo
 
 extern "C" int hfb_transform_lines_x(hfb_plan* p, double* data, int y0, int y1, void* work,
                                      void* stream) {
+  const NvtxRange nvtx_("hfb_transform_lines_x");
   if (!p || !data) return HFB_ERR_ARGUMENT;
   if (y0 < 0 || y0 > y1 || y1 > p->ny) return HFB_ERR_RANGE;
   HFB_CUDA(cudaSetDevice(p->device));
@@ -317,6 +319,7 @@ extern "C" int hfb_transform_lines_x(hfb_plan* p, double* data, int y0, int y1, 
 
 extern "C" int hfb_transform_lines_y(hfb_plan* p, double* data, int x0, int x1, void* work,
                                      void* stream) {
+  const NvtxRange nvtx_("hfb_transform_lines_y");
   if (!p || !data) return HFB_ERR_ARGUMENT;
   if (x0 < 0 || x0 > x1 || x1 > p->nx) return HFB_ERR_RANGE;
   HFB_CUDA(cudaSetDevice(p->device));
@@ -325,6 +328,7 @@ extern "C" int hfb_transform_lines_y(hfb_plan* p, double* data, int x0, int x1, 
 
 extern "C" int hfb_solve_slab(hfb_plan* p, double* slab, int m_count, int m_offset, void* work,
                               void* stream) {
+  const NvtxRange nvtx_("hfb_solve_slab");
   if (!p || !slab || !work) return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
   if (p->coef_i) return HFB_ERR_ARGUMENT;  // complex table: hfb_solve_slab_z
@@ -334,6 +338,7 @@ extern "C" int hfb_solve_slab(hfb_plan* p, double* slab, int m_count, int m_offs
 }
 
 extern "C" int hfb_solve(hfb_plan* p, const double* rhs, double* out, void* work, void* stream) {
+  const NvtxRange nvtx_("hfb_solve");
   if (!p || !rhs || !out || !work) return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
   if (p->coef_i) return HFB_ERR_ARGUMENT;  // complex table: hfb_solve_z
@@ -360,6 +365,7 @@ extern "C" int hfb_solve(hfb_plan* p, const double* rhs, double* out, void* work
 
 extern "C" int hfb_solve_slab_z(hfb_plan* p, double* re, double* im, int m_count, int m_offset,
                                 void* work, void* stream) {
+  const NvtxRange nvtx_("hfb_solve_slab_z");
   if (!p || !re || !im || !work) return HFB_ERR_ARGUMENT;
   if (!p->have_coef || !p->coef_i) return HFB_ERR_NO_COEFFICIENTS;
   if (m_count < 0 || m_offset < 0 || m_offset + m_count > p->ny) return HFB_ERR_RANGE;
@@ -369,6 +375,7 @@ extern "C" int hfb_solve_slab_z(hfb_plan* p, double* re, double* im, int m_count
 
 extern "C" int hfb_solve_z(hfb_plan* p, const double* rhs_re, const double* rhs_im,
                            double* out_re, double* out_im, void* work, void* stream) {
+  const NvtxRange nvtx_("hfb_solve_z");
   if (!p || !rhs_re || !rhs_im || !out_re || !out_im || !work) return HFB_ERR_ARGUMENT;
   if (!p->have_coef || !p->coef_i) return HFB_ERR_NO_COEFFICIENTS;
   HFB_CUDA(cudaSetDevice(p->device));
@@ -421,6 +428,7 @@ extern "C" int hfb_status_fetch(hfb_plan* p, void* stream, hfb_status* s) {
 
 extern "C" int hfb_solve_host(hfb_plan* p, const double* hin, double* hout, void* work,
                               void* stream, hfb_status* s) {
+  const NvtxRange nvtx_("hfb_solve_host");
   if (!p || !hin || !hout || !work) return HFB_ERR_ARGUMENT;
   HFB_CUDA(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -483,6 +491,7 @@ static int host_pipe(hfb_plan* p, size_t bytes) {
 
 extern "C" int hfb_solve_host_async(hfb_plan* p, const double* hin, double* hout, void* work,
                                     void* stream) {
+  const NvtxRange nvtx_("hfb_solve_host_async");
   if (!p || !hin || !hout || !work) return HFB_ERR_ARGUMENT;
   HFB_CUDA(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;

@@ -494,6 +494,7 @@ static unsigned grid_for(long long n, int threads) {
 
 extern "C" int hfb_rhs_fourth(hfb_plan* p, const double* f, double* F, double hz2,
                               void* stream) {
+  const NvtxRange nvtx_("hfb_rhs_fourth");
   if (!p || !f || !F) return HFB_ERR_ARGUMENT;
   HFB_CUDA(cudaSetDevice(p->device));
   const int v = tuning(20);
@@ -553,6 +554,7 @@ extern "C" int hfb_rhs_convdiff(hfb_plan* p, const double* f, const double* fxx,
 // Thomas sweep and the raw (a,b,c,d) copy right after it.
 extern "C" int hfb_apply27(hfb_plan* p, const double* ext, const double* rhs, double* out,
                            uint32_t mask, int mode, void* stream) {
+  const NvtxRange nvtx_("hfb_apply27");
   if (!p || !ext || !out || (mode == 1 && !rhs)) return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
   HFB_CUDA(cudaSetDevice(p->device));
@@ -578,6 +580,7 @@ extern "C" int hfb_residual_partials(const hfb_plan* p) {
 
 extern "C" int hfb_residual_sq(hfb_plan* p, const double* u, const double* F, double* partial,
                                uint32_t mask, void* stream) {
+  const NvtxRange nvtx_("hfb_residual_sq");
   if (!p || !u || !F || !partial) return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
   HFB_CUDA(cudaSetDevice(p->device));
@@ -636,6 +639,7 @@ extern "C" int hfb_unpack_yblocks(hfb_plan* p, const double* recv, double* slab,
 extern "C" int hfb_apply27_z(hfb_plan* p, const double* ext_re, const double* ext_im,
                              const double* rhs_re, const double* rhs_im, double* out_re,
                              double* out_im, uint32_t mask, int mode, void* stream) {
+  const NvtxRange nvtx_("hfb_apply27_z");
   if (!p || !ext_re || !ext_im || !out_re || !out_im) return HFB_ERR_ARGUMENT;
   if (mode == 1 && (!rhs_re || !rhs_im)) return HFB_ERR_ARGUMENT;
   if (!p->have_coef || !p->coef_i) return HFB_ERR_NO_COEFFICIENTS;
@@ -651,6 +655,7 @@ extern "C" int hfb_apply27_z(hfb_plan* p, const double* ext_re, const double* ex
 extern "C" int hfb_residual_sq_z(hfb_plan* p, const double* u_re, const double* u_im,
                                  const double* rhs_re, const double* rhs_im, double* partial,
                                  uint32_t mask, void* stream) {
+  const NvtxRange nvtx_("hfb_residual_sq_z");
   if (!p || !u_re || !u_im || !rhs_re || !rhs_im || !partial) return HFB_ERR_ARGUMENT;
   if (!p->have_coef || !p->coef_i) return HFB_ERR_NO_COEFFICIENTS;
   HFB_CUDA(cudaSetDevice(p->device));
@@ -715,12 +720,14 @@ extern "C" int hfb_modes_ld(const hfb_plan* p) { return p ? (int)modes_ld(p) : 0
 
 extern "C" int hfb_forward_modes(hfb_plan* p, const double* src, double* modes, void* work,
                                  void* stream) {
+  const NvtxRange nvtx_("hfb_forward_modes");
   if (!p || !src || !modes || !work) return HFB_ERR_ARGUMENT;
   HFB_CUDA(cudaSetDevice(p->device));
   return forward_modes(p, src, modes, (double*)work, (cudaStream_t)stream);
 }
 
 extern "C" int hfb_inverse_modes(hfb_plan* p, double* modes, double* out, void* stream) {
+  const NvtxRange nvtx_("hfb_inverse_modes");
   if (!p || !modes || !out) return HFB_ERR_ARGUMENT;
   HFB_CUDA(cudaSetDevice(p->device));
   return inverse_modes(p, modes, out, (cudaStream_t)stream);
@@ -728,6 +735,7 @@ extern "C" int hfb_inverse_modes(hfb_plan* p, double* modes, double* out, void* 
 
 extern "C" int hfb_solve_modes(hfb_plan* p, double* data, int ld, int m_count, int m_offset,
                                void* cp_work, void* stream) {
+  const NvtxRange nvtx_("hfb_solve_modes");
   if (!p || !data || !cp_work || ld < m_count || (ld & 1)) return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
   if (p->coef_i) return HFB_ERR_ARGUMENT;

@@ -697,6 +697,7 @@ extern "C" int hfb_carry_layout(hfb_plan* p, int ld, long long* region_doubles, 
 extern "C" int hfb_zsolve_carry(hfb_plan* p, int dir, double* modes, int ld, int z0, int nzl,
                                 void* cp_work, double* mine, double* peer, uint32_t epoch,
                                 void* stream) {
+  const NvtxRange nvtx_("hfb_zsolve_carry");
   if (!p || !modes || !cp_work || !mine || ld < p->ny || (ld & 1) || (dir != 0 && dir != 1))
     return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
@@ -713,6 +714,7 @@ extern "C" int hfb_zsolve_carry_vranks(hfb_plan* p, int dir, int nranks, double*
                                        int ld, const int* z0s, const int* nzls,
                                        void* const* cp_works, double* const* regions,
                                        uint32_t epoch, void* stream) {
+  const NvtxRange nvtx_("hfb_zsolve_carry_vranks");
   if (!p || !modes || !z0s || !nzls || !cp_works || !regions || nranks < 1 || ld < p->ny ||
       (ld & 1) || (dir != 0 && dir != 1))
     return HFB_ERR_ARGUMENT;
@@ -743,6 +745,7 @@ extern "C" int hfb_carry_layout_z(hfb_plan* p, int ld, long long* region_doubles
 extern "C" int hfb_zsolve_carry_z(hfb_plan* p, int dir, double* modes_re, double* modes_im,
                                   int ld, int z0, int nzl, void* cp_work, double* mine,
                                   double* peer, uint32_t epoch, void* stream) {
+  const NvtxRange nvtx_("hfb_zsolve_carry_z");
   if (!p || !modes_re || !modes_im || !cp_work || !mine || ld < p->ny || (ld & 1) ||
       (dir != 0 && dir != 1))
     return HFB_ERR_ARGUMENT;
