@@ -841,6 +841,9 @@ static int g_tune_thomas_smem = 1;  // one-call z-solve with whole columns in sh
 // 34.7 vs 22.1 ms at 1023^3 — the carry / cp loads stall the
 // 12 warps per SM the register-resident engine leaves (long scoreboard 3-8 per issue)
 static int g_tune_wave = 0;
+static int g_tune_xsparse = 1;  // one-call z-solve stores x' once per chunk, recomputes the rest (key 23)
+static int g_tune_s27 = 64;  // streamed 27-point apply / residual: levels per CTA (key 24; 0 = key 20's kernels)
+static int g_tune_s27_rj = 4;  // rows per warp of the streamed 27-point kernels (key 25: 2 or 4)
 static int g_tune_wave_dbg = 0;  // its measurement variants (key 22; wrong results for bit 1)
 
 template <int P, int E, int MODE>
@@ -1094,6 +1097,9 @@ int tuning(int key) {
     case 20: return g_tune_rhs_march;
     case 21: return g_tune_wave;
     case 22: return g_tune_wave_dbg;
+    case 23: return g_tune_xsparse;
+    case 24: return g_tune_s27;
+    case 25: return g_tune_s27_rj;
     default: return 0;
   }
 }
@@ -1121,6 +1127,9 @@ void set_tuning(int key, int value) {
   if (key == 20) g_tune_rhs_march = value;
   if (key == 21) g_tune_wave = value ? 1 : 0;
   if (key == 22) g_tune_wave_dbg = value;
+  if (key == 23) g_tune_xsparse = value ? 1 : 0;
+  if (key == 24) g_tune_s27 = value;
+  if (key == 25) g_tune_s27_rj = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

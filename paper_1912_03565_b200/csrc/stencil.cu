@@ -371,6 +371,150 @@ __global__ void __launch_bounds__(TX * TY) residual_sq_march_kernel(
   }
 }
 
+// The 27-point operator streamed plane by plane (tuning key 24 > 0: levels per
+// CTA). A warp owns 32 consecutive x-points of RJ consecutive rows; every closed
+// plane P is loaded once per warp (rows j0-1 .. j0+RJ, columns i-1 .. i+1, 3 (RJ+2)
+// loads for RJ points instead of 9 per point) and immediately contributes its
+// k = 0, 1, 2 terms to the running sums of output levels P, P-1 and P-2. Plane P
+// arrives after P-1, so each output still adds (k = 0 terms, k = 1, k = 2) in
+// the reference's order (assembly.py:229-244), every term DMUL then DADD: bit for
+// bit apply27_point. Three sums per point live in registers instead of the
+// 27-value window of the marching kernels.
+//   KIND 0: out = A ext;  KIND 1: out = rhs - A ext (ext closed, (nz+2, ny+2, nx+2))
+//   KIND 2: sum of (A u - F)^2 with u interior and zero outside (assembly.py:277-289);
+//           one partial per CTA (hfb_residual_partials)
+template <int RJ, int KIND>
+__global__ void __launch_bounds__(256, (RJ <= 2 ? 3 : 2)) s27_stream_kernel(
+    const double* __restrict__ src, const double* __restrict__ rhs, double* __restrict__ out,
+    const double* __restrict__ raw, int nx, int ny, int nz, uint32_t mask, int lz,
+    double* __restrict__ partial) {
+  constexpr int DI[9] = {-1, 1, -1, 1, -1, 1, 0, 0, 0};
+  constexpr int DJ[9] = {-1, -1, 1, 1, 0, 0, -1, 1, 0};
+  constexpr int WI[9] = {0, 0, 0, 0, 1, 1, 2, 2, 3};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  const int j0 = (blockIdx.y * 8 + warp) * RJ;
+  const int l0 = blockIdx.z * lz, l1 = min(nz, l0 + lz);
+  const long long X = KIND == 2 ? nx : nx + 2;
+  const long long XY = X * (KIND == 2 ? ny : ny + 2);
+  // per-thread column offsets (clamped into the array: lanes past nx compute
+  // garbage they never store)
+  long long coff[3];
+  bool cok[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int ii = i - 1 + c;  // interior column
+    if constexpr (KIND == 2) {
+      cok[c] = ii >= 0 && ii < nx;
+      coff[c] = min(max(ii, 0), nx - 1);
+    } else {
+      cok[c] = true;
+      coff[c] = min(ii + 1, nx + 1);
+    }
+  }
+  double a0[RJ], a1[RJ], a2[RJ];  // running sums of output levels P-2, P-1, P
+#pragma unroll
+  for (int q = 0; q < RJ; ++q) a0[q] = a1[q] = 0.0;
+  double ssq = 0.0;
+  for (int P = l0; P <= l1 + 1; ++P) {  // closed plane P = interior plane P - 1
+    double v[RJ + 2][3];
+    const int ql = P - 1;
+    const bool pok = KIND != 2 || (ql >= 0 && ql < nz);
+#pragma unroll
+    for (int r = 0; r < RJ + 2; ++r) {
+      const int jr = j0 - 1 + r;  // interior row
+      long long rb;
+      bool rok;
+      if constexpr (KIND == 2) {
+        rok = pok && jr >= 0 && jr < ny;
+        rb = (long long)min(max(ql, 0), nz - 1) * XY + (long long)min(max(jr, 0), ny - 1) * X;
+      } else {
+        rok = true;
+        rb = (long long)P * XY + (long long)min(jr + 1, ny + 1) * X;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[r][c] = (rok && cok[c]) ? __ldg(src + rb + coff[c]) : 0.0;
+    }
+    // weights of the three output levels this plane serves (clamped indices for
+    // levels outside [l0, l1): their sums are never stored)
+    const double* w0 = raw + (long long)min(P, nz - 1) * 12;                   // level P, k = 0
+    const double* w1 = raw + (long long)min(max(P - 1, 0), nz - 1) * 12 + 4;   // level P-1, k = 1
+    const double* w2 = raw + (long long)max(P - 2, 0) * 12 + 8;                // level P-2, k = 2
+    double wk0[4], wk1[4], wk2[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      wk0[q] = __ldg(w0 + q);
+      wk1[q] = __ldg(w1 + q);
+      wk2[q] = __ldg(w2 + q);
+    }
+#pragma unroll
+    for (int q = 0; q < RJ; ++q) {
+      double t0 = 0.0, t1 = a1[q], t2 = a0[q];
+#pragma unroll
+      for (int o = 0; o < 9; ++o) {
+        const double x = v[q + 1 + DJ[o]][1 + DI[o]];
+        if (mask & (1u << o)) t0 = DADD(t0, DMUL(wk0[WI[o]], x));
+      }
+#pragma unroll
+      for (int o = 0; o < 9; ++o) {
+        const double x = v[q + 1 + DJ[o]][1 + DI[o]];
+        if (mask & (1u << (9 + o))) t1 = DADD(t1, DMUL(wk1[WI[o]], x));
+      }
+#pragma unroll
+      for (int o = 0; o < 9; ++o) {
+        const double x = v[q + 1 + DJ[o]][1 + DI[o]];
+        if (mask & (1u << (18 + o))) t2 = DADD(t2, DMUL(wk2[WI[o]], x));
+      }
+      // t2 completes output level P - 2
+      const int L = P - 2, j = j0 + q;
+      if (L >= l0 && i < nx && j < ny) {
+        const long long oo = ((long long)L * ny + j) * nx + i;
+        if constexpr (KIND == 0) out[oo] = t2;
+        if constexpr (KIND == 1) out[oo] = __dsub_rn(__ldg(rhs + oo), t2);
+        if constexpr (KIND == 2) {
+          const double rr = t2 - __ldg(rhs + oo);
+          ssq = fma(rr, rr, ssq);
+        }
+      }
+      a0[q] = t1;
+      a1[q] = t0;
+    }
+  }
+  if constexpr (KIND == 2) {
+    __shared__ double red[8];
+    for (int o = 16; o > 0; o >>= 1) ssq += __shfl_down_sync(0xffffffffu, ssq, o);
+    if (lane == 0) red[warp] = ssq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += red[w];
+      partial[blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z)] = t;
+    }
+  }
+}
+
+constexpr int kS27ResLz = 64;  // levels per CTA of the streamed residual (fixes the partial count)
+
+// rows per warp of the streamed 27-point kernels (tuning key 25: 2 or 4)
+static int s27_rj() { return tuning(25) == 2 ? 2 : 4; }
+
+static dim3 s27_grid(const hfb_plan* p, int lz, int rj) {
+  return dim3((p->nx + 31) / 32, (p->ny + 8 * rj - 1) / (8 * rj), (p->nz + lz - 1) / lz);
+}
+
+template <int KIND>
+static void s27_launch(const hfb_plan* p, int lz, const double* src, const double* rhs,
+                       double* out, uint32_t mask, double* partial, cudaStream_t st) {
+  const int rj = s27_rj();
+  const double* raw = p->coef + 12LL * p->nz;
+  if (rj == 2)
+    s27_stream_kernel<2, KIND><<<s27_grid(p, lz, 2), 256, 0, st>>>(
+        src, rhs, out, raw, p->nx, p->ny, p->nz, mask, lz, partial);
+  else
+    s27_stream_kernel<4, KIND><<<s27_grid(p, lz, 4), 256, 0, st>>>(
+        src, rhs, out, raw, p->nx, p->ny, p->nz, mask, lz, partial);
+}
+
 // Complex weights (complex k(z)): out = A ext or rhs - A ext with complex
 // arithmetic, each term w * v = (wr vr - wi vi, wr vi + wi vr) added in the
 // reference's order (assembly.py:229-244 on complex128).
@@ -558,8 +702,13 @@ extern "C" int hfb_apply27(hfb_plan* p, const double* ext, const double* rhs, do
   if (!p || !ext || !out || (mode == 1 && !rhs)) return HFB_ERR_ARGUMENT;
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
   HFB_CUDA(cudaSetDevice(p->device));
-  const int lz = tuning(20);
-  if (lz > 0) {
+  const int lz = tuning(20), ls = tuning(24);
+  if (ls > 0) {
+    if (mode == 0)
+      s27_launch<0>(p, ls, ext, rhs, out, mask, nullptr, (cudaStream_t)stream);
+    else
+      s27_launch<1>(p, ls, ext, rhs, out, mask, nullptr, (cudaStream_t)stream);
+  } else if (lz > 0) {
     constexpr int TX = 64, TY = 4;
     dim3 grid((p->nx + TX - 1) / TX, (p->ny + TY - 1) / TY, (p->nz + lz - 1) / lz);
     apply27_march_kernel<TX, TY><<<grid, TX * TY, 0, (cudaStream_t)stream>>>(
@@ -573,9 +722,13 @@ extern "C" int hfb_apply27(hfb_plan* p, const double* ext, const double* rhs, do
   return HFB_OK;
 }
 
+// One partial per CTA of the streamed residual (its tile count), at least the
+// 148 x 8 persistent CTAs of the marching / gather / complex kernels.
 extern "C" int hfb_residual_partials(const hfb_plan* p) {
-  (void)p;
-  return 148 * 8;
+  if (!p) return 148 * 8;
+  const dim3 g = s27_grid(p, kS27ResLz, 2);  // the larger of the two tile counts
+  const long long tiles = (long long)g.x * g.y * g.z;
+  return (int)std::max<long long>(tiles, 148 * 8);
 }
 
 extern "C" int hfb_residual_sq(hfb_plan* p, const double* u, const double* F, double* partial,
@@ -585,12 +738,21 @@ extern "C" int hfb_residual_sq(hfb_plan* p, const double* u, const double* F, do
   if (!p->have_coef) return HFB_ERR_NO_COEFFICIENTS;
   HFB_CUDA(cudaSetDevice(p->device));
   const int lz = tuning(20);
-  if (lz > 0)
-    residual_sq_march_kernel<64, 4><<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+  const unsigned npart = (unsigned)hfb_residual_partials(p);
+  if (tuning(24) > 0) {
+    const dim3 g = s27_grid(p, kS27ResLz, s27_rj());
+    s27_launch<2>(p, kS27ResLz, u, F, nullptr, mask, partial, (cudaStream_t)stream);
+    const unsigned used = g.x * g.y * g.z;
+    if (npart > used)
+      HFB_CUDA(cudaMemsetAsync(partial + used, 0, sizeof(double) * (npart - used),
+                               (cudaStream_t)stream));
+  } else if (lz > 0) {
+    residual_sq_march_kernel<64, 4><<<npart, 256, 0, (cudaStream_t)stream>>>(
         u, F, p->coef + 12LL * p->nz, p->nx, p->ny, p->nz, mask, partial, lz);
-  else
-    residual_sq_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+  } else {
+    residual_sq_kernel<<<npart, 256, 0, (cudaStream_t)stream>>>(
         u, F, p->coef + 12LL * p->nz, p->nx, p->ny, p->nz, mask, partial);
+  }
   HFB_LAUNCHED();
   return HFB_OK;
 }
@@ -659,7 +821,7 @@ extern "C" int hfb_residual_sq_z(hfb_plan* p, const double* u_re, const double* 
   if (!p || !u_re || !u_im || !rhs_re || !rhs_im || !partial) return HFB_ERR_ARGUMENT;
   if (!p->have_coef || !p->coef_i) return HFB_ERR_NO_COEFFICIENTS;
   HFB_CUDA(cudaSetDevice(p->device));
-  residual_sq_z_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+  residual_sq_z_kernel<<<(unsigned)hfb_residual_partials(p), 256, 0, (cudaStream_t)stream>>>(
       u_re, u_im, rhs_re, rhs_im, p->coef + 12LL * p->nz, p->coef_i + 12LL * p->nz, p->nx,
       p->ny, p->nz, mask, partial);
   HFB_LAUNCHED();

@@ -1199,12 +1199,14 @@ def test_dmma_dst2d_vs_scipy(cuda, nx, ny, nz):
         assert np.abs(f.values - ref).max() < 1e-13 * np.abs(ref).max(), knobs
 
 
-@pytest.mark.parametrize("shape", [(37, 23, 19), (64, 4, 33), (5, 130, 7), (129, 9, 65)])
+@pytest.mark.parametrize("shape", [(37, 23, 19), (64, 4, 33), (5, 130, 7), (129, 9, 65),
+                                   (1, 1, 1), (33, 1, 2), (2, 33, 70)])
 def test_marching_stencils_match_gather_kernels(cuda, shape):
     """The level-marching RHS operator, 27-point apply and residual (tuning key
-    20 > 0, default 32) against the per-point gather kernels (key 20 = 0) on
-    shapes that do not fill the 64 x 4 x 32 tiles: bitwise for the operators,
-    1e-14 for the (reordered) sum of squares."""
+    20 > 0, default 32) and the plane-streamed 27-point apply and residual
+    (key 24 > 0 levels per CTA, default 64; key 25 rows per warp) against the
+    per-point gather kernels (keys 20 = 24 = 0) on shapes that do not fill the
+    tiles: bitwise for the operators, 1e-14 for the (reordered) sum of squares."""
     import torch
     nx, ny, nz = shape
     g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
@@ -1220,8 +1222,11 @@ def test_marching_stencils_match_gather_kernels(cuda, shape):
                        device="cuda")
     outs = []
     try:
-        for v in (0, 32, 5):
+        for v, ls, rj in ((0, 0, 4), (32, 0, 4), (5, 0, 4), (32, 64, 4), (32, 7, 4), (32, 64, 2),
+                          (32, 1, 2)):
             lib.hfb_set_tuning(20, v)
+            lib.hfb_set_tuning(24, ls)
+            lib.hfb_set_tuning(25, rj)
             F = torch.empty((nz, ny, nx), dtype=torch.float64, device="cuda")
             hb._native.check(lib.hfb_rhs_fourth(plan.handle, P(f), P(F), 0.37, st), "rhs4")
             A0 = torch.empty_like(F)
@@ -1235,6 +1240,8 @@ def test_marching_stencils_match_gather_kernels(cuda, shape):
             outs.append((F, A0, A1, float(part.sum())))
     finally:
         lib.hfb_set_tuning(20, 32)
+        lib.hfb_set_tuning(24, 64)
+        lib.hfb_set_tuning(25, 4)
     ref = outs[0]
     for o in outs[1:]:
         for a, b in zip(o[:3], ref[:3]):
