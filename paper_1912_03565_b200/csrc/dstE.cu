@@ -101,6 +101,8 @@ struct StreamArgs {
   double* wc;
   int desc;
   int dbg;  // measurement only (tuning key 22): 1 no waits, 2 acq_rel fences, 4 no fences
+  int late;               // issue the next batch's prefetch after this batch's pre-processing
+                          // (tuning key 29) instead of before waiting for this batch
   long long per;          // batches per CTA (one contiguous run), 0 = interleaved
   int run;                // > 1: interleaved runs of `run` consecutive batches
 };
@@ -369,10 +371,13 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
       issue(0, 0);
     }
   }
-  for (long long it = 0;; ++it) {
-    long long plane;
-    int g;
-    if (!batch_of(a, it, plane, g)) break;
+  // Prefetch batch it + 1 into the other stage. Its buffer's previous batch
+  // (it - 1) must have been read out by its store: issued right at the start
+  // of batch it, the leader waits for the store committed a moment before
+  // while the rest of its group (or CTA) goes on, then waits for the leader;
+  // issued after the pre-processing (a.late) the store has long finished and
+  // the copy still has the FFT, post-processing and store of batch it to land.
+  auto prefetch_next = [&](long long it) {
     {
       long long pl2;
       int g2;
@@ -388,6 +393,12 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         issue(it + 1, s ^ 1);
       }
     }
+  };
+  for (long long it = 0;; ++it) {
+    long long plane;
+    int g;
+    if (!batch_of(a, it, plane, g)) break;
+    if (!a.late) prefetch_next(it);
     mbar_wait(indep ? &gbar[s][f] : &bar[s], s == 0 ? phase0 : phase1);
     if (s == 0) phase0 ^= 1; else phase1 ^= 1;
 
@@ -405,6 +416,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         dstE_pre<P, E>(v, c.sn, etw, t,
                        [&](int e) -> double2 { return bx[(e + M - 1) & (M - 1)]; });
         group_sync<T>(f);
+        if (a.late) prefetch_next(it);
       } else {
         const double2* bx = reinterpret_cast<const double2*>(gbuf(s, 0));
         dstE_pre<P, E>(v, c.sn, etw, t, [&](int e) -> double2 {
@@ -412,6 +424,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
           return bx[gr ^ ((gr >> 3) & (a.NF - 1))];
         });
         __syncthreads();  // the box interleaves all groups' lines
+        if (a.late) prefetch_next(it);
       }
     } else {
       if constexpr (MODE == kYB) {
@@ -457,6 +470,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         return make_double2(v0 ? r0[e] : 0.0, v1 ? r1[e] : 0.0);
       });
       group_sync<T>(f);  // staged rows consumed: the group buffer becomes FFT scratch
+      if (a.late) prefetch_next(it);
     }
     double2* sb = reinterpret_cast<double2*>(gb);
     fftE_forward<P, E>(v, sb, etw, t, f);
@@ -842,8 +856,12 @@ static int g_tune_thomas_smem = 1;  // one-call z-solve with whole columns in sh
 // 12 warps per SM the register-resident engine leaves (long scoreboard 3-8 per issue)
 static int g_tune_wave = 0;
 static int g_tune_xsparse = 1;  // one-call z-solve stores x' once per chunk, recomputes the rest (key 23)
-static int g_tune_s27 = 64;  // streamed 27-point apply / residual: levels per CTA (key 24; 0 = key 20's kernels)
+static int g_tune_s27 = 32;  // streamed 27-point apply / residual: levels per CTA (key 24; 0 = key 20's kernels)
 static int g_tune_s27_rj = 4;  // rows per warp of the streamed 27-point kernels (key 25: 2 or 4)
+static int g_tune_thomas_stages = 3;  // ring stages of the TMA z-solve (key 26: 3 or 4)
+static int g_tune_s27_tile = 1;  // streamed 27-point kernels: planes staged in shared memory (key 27)
+static int g_tune_late = 2;  // DST passes: prefetch after the pre-processing (key 29; 2 = flat-row-store passes)
+static int g_tune_thomas_mpt = 1;  // modes per thread of the TMA z-solve (key 28: 1 or 2)
 static int g_tune_wave_dbg = 0;  // its measurement variants (key 22; wrong results for bit 1)
 
 template <int P, int E, int MODE>
@@ -964,6 +982,10 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   // decoupled groups: row passes, and column passes at M = 2048 (measured: x 3.90 -> 3.78,
   // inverse y 3.92 -> 3.82 ms at 1023^3; final x-pass 46.3 -> 42.3 ms at 2047^3; the
   // column passes at M = 1024 got slower with per-group boxes, 4.28 -> 4.57 ms)
+  // late prefetch (key 29: 1 all passes, 2 the flat-row-store passes only).
+  // Measured at 1023^3 (same box): final pass 4.87 -> 4.62 ms, the other
+  // passes 0.05-0.12 ms slower.
+  a.late = tuning(29) == 1 || (tuning(29) == 2 && a.ustore);
   a.indep = (k.mode == kRow || k.mode == kYB || (k.mode == kTload && M == 2048)) &&
             (a.tstore || a.ustore) && (g_tune_indep || k.mode == kYB) && T >= 32;
   if (k.mode == kYB && !a.indep) return HFB_ERR_ARGUMENT;
@@ -1100,6 +1122,10 @@ int tuning(int key) {
     case 23: return g_tune_xsparse;
     case 24: return g_tune_s27;
     case 25: return g_tune_s27_rj;
+    case 26: return g_tune_thomas_stages;
+    case 27: return g_tune_s27_tile;
+    case 28: return g_tune_thomas_mpt;
+    case 29: return g_tune_late;
     default: return 0;
   }
 }
@@ -1130,6 +1156,10 @@ void set_tuning(int key, int value) {
   if (key == 23) g_tune_xsparse = value ? 1 : 0;
   if (key == 24) g_tune_s27 = value;
   if (key == 25) g_tune_s27_rj = value;
+  if (key == 26) g_tune_thomas_stages = value;
+  if (key == 27) g_tune_s27_tile = value ? 1 : 0;
+  if (key == 28) g_tune_thomas_mpt = value;
+  if (key == 29) g_tune_late = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

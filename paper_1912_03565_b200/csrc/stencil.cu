@@ -8,6 +8,7 @@
 // arithmetic of the reference reduces to these real operations when the
 // imaginary parts are zero).
 #include "hfb_internal.cuh"
+#include "tma.cuh"
 
 namespace hfb {
 
@@ -493,7 +494,175 @@ __global__ void __launch_bounds__(256, (RJ <= 2 ? 3 : 2)) s27_stream_kernel(
   }
 }
 
-constexpr int kS27ResLz = 64;  // levels per CTA of the streamed residual (fixes the partial count)
+// The same streamed 27-point sums with the planes staged in shared memory
+// (tuning key 27, default): a CTA owns a 32 x 32 output tile and marches
+// lz levels; the 34 x 34 input tile of each plane (halo included) arrives by
+// 8-byte cp.async four planes ahead of the arithmetic (zero-filled outside the
+// array, which is the residual's zero boundary), so the FP64 pipe no longer
+// waits on the loads that head every plane of s27_stream_kernel. rhs / F of
+// the level being completed are prefetched into registers one plane ahead.
+// Same term order, same bits.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int kT27NS = 4;                   // plane stages
+constexpr int kT27Pitch = 36;               // doubles per staged row (34 used)
+constexpr int kT27Stage = 34 * kT27Pitch;   // doubles per stage
+
+// CM != 0: the term mask as a compile-time constant (the full 27-term mask of
+// the 6th-order and general tables, the 19-term mask of the 4th-order and cd4
+// tables): the per-term tests fold away (with a runtime mask they cost more
+// instructions than the arithmetic).
+constexpr uint32_t kMask27 = 0x7FFFFFFu, kMask19 = 0x7C3FFF0u;
+
+template <int KIND, uint32_t CM>
+__global__ void __launch_bounds__(256, 2) s27_tile_kernel(
+    const double* __restrict__ src, const double* __restrict__ rhs, double* __restrict__ out,
+    const double* __restrict__ raw, int nx, int ny, int nz, uint32_t mask_rt, int lz,
+    double* __restrict__ partial) {
+  const uint32_t mask = CM ? CM : mask_rt;
+  constexpr int RJ = 4, NS = kT27NS, PT = kT27Pitch;
+  constexpr int DI[9] = {-1, 1, -1, 1, -1, 1, 0, 0, 0};
+  constexpr int DJ[9] = {-1, -1, 1, 1, 0, 0, -1, 1, 0};
+  constexpr int WI[9] = {0, 0, 0, 0, 1, 1, 2, 2, 3};
+  extern __shared__ __align__(16) double smt[];
+  // this CTA's levels' raw weights, after the plane stages and (KIND != 0)
+  // the rhs stages
+  double* wsm = smt + NS * kT27Stage + (KIND != 0 ? NS * 1024 : 0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int l0 = blockIdx.z * lz, l1 = min(nz, l0 + lz);
+  const int i = x0 + lane, jw = y0 + warp * RJ;
+  for (int e = threadIdx.x; e < (l1 - l0) * 12; e += 256) wsm[e] = __ldg(raw + l0 * 12LL + e);
+  // this thread's (at most 5) elements of the 34 x 34 input tile: shared
+  // offset, offset from the plane base, and whether the element lies in the
+  // array (plane independent; the residual also checks the plane)
+  // this thread's (at most 5) elements of the 34 x 34 input tile: shared
+  // offset, offset from the plane base, and whether the element lies in the
+  // array (plane independent; the residual also checks the plane)
+  constexpr int NE = (34 * 34 + 255) / 256;
+  int soff[NE];
+  long long goff[NE];
+  bool eok[NE];
+#pragma unroll
+  for (int q = 0; q < NE; ++q) {
+    const int e = threadIdx.x + 256 * q;
+    const int r = e / 34, c = e - r * 34;
+    const int gy = y0 - 1 + r, gx = x0 - 1 + c;  // interior coordinates
+    soff[q] = e < 34 * 34 ? r * PT + c : -1;
+    if constexpr (KIND == 2) {
+      eok[q] = gy >= 0 && gy < ny && gx >= 0 && gx < nx;
+      goff[q] = (long long)gy * nx + gx;
+    } else {
+      eok[q] = gy + 1 <= ny + 1 && gx + 1 <= nx + 1;
+      goff[q] = (long long)(gy + 1) * (nx + 2) + gx + 1;
+    }
+  }
+  const long long pstride = KIND == 2 ? (long long)nx * ny : (long long)(nx + 2) * (ny + 2);
+  // rhs / F of output level P - 2 rides with plane P: this thread's own 4 values
+  auto load_plane = [&](int P, int st) {
+    double* dst = smt + st * kT27Stage;
+    const bool pok = KIND != 2 || (P >= 1 && P <= nz);
+    const double* base = src + (KIND == 2 ? (long long)(P - 1) : (long long)P) * pstride;
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+      if (soff[q] < 0) continue;
+      const bool ok = pok && eok[q];
+      cp_async8(dst + soff[q], ok ? base + goff[q] : src, ok ? 8 : 0);
+    }
+    if constexpr (KIND != 0) {
+      const int L = P - 2;
+      double* rd = smt + NS * kT27Stage + st * 1024 + warp * RJ * 32 + lane;
+#pragma unroll
+      for (int q = 0; q < RJ; ++q) {
+        const int j = jw + q;
+        const bool ok = L >= l0 && L < l1 && i < nx && j < ny;
+        cp_async8(rd + q * 32, ok ? rhs + ((long long)L * ny + j) * nx + i : rhs, ok ? 8 : 0);
+      }
+    }
+  };
+  const int Pend = l1 + 1;  // planes l0 .. l1 + 1 serve levels l0 .. l1 - 1
+#pragma unroll
+  for (int q = 0; q < NS - 1; ++q) {
+    if (l0 + q <= Pend) load_plane(l0 + q, q);
+    cp_async_commit();
+  }
+  double a0[RJ], a1[RJ];
+#pragma unroll
+  for (int q = 0; q < RJ; ++q) a0[q] = a1[q] = 0.0;
+  double ssq = 0.0;
+  for (int P = l0; P <= Pend; ++P) {
+    cp_async_wait<NS - 2>();
+    __syncthreads();  // plane P staged for everyone; stage (P - 1) free
+    if (P + NS - 1 <= Pend) load_plane(P + NS - 1, (P + NS - 1 - l0) % NS);
+    cp_async_commit();
+    const double* pl = smt + ((P - l0) % NS) * kT27Stage + warp * RJ * PT + lane;
+    const double* rl = smt + NS * kT27Stage + ((P - l0) % NS) * 1024 + warp * RJ * 32 + lane;
+    const double* w0 = wsm + (min(P, l1 - 1) - l0) * 12;                  // level P, k = 0
+    const double* w1 = wsm + (min(max(P - 1, l0), l1 - 1) - l0) * 12 + 4;  // level P-1, k = 1
+    const double* w2 = wsm + (max(P - 2, l0) - l0) * 12 + 8;               // level P-2, k = 2
+    double wk0[4], wk1[4], wk2[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      wk0[q] = w0[q];
+      wk1[q] = w1[q];
+      wk2[q] = w2[q];
+    }
+    const int L = P - 2;
+#pragma unroll
+    for (int q = 0; q < RJ; ++q) {
+      double v[9];
+#pragma unroll
+      for (int o = 0; o < 9; ++o) v[o] = pl[(q + 1 + DJ[o]) * PT + 1 + DI[o]];
+      double t0 = 0.0, t1 = a1[q], t2 = a0[q];
+#pragma unroll
+      for (int o = 0; o < 9; ++o)
+        if (mask & (1u << o)) t0 = DADD(t0, DMUL(wk0[WI[o]], v[o]));
+#pragma unroll
+      for (int o = 0; o < 9; ++o)
+        if (mask & (1u << (9 + o))) t1 = DADD(t1, DMUL(wk1[WI[o]], v[o]));
+#pragma unroll
+      for (int o = 0; o < 9; ++o)
+        if (mask & (1u << (18 + o))) t2 = DADD(t2, DMUL(wk2[WI[o]], v[o]));
+      const int j = jw + q;
+      if (L >= l0 && i < nx && j < ny) {
+        const long long oo = ((long long)L * ny + j) * nx + i;
+        if constexpr (KIND == 0) out[oo] = t2;
+        if constexpr (KIND == 1) out[oo] = __dsub_rn(rl[q * 32], t2);
+        if constexpr (KIND == 2) {
+          const double rr = t2 - rl[q * 32];
+          ssq = fma(rr, rr, ssq);
+        }
+      }
+      a0[q] = t1;
+      a1[q] = t0;
+    }
+  }
+  cp_async_wait<0>();
+  if constexpr (KIND == 2) {
+    __shared__ double red[8];
+    for (int o = 16; o > 0; o >>= 1) ssq += __shfl_down_sync(0xffffffffu, ssq, o);
+    if (lane == 0) red[warp] = ssq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += red[w];
+      partial[blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z)] = t;
+    }
+  }
+}
+
+constexpr int kS27ResLz = 32;  // levels per CTA of the streamed residual (fixes the partial count)
 
 // rows per warp of the streamed 27-point kernels (tuning key 25: 2 or 4)
 static int s27_rj() { return tuning(25) == 2 ? 2 : 4; }
@@ -507,6 +676,17 @@ static void s27_launch(const hfb_plan* p, int lz, const double* src, const doubl
                        double* out, uint32_t mask, double* partial, cudaStream_t st) {
   const int rj = s27_rj();
   const double* raw = p->coef + 12LL * p->nz;
+  if (tuning(27)) {  // shared-memory staged planes (32 x 32 tiles = the rj = 4 grid)
+    const size_t sm = sizeof(double) * ((size_t)kT27NS * (kT27Stage + (KIND ? 1024 : 0)) +
+                                        12 * (size_t)lz);
+    auto kern = mask == kMask27 ? s27_tile_kernel<KIND, kMask27>
+                : mask == kMask19 ? s27_tile_kernel<KIND, kMask19>
+                                  : s27_tile_kernel<KIND, 0>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<s27_grid(p, lz, 4), 256, sm, st>>>(src, rhs, out, raw, p->nx, p->ny, p->nz, mask, lz,
+                                              partial);
+    return;
+  }
   if (rj == 2)
     s27_stream_kernel<2, KIND><<<s27_grid(p, lz, 2), 256, 0, st>>>(
         src, rhs, out, raw, p->nx, p->ny, p->nz, mask, lz, partial);
@@ -740,7 +920,7 @@ extern "C" int hfb_residual_sq(hfb_plan* p, const double* u, const double* F, do
   const int lz = tuning(20);
   const unsigned npart = (unsigned)hfb_residual_partials(p);
   if (tuning(24) > 0) {
-    const dim3 g = s27_grid(p, kS27ResLz, s27_rj());
+    const dim3 g = s27_grid(p, kS27ResLz, tuning(27) ? 4 : s27_rj());
     s27_launch<2>(p, kS27ResLz, u, F, nullptr, mask, partial, (cudaStream_t)stream);
     const unsigned used = g.x * g.y * g.z;
     if (npart > used)

@@ -44,6 +44,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// plain arrival (count 1; release semantics at CTA scope)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // generic-proxy accesses to shared memory before this point are ordered
 // before subsequent async-proxy (TMA) writes to it
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -94,6 +99,19 @@ __device__ __forceinline__ void bulk_wait_read() {
 template <int N>
 __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// wait until at most n (runtime, capped at 7) committed groups are pending
+__device__ __forceinline__ void bulk_wait_upto(int n) {
+  switch (n < 0 ? 0 : n) {
+    case 0: bulk_wait<0>(); break;
+    case 1: bulk_wait<1>(); break;
+    case 2: bulk_wait<2>(); break;
+    case 3: bulk_wait<3>(); break;
+    case 4: bulk_wait<4>(); break;
+    case 5: bulk_wait<5>(); break;
+    case 6: bulk_wait<6>(); break;
+    default: bulk_wait<7>(); break;
+  }
 }
 // 3D tiled tensor load (box of a CUtensorMap at coordinates c0, c1, c2 — c0 the
 // innermost) into shared memory, completing on an mbarrier.

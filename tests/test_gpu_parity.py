@@ -416,6 +416,7 @@ def tuning():
     lib.hfb_set_tuning(10, 0)
     lib.hfb_set_tuning(13, 1)
     lib.hfb_set_tuning(14, 1)
+    lib.hfb_set_tuning(29, 2)
 
 
 @pytest.mark.parametrize("knobs", [((0, 32),), ((0, 32), (1, 2)), ((0, 32), (1, 1)), ((1, 1),),
@@ -423,6 +424,7 @@ def tuning():
                                    ((0, 32), (4, 0)), ((5, 0),), ((0, 32), (5, 1)),
                                    ((6, 1),), ((6, 1), (7, 1), (8, 2)), ((9, 1),),
                                    ((14, 0),), ((14, 0), (13, 0)), ((1, 1), (14, 1)),
+                                   ((29, 0),), ((29, 1),),
                                    ((10, 2),)])
 def test_tuning_variants_match_oracle(cuda, tuning, knobs):
     """Performance knobs change the FFT factorisation or the CTA shape, never
@@ -1204,7 +1206,8 @@ def test_dmma_dst2d_vs_scipy(cuda, nx, ny, nz):
 def test_marching_stencils_match_gather_kernels(cuda, shape):
     """The level-marching RHS operator, 27-point apply and residual (tuning key
     20 > 0, default 32) and the plane-streamed 27-point apply and residual
-    (key 24 > 0 levels per CTA, default 64; key 25 rows per warp) against the
+    (key 24 > 0 levels per CTA, default 64; key 25 rows per warp; key 27 the
+    shared-memory staged planes, default) against the
     per-point gather kernels (keys 20 = 24 = 0) on shapes that do not fill the
     tiles: bitwise for the operators, 1e-14 for the (reordered) sum of squares."""
     import torch
@@ -1222,11 +1225,13 @@ def test_marching_stencils_match_gather_kernels(cuda, shape):
                        device="cuda")
     outs = []
     try:
-        for v, ls, rj in ((0, 0, 4), (32, 0, 4), (5, 0, 4), (32, 64, 4), (32, 7, 4), (32, 64, 2),
-                          (32, 1, 2)):
+        for v, ls, rj, tile in ((0, 0, 4, 0), (32, 0, 4, 0), (5, 0, 4, 0), (32, 64, 4, 0),
+                                (32, 7, 4, 0), (32, 64, 2, 0), (32, 1, 2, 0), (32, 64, 4, 1),
+                                (32, 7, 4, 1), (32, 1, 4, 1), (32, 200, 4, 1)):
             lib.hfb_set_tuning(20, v)
             lib.hfb_set_tuning(24, ls)
             lib.hfb_set_tuning(25, rj)
+            lib.hfb_set_tuning(27, tile)
             F = torch.empty((nz, ny, nx), dtype=torch.float64, device="cuda")
             hb._native.check(lib.hfb_rhs_fourth(plan.handle, P(f), P(F), 0.37, st), "rhs4")
             A0 = torch.empty_like(F)
@@ -1240,8 +1245,9 @@ def test_marching_stencils_match_gather_kernels(cuda, shape):
             outs.append((F, A0, A1, float(part.sum())))
     finally:
         lib.hfb_set_tuning(20, 32)
-        lib.hfb_set_tuning(24, 64)
+        lib.hfb_set_tuning(24, 32)
         lib.hfb_set_tuning(25, 4)
+        lib.hfb_set_tuning(27, 1)
     ref = outs[0]
     for o in outs[1:]:
         for a, b in zip(o[:3], ref[:3]):

@@ -212,3 +212,75 @@ def test_guard_bands_untouched(cuda, shape, lean, inplace):
     if not inplace:
         assert np.array_equal(X.cpu().numpy().reshape(g.shape), F)
     assert torch.isfinite(Y).all()
+
+
+# ------------------------------------------- z-solve variants (round 2)
+def _one_call(shape, scheme, seed, knobs, lean=False):
+    """hfb_solve of a seeded F under tuning knobs; returns U on the host."""
+    import torch
+    nx, ny, nz = shape
+    h = 1.0 / 64  # uniform spacing (the 6th-order scheme requires it)
+    g = hb.make_grid(hb.Domain(0, (nx + 1) * h, 0, (ny + 1) * h, 0, (nz + 1) * h), nx, ny, nz)
+    prof = hb.constant_profile(0.0, g, gamma=-1.5) if scheme == "cd4" else wl.profile_a(g)
+    sk = hb.SchemeKind.CONVECTION_DIFFUSION_4 if scheme == "cd4" else hb.SchemeKind.SIXTH_ORDER
+    lib = _native.load_library()
+    plan = _native.get_plan(nx, ny, nz, torch.device("cuda", 0))
+    device_coefficients(plan, sk, prof, g)
+    plan.set_workspace_mode(lean)
+    F = torch.from_numpy(np.random.default_rng(seed).standard_normal((nz, ny, nx))).cuda()
+    U = F if lean else torch.empty_like(F)
+    work = plan.workspace(0)
+    try:
+        for k, v in knobs:
+            lib.hfb_set_tuning(k, v)
+        _native.check(lib.hfb_solve(plan.handle, _native.ptr(F), _native.ptr(U),
+                                    _native.ptr(work), plan.stream()), "solve")
+        plan.fetch_status()
+    finally:
+        lib.hfb_set_tuning(23, 1)
+        lib.hfb_set_tuning(26, 3)
+        lib.hfb_set_tuning(19, 1)
+        lib.hfb_set_tuning(29, 2)
+    return U.cpu().numpy(), (F, sk, prof, g)
+
+
+@pytest.mark.parametrize("shape", [(1023, 1023, 20), (255, 127, 9), (63, 300, 8), (33, 31, 1),
+                                   (64, 513, 17), (127, 127, 300), (31, 600, 16)])
+def test_zsolve_variants_bitwise(cuda, shape):
+    """The one-call z-solve's variants are bitwise equal: the 3-stage TMA ring
+    with dense x' rows (key 23 = 0, key 26 = 3) against sparse x' (key 23, x'
+    stored once per 8-level chunk and recomputed in the back substitution) and
+    the 4-stage ring (key 26 = 4); shapes with n_z below, at and just above a
+    chunk, partial mode blocks, many blocks per CTA; the small-n_z shared-memory
+    kernel is switched off (key 19)."""
+    scheme = "cd4" if shape[2] % 2 else "6"
+    ref, _ = _one_call(shape, scheme, 7, [(19, 0), (23, 0), (26, 3)])
+    for knobs in ([(19, 0), (23, 1), (26, 3)], [(19, 0), (23, 1), (26, 4)],
+                  [(19, 0), (23, 0), (26, 4)]):
+        u, _ = _one_call(shape, scheme, 7, knobs)
+        assert np.array_equal(u, ref), knobs
+
+
+def test_zsolve_default_vs_oracle(cuda):
+    """The default z-solve (sparse x', warp-specialised) against the oracle at
+    a size that runs many blocks per CTA (1023^2 x 24, 6th order, k(z))."""
+    u, (F, sk, prof, g) = _one_call((1023, 1023, 24), "6", 11, [])
+    T = orc.weight_table("6", np.real(prof.k2), np.real(prof.k2_z), np.real(prof.k2_zz), 0.0,
+                         (g.h_x, g.h_y, g.h_z), g.n_z)
+    ref = orc.solve(F.cpu().numpy(), T, *orc.mode_cosines(g.n_x, g.n_y),
+                    workers=orc.default_workers())
+    err = rel_l2(u, ref)
+    print(f"default z-solve 1023^2 x 24 vs oracle: {err:.3e}")
+    assert err < TOL
+
+
+@pytest.mark.parametrize("shape", [(1023, 1023, 9), (511, 255, 5), (2047, 2047, 3),
+                                   (1023, 31, 17)])
+def test_late_prefetch_bitwise(cuda, shape):
+    """The DST passes' prefetch point (tuning key 29: before the batch, after
+    its pre-processing for every pass, or for the flat-row-store passes only,
+    the default) never changes a bit of the one-call solve."""
+    ref, _ = _one_call(shape, "cd4", 3, [(29, 0)])
+    for v in (1, 2):
+        u, _ = _one_call(shape, "cd4", 3, [(29, v)])
+        assert np.array_equal(u, ref), v

@@ -58,22 +58,24 @@ ext = f
 rhs = torch.rand((n, n, n), dtype=torch.float64, device=dev)
 refs = {}
 # (key 20, key 24, key 25): gathers, marching, streamed (levels per CTA, rows per warp)
-VARIANTS = [(0, 0, 4), (32, 0, 4), (32, 32, 4), (32, 64, 4), (32, 128, 4), (32, 64, 2)]
-for v20, v24, v25 in VARIANTS:
+VARIANTS = [(0, 0, 4, 0), (32, 0, 4, 0), (32, 64, 4, 0), (32, 64, 2, 0), (32, 32, 4, 1),
+            (32, 64, 4, 1), (32, 128, 4, 1)]
+for v20, v24, v25, v27 in VARIANTS:
     lib.hfb_set_tuning(20, v20)
     lib.hfb_set_tuning(24, v24)
     lib.hfb_set_tuning(25, v25)
+    lib.hfb_set_tuning(27, v27)
     for mode in (0, 1):
         timed(lambda: _native.check(lib.hfb_apply27(plan.handle, P(ext), P(rhs), P(F), 0x7FFFFFF,
                                                     mode, st), "apply27"),
               8 * ((n + 2) ** 3 + (2 if mode else 1) * n ** 3),
-              f"apply27 mode {mode}, tuning 20/24/25 = {v20}/{v24}/{v25}")
+              f"apply27 mode {mode}, tuning 20/24/25/27 = {v20}/{v24}/{v25}/{v27}")
         if mode not in refs:
             refs[mode] = F.clone()
         else:
-            assert torch.equal(F, refs[mode]), (mode, v20, v24, v25)
+            assert torch.equal(F, refs[mode]), (mode, v20, v24, v25, v27)
 lib.hfb_set_tuning(20, 32)
-lib.hfb_set_tuning(24, 64)
+lib.hfb_set_tuning(24, 32)
 lib.hfb_set_tuning(25, 4)
 print("apply27 bitwise equal across variants")
 
@@ -82,17 +84,19 @@ u = torch.rand((n, n, n), dtype=torch.float64, device=dev)
 npart = int(lib.hfb_residual_partials(plan.handle))
 part = torch.empty(npart, dtype=torch.float64, device=dev)
 vals = {}
-for v20, v24, v25 in VARIANTS:
+for v20, v24, v25, v27 in VARIANTS:
     lib.hfb_set_tuning(20, v20)
     lib.hfb_set_tuning(24, v24)
     lib.hfb_set_tuning(25, v25)
+    lib.hfb_set_tuning(27, v27)
     timed(lambda: _native.check(lib.hfb_residual_sq(plan.handle, P(u), P(rhs), P(part), 0x7FFFFFF,
                                                     st), "residual"),
-          8 * 2 * n ** 3, f"residual_sq, tuning 20/24/25 = {v20}/{v24}/{v25}")
-    vals[(v20, v24, v25)] = float(part.sum())
+          8 * 2 * n ** 3, f"residual_sq, tuning 20/24/25/27 = {v20}/{v24}/{v25}/{v27}")
+    vals[(v20, v24, v25, v27)] = float(part.sum())
 lib.hfb_set_tuning(20, 32)
-lib.hfb_set_tuning(24, 64)
+lib.hfb_set_tuning(24, 32)
 lib.hfb_set_tuning(25, 4)
+lib.hfb_set_tuning(27, 1)
 print("residual sums", vals)
 r0 = list(vals.values())[0]
 assert all(abs(x - r0) <= 1e-12 * abs(r0) for x in vals.values()), vals
