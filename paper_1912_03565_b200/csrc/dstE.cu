@@ -861,7 +861,7 @@ static int g_tune_s27_rj = 4;  // rows per warp of the streamed 27-point kernels
 static int g_tune_thomas_stages = 3;  // ring stages of the TMA z-solve (key 26: 3 or 4)
 static int g_tune_s27_tile = 1;  // streamed 27-point kernels: planes staged in shared memory (key 27)
 static int g_tune_late = 2;  // DST passes: prefetch after the pre-processing (key 29; 2 = flat-row-store passes)
-static int g_tune_thomas_mpt = 1;  // modes per thread of the TMA z-solve (key 28: 1 or 2)
+static int g_tune_thomas_narrow = 0;  // TMA z-solve with 128-mode blocks (key 28)
 static int g_tune_wave_dbg = 0;  // its measurement variants (key 22; wrong results for bit 1)
 
 template <int P, int E, int MODE>
@@ -1124,7 +1124,7 @@ int tuning(int key) {
     case 25: return g_tune_s27_rj;
     case 26: return g_tune_thomas_stages;
     case 27: return g_tune_s27_tile;
-    case 28: return g_tune_thomas_mpt;
+    case 28: return g_tune_thomas_narrow;
     case 29: return g_tune_late;
     default: return 0;
   }
@@ -1158,7 +1158,7 @@ void set_tuning(int key, int value) {
   if (key == 25) g_tune_s27_rj = value;
   if (key == 26) g_tune_thomas_stages = value;
   if (key == 27) g_tune_s27_tile = value ? 1 : 0;
-  if (key == 28) g_tune_thomas_mpt = value;
+  if (key == 28) g_tune_thomas_narrow = value;
   if (key == 29) g_tune_late = value;
 }
 

@@ -45,13 +45,8 @@ __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, 
 }
 }  // namespace
 
-// MPT modes per thread (tuning key 28: 1, or 2 for BM = 512 modes on 256
-// threads): thread tid owns modes tid and tid + BM / 2 of the block, two
-// independent recurrences whose division chains interleave, and the level
-// weights loaded from shared memory serve both.
-template <int BM, int S, int MPT>
-__global__ void __launch_bounds__(BM / MPT) thomas_tma_kernel(TmaArgs a) {
-  constexpr int NT = BM / MPT;  // threads
+template <int BM, int S>
+__global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
   extern __shared__ __align__(16) double dyn[];
   double(*sdat)[K][BM] = reinterpret_cast<double(*)[K][BM]>(dyn);
   double(*scoef)[K * 12] = reinterpret_cast<double(*)[K * 12]>(dyn + S * K * BM);
@@ -83,26 +78,12 @@ __global__ void __launch_bounds__(BM / MPT) thomas_tma_kernel(TmaArgs a) {
         bulk_g2s(&sdat[s][i][0], base + plane_of(l0 + i) * a.ps, rowbytes, &bar[s]);
       bulk_g2s(&scoef[s][0], a.coef + (long long)l0 * 12, (uint32_t)(nl * 12 * 8), &bar[s]);
     };
+    const bool live = tid < cols;
+    const int m = m0 + tid;
     const double cxv = __ldg(a.cx + n);
-    bool live[MPT];
-    int m[MPT];
-    double cyv[MPT], cxy[MPT];
-    double* ck[MPT];
-#pragma unroll
-    for (int u = 0; u < MPT; ++u) {
-      const int j = tid + u * NT;  // mode of the block
-      live[u] = j < cols;
-      m[u] = m0 + j;
-      cyv[u] = live[u] ? __ldg(a.cy + a.m_off + m[u]) : 0.0;
-      cxy[u] = cxv * cyv[u];
-      ck[u] = a.cpk + (long long)n * a.ld + m0 + j;
-    }
-    auto key_of = [&](int l, int u) {
-      return ((unsigned long long)l * (unsigned long long)a.ny_total +
-              (unsigned long long)(a.m_off + m[u])) *
-                 (unsigned long long)a.nx +
-             (unsigned long long)n;
-    };
+    const double cyv = live ? __ldg(a.cy + a.m_off + m) : 0.0;
+    const double cxy = cxv * cyv;
+    double* ck = a.cpk + (long long)n * a.ld + m0 + tid;
 
     // The last forward chunk stays in its stage and is the first backward chunk
     // (no store, no reload), so stages run task % S forward and (task-1) % S
@@ -125,15 +106,13 @@ __global__ void __launch_bounds__(BM / MPT) thomas_tma_kernel(TmaArgs a) {
     // (the recomputed values go back into the staged chunk). The last forward
     // chunk stays on chip with every x' as before.
     const bool xs = a.xsparse && !a.bwd_only;
-    double c[MPT], x[MPT], cknext[MPT];
-#pragma unroll
-    for (int u = 0; u < MPT; ++u) {
-      c[u] = x[u] = cknext[u] = 0.0;
-      if (a.bwd_only && live[u] && nchunk > 1) cknext[u] = ck[u][(long long)(nchunk - 2) * a.ps];
-    }
+    double c = 0.0, x = 0.0, cknext = 0.0;
+    if (a.bwd_only && live && nchunk > 1) cknext = ck[(long long)(nchunk - 2) * a.ps];
     for (int task = task0; task < ntask; ++task) {
       const int s = stage_of(task);
       if (tid == 0 && task + 2 < ntask && needs_load(task + 2)) {
+        // backward reloads must see the forward stores; otherwise only the
+        // stage's previous store has to be done reading shared memory
         // The stage's previous user must have been read out by its store.
         // With 3 stages that store is the one issued at the end of the last
         // task; with 4 it is the store before that.
@@ -166,127 +145,106 @@ __global__ void __launch_bounds__(BM / MPT) thomas_tma_kernel(TmaArgs a) {
         // forward elimination over levels l0 .. l0 + nl - 1
         const bool keep_all = !xs || task == nchunk - 1;
         if (inner) {
-          int bad[MPT];
-#pragma unroll
-          for (int u = 0; u < MPT; ++u) bad[u] = K;
+          int bad = K;
 #pragma unroll
           for (int i = 0; i < K; ++i) {
-#pragma unroll
-            for (int u = 0; u < MPT; ++u) {
-              const double lo = eig_s(co + i * 12, cxv, cyv[u], cxy[u]);
-              const double di = eig_s(co + i * 12 + 4, cxv, cyv[u], cxy[u]);
-              const double up = eig_s(co + i * 12 + 8, cxv, cyv[u], cxy[u]);
-              const double den = fma(-lo, c[u], di);
-              bad[u] = (fabs(den) < a.thr && bad[u] == K) ? i : bad[u];
-              const double rr = 1.0 / den;
-              double& d = sdat[s][i][tid + u * NT];
-              x[u] = fma(-lo, x[u], d) * rr;
-              if (keep_all || i == 0) d = x[u];
-              c[u] = up * rr;
-            }
+            const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
+            const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
+            const double up = eig_s(co + i * 12 + 8, cxv, cyv, cxy);
+            const double den = fma(-lo, c, di);
+            bad = (fabs(den) < a.thr && bad == K) ? i : bad;
+            const double rr = 1.0 / den;
+            x = fma(-lo, x, sdat[s][i][tid]) * rr;
+            if (keep_all || i == 0) sdat[s][i][tid] = x;
+            c = up * rr;
           }
-#pragma unroll
-          for (int u = 0; u < MPT; ++u) {
-            if (live[u]) ck[u][(long long)cidx * a.ps] = c[u];
-            if (live[u] && bad[u] < K) atomicMin(a.err, key_of(l0 + bad[u], u));
+          if (live) ck[(long long)cidx * a.ps] = c;
+          if (live && bad < K) {
+            const unsigned long long key =
+                ((unsigned long long)(l0 + bad) * (unsigned long long)a.ny_total +
+                 (unsigned long long)(a.m_off + m)) *
+                    (unsigned long long)a.nx +
+                (unsigned long long)n;
+            atomicMin(a.err, key);
           }
         } else {
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             if (i < nl) {
               const int l = l0 + i;
-#pragma unroll
-              for (int u = 0; u < MPT; ++u) {
-                const double lo = eig_s(co + i * 12, cxv, cyv[u], cxy[u]);
-                const double di = eig_s(co + i * 12 + 4, cxv, cyv[u], cxy[u]);
-                const double up = eig_s(co + i * 12 + 8, cxv, cyv[u], cxy[u]);
-                const double den = (l == 0) ? di : fma(-lo, c[u], di);
-                if (live[u] && fabs(den) < a.thr) atomicMin(a.err, key_of(l, u));
-                const double rr = 1.0 / den;
-                double& d = sdat[s][i][tid + u * NT];
-                x[u] = ((l == 0) ? d : fma(-lo, x[u], d)) * rr;
-                if (keep_all || i == 0) d = x[u];
-                if (l < a.nz - 1) {
-                  c[u] = up * rr;
-                  if (i == K - 1 && live[u]) ck[u][(long long)cidx * a.ps] = c[u];
-                }
+              const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
+              const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
+              const double up = eig_s(co + i * 12 + 8, cxv, cyv, cxy);
+              const double den = (l == 0) ? di : fma(-lo, c, di);
+              if (live && fabs(den) < a.thr) {
+                const unsigned long long key =
+                    ((unsigned long long)l * (unsigned long long)a.ny_total +
+                     (unsigned long long)(a.m_off + m)) *
+                        (unsigned long long)a.nx +
+                    (unsigned long long)n;
+                atomicMin(a.err, key);
+              }
+              const double rr = 1.0 / den;
+              x = ((l == 0) ? sdat[s][i][tid] : fma(-lo, x, sdat[s][i][tid])) * rr;
+              if (keep_all || i == 0) sdat[s][i][tid] = x;
+              if (l < a.nz - 1) {
+                c = up * rr;
+                if (i == K - 1 && live) ck[(long long)cidx * a.ps] = c;
               }
             }
           }
         }
-#pragma unroll
-        for (int u = 0; u < MPT; ++u)
-          if (live[u] && task == nchunk - 1 && nchunk > 1)
-            cknext[u] = ck[u][(long long)(nchunk - 2) * a.ps];
+        if (live && task == nchunk - 1 && nchunk > 1) cknext = ck[(long long)(nchunk - 2) * a.ps];
       } else {
         // back substitution over levels l0 + nl - 1 .. l0 (x holds W at the level above)
-        double cprev[MPT], xr[MPT], cb[MPT][K];
+        if (a.bwd_only && task == task0) x = sdat[s][nl - 1][tid];  // W = x' at the top
+        double cprev = cknext;
+        if (cidx >= 2 && live) cknext = ck[(long long)(cidx - 2) * a.ps];
+        double cb[K];
         // x' of this chunk to recompute (every chunk but the on-chip last one)
         const bool rec = xs && task != nchunk;
-#pragma unroll
-        for (int u = 0; u < MPT; ++u) {
-          if (a.bwd_only && task == task0) x[u] = sdat[s][nl - 1][tid + u * NT];  // W = x' at top
-          cprev[u] = cknext[u];
-          if (cidx >= 2 && live[u]) cknext[u] = ck[u][(long long)(cidx - 2) * a.ps];
-          xr[u] = rec ? sdat[s][0][tid + u * NT] : 0.0;
-        }
+        double xr = rec ? sdat[s][0][tid] : 0.0;
         if (inner) {
 #pragma unroll
           for (int i = 0; i < K; ++i) {
-#pragma unroll
-            for (int u = 0; u < MPT; ++u) {
-              const double di = eig_s(co + i * 12 + 4, cxv, cyv[u], cxy[u]);
-              const double lo = eig_s(co + i * 12, cxv, cyv[u], cxy[u]);
-              const double rr = 1.0 / fma(-lo, cprev[u], di);
-              if (rec && i > 0) {
-                double& d = sdat[s][i][tid + u * NT];
-                xr[u] = fma(-lo, xr[u], d) * rr;
-                d = xr[u];
-              }
-              cprev[u] = eig_s(co + i * 12 + 8, cxv, cyv[u], cxy[u]) * rr;
-              cb[u][i] = cprev[u];
+            const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
+            const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
+            const double rr = 1.0 / fma(-lo, cprev, di);
+            if (rec && i > 0) {
+              xr = fma(-lo, xr, sdat[s][i][tid]) * rr;
+              sdat[s][i][tid] = xr;
             }
+            cprev = eig_s(co + i * 12 + 8, cxv, cyv, cxy) * rr;
+            cb[i] = cprev;
           }
 #pragma unroll
           for (int i = K - 1; i >= 0; --i) {
-#pragma unroll
-            for (int u = 0; u < MPT; ++u) {
-              double& d = sdat[s][i][tid + u * NT];
-              x[u] = fma(-cb[u][i], x[u], d);
-              d = x[u];
-            }
+            x = fma(-cb[i], x, sdat[s][i][tid]);
+            sdat[s][i][tid] = x;
           }
         } else {
 #pragma unroll
           for (int i = 0; i < K; ++i) {
             const int l = l0 + i;
             if (i < nl && l < a.nz - 1) {
-#pragma unroll
-              for (int u = 0; u < MPT; ++u) {
-                const double di = eig_s(co + i * 12 + 4, cxv, cyv[u], cxy[u]);
-                const double lo = eig_s(co + i * 12, cxv, cyv[u], cxy[u]);
-                const double dl = (l == 0) ? di : fma(-lo, cprev[u], di);
-                const double rr = 1.0 / dl;
-                if (rec && i > 0) {
-                  double& d = sdat[s][i][tid + u * NT];
-                  xr[u] = fma(-lo, xr[u], d) * rr;
-                  d = xr[u];
-                }
-                cprev[u] = eig_s(co + i * 12 + 8, cxv, cyv[u], cxy[u]) * rr;
-                cb[u][i] = cprev[u];
+              const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
+              const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
+              const double dl = (l == 0) ? di : fma(-lo, cprev, di);
+              const double rr = 1.0 / dl;
+              if (rec && i > 0) {
+                xr = fma(-lo, xr, sdat[s][i][tid]) * rr;
+                sdat[s][i][tid] = xr;
               }
+              cprev = eig_s(co + i * 12 + 8, cxv, cyv, cxy) * rr;
+              cb[i] = cprev;
             }
           }
 #pragma unroll
           for (int i = K - 1; i >= 0; --i) {
             const int l = l0 + i;
             if (i < nl && l < a.nz - 1) {
-#pragma unroll
-              for (int u = 0; u < MPT; ++u) {
-                double& d = sdat[s][i][tid + u * NT];
-                x[u] = fma(-cb[u][i], x[u], d);
-                d = x[u];
-              }
+              x = fma(-cb[i], x, sdat[s][i][tid]);
+              sdat[s][i][tid] = x;
             }
           }
         }
@@ -430,7 +388,8 @@ int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld,
   a.nrows = row1 - row0;
   a.ncols = ncols;
   // narrow y-slabs (multi-GPU, P >= 8) would leave half of a 256-mode block idle
-  const int BM = ncols <= 128 ? 128 : BMAX;
+  // (tuning key 28 = 1: 128-mode blocks everywhere — 4-warp barriers, more CTAs)
+  const int BM = (ncols <= 128 || tuning(28) == 1) ? 128 : BMAX;
   a.nbpr = (ncols + BM - 1) / BM;
   a.ld = ld;
   a.ps = ps;
@@ -441,14 +400,9 @@ int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld,
   // ring stages (tuning key 26: 3 or 4; 4 lets the refill skip waiting for the
   // store issued just before, at 16 KB more shared memory per 256-mode CTA)
   const int S = (bwd_only || tuning(26) != 4) ? 3 : 4;
-  // two modes per thread (key 28 = 2): 512-mode blocks on 256 threads
-  const bool two = !bwd_only && tuning(28) == 2 && BM == BMAX;
-  const int BB = two ? 2 * BMAX : BM;  // modes per block
-  a.nbpr = (ncols + BB - 1) / BB;
-  const size_t sm = sizeof(double) * (size_t)S * (K * BB + K * 12);
-  auto kern = two ? (S == 4 ? thomas_tma_kernel<2 * BMAX, 4, 2> : thomas_tma_kernel<2 * BMAX, 3, 2>)
-              : BM == 128 ? (S == 4 ? thomas_tma_kernel<128, 4, 1> : thomas_tma_kernel<128, 3, 1>)
-                          : (S == 4 ? thomas_tma_kernel<BMAX, 4, 1> : thomas_tma_kernel<BMAX, 3, 1>);
+  const size_t sm = sizeof(double) * (size_t)S * (K * BM + K * 12);
+  auto kern = BM == 128 ? (S == 4 ? thomas_tma_kernel<128, 4> : thomas_tma_kernel<128, 3>)
+                        : (S == 4 ? thomas_tma_kernel<BMAX, 4> : thomas_tma_kernel<BMAX, 3>);
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 1, sms = 148, dev = 0;
   HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BM, sm));

@@ -1,2 +1,3 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python bench.py > gpurun_out/bench2.json 2> gpurun_out/bench2.err; tail -c 600 gpurun_out/bench2.json
+python -m pytest tests/test_gpu_parity_r2.py -x -q -k "zsolve" 2>&1 | tail -1
+for r in 1 2; do for k in 0 1; do python tools/one_solve.py --cfg 4 --reps 10 --time --stages --tune 28=$k; done; done
+for k in 0 1; do python tools/one_solve.py --cfg 3 --reps 20 --time --stages --tune 28=$k; done
