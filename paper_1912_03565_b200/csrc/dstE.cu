@@ -862,6 +862,7 @@ static int g_tune_thomas_stages = 3;  // ring stages of the TMA z-solve (key 26:
 static int g_tune_s27_tile = 1;  // streamed 27-point kernels: planes staged in shared memory (key 27)
 static int g_tune_late = 2;  // DST passes: prefetch after the pre-processing (key 29; 2 = flat-row-store passes)
 static int g_tune_thomas_narrow = 0;  // TMA z-solve with 128-mode blocks (key 28)
+static int g_tune_thomas_kc = 0;  // TMA z-solve chunks (key 30: 0 = 8 levels, 1 = 16 levels 3 stages, 2 = 16 levels 2 stages)
 static int g_tune_wave_dbg = 0;  // its measurement variants (key 22; wrong results for bit 1)
 
 template <int P, int E, int MODE>
@@ -1126,6 +1127,7 @@ int tuning(int key) {
     case 27: return g_tune_s27_tile;
     case 28: return g_tune_thomas_narrow;
     case 29: return g_tune_late;
+    case 30: return g_tune_thomas_kc;
     default: return 0;
   }
 }
@@ -1160,6 +1162,7 @@ void set_tuning(int key, int value) {
   if (key == 27) g_tune_s27_tile = value ? 1 : 0;
   if (key == 28) g_tune_thomas_narrow = value;
   if (key == 29) g_tune_late = value;
+  if (key == 30) g_tune_thomas_kc = value;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

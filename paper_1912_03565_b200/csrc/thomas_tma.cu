@@ -45,8 +45,11 @@ __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, 
 }
 }  // namespace
 
-template <int BM, int S>
+// KC levels per chunk (tuning key 30; 16 halves the chunk barriers and the
+// checkpoint traffic, at twice the shared memory per stage).
+template <int BM, int S, int KC>
 __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
+  constexpr int K = KC;
   extern __shared__ __align__(16) double dyn[];
   double(*sdat)[K][BM] = reinterpret_cast<double(*)[K][BM]>(dyn);
   double(*scoef)[K * 12] = reinterpret_cast<double(*)[K * 12]>(dyn + S * K * BM);
@@ -94,10 +97,10 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
       return a.bwd_only ? (task - task0) % S : task < nchunk ? task % S : (task - 1) % S;
     };
     auto needs_load = [&](int task) { return a.bwd_only || task != nchunk; };
-    if (tid == 0) {
-      issue(task0, stage_of(task0));
-      if (task0 + 1 < ntask && needs_load(task0 + 1)) issue(task0 + 1, stage_of(task0 + 1));
-    }
+    constexpr int D = S - 1;  // prefetch distance in tasks
+    if (tid == 0)
+      for (int q = 0; q < D; ++q)
+        if (task0 + q < ntask && needs_load(task0 + q)) issue(task0 + q, stage_of(task0 + q));
     // Sparse x' (tuning key 23, not with bwd_only): the forward sweep stores x'
     // only at level l0 of every chunk (levels l0+1 .. l0+K-1 keep F-hat in
     // place), and the back substitution recomputes x'_l = (F_l - lo x'_{l-1}) rr_l
@@ -110,24 +113,24 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
     if (a.bwd_only && live && nchunk > 1) cknext = ck[(long long)(nchunk - 2) * a.ps];
     for (int task = task0; task < ntask; ++task) {
       const int s = stage_of(task);
-      if (tid == 0 && task + 2 < ntask && needs_load(task + 2)) {
+      if (tid == 0 && task + D < ntask && needs_load(task + D)) {
         // backward reloads must see the forward stores; otherwise only the
         // stage's previous store has to be done reading shared memory
         // The stage's previous user must have been read out by its store.
         // With 3 stages that store is the one issued at the end of the last
         // task; with 4 it is the store before that.
         if constexpr (S >= 4) bulk_wait_read<1>(); else bulk_wait_read<0>();
-        if (!a.bwd_only && task + 2 > nchunk) {
+        if (!a.bwd_only && task + D > nchunk) {
           // a backward reload needs its chunk's forward store complete in
           // global memory; the store groups committed after it (one per task
           // but nchunk - 1, the last at the end of task - 1) may be in flight
-          const int cc = ntask - 1 - (task + 2);
+          const int cc = ntask - 1 - (task + D);
           const int after =
               (task - 1 - cc) - ((cc < nchunk - 1 && nchunk - 1 <= task - 1) ? 1 : 0);
           bulk_wait_upto(after);
         }
         fence_proxy_async_smem();
-        issue(task + 2, stage_of(task + 2));
+        issue(task + D, stage_of(task + D));
       }
       if (needs_load(task)) {
         mbar_wait(&bar[s], (phase >> s) & 1u);
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
             const double up = eig_s(co + i * 12 + 8, cxv, cyv, cxy);
             const double den = fma(-lo, c, di);
             bad = (fabs(den) < a.thr && bad == K) ? i : bad;
-            const double rr = 1.0 / den;
+            const double rr = rcp_fast(den);
             x = fma(-lo, x, sdat[s][i][tid]) * rr;
             if (keep_all || i == 0) sdat[s][i][tid] = x;
             c = up * rr;
@@ -184,7 +187,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
                     (unsigned long long)n;
                 atomicMin(a.err, key);
               }
-              const double rr = 1.0 / den;
+              const double rr = rcp_fast(den);
               x = ((l == 0) ? sdat[s][i][tid] : fma(-lo, x, sdat[s][i][tid])) * rr;
               if (keep_all || i == 0) sdat[s][i][tid] = x;
               if (l < a.nz - 1) {
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
           for (int i = 0; i < K; ++i) {
             const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
             const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
-            const double rr = 1.0 / fma(-lo, cprev, di);
+            const double rr = rcp_fast(fma(-lo, cprev, di));
             if (rec && i > 0) {
               xr = fma(-lo, xr, sdat[s][i][tid]) * rr;
               sdat[s][i][tid] = xr;
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
               const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
               const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
               const double dl = (l == 0) ? di : fma(-lo, cprev, di);
-              const double rr = 1.0 / dl;
+              const double rr = rcp_fast(dl);
               if (rec && i > 0) {
                 xr = fma(-lo, xr, sdat[s][i][tid]) * rr;
                 sdat[s][i][tid] = xr;
@@ -400,9 +403,16 @@ int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld,
   // ring stages (tuning key 26: 3 or 4; 4 lets the refill skip waiting for the
   // store issued just before, at 16 KB more shared memory per 256-mode CTA)
   const int S = (bwd_only || tuning(26) != 4) ? 3 : 4;
-  const size_t sm = sizeof(double) * (size_t)S * (K * BM + K * 12);
-  auto kern = BM == 128 ? (S == 4 ? thomas_tma_kernel<128, 4> : thomas_tma_kernel<128, 3>)
-                        : (S == 4 ? thomas_tma_kernel<BMAX, 4> : thomas_tma_kernel<BMAX, 3>);
+  // chunk shape (tuning key 30, one-call and mode-slab paths; bwd_only keeps the
+  // 8-level checkpoints its producers wrote): 1 = 16 levels, 3 stages;
+  // 2 = 16 levels, 2 stages
+  const int kc = bwd_only ? 0 : tuning(30);
+  const int KC = kc ? 16 : K, SS = kc == 2 ? 2 : S;
+  const size_t sm = sizeof(double) * (size_t)SS * (KC * BM + KC * 12);
+  auto kern = kc == 1 ? (BM == 128 ? thomas_tma_kernel<128, 3, 16> : thomas_tma_kernel<BMAX, 3, 16>)
+              : kc == 2 ? (BM == 128 ? thomas_tma_kernel<128, 2, 16> : thomas_tma_kernel<BMAX, 2, 16>)
+              : BM == 128 ? (S == 4 ? thomas_tma_kernel<128, 4, K> : thomas_tma_kernel<128, 3, K>)
+                          : (S == 4 ? thomas_tma_kernel<BMAX, 4, K> : thomas_tma_kernel<BMAX, 3, K>);
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 1, sms = 148, dev = 0;
   HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BM, sm));

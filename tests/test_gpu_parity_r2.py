@@ -240,6 +240,7 @@ def _one_call(shape, scheme, seed, knobs, lean=False):
         lib.hfb_set_tuning(23, 1)
         lib.hfb_set_tuning(26, 3)
         lib.hfb_set_tuning(28, 0)
+        lib.hfb_set_tuning(30, 0)
         lib.hfb_set_tuning(19, 1)
         lib.hfb_set_tuning(29, 2)
     return U.cpu().numpy(), (F, sk, prof, g)
@@ -251,13 +252,16 @@ def test_zsolve_variants_bitwise(cuda, shape):
     """The one-call z-solve's variants are bitwise equal: the 3-stage TMA ring
     with dense x' rows (key 23 = 0, key 26 = 3) against sparse x' (key 23, x'
     stored once per 8-level chunk and recomputed in the back substitution) and
-    the 4-stage ring (key 26 = 4) and 128-mode blocks (key 28 = 1); shapes with n_z below, at and just above a
+    the 4-stage ring (key 26 = 4), 128-mode blocks (key 28 = 1) and 16-level
+    chunks with 3 or 2 stages (key 30 = 1, 2); shapes with n_z below, at and just above a
     chunk, partial mode blocks, many blocks per CTA; the small-n_z shared-memory
     kernel is switched off (key 19)."""
     scheme = "cd4" if shape[2] % 2 else "6"
     ref, _ = _one_call(shape, scheme, 7, [(19, 0), (23, 0), (26, 3)])
     for knobs in ([(19, 0), (23, 1), (26, 3)], [(19, 0), (23, 1), (26, 4)],
-                  [(19, 0), (23, 0), (26, 4)], [(19, 0), (23, 1), (28, 1)]):
+                  [(19, 0), (23, 0), (26, 4)], [(19, 0), (23, 1), (28, 1)],
+                  [(19, 0), (23, 1), (30, 1)], [(19, 0), (23, 1), (30, 2)],
+                  [(19, 0), (23, 0), (30, 2)], [(19, 0), (23, 1), (30, 1), (28, 1)]):
         u, _ = _one_call(shape, scheme, 7, knobs)
         assert np.array_equal(u, ref), knobs
 
