@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
                   (unsigned long long)n;
               atomicMin(a.err, key);
             }
-            const double rr = 1.0 / den;
+            const double rr = rcp_fast(den);
             const double F = gb[phys(L, m)];
             xo[T * (h + i)] = ((l == 0) ? F : fma(-lo, xin[i], F)) * rr;
             if (l < nzt - 1) co[T * (h + i)] = up * rr;
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
                   (unsigned long long)n;
               atomicMin(a.err, key);
             }
-            const double rr = 1.0 / den;
+            const double rr = rcp_fast(den);
             const double F = L ? out[j].y : out[j].x;
             const double x = ((l == 0) ? F : fma(-lo, yx[L][j], F)) * rr;
             yx[L][j] = x;

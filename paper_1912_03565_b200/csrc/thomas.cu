@@ -25,7 +25,7 @@ __device__ __forceinline__ double eig(const double* __restrict__ co, double cx, 
   return fma(w0.x, cxy, fma(w0.y, cx, fma(w1.x, cy, w1.y)));
 }
 
-__device__ __forceinline__ double rcp(double d) { return 1.0 / d; }
+__device__ __forceinline__ double rcp(double d) { return rcp_fast(d); }
 
 __device__ __forceinline__ void latch(unsigned long long* err, long long l, long long m,
                                       long long n, long long ny_total, long long nx) {

@@ -207,7 +207,7 @@ __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, lo
                   (unsigned long long)n;
               atomicMin(a.err, key);
             }
-            const double rr = 1.0 / den;
+            const double rr = rcp_fast(den);
             x = ((l == 0) ? sdat[s][i][tid] : fma(-lo, x, sdat[s][i][tid])) * rr;
             sdat[s][i][tid] = x;
             if (l < a.nz - 1) {
@@ -226,7 +226,7 @@ __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, lo
           if (i < nl && l < a.nz - 1) {
             const double di = eig_c(co + i * 12 + 4, cxv, cyv, cxy);
             const double dl = (l == 0) ? di : fma(-eig_c(co + i * 12, cxv, cyv, cxy), cprev, di);
-            cprev = eig_c(co + i * 12 + 8, cxv, cyv, cxy) * (1.0 / dl);
+            cprev = eig_c(co + i * 12 + 8, cxv, cyv, cxy) * rcp_fast(dl);
             cb[i] = cprev;
           }
         }

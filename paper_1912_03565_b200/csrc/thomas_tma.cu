@@ -97,7 +97,10 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
       return a.bwd_only ? (task - task0) % S : task < nchunk ? task % S : (task - 1) % S;
     };
     auto needs_load = [&](int task) { return a.bwd_only || task != nchunk; };
-    constexpr int D = S - 1;  // prefetch distance in tasks
+    // prefetch distance in tasks: 2 (1 with two stages). The stage that task
+    // t + D fills was last used by task t + D - S: task t - 1 with 3 (or 2)
+    // stages, whose store is the last one committed; task t - 2 with 4.
+    constexpr int D = S >= 3 ? 2 : 1;
     if (tid == 0)
       for (int q = 0; q < D; ++q)
         if (task0 + q < ntask && needs_load(task0 + q)) issue(task0 + q, stage_of(task0 + q));
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(32) thomas_smem_kernel(TmaArgs a) {
           (unsigned long long)n;
       atomicMin(a.err, key);
     }
-    const double rr = 1.0 / den;
+    const double rr = rcp_fast(den);
     x = ((l == 0) ? sd[l * 32 + t] : fma(-lo, x, sd[l * 32 + t])) * rr;
     sd[l * 32 + t] = x;
     if (l < a.nz - 1) {
