@@ -1,2 +1,2 @@
-python -m pytest tests/test_gpu_parity_r2.py -x -q -k "zsolve" 2>&1 | grep -E "Error|assert|FAILED|knobs|passed|failed" | head -20
-python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+python bench.py > gpurun_out/bench3.json 2> gpurun_out/bench3.err; tail -c 300 gpurun_out/bench3.json
+for c in 1 2 3; do python tools/one_solve.py --cfg $c --reps 20 --time --stages; done
