@@ -208,6 +208,7 @@ extern "C" int hfb_plan_set_coefficients_z(hfb_plan* p, const double* table_re,
   const size_t nlev = (size_t)p->nz * 12;
   std::vector<double> buf(2 * nlev);
   scaled_table(table_im, nlev, buf.data());
+  p->zinv = 0;  // the complex z-solve keeps per-level weights
   if (!p->coef_i) HFB_CUDA(cudaMalloc(&p->coef_i, sizeof(double) * 2 * nlev));
   HFB_CUDA(cudaMemcpy(p->coef_i, buf.data(), sizeof(double) * 2 * nlev, cudaMemcpyHostToDevice));
   return HFB_OK;
@@ -217,7 +218,6 @@ extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const
                                          const double* cy, double thr) {
   if (!p || !table || !cx || !cy) return HFB_ERR_ARGUMENT;
   HFB_CUDA(cudaSetDevice(p->device));
-  if (p->have_coef) HFB_CUDA(cudaDeviceSynchronize());  // see hfb_plan_set_coefficients
   // kernels queued on any stream (torch side streams do not order against the
   // synchronous copies below) may still read the old table: let them finish
   if (p->have_coef) HFB_CUDA(cudaDeviceSynchronize());
@@ -236,6 +236,9 @@ extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const
   HFB_CUDA(cudaMemcpy(p->cy, cy, sizeof(double) * p->ny, cudaMemcpyHostToDevice));
   p->thr = thr;
   p->have_coef = 1;
+  p->zinv = 1;  // all levels' scaled weights equal (bitwise)
+  for (size_t e = 12; e < nlev && p->zinv; ++e)
+    if (std::memcmp(&buf[e], &buf[e % 12], sizeof(double)) != 0) p->zinv = 0;
   return HFB_OK;
 }
 

@@ -863,6 +863,7 @@ static int g_tune_s27_tile = 1;  // streamed 27-point kernels: planes staged in 
 static int g_tune_late = 2;  // DST passes: prefetch after the pre-processing (key 29; 2 = flat-row-store passes)
 static int g_tune_thomas_narrow = 0;  // TMA z-solve with 128-mode blocks (key 28)
 static int g_tune_thomas_kc = 0;  // TMA z-solve chunks (key 30: 0 = 8 levels, 1 = 16 levels 3 stages, 2 = 16 levels 2 stages)
+static int g_tune_zinv = 1;  // TMA z-solve: eigenvalues once per mode for z-invariant weights (key 31)
 static int g_tune_wave_dbg = 0;  // its measurement variants (key 22; wrong results for bit 1)
 
 template <int P, int E, int MODE>
@@ -1128,6 +1129,7 @@ int tuning(int key) {
     case 28: return g_tune_thomas_narrow;
     case 29: return g_tune_late;
     case 30: return g_tune_thomas_kc;
+    case 31: return g_tune_zinv;
     default: return 0;
   }
 }
@@ -1163,6 +1165,7 @@ void set_tuning(int key, int value) {
   if (key == 28) g_tune_thomas_narrow = value;
   if (key == 29) g_tune_late = value;
   if (key == 30) g_tune_thomas_kc = value;
+  if (key == 31) g_tune_zinv = value ? 1 : 0;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

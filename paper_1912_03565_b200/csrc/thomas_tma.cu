@@ -47,7 +47,13 @@ __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, 
 
 // KC levels per chunk (tuning key 30; 16 halves the chunk barriers and the
 // checkpoint traffic, at twice the shared memory per stage).
-template <int BM, int S, int KC>
+//
+// ZI: the weight table is the same on every level (a z-invariant operator, e.g.
+// constant k or the constant-coefficient convection-diffusion of cfg4; flagged
+// by hfb_plan_set_coefficients, tuning key 31). The three eigenvalues of each
+// mode are then computed once per block, with the same expressions (so the same
+// bits), and the chunks carry no weights.
+template <int BM, int S, int KC, bool ZI>
 __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
   constexpr int K = KC;
   extern __shared__ __align__(16) double dyn[];
@@ -76,10 +82,11 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
     auto issue = [&](int task, int s) {
       const int c = chunk_of(task);
       const int l0 = c * K, nl = min(K, a.nz - l0);
-      mbar_arrive_expect_tx(&bar[s], nl * rowbytes + (uint32_t)(nl * 12 * 8));
+      mbar_arrive_expect_tx(&bar[s], nl * rowbytes + (ZI ? 0u : (uint32_t)(nl * 12 * 8)));
       for (int i = 0; i < nl; ++i)
         bulk_g2s(&sdat[s][i][0], base + plane_of(l0 + i) * a.ps, rowbytes, &bar[s]);
-      bulk_g2s(&scoef[s][0], a.coef + (long long)l0 * 12, (uint32_t)(nl * 12 * 8), &bar[s]);
+      if (!ZI)
+        bulk_g2s(&scoef[s][0], a.coef + (long long)l0 * 12, (uint32_t)(nl * 12 * 8), &bar[s]);
     };
     const bool live = tid < cols;
     const int m = m0 + tid;
@@ -87,6 +94,12 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
     const double cyv = live ? __ldg(a.cy + a.m_off + m) : 0.0;
     const double cxy = cxv * cyv;
     double* ck = a.cpk + (long long)n * a.ld + m0 + tid;
+    double zl = 0.0, zd = 0.0, zu = 0.0;
+    if constexpr (ZI) {
+      zl = eig_s(a.coef, cxv, cyv, cxy);
+      zd = eig_s(a.coef + 4, cxv, cyv, cxy);
+      zu = eig_s(a.coef + 8, cxv, cyv, cxy);
+    }
 
     // The last forward chunk stays in its stage and is the first backward chunk
     // (no store, no reload), so stages run task % S forward and (task-1) % S
@@ -142,6 +155,10 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
       const int cidx = chunk_of(task);
       const int l0 = cidx * K, nl = min(K, a.nz - l0);
       const double* co = &scoef[s][0];
+      // the level's (lower, diagonal, upper) eigenvalues of this mode
+      auto EL = [&](int i) { return ZI ? zl : eig_s(co + i * 12, cxv, cyv, cxy); };
+      auto ED = [&](int i) { return ZI ? zd : eig_s(co + i * 12 + 4, cxv, cyv, cxy); };
+      auto EU = [&](int i) { return ZI ? zu : eig_s(co + i * 12 + 8, cxv, cyv, cxy); };
       // Interior chunks (all K levels present, not level 0, below the top
       // level) run a copy of the loops without the per-level guards, and note
       // a vanishing pivot as the chunk's first failing level (one select per
@@ -154,9 +171,9 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
           int bad = K;
 #pragma unroll
           for (int i = 0; i < K; ++i) {
-            const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
-            const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
-            const double up = eig_s(co + i * 12 + 8, cxv, cyv, cxy);
+            const double lo = EL(i);
+            const double di = ED(i);
+            const double up = EU(i);
             const double den = fma(-lo, c, di);
             bad = (fabs(den) < a.thr && bad == K) ? i : bad;
             const double rr = rcp_fast(den);
@@ -178,9 +195,9 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
           for (int i = 0; i < K; ++i) {
             if (i < nl) {
               const int l = l0 + i;
-              const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
-              const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
-              const double up = eig_s(co + i * 12 + 8, cxv, cyv, cxy);
+              const double lo = EL(i);
+              const double di = ED(i);
+              const double up = EU(i);
               const double den = (l == 0) ? di : fma(-lo, c, di);
               if (live && fabs(den) < a.thr) {
                 const unsigned long long key =
@@ -213,14 +230,14 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
         if (inner) {
 #pragma unroll
           for (int i = 0; i < K; ++i) {
-            const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
-            const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
+            const double di = ED(i);
+            const double lo = EL(i);
             const double rr = rcp_fast(fma(-lo, cprev, di));
             if (rec && i > 0) {
               xr = fma(-lo, xr, sdat[s][i][tid]) * rr;
               sdat[s][i][tid] = xr;
             }
-            cprev = eig_s(co + i * 12 + 8, cxv, cyv, cxy) * rr;
+            cprev = EU(i) * rr;
             cb[i] = cprev;
           }
 #pragma unroll
@@ -233,15 +250,15 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
           for (int i = 0; i < K; ++i) {
             const int l = l0 + i;
             if (i < nl && l < a.nz - 1) {
-              const double di = eig_s(co + i * 12 + 4, cxv, cyv, cxy);
-              const double lo = eig_s(co + i * 12, cxv, cyv, cxy);
+              const double di = ED(i);
+              const double lo = EL(i);
               const double dl = (l == 0) ? di : fma(-lo, cprev, di);
               const double rr = rcp_fast(dl);
               if (rec && i > 0) {
                 xr = fma(-lo, xr, sdat[s][i][tid]) * rr;
                 sdat[s][i][tid] = xr;
               }
-              cprev = eig_s(co + i * 12 + 8, cxv, cyv, cxy) * rr;
+              cprev = EU(i) * rr;
               cb[i] = cprev;
             }
           }
@@ -412,10 +429,19 @@ int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld,
   const int kc = bwd_only ? 0 : tuning(30);
   const int KC = kc ? 16 : K, SS = kc == 2 ? 2 : S;
   const size_t sm = sizeof(double) * (size_t)SS * (KC * BM + KC * 12);
-  auto kern = kc == 1 ? (BM == 128 ? thomas_tma_kernel<128, 3, 16> : thomas_tma_kernel<BMAX, 3, 16>)
-              : kc == 2 ? (BM == 128 ? thomas_tma_kernel<128, 2, 16> : thomas_tma_kernel<BMAX, 2, 16>)
-              : BM == 128 ? (S == 4 ? thomas_tma_kernel<128, 4, K> : thomas_tma_kernel<128, 3, K>)
-                          : (S == 4 ? thomas_tma_kernel<BMAX, 4, K> : thomas_tma_kernel<BMAX, 3, K>);
+  // z-invariant weights (key 31): eigenvalues once per mode block
+  const bool zi = p->zinv && tuning(31);
+  decltype(&thomas_tma_kernel<BMAX, 3, K, false>) kern;
+  if (zi)
+    kern = kc == 1 ? (BM == 128 ? thomas_tma_kernel<128, 3, 16, true> : thomas_tma_kernel<BMAX, 3, 16, true>)
+           : kc == 2 ? (BM == 128 ? thomas_tma_kernel<128, 2, 16, true> : thomas_tma_kernel<BMAX, 2, 16, true>)
+           : BM == 128 ? (S == 4 ? thomas_tma_kernel<128, 4, K, true> : thomas_tma_kernel<128, 3, K, true>)
+                       : (S == 4 ? thomas_tma_kernel<BMAX, 4, K, true> : thomas_tma_kernel<BMAX, 3, K, true>);
+  else
+    kern = kc == 1 ? (BM == 128 ? thomas_tma_kernel<128, 3, 16, false> : thomas_tma_kernel<BMAX, 3, 16, false>)
+           : kc == 2 ? (BM == 128 ? thomas_tma_kernel<128, 2, 16, false> : thomas_tma_kernel<BMAX, 2, 16, false>)
+           : BM == 128 ? (S == 4 ? thomas_tma_kernel<128, 4, K, false> : thomas_tma_kernel<128, 3, K, false>)
+                       : (S == 4 ? thomas_tma_kernel<BMAX, 4, K, false> : thomas_tma_kernel<BMAX, 3, K, false>);
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 1, sms = 148, dev = 0;
   HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BM, sm));

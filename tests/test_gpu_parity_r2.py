@@ -241,6 +241,7 @@ def _one_call(shape, scheme, seed, knobs, lean=False):
         lib.hfb_set_tuning(26, 3)
         lib.hfb_set_tuning(28, 0)
         lib.hfb_set_tuning(30, 0)
+        lib.hfb_set_tuning(31, 1)
         lib.hfb_set_tuning(19, 1)
         lib.hfb_set_tuning(29, 2)
     return U.cpu().numpy(), (F, sk, prof, g)
@@ -253,7 +254,8 @@ def test_zsolve_variants_bitwise(cuda, shape):
     with dense x' rows (key 23 = 0, key 26 = 3) against sparse x' (key 23, x'
     stored once per 8-level chunk and recomputed in the back substitution) and
     the 4-stage ring (key 26 = 4), 128-mode blocks (key 28 = 1) and 16-level
-    chunks with 3 or 2 stages (key 30 = 1, 2); shapes with n_z below, at and just above a
+    chunks with 3 or 2 stages (key 30 = 1, 2), and per-level eigenvalues for a
+    z-invariant table (key 31 = 0; the cd4 cases here are z-invariant); shapes with n_z below, at and just above a
     chunk, partial mode blocks, many blocks per CTA; the small-n_z shared-memory
     kernel is switched off (key 19)."""
     scheme = "cd4" if shape[2] % 2 else "6"
@@ -261,21 +263,24 @@ def test_zsolve_variants_bitwise(cuda, shape):
     for knobs in ([(19, 0), (23, 1), (26, 3)], [(19, 0), (23, 1), (26, 4)],
                   [(19, 0), (23, 0), (26, 4)], [(19, 0), (23, 1), (28, 1)],
                   [(19, 0), (23, 1), (30, 1)], [(19, 0), (23, 1), (30, 2)],
-                  [(19, 0), (23, 0), (30, 2)], [(19, 0), (23, 1), (30, 1), (28, 1)]):
+                  [(19, 0), (23, 0), (30, 2)], [(19, 0), (23, 1), (30, 1), (28, 1)],
+                  [(19, 0), (23, 1), (31, 0)], [(19, 0), (23, 1), (31, 0), (30, 2)]):
         u, _ = _one_call(shape, scheme, 7, knobs)
         assert np.array_equal(u, ref), knobs
 
 
-def test_zsolve_default_vs_oracle(cuda):
-    """The default z-solve (sparse x', warp-specialised) against the oracle at
-    a size that runs many blocks per CTA (1023^2 x 24, 6th order, k(z))."""
-    u, (F, sk, prof, g) = _one_call((1023, 1023, 24), "6", 11, [])
-    T = orc.weight_table("6", np.real(prof.k2), np.real(prof.k2_z), np.real(prof.k2_zz), 0.0,
-                         (g.h_x, g.h_y, g.h_z), g.n_z)
+@pytest.mark.parametrize("scheme", ["6", "cd4"])
+def test_zsolve_default_vs_oracle(cuda, scheme):
+    """The default z-solve (sparse x', guard-free interior chunks; for the
+    z-invariant cd4 table the eigenvalues once per mode) against the oracle at a
+    size that runs many blocks per CTA (1023^2 x 24; 6th order with k(z), cd4)."""
+    u, (F, sk, prof, g) = _one_call((1023, 1023, 24), scheme, 11, [])
+    T = orc.weight_table(scheme, np.real(prof.k2), np.real(prof.k2_z), np.real(prof.k2_zz),
+                         np.real(prof.gamma), (g.h_x, g.h_y, g.h_z), g.n_z)
     ref = orc.solve(F.cpu().numpy(), T, *orc.mode_cosines(g.n_x, g.n_y),
                     workers=orc.default_workers())
     err = rel_l2(u, ref)
-    print(f"default z-solve 1023^2 x 24 vs oracle: {err:.3e}")
+    print(f"default z-solve 1023^2 x 24 ({scheme}) vs oracle: {err:.3e}")
     assert err < TOL
 
 
