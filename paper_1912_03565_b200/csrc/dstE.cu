@@ -988,7 +988,10 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   // Measured at 1023^3 (same box): final pass 4.87 -> 4.62 ms, the other
   // passes 0.05-0.12 ms slower.
   a.late = tuning(29) == 1 || (tuning(29) == 2 && a.ustore);
-  a.indep = (k.mode == kRow || k.mode == kYB || (k.mode == kTload && M == 2048)) &&
+  // key 14 = 2: also decouple the groups of the M = 1024 column pass that stores
+  // into the user's array (flat-row stores; the final inverse-x pass)
+  a.indep = (k.mode == kRow || k.mode == kYB || (k.mode == kTload && M == 2048) ||
+             (k.mode == kTload && a.ustore && g_tune_indep == 2)) &&
             (a.tstore || a.ustore) && (g_tune_indep || k.mode == kYB) && T >= 32;
   if (k.mode == kYB && !a.indep) return HFB_ERR_ARGUMENT;
   CUtensorMap umap;
@@ -1149,7 +1152,7 @@ void set_tuning(int key, int value) {
   if (key == 11) g_tune_carry_ms = value;
   if (key == 12) g_tune_carry_cap = value;
   if (key == 13) g_tune_ustore = value ? 1 : 0;
-  if (key == 14) g_tune_indep = value ? 1 : 0;
+  if (key == 14) g_tune_indep = value;
   if (key == 16) g_tune_dmma = value ? 1 : 0;
   if (key == 17) g_tune_dense_max = value;
   if (key == 18) g_tune_dmma2d = value;
