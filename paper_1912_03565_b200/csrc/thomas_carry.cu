@@ -62,6 +62,7 @@ struct CarryArgs {
   unsigned epoch;
   unsigned long long timeout_ns;
   unsigned* xerr;
+  int zinv;  // z-invariant weights: eigenvalues once per block, no weight copies
 };
 
 __device__ __forceinline__ double eig_c(const double* co, double cx, double cy, double cxy) {
@@ -106,9 +107,10 @@ __device__ __forceinline__ void issue_chunk(const CarryArgs& a, double (*sdat)[K
                                             double (*scoef)[K * 12], uint64_t* bar,
                                             const double* base, uint32_t rowbytes, int c, int s) {
   const int l0 = c * K, nl = min(K, a.nzl - l0);
-  mbar_arrive_expect_tx(&bar[s], nl * rowbytes + (uint32_t)(nl * 12 * 8));
+  mbar_arrive_expect_tx(&bar[s], nl * rowbytes + (a.zinv ? 0u : (uint32_t)(nl * 12 * 8)));
   for (int i = 0; i < nl; ++i) bulk_g2s(&sdat[s][i][0], base + (long long)(l0 + i) * a.ps, rowbytes, &bar[s]);
-  bulk_g2s(&scoef[s][0], a.coef + (long long)(a.z0 + l0) * 12, (uint32_t)(nl * 12 * 8), &bar[s]);
+  if (!a.zinv)
+    bulk_g2s(&scoef[s][0], a.coef + (long long)(a.z0 + l0) * 12, (uint32_t)(nl * 12 * 8), &bar[s]);
 }
 }  // namespace
 
@@ -116,7 +118,7 @@ __device__ __forceinline__ void issue_chunk(const CarryArgs& a, double (*sdat)[K
 // (chunks descending); one launch per direction and rank. The CTA walks the
 // mode blocks cta, cta + ncta, ... (ascending: a block waits only on the same
 // block of the neighbour, which that rank's CTA reaches no later).
-template <int DIR, int S>
+template <int DIR, int S, bool ZI>
 __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, long long ncta) {
   extern __shared__ __align__(16) double dyn[];
   double(*sdat)[K][BM] = reinterpret_cast<double(*)[K][BM]>(dyn);
@@ -151,6 +153,14 @@ __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, lo
     const double cyv = live ? __ldg(a.cy + m) : 0.0;
     const double cxy = cxv * cyv;
     double* ck = a.cpk + (long long)n * a.ld + m0 + tid;
+    // z-invariant weights (thomas_tma.cu, tuning key 31): the mode's three
+    // eigenvalues once per block, the same expressions and bits
+    double zl = 0.0, zd = 0.0, zu = 0.0;
+    if constexpr (ZI) {
+      zl = eig_c(a.coef, cxv, cyv, cxy);
+      zd = eig_c(a.coef + 4, cxv, cyv, cxy);
+      zu = eig_c(a.coef + 8, cxv, cyv, cxy);
+    }
     if (tid == 0) {
       for (int t = 0; t < S - 1 && t < nchunk; ++t)
         issue_chunk(a, sdat, scoef, bar, base, rowbytes, chunk_of(t), t);
@@ -196,9 +206,9 @@ __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, lo
         for (int i = 0; i < K; ++i) {
           if (i < nl) {
             const int l = a.z0 + l0 + i;
-            const double lo = eig_c(co + i * 12, cxv, cyv, cxy);
-            const double di = eig_c(co + i * 12 + 4, cxv, cyv, cxy);
-            const double up = eig_c(co + i * 12 + 8, cxv, cyv, cxy);
+            const double lo = (ZI ? zl : eig_c(co + i * 12, cxv, cyv, cxy));
+            const double di = (ZI ? zd : eig_c(co + i * 12 + 4, cxv, cyv, cxy));
+            const double up = (ZI ? zu : eig_c(co + i * 12 + 8, cxv, cyv, cxy));
             const double den = (l == 0) ? di : fma(-lo, c, di);
             if (live && fabs(den) < a.thr) {
               const unsigned long long key =
@@ -224,9 +234,11 @@ __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, lo
         for (int i = 0; i < K; ++i) {
           const int l = a.z0 + l0 + i;
           if (i < nl && l < a.nz - 1) {
-            const double di = eig_c(co + i * 12 + 4, cxv, cyv, cxy);
-            const double dl = (l == 0) ? di : fma(-eig_c(co + i * 12, cxv, cyv, cxy), cprev, di);
-            cprev = eig_c(co + i * 12 + 8, cxv, cyv, cxy) * rcp_fast(dl);
+            const double di = (ZI ? zd : eig_c(co + i * 12 + 4, cxv, cyv, cxy));
+            const double lo = (ZI ? zl : eig_c(co + i * 12, cxv, cyv, cxy));
+            const double dl = (l == 0) ? di : fma(-lo, cprev, di);
+            const double rr = rcp_fast(dl);
+            cprev = (ZI ? zu : eig_c(co + i * 12 + 8, cxv, cyv, cxy)) * rr;
             cb[i] = cprev;
           }
         }
@@ -271,9 +283,9 @@ __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, lo
   }
 }
 
-template <int DIR, int S>
+template <int DIR, int S, bool ZI>
 __global__ void __launch_bounds__(BM, 4) thomas_carry_kernel(CarryArgs a) {
-  carry_body<DIR, S>(a, blockIdx.x, gridDim.x);
+  carry_body<DIR, S, ZI>(a, blockIdx.x, gridDim.x);
 }
 
 // Verification of the cross-rank protocol on ONE device: every virtual rank's
@@ -281,11 +293,11 @@ __global__ void __launch_bounds__(BM, 4) thomas_carry_kernel(CarryArgs a) {
 // rank r. Rank r's CTAs really spin on flags that rank r -/+ 1's CTAs release
 // while running concurrently — the live acquire/release path of the
 // multi-GPU run, without separate launches waiting on one another.
-template <int DIR, int S>
+template <int DIR, int S, bool ZI>
 __global__ void __launch_bounds__(BM, 4) thomas_carry_vranks_kernel(const CarryArgs* va, int per) {
   const int r = blockIdx.x / per;
   const CarryArgs a = va[r];
-  carry_body<DIR, S>(a, blockIdx.x - (long long)r * per, per);
+  carry_body<DIR, S, ZI>(a, blockIdx.x - (long long)r * per, per);
 }
 
 // ---------------------------------------------------------------------------
@@ -599,6 +611,7 @@ int launch_thomas_carry(hfb_plan* p, int dir, double* data, long long ld, int z0
   const int ms = tuning(11);
   a.timeout_ns = (unsigned long long)(ms > 0 ? ms : 30000) * 1000000ULL;
   a.xerr = p->xerr;
+  a.zinv = p->zinv && tuning(31);
   // tuning key 12: CTAs per SM (0 = occupancy, 3-stage ring). Capped at one or
   // two, the ring deepens to 6 stages (the HBM-bound sweep keeps its bytes in
   // flight) and the blocks come in more, shorter waves: the pipeline bubble of
@@ -606,8 +619,10 @@ int launch_thomas_carry(hfb_plan* p, int dir, double* data, long long ld, int z0
   const int cap = tuning(12);
   const int S = (cap == 1 || cap == 2) ? SMAX : 3;
   const size_t sm = sizeof(double) * (size_t)S * (K * BM + K * 12);
-  auto kern = dir ? (S == 3 ? thomas_carry_kernel<1, 3> : thomas_carry_kernel<1, SMAX>)
-                  : (S == 3 ? thomas_carry_kernel<0, 3> : thomas_carry_kernel<0, SMAX>);
+  auto kern = a.zinv ? (dir ? (S == 3 ? thomas_carry_kernel<1, 3, true> : thomas_carry_kernel<1, SMAX, true>)
+                            : (S == 3 ? thomas_carry_kernel<0, 3, true> : thomas_carry_kernel<0, SMAX, true>))
+                     : (dir ? (S == 3 ? thomas_carry_kernel<1, 3, false> : thomas_carry_kernel<1, SMAX, false>)
+                            : (S == 3 ? thomas_carry_kernel<0, 3, false> : thomas_carry_kernel<0, SMAX, false>));
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 1, sms = 148, dev = 0;
   HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BM, sm));
@@ -655,10 +670,12 @@ int launch_thomas_carry_vranks(hfb_plan* p, int dir, int nranks, double* const* 
     a.epoch = epoch;
     a.timeout_ns = (unsigned long long)(ms > 0 ? ms : 30000) * 1000000ULL;
     a.xerr = p->xerr;
-  }
+    a.zinv = p->zinv && tuning(31);
+    }
   constexpr int S = 3;
   const size_t sm = sizeof(double) * (size_t)S * (K * BM + K * 12);
-  auto kern = dir ? thomas_carry_vranks_kernel<1, S> : thomas_carry_vranks_kernel<0, S>;
+  auto kern = host[0].zinv ? (dir ? thomas_carry_vranks_kernel<1, S, true> : thomas_carry_vranks_kernel<0, S, true>)
+                           : (dir ? thomas_carry_vranks_kernel<1, S, false> : thomas_carry_vranks_kernel<0, S, false>);
   HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int per_sm = 1, sms = 148, dev = 0;
   HFB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BM, sm));

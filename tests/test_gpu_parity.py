@@ -267,10 +267,11 @@ def test_anisotropic_dense_path(golden, cuda):
     assert rel_l2(u, golden["aniso_U"]) < PARITY
 
 
-@pytest.mark.parametrize("cfg,planes", [(3, 511), (4, 64)])
+@pytest.mark.parametrize("cfg,planes", [(1, 31), (2, 127), (3, 511), (4, 64)])
 def test_large_configs_vs_oracle(cuda, cfg, planes):
-    """cfg3 at full size; cfg4 on a 64-plane slab of the full 1023^2 planes (the
-    oracle needs ~4 GB and minutes for the full 1023^3)."""
+    """cfg1, cfg2 and cfg3 at full size with their seeded RHS; cfg4 on a 64-plane
+    slab of the full 1023^2 planes here (its full 1023^3 is in
+    test_gpu_parity_r2.py)."""
     w = wl.workload(cfg)
     # a slab keeps the full grid's step h = 1/(n+1): z-extent (planes + 1) h
     g = w.grid if planes == w.n else hb.make_grid(
