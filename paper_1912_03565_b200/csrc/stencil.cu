@@ -671,9 +671,13 @@ static dim3 s27_grid(const hfb_plan* p, int lz, int rj) {
   return dim3((p->nx + 31) / 32, (p->ny + 8 * rj - 1) / (8 * rj), (p->nz + lz - 1) / lz);
 }
 
+// levels per CTA of the streamed kernels: at least enough to keep gridDim.z
+// within its 65535 limit
+static int s27_lz(const hfb_plan* p, int lz) { return std::max(lz, (p->nz + 65534) / 65535); }
+
 template <int KIND>
-static void s27_launch(const hfb_plan* p, int lz, const double* src, const double* rhs,
-                       double* out, uint32_t mask, double* partial, cudaStream_t st) {
+static int s27_launch(const hfb_plan* p, int lz, const double* src, const double* rhs,
+                      double* out, uint32_t mask, double* partial, cudaStream_t st) {
   const int rj = s27_rj();
   const double* raw = p->coef + 12LL * p->nz;
   if (tuning(27)) {  // shared-memory staged planes (32 x 32 tiles = the rj = 4 grid)
@@ -682,10 +686,10 @@ static void s27_launch(const hfb_plan* p, int lz, const double* src, const doubl
     auto kern = mask == kMask27 ? s27_tile_kernel<KIND, kMask27>
                 : mask == kMask19 ? s27_tile_kernel<KIND, kMask19>
                                   : s27_tile_kernel<KIND, 0>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    HFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     kern<<<s27_grid(p, lz, 4), 256, sm, st>>>(src, rhs, out, raw, p->nx, p->ny, p->nz, mask, lz,
                                               partial);
-    return;
+    return HFB_OK;
   }
   if (rj == 2)
     s27_stream_kernel<2, KIND><<<s27_grid(p, lz, 2), 256, 0, st>>>(
@@ -693,6 +697,7 @@ static void s27_launch(const hfb_plan* p, int lz, const double* src, const doubl
   else
     s27_stream_kernel<4, KIND><<<s27_grid(p, lz, 4), 256, 0, st>>>(
         src, rhs, out, raw, p->nx, p->ny, p->nz, mask, lz, partial);
+  return HFB_OK;
 }
 
 // Complex weights (complex k(z)): out = A ext or rhs - A ext with complex
@@ -884,10 +889,11 @@ extern "C" int hfb_apply27(hfb_plan* p, const double* ext, const double* rhs, do
   HFB_CUDA(cudaSetDevice(p->device));
   const int lz = tuning(20), ls = tuning(24);
   if (ls > 0) {
-    if (mode == 0)
-      s27_launch<0>(p, ls, ext, rhs, out, mask, nullptr, (cudaStream_t)stream);
-    else
-      s27_launch<1>(p, ls, ext, rhs, out, mask, nullptr, (cudaStream_t)stream);
+    const int rc = mode == 0 ? s27_launch<0>(p, s27_lz(p, ls), ext, rhs, out, mask, nullptr,
+                                             (cudaStream_t)stream)
+                             : s27_launch<1>(p, s27_lz(p, ls), ext, rhs, out, mask, nullptr,
+                                             (cudaStream_t)stream);
+    if (rc) return rc;
   } else if (lz > 0) {
     constexpr int TX = 64, TY = 4;
     dim3 grid((p->nx + TX - 1) / TX, (p->ny + TY - 1) / TY, (p->nz + lz - 1) / lz);
@@ -906,7 +912,7 @@ extern "C" int hfb_apply27(hfb_plan* p, const double* ext, const double* rhs, do
 // 148 x 8 persistent CTAs of the marching / gather / complex kernels.
 extern "C" int hfb_residual_partials(const hfb_plan* p) {
   if (!p) return 148 * 8;
-  const dim3 g = s27_grid(p, kS27ResLz, 2);  // the larger of the two tile counts
+  const dim3 g = s27_grid(p, s27_lz(p, kS27ResLz), 2);  // the larger of the two tile counts
   const long long tiles = (long long)g.x * g.y * g.z;
   return (int)std::max<long long>(tiles, 148 * 8);
 }
@@ -920,8 +926,10 @@ extern "C" int hfb_residual_sq(hfb_plan* p, const double* u, const double* F, do
   const int lz = tuning(20);
   const unsigned npart = (unsigned)hfb_residual_partials(p);
   if (tuning(24) > 0) {
-    const dim3 g = s27_grid(p, kS27ResLz, tuning(27) ? 4 : s27_rj());
-    s27_launch<2>(p, kS27ResLz, u, F, nullptr, mask, partial, (cudaStream_t)stream);
+    const int lr = s27_lz(p, kS27ResLz);
+    const dim3 g = s27_grid(p, lr, tuning(27) ? 4 : s27_rj());
+    const int rc = s27_launch<2>(p, lr, u, F, nullptr, mask, partial, (cudaStream_t)stream);
+    if (rc) return rc;
     const unsigned used = g.x * g.y * g.z;
     if (npart > used)
       HFB_CUDA(cudaMemsetAsync(partial + used, 0, sizeof(double) * (npart - used),
