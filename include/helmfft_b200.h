@@ -104,9 +104,27 @@ uint64_t hfb_launch_count(void);
  * one-call solve's wavefront-fused z-solve (forward elimination inside the
  * y-pass, back substitution inside the inverse y-pass, carries through L2 with
  * per-block level counters; fast layout, y-lines of 511 / 1023; bitwise equal;
- * 0, default: measured slower); key 22 = its measurement variants. Keys 5, 6, 9
- * and 21 keep measured-slower variants for A/B runs; keys 17 and 22 are
- * measurement knobs (22 bit 0 skips the waits: wrong results). */
+ * 0, default: measured slower); key 22 = its measurement variants;
+ * key 23 = the TMA z-solve stores x' only at the first level of each 8-level
+ * chunk and recomputes the rest in the back substitution (1, default: 27
+ * instead of 34 B/point) or every level (0); key 24 = levels per CTA of the
+ * plane-streamed 27-point apply / fold / residual (32, default; 0 = key 20's
+ * kernels); key 25 = their rows per warp without shared memory (2 or 4,
+ * default 4); key 26 = ring stages of the TMA z-solve (3, default, or 4);
+ * key 27 = the streamed 27-point kernels stage their planes in shared memory
+ * by cp.async (1, default) or read them from registers (0); key 28 = TMA
+ * z-solve blocks of 128 modes everywhere (1) or 256 where the slab is wide
+ * (0, default); key 29 = the DST passes prefetch the next batch after the
+ * current one's pre-processing: 1 every pass, 2 (default) the passes that
+ * store into the user's odd-pitch array, 0 none; key 30 = TMA z-solve chunks
+ * of 16 levels with 3 (1) or 2 (2) stages, or 8 levels (0, default); key 31 =
+ * z-invariant weight tables (every level's weights bitwise equal) get their
+ * eigenvalues once per mode block in the z-solves (1, default) or per level
+ * (0). Key 14 = 2 also decouples the groups of the flat-row-store column pass.
+ * Keys 5, 6, 9, 21, 26 = 4, 28 and 30 keep measured-slower variants for A/B
+ * runs; keys 17 and 22 are measurement knobs (22 bit 0 skips the waits: wrong
+ * results). All of them keep the bits of the default path except keys 0, 17,
+ * 18 and the residual order of 20 / 24 / 27. */
 void hfb_set_tuning(int key, int value);
 
 /* Plan for an (n_z, n_y, n_x) interior grid on CUDA device `device`.
