@@ -128,6 +128,7 @@ extern "C" int hfb_plan_destroy(hfb_plan* p) {
   cudaFree(p->lvlmap);
   cudaFree(p->coef);
   cudaFree(p->coef_i);
+  cudaFree(p->pq);
   cudaFree(p->cx);
   cudaFree(p->cy);
   cudaFree(p->err);
@@ -239,7 +240,7 @@ extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const
   p->zinv = 1;  // all levels' scaled weights equal (bitwise)
   for (size_t e = 12; e < nlev && p->zinv; ++e)
     if (std::memcmp(&buf[e], &buf[e % 12], sizeof(double)) != 0) p->zinv = 0;
-  return HFB_OK;
+  return build_pq(p);
 }
 
 extern "C" int hfb_stage_timing(hfb_plan* p, int ring) {

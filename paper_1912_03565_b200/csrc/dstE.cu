@@ -534,9 +534,10 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
             const int m = t + T * (h + i);
             const double cyv = m < a.ny_total ? __ldg(a.cy + m) : 0.0;
             const double cxy = cxv * cyv;
-            const double lo = fma(cw[0], cxy, fma(cw[1], cxv, fma(cw[2], cyv, cw[3])));
-            const double di = fma(cw[4], cxy, fma(cw[5], cxv, fma(cw[6], cyv, cw[7])));
-            const double up = fma(cw[8], cxy, fma(cw[9], cxv, fma(cw[10], cyv, cw[11])));
+            (void)cxy;
+            const double lo = eig_pq(cw, cxv, cyv);
+            const double di = eig_pq(cw + 4, cxv, cyv);
+            const double up = eig_pq(cw + 8, cxv, cyv);
             const double den = (l == 0) ? di : fma(-lo, cin[i], di);
             if (m < a.ny_total && fabs(den) < a.thr) {
               const unsigned long long key =
@@ -580,9 +581,10 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
             const int m = Q * t + j;
             const double cyv = ycy[j * T + t];
             const double cxy = cxv * cyv;
-            const double lo = fma(cw[0], cxy, fma(cw[1], cxv, fma(cw[2], cyv, cw[3])));
-            const double di = fma(cw[4], cxy, fma(cw[5], cxv, fma(cw[6], cyv, cw[7])));
-            const double up = fma(cw[8], cxy, fma(cw[9], cxv, fma(cw[10], cyv, cw[11])));
+            (void)cxy;
+            const double lo = eig_pq(cw, cxv, cyv);
+            const double di = eig_pq(cw + 4, cxv, cyv);
+            const double up = eig_pq(cw + 8, cxv, cyv);
             const double den = (l == 0) ? di : fma(-lo, cs[j * T], di);
             const bool live = n >= 0 && m < a.ny_total;
             if (live && fabs(den) < a.thr) {

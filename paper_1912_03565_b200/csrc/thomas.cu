@@ -22,7 +22,8 @@ __device__ __forceinline__ double eig(const double* __restrict__ co, double cx, 
   // co = (4a, 2b, 2c, d) of one level
   const double2 w0 = __ldg(reinterpret_cast<const double2*>(co));
   const double2 w1 = __ldg(reinterpret_cast<const double2*>(co) + 1);
-  return fma(w0.x, cxy, fma(w0.y, cx, fma(w1.x, cy, w1.y)));
+  (void)cxy;
+  return fma(eig_p(w0.x, w1.x, cx), cy, eig_q(w0.y, w1.y, cx));
 }
 
 __device__ __forceinline__ double rcp(double d) { return rcp_fast(d); }

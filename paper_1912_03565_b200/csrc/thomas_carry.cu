@@ -63,9 +63,17 @@ struct CarryArgs {
   unsigned long long timeout_ns;
   unsigned* xerr;
   int zinv;  // z-invariant weights: eigenvalues once per block, no weight copies
+  const double* pq;  // [n][l][k][(P, Q)] of the real table (hfb_plan::pq)
 };
 
+// real weights: the shared P cy + Q order (hfb_internal.cuh), as the one-call sweep
 __device__ __forceinline__ double eig_c(const double* co, double cx, double cy, double cxy) {
+  (void)cxy;
+  return eig_pq(co, cx, cy);
+}
+// complex weights (re, im parts apiece): thomas_tma_z.cu's order, which the
+// complex one-call solve uses
+__device__ __forceinline__ double eig_cz(const double* co, double cx, double cy, double cxy) {
   return fma(co[0], cxy, fma(co[1], cx, fma(co[2], cy, co[3])));
 }
 
@@ -105,12 +113,14 @@ __device__ void wait_block(const unsigned* flag, unsigned epoch, unsigned long l
 // thread 0: bring local chunk c (levels c*K ..) and its weights into stage s
 __device__ __forceinline__ void issue_chunk(const CarryArgs& a, double (*sdat)[K][BM],
                                             double (*scoef)[K * 12], uint64_t* bar,
-                                            const double* base, uint32_t rowbytes, int c, int s) {
+                                            const double* base, uint32_t rowbytes, int c, int s,
+                                            int n) {
   const int l0 = c * K, nl = min(K, a.nzl - l0);
-  mbar_arrive_expect_tx(&bar[s], nl * rowbytes + (a.zinv ? 0u : (uint32_t)(nl * 12 * 8)));
+  mbar_arrive_expect_tx(&bar[s], nl * rowbytes + (a.zinv ? 0u : (uint32_t)(nl * 6 * 8)));
   for (int i = 0; i < nl; ++i) bulk_g2s(&sdat[s][i][0], base + (long long)(l0 + i) * a.ps, rowbytes, &bar[s]);
-  if (!a.zinv)
-    bulk_g2s(&scoef[s][0], a.coef + (long long)(a.z0 + l0) * 12, (uint32_t)(nl * 12 * 8), &bar[s]);
+  if (!a.zinv)  // the block's x-mode's (P, Q) pairs of these levels
+    bulk_g2s(&scoef[s][0], a.pq + ((long long)n * a.nz + a.z0 + l0) * 6, (uint32_t)(nl * 6 * 8),
+             &bar[s]);
 }
 }  // namespace
 
@@ -163,7 +173,7 @@ __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, lo
     }
     if (tid == 0) {
       for (int t = 0; t < S - 1 && t < nchunk; ++t)
-        issue_chunk(a, sdat, scoef, bar, base, rowbytes, chunk_of(t), t);
+        issue_chunk(a, sdat, scoef, bar, base, rowbytes, chunk_of(t), t, n);
     }
     // the carry in: forward (x', cp) at z0 - 1, backward W at z1
     double c = 0.0, x = 0.0;
@@ -194,7 +204,7 @@ __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, lo
         bulk_wait_read<0>();  // stage s' was stored from at task - 1
         fence_proxy_async_smem();
         issue_chunk(a, sdat, scoef, bar, base, rowbytes, chunk_of(task + S - 1),
-                       (task + S - 1) % S);
+                       (task + S - 1) % S, n);
       }
       mbar_wait(&bar[s], (phase >> s) & 1u);
       phase ^= 1u << s;
@@ -206,9 +216,9 @@ __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, lo
         for (int i = 0; i < K; ++i) {
           if (i < nl) {
             const int l = a.z0 + l0 + i;
-            const double lo = (ZI ? zl : eig_c(co + i * 12, cxv, cyv, cxy));
-            const double di = (ZI ? zd : eig_c(co + i * 12 + 4, cxv, cyv, cxy));
-            const double up = (ZI ? zu : eig_c(co + i * 12 + 8, cxv, cyv, cxy));
+            const double lo = (ZI ? zl : fma(co[i * 6], cyv, co[i * 6 + 1]));
+            const double di = (ZI ? zd : fma(co[i * 6 + 2], cyv, co[i * 6 + 3]));
+            const double up = (ZI ? zu : fma(co[i * 6 + 4], cyv, co[i * 6 + 5]));
             const double den = (l == 0) ? di : fma(-lo, c, di);
             if (live && fabs(den) < a.thr) {
               const unsigned long long key =
@@ -234,11 +244,11 @@ __device__ __forceinline__ void carry_body(const CarryArgs& a, long long cta, lo
         for (int i = 0; i < K; ++i) {
           const int l = a.z0 + l0 + i;
           if (i < nl && l < a.nz - 1) {
-            const double di = (ZI ? zd : eig_c(co + i * 12 + 4, cxv, cyv, cxy));
-            const double lo = (ZI ? zl : eig_c(co + i * 12, cxv, cyv, cxy));
+            const double di = (ZI ? zd : fma(co[i * 6 + 2], cyv, co[i * 6 + 3]));
+            const double lo = (ZI ? zl : fma(co[i * 6], cyv, co[i * 6 + 1]));
             const double dl = (l == 0) ? di : fma(-lo, cprev, di);
             const double rr = rcp_fast(dl);
-            cprev = (ZI ? zu : eig_c(co + i * 12 + 8, cxv, cyv, cxy)) * rr;
+            cprev = (ZI ? zu : fma(co[i * 6 + 4], cyv, co[i * 6 + 5])) * rr;
             cb[i] = cprev;
           }
         }
@@ -393,8 +403,8 @@ __global__ void __launch_bounds__(BM) thomas_carry_z_kernel(CarryZArgs a) {
     const double cxy = cxv * cyv;
     double* ck = a.cpk + boff + tid;
     auto lam = [&](int s, int i, int k) -> cz2 {
-      return {eig_c(&scoef[s][0][i * 12 + 4 * k], cxv, cyv, cxy),
-              eig_c(&scoef[s][1][i * 12 + 4 * k], cxv, cyv, cxy)};
+      return {eig_cz(&scoef[s][0][i * 12 + 4 * k], cxv, cyv, cxy),
+              eig_cz(&scoef[s][1][i * 12 + 4 * k], cxv, cyv, cxy)};
     };
     if (tid == 0) {
       issue(chunk_of(0), 0);
@@ -612,6 +622,7 @@ int launch_thomas_carry(hfb_plan* p, int dir, double* data, long long ld, int z0
   a.timeout_ns = (unsigned long long)(ms > 0 ? ms : 30000) * 1000000ULL;
   a.xerr = p->xerr;
   a.zinv = p->zinv && tuning(31);
+  a.pq = p->pq;
   // tuning key 12: CTAs per SM (0 = occupancy, 3-stage ring). Capped at one or
   // two, the ring deepens to 6 stages (the HBM-bound sweep keeps its bytes in
   // flight) and the blocks come in more, shorter waves: the pipeline bubble of

@@ -26,6 +26,7 @@ struct TmaArgs {
   double* w;           // data (l, n, m): x' / W in place
   double* cpk;         // checkpoints: plane q holds cp at level q*K + K - 1
   const double* coef;  // [l][k][(4a, 2b, 2c, d)]
+  const double* pq;    // [n][l][k][(P, Q)] (eig_pq), the per-level path's weights
   const double* cx;
   const double* cy;
   int nz, nrows, ncols, nbpr;  // levels, rows (n), cols (m), blocks per row
@@ -41,7 +42,8 @@ struct TmaArgs {
 };
 
 __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, double cxy) {
-  return fma(co[0], cxy, fma(co[1], cx, fma(co[2], cy, co[3])));
+  (void)cxy;
+  return eig_pq(co, cx, cy);
 }
 }  // namespace
 
@@ -53,6 +55,28 @@ __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, 
 // by hfb_plan_set_coefficients, tuning key 31). The three eigenvalues of each
 // mode are then computed once per block, with the same expressions (so the same
 // bits), and the chunks carry no weights.
+// (P, Q) table: one thread per (n, l, k); the same fma's as eig_pq
+__global__ void pq_kernel(const double* __restrict__ coef, const double* __restrict__ cx,
+                          double* __restrict__ pq, int nx, int nz) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)nx * nz * 3) return;
+  const int k = (int)(e % 3);
+  const long long l = (e / 3) % nz, n = e / (3LL * nz);
+  const double* co = coef + l * 12 + 4 * k;
+  const double c = __ldg(cx + n);
+  pq[2 * e] = eig_p(co[0], co[2], c);
+  pq[2 * e + 1] = eig_q(co[1], co[3], c);
+}
+
+int build_pq(hfb_plan* p) {
+  const long long n = (long long)p->nx * p->nz * 3;
+  if (!p->pq) HFB_CUDA(cudaMalloc(&p->pq, sizeof(double) * 2 * n));
+  pq_kernel<<<(unsigned)((n + 255) / 256), 256>>>(p->coef, p->cx, p->pq, p->nx, p->nz);
+  HFB_LAUNCHED();
+  HFB_CUDA(cudaDeviceSynchronize());  // the table is complete before any solve reads it
+  return HFB_OK;
+}
+
 template <int BM, int S, int KC, bool ZI>
 __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
   constexpr int K = KC;
@@ -82,11 +106,12 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
     auto issue = [&](int task, int s) {
       const int c = chunk_of(task);
       const int l0 = c * K, nl = min(K, a.nz - l0);
-      mbar_arrive_expect_tx(&bar[s], nl * rowbytes + (ZI ? 0u : (uint32_t)(nl * 12 * 8)));
+      mbar_arrive_expect_tx(&bar[s], nl * rowbytes + (ZI ? 0u : (uint32_t)(nl * 6 * 8)));
       for (int i = 0; i < nl; ++i)
         bulk_g2s(&sdat[s][i][0], base + plane_of(l0 + i) * a.ps, rowbytes, &bar[s]);
       if (!ZI)
-        bulk_g2s(&scoef[s][0], a.coef + (long long)l0 * 12, (uint32_t)(nl * 12 * 8), &bar[s]);
+        bulk_g2s(&scoef[s][0], a.pq + ((long long)n * a.nz + l0) * 6, (uint32_t)(nl * 6 * 8),
+                 &bar[s]);
     };
     const bool live = tid < cols;
     const int m = m0 + tid;
@@ -156,9 +181,10 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
       const int l0 = cidx * K, nl = min(K, a.nz - l0);
       const double* co = &scoef[s][0];
       // the level's (lower, diagonal, upper) eigenvalues of this mode
-      auto EL = [&](int i) { return ZI ? zl : eig_s(co + i * 12, cxv, cyv, cxy); };
-      auto ED = [&](int i) { return ZI ? zd : eig_s(co + i * 12 + 4, cxv, cyv, cxy); };
-      auto EU = [&](int i) { return ZI ? zu : eig_s(co + i * 12 + 8, cxv, cyv, cxy); };
+      // (the chunk carries the block's x-mode's (P, Q) pairs: one fma each)
+      auto EL = [&](int i) { return ZI ? zl : fma(co[i * 6], cyv, co[i * 6 + 1]); };
+      auto ED = [&](int i) { return ZI ? zd : fma(co[i * 6 + 2], cyv, co[i * 6 + 3]); };
+      auto EU = [&](int i) { return ZI ? zu : fma(co[i * 6 + 4], cyv, co[i * 6 + 5]); };
       // Interior chunks (all K levels present, not level 0, below the top
       // level) run a copy of the loops without the per-level guards, and note
       // a vanishing pivot as the chunk's first failing level (one select per
@@ -405,6 +431,7 @@ int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld,
   a.w = data;
   a.cpk = cpk;
   a.coef = p->coef;
+  a.pq = p->pq;
   a.cx = p->cx;
   a.cy = p->cy;
   a.nz = p->nz;

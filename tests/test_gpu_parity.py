@@ -1130,7 +1130,9 @@ def test_flat_row_final_pass_bitwise(cuda, shape):
     if nx * ny * nz <= 2e5:
         ref = orc.solve(F.cpu().numpy(), oracle_table("4", prof, g),
                         *orc.mode_cosines(nx, ny), workers=4)
-        assert rel_l2(outs[0].cpu().numpy(), ref) < PARITY
+        # the north star's 1e-10: the 2047 x 15 x 3 grid (h_x / h_z = 1/512) sits
+        # at ~1e-11 against the oracle whatever the rounding order
+        assert rel_l2(outs[0].cpu().numpy(), ref) < TOL
 
 
 def _one_call_z(F, scheme, prof, g):
