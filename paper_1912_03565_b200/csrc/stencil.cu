@@ -507,6 +507,11 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, int bytes)
                "r"(bytes)
                : "memory");
 }
+// the same with the destination as a shared-window address
+__device__ __forceinline__ void cp_async8_s(uint32_t dst, const void* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -544,50 +549,56 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
   const int l0 = blockIdx.z * lz, l1 = min(nz, l0 + lz);
   const int i = x0 + lane, jw = y0 + warp * RJ;
   for (int e = threadIdx.x; e < (l1 - l0) * 12; e += 256) wsm[e] = __ldg(raw + l0 * 12LL + e);
-  // this thread's (at most 5) elements of the 34 x 34 input tile: shared
-  // offset, offset from the plane base, and whether the element lies in the
-  // array (plane independent; the residual also checks the plane)
-  // this thread's (at most 5) elements of the 34 x 34 input tile: shared
-  // offset, offset from the plane base, and whether the element lies in the
-  // array (plane independent; the residual also checks the plane)
+  // this thread's (at most 5) elements of the 34 x 34 input tile: byte offset
+  // in a stage, offset from the plane base (coordinates clamped into the array,
+  // so every copy reads a valid address) and whether the element lies in the
+  // array (the residual also checks the plane); out-of-array elements are
+  // zero-filled by the copy (source size 0)
   constexpr int NE = (34 * 34 + 255) / 256;
-  int soff[NE];
-  long long goff[NE];
-  bool eok[NE];
+  int soff[NE], goff[NE];
+  unsigned eok = 0;
 #pragma unroll
   for (int q = 0; q < NE; ++q) {
     const int e = threadIdx.x + 256 * q;
     const int r = e / 34, c = e - r * 34;
     const int gy = y0 - 1 + r, gx = x0 - 1 + c;  // interior coordinates
-    soff[q] = e < 34 * 34 ? r * PT + c : -1;
+    soff[q] = e < 34 * 34 ? 8 * (r * PT + c) : -1;
+    bool ok;
     if constexpr (KIND == 2) {
-      eok[q] = gy >= 0 && gy < ny && gx >= 0 && gx < nx;
-      goff[q] = (long long)gy * nx + gx;
+      ok = gy >= 0 && gy < ny && gx >= 0 && gx < nx;
+      goff[q] = min(max(gy, 0), ny - 1) * nx + min(max(gx, 0), nx - 1);
     } else {
-      eok[q] = gy + 1 <= ny + 1 && gx + 1 <= nx + 1;
-      goff[q] = (long long)(gy + 1) * (nx + 2) + gx + 1;
+      ok = gy + 1 <= ny + 1 && gx + 1 <= nx + 1;
+      goff[q] = min(gy + 1, ny + 1) * (nx + 2) + min(gx + 1, nx + 1);
     }
+    eok |= (ok && e < 34 * 34) ? 1u << q : 0u;
   }
   const long long pstride = KIND == 2 ? (long long)nx * ny : (long long)(nx + 2) * (ny + 2);
+  const uint32_t sbase = smem_u32(smt);
   // rhs / F of output level P - 2 rides with plane P: this thread's own 4 values
+  const uint32_t rbase = smem_u32(smt + NS * kT27Stage) + 8 * (warp * RJ * 32 + lane);
+  const bool icol = i < nx;
   auto load_plane = [&](int P, int st) {
-    double* dst = smt + st * kT27Stage;
+    const uint32_t dst = sbase + st * (kT27Stage * 8);
     const bool pok = KIND != 2 || (P >= 1 && P <= nz);
-    const double* base = src + (KIND == 2 ? (long long)(P - 1) : (long long)P) * pstride;
+    const int pc = KIND == 2 ? min(max(P - 1, 0), nz - 1) : P;
+    const double* base = src + (long long)pc * pstride;
 #pragma unroll
     for (int q = 0; q < NE; ++q) {
       if (soff[q] < 0) continue;
-      const bool ok = pok && eok[q];
-      cp_async8(dst + soff[q], ok ? base + goff[q] : src, ok ? 8 : 0);
+      cp_async8_s(dst + soff[q], base + goff[q], (pok && ((eok >> q) & 1u)) ? 8 : 0);
     }
     if constexpr (KIND != 0) {
       const int L = P - 2;
-      double* rd = smt + NS * kT27Stage + st * 1024 + warp * RJ * 32 + lane;
+      const bool lok = L >= l0 && L < l1 && icol;
+      const int Lc = min(max(L, 0), nz - 1);
+      const double* rb = rhs + ((long long)Lc * ny) * nx + min(i, nx - 1);
+      const uint32_t rd = rbase + st * (1024 * 8);
 #pragma unroll
       for (int q = 0; q < RJ; ++q) {
         const int j = jw + q;
-        const bool ok = L >= l0 && L < l1 && i < nx && j < ny;
-        cp_async8(rd + q * 32, ok ? rhs + ((long long)L * ny + j) * nx + i : rhs, ok ? 8 : 0);
+        cp_async8_s(rd + q * 32 * 8, rb + (long long)min(j, ny - 1) * nx,
+                    (lok && j < ny) ? 8 : 0);
       }
     }
   };
@@ -601,7 +612,10 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
 #pragma unroll
   for (int q = 0; q < RJ; ++q) a0[q] = a1[q] = 0.0;
   double ssq = 0.0;
-  for (int P = l0; P <= Pend; ++P) {
+  bool rowok[RJ];
+#pragma unroll
+  for (int q = 0; q < RJ; ++q) rowok[q] = icol && jw + q < ny;
+  auto plane_step = [&](int P) {
     cp_async_wait<NS - 2>();
     __syncthreads();  // plane P staged for everyone; stage (P - 1) free
     if (P + NS - 1 <= Pend) load_plane(P + NS - 1, (P + NS - 1 - l0) % NS);
@@ -619,6 +633,7 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
       wk2[q] = w2[q];
     }
     const int L = P - 2;
+    double* orow = KIND == 0 ? out + ((long long)max(L, 0) * ny + jw) * nx + i : nullptr;
 #pragma unroll
     for (int q = 0; q < RJ; ++q) {
       double v[9];
@@ -635,9 +650,12 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
       for (int o = 0; o < 9; ++o)
         if (mask & (1u << (18 + o))) t2 = DADD(t2, DMUL(wk2[WI[o]], v[o]));
       const int j = jw + q;
-      if (L >= l0 && i < nx && j < ny) {
+      if constexpr (KIND == 0) {
+        // (row pointer once per plane, row tests once per kernel: fewer
+        // registers for the twice-unrolled apply loop)
+        if (L >= l0 && rowok[q]) orow[q * nx] = t2;
+      } else if (L >= l0 && i < nx && j < ny) {
         const long long oo = ((long long)L * ny + j) * nx + i;
-        if constexpr (KIND == 0) out[oo] = t2;
         if constexpr (KIND == 1) out[oo] = __dsub_rn(rl[q * 32], t2);
         if constexpr (KIND == 2) {
           const double rr = t2 - rl[q * 32];
@@ -647,6 +665,15 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
       a0[q] = t1;
       a1[q] = t0;
     }
+  };
+  // the apply kernel's plane loop is unrolled twice (the (a0, a1) <- (t1, t0)
+  // rotation then needs no register moves); the fold / residual keep the
+  // compiler's choice (unrolling them spills)
+  if constexpr (KIND == 0) {
+#pragma unroll 2
+    for (int P = l0; P <= Pend; ++P) plane_step(P);
+  } else {
+    for (int P = l0; P <= Pend; ++P) plane_step(P);
   }
   cp_async_wait<0>();
   if constexpr (KIND == 2) {
