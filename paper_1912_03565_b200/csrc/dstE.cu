@@ -656,8 +656,11 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
 #pragma unroll
           for (int L = 0; L < 2; ++L) {
             const int u0 = L * a.N + Q * t - ha;
-            auto at = [&](int u) { const int q = u >> 4, cc = u & 15;
-                                   return ub + q * 16 + 2 * ((cc >> 1) ^ (q & 7)) + (cc & 1); };
+            // element u at box row u >> 4, 16-byte granule ((u >> 1) & 7) ^ (row & 7):
+            // with hp = u >> 1 that is slot 2 (hp ^ ((hp >> 3) & 7)) + (u & 1) (row -1
+            // included: the arithmetic shifts keep hp in [-8, -1] there)
+            auto at = [&](int u) { const int hp = u >> 1;
+                                   return ub + 2 * (hp ^ ((hp >> 3) & 7)) + (u & 1); };
             auto val = [&](int jj) { return L ? out[jj].y : out[jj].x; };
             const bool last = Q * t + Q > a.N;  // the segment holding the padding position
             if (!(u0 & 1)) {
