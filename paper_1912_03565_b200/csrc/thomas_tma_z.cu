@@ -20,6 +20,7 @@ constexpr int K = kThomasChunk;
 constexpr int S = 3;
 
 struct TmaZArgs {
+  int xsparse;          // x' stored once per chunk, recomputed (thomas_tma.cu, key 23)
   double* wr;           // real parts (l, n, m): x' / W in place
   double* wi;           // imaginary parts, same layout
   double* cpk;          // checkpoints: planes 2q (re) and 2q+1 (im) for chunk q
@@ -50,7 +51,7 @@ __device__ __forceinline__ cz zfms(cz a, cz b, cz c) {
 }
 __device__ __forceinline__ cz zrcp(cz d, double& n2) {
   n2 = fma(d.r, d.r, d.i * d.i);
-  const double inv = 1.0 / n2;
+  const double inv = rcp_fast(n2);  // bitwise 1.0 / n2 for normal n2
   return {d.r * inv, -d.i * inv};
 }
 }  // namespace
@@ -138,8 +139,10 @@ __global__ void __launch_bounds__(BM) thomas_tma_z_kernel(TmaZArgs a) {
             }
             const cz f = {sdat[s][0][i][tid], sdat[s][1][i][tid]};
             x = zmul((l == 0) ? f : zfms(f, lo, x), rr);
-            sdat[s][0][i][tid] = x.r;
-            sdat[s][1][i][tid] = x.i;
+            if (!a.xsparse || i == 0 || task == nchunk - 1) {
+              sdat[s][0][i][tid] = x.r;
+              sdat[s][1][i][tid] = x.i;
+            }
             if (l < a.nz - 1) {
               c = zmul(up, rr);
               if (i == K - 1 && live) {
@@ -158,14 +161,25 @@ __global__ void __launch_bounds__(BM) thomas_tma_z_kernel(TmaZArgs a) {
           cknext = {ck[(long long)(2 * (cidx - 2)) * a.ps],
                     ck[(long long)(2 * (cidx - 2) + 1) * a.ps]};
         cz cb[K];
+        // sparse x': recompute the chunk's rows from its stored first row with the
+        // forward's expressions (every chunk but the on-chip last one)
+        const bool rec = a.xsparse && task != nchunk;
+        cz xr = rec ? cz{sdat[s][0][0][tid], sdat[s][1][0][tid]} : cz{0.0, 0.0};
 #pragma unroll
         for (int i = 0; i < K; ++i) {
           const int l = l0 + i;
           if (i < nl && l < a.nz - 1) {
             const cz di = lam(s, i, 1);
-            const cz dl = (l == 0) ? di : zfms(di, lam(s, i, 0), cprev);
+            const cz lo = lam(s, i, 0);
+            const cz dl = (l == 0) ? di : zfms(di, lo, cprev);
             double n2;
-            cprev = zmul(lam(s, i, 2), zrcp(dl, n2));
+            const cz rr = zrcp(dl, n2);
+            if (rec && i > 0) {
+              xr = zmul(zfms({sdat[s][0][i][tid], sdat[s][1][i][tid]}, lo, xr), rr);
+              sdat[s][0][i][tid] = xr.r;
+              sdat[s][1][i][tid] = xr.i;
+            }
+            cprev = zmul(lam(s, i, 2), rr);
             cb[i] = cprev;
           }
         }
@@ -182,7 +196,8 @@ __global__ void __launch_bounds__(BM) thomas_tma_z_kernel(TmaZArgs a) {
       __syncthreads();
       if (tid == 0 && task != nchunk - 1) {
         fence_proxy_async_smem();
-        for (int i = 0; i < nl; ++i) {
+        const int nst = (a.xsparse && task < nchunk) ? 1 : nl;  // sparse x': level l0 only
+        for (int i = 0; i < nst; ++i) {
           const long long off = boff + (long long)(l0 + i) * a.ps;
           bulk_s2g(a.wr + off, &sdat[s][0][i][0], rowbytes);
           bulk_s2g(a.wi + off, &sdat[s][1][i][0], rowbytes);
@@ -200,6 +215,7 @@ int launch_thomas_tma_z(hfb_plan* p, double* re, double* im, double* cpk, long l
   if (p->nz < 1) return HFB_OK;
   if (!p->coef_i) return HFB_ERR_NO_COEFFICIENTS;
   TmaZArgs a;
+  a.xsparse = tuning(23);
   a.wr = re;
   a.wi = im;
   a.cpk = cpk;
