@@ -21,7 +21,14 @@ METRICS = {
     "smsp__inst_executed.sum": "inst",
     "sm__inst_executed_pipe_fp64.sum": "inst_fp64",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_conflicts",
+    # the on-chip bound of the DST passes: shared-memory wavefronts (128 B each,
+    # one per SM per clock at peak) and their share of that peak
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "smem_wavefronts",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_pct",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pct",
 }
+STALLS = ["barrier", "wait", "short_scoreboard", "long_scoreboard", "not_selected",
+          "no_instruction", "math_pipe_throttle", "dispatch_stall", "mio_throttle"]
 
 
 def main(path):
@@ -39,6 +46,13 @@ def main(path):
                 vals.append(f"{short}={r[i]}{units[i] if units[i] not in ('', '%') else ''}")
         print(name)
         print("   " + "  ".join(vals))
+        st = []
+        for k in STALLS:
+            m = f"smsp__average_warps_issue_stalled_{k}_per_issue_active.ratio"
+            if m in hdr and r[hdr.index(m)]:
+                st.append(f"{k}={float(r[hdr.index(m)]):.2f}")
+        if st:
+            print("   stalls/issue: " + "  ".join(st))
 
 
 if __name__ == "__main__":
