@@ -66,6 +66,56 @@ def device_tensor(x, device=None):
     return x.contiguous()
 
 
+def device_parts(x, copy=False):
+    """CUDA tensor -> its real parts for the kernels: [re] for float64, [re, im]
+    for complex128 (torch stores complex interleaved; the kernels take split
+    planes, so the two parts are new contiguous tensors). copy=True also gives
+    a float64 tensor a private copy (operators that must not touch the caller's
+    field)."""
+    torch = _torch()
+    if not x.is_cuda:
+        raise NativeUnavailableError("device fields must live on a CUDA device")
+    if x.dtype == torch.complex128:
+        return [x.real.contiguous(), x.imag.contiguous()]
+    if x.dtype != torch.float64:
+        raise TypeError(f"device fields must be float64 or complex128, got {x.dtype}")
+    t = x.contiguous()
+    return [t.clone() if copy and t.data_ptr() == x.data_ptr() else t]
+
+
+def join_device(parts, like):
+    """Inverse of device_parts: complex128 when the caller's field is complex or
+    the result gained an imaginary part (complex k(z), complex boundary data)."""
+    torch = _torch()
+    if like.dtype == torch.complex128 or len(parts) > 1:
+        im = parts[1] if len(parts) > 1 else torch.zeros_like(parts[0])
+        return torch.complex(parts[0], im)
+    return parts[0]
+
+
+def store_device(dst, parts):
+    """Write real parts back into the caller's CUDA tensor (in-place operators)."""
+    torch = _torch()
+    if dst.dtype == torch.complex128:
+        dst.real.copy_(parts[0])
+        if len(parts) > 1:
+            dst.imag.copy_(parts[1])
+        else:
+            dst.imag.zero_()
+    elif parts[0].data_ptr() != dst.data_ptr() or not dst.is_contiguous():
+        dst.copy_(parts[0])
+
+
+def apply_inplace(x, fn):
+    """Run an in-place real operator on every real part of the CUDA tensor x and
+    store the results in x (also for non-contiguous views, whose kernel input is
+    a contiguous copy)."""
+    parts = device_parts(x)
+    for p in parts:
+        fn(p)
+    store_device(x, parts)
+
+
 def join_parts(parts, like):
     """Inverse of real_parts: rebuild an array of the caller's dtype."""
     if len(parts) == 1:

@@ -238,7 +238,7 @@ def build_rhs(scheme, source: SourceSpec, profile: CoefficientProfile, grid: Gri
         outs = None
     if outs is not None:
         if keep_on_device:
-            raise NotImplementedError("complex sources cannot stay on the real device path")
+            return Field3D(dv.join_device(outs, outs[0]))
         return Field3D(dv.download(outs[0]) + 1j * dv.download(outs[1]))
     outs = []
     with plan.lock:
@@ -264,9 +264,7 @@ def build_rhs(scheme, source: SourceSpec, profile: CoefficientProfile, grid: Gri
                                                 ptr(out), st), "rhs_convdiff")
             outs.append(out)
     if keep_on_device:
-        if len(outs) > 1:
-            raise NotImplementedError("complex sources cannot stay on the real device path")
-        return Field3D(outs[0])
+        return Field3D(dv.join_device(outs, outs[0]))
     parts = [dv.download(o) for o in outs]
     return Field3D(parts[0] if len(parts) == 1 else parts[0] + 1j * parts[1])
 
@@ -310,15 +308,13 @@ def _apply_parts(ext_parts, rhs_parts, scheme, profile, grid, mode, device):
 
 def _parts_of(values, device):
     if dv.is_tensor(values):
-        return [dv.device_tensor(values)]
+        return dv.device_parts(values)
     return dv.upload_parts(values, device)
 
 
 def _result(outs, like):
     if dv.is_tensor(like):
-        if len(outs) > 1:
-            raise NotImplementedError("complex results (complex k(z)) need numpy fields")
-        return Field3D(outs[0])
+        return Field3D(dv.join_device(outs, like))
     return Field3D(dv.download_parts(outs, like))
 
 
@@ -351,8 +347,6 @@ def fold_dirichlet(rhs: Field3D, boundary: BoundaryData, scheme, profile: Coeffi
     ext_parts = _parts_of(box, device)
     rhs_parts = _parts_of(values, device)
     outs = _apply_parts(ext_parts, rhs_parts, scheme, profile, grid, 1, device)
-    if dv.is_tensor(values) and len(outs) > 1:
-        raise NotImplementedError("complex boundary data on a real device field")
     return _result(outs, values)
 
 

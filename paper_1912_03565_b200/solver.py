@@ -540,8 +540,10 @@ def solve_discrete(rhs: Field3D, boundary: BoundaryData, scheme, profile: Coeffi
     with plan.lock:
         device_coefficients(plan, scheme, profile, grid)
         if on_device:
-            work = fold_dirichlet(Field3D(values), boundary, scheme, profile, grid).values
-            parts = [dv.device_tensor(work)]
+            # float64 or complex128 CUDA tensors: private real parts (the caller's
+            # field is never modified), then the fold on the device
+            parts = fold_device_parts(dv.device_parts(values, copy=True), boundary, scheme,
+                                      profile, grid, device)
         else:
             # host arrays: pipelined pinned upload of the caller's array (never
             # modified), then the Dirichlet fold on the device (assembly.py:258-274)
@@ -554,15 +556,11 @@ def solve_discrete(rhs: Field3D, boundary: BoundaryData, scheme, profile: Coeffi
         clock = _EventClock(torch, device)
         transform_s = exchange_s = tridiag_s = 0.0
         if isinstance(config.mode, Partitioned) and config.transport_factory is not None:
-            if on_device and plan.complex_coef:
-                raise NotImplementedError("complex k(z) needs numpy (complex) fields")
             if plan.complex_coef:
                 while len(parts) < 2:
                     parts.append(torch.zeros_like(parts[0]))
             transform_s, exchange_s, tridiag_s = _solve_transport(plan, parts, grid, config)
         elif plan.complex_coef:
-            if on_device:
-                raise NotImplementedError("complex k(z) needs numpy (complex) fields")
             while len(parts) < 2:
                 parts.append(torch.zeros_like(parts[0]))
             transform_s, exchange_s, tridiag_s = _solve_z_device(plan, parts[0], parts[1],
@@ -575,7 +573,7 @@ def solve_discrete(rhs: Field3D, boundary: BoundaryData, scheme, profile: Coeffi
                 tridiag_s += tri
         plan.fetch_status()
     if on_device:
-        out = Field3D(parts[0])
+        out = Field3D(dv.join_device(parts, values))
     else:
         out = Field3D(dv.download_parts(parts, values))
     timings = PhaseTimings(setup_s=setup_s, transform_s=transform_s, exchange_s=exchange_s,

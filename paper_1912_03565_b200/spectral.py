@@ -94,9 +94,10 @@ def dst_lines(values, axis: int):
     (strided columns), which covers every use in the reference.
     """
     if dv.is_tensor(values):
-        t = dv.device_tensor(values).clone()
-        _dst_lines_tensor(t, axis)
-        return t
+        parts = dv.device_parts(values, copy=True)
+        for t in parts:
+            _dst_lines_tensor(t, axis)
+        return dv.join_device(parts, values)
     arr = np.asarray(values)
     parts = _apply_host(arr, lambda t: _dst_lines_tensor(t, axis))
     return dv.join_parts(parts, arr)
@@ -124,9 +125,10 @@ def dst2d(plan: TransformPlan, plane):
     if shape != (plan.n_y, plan.n_x):
         raise ValueError(f"plane shape {shape} != plan ({plan.n_y}, {plan.n_x})")
     if dv.is_tensor(plane):
-        t = dv.device_tensor(plane).clone()
-        _stack(t.view(1, plan.n_y, plan.n_x), 0, 1)
-        return t
+        parts = dv.device_parts(plane, copy=True)
+        for t in parts:
+            _stack(t.view(1, plan.n_y, plan.n_x), 0, 1)
+        return dv.join_device(parts, plane)
     arr = np.asarray(plane)
     parts = _apply_host(arr.reshape(1, plan.n_y, plan.n_x), lambda t: _stack(t, 0, 1))
     return dv.join_parts([p.reshape(shape) for p in parts], arr)
@@ -142,7 +144,7 @@ def dst2d_reference(plan: TransformPlan, plane):
     sx = torch.from_numpy(plan.dense_kernel(plan.n_x)).to(dev)
     sy = torch.from_numpy(plan.dense_kernel(plan.n_y)).to(dev)
     if dv.is_tensor(plane):
-        return sy @ dv.device_tensor(plane) @ sx
+        return dv.join_device([sy @ p @ sx for p in dv.device_parts(plane)], plane)
     arr = np.asarray(plane)
     parts = [dv.download(sy @ dv.upload(p, dev) @ sx) for p in dv.real_parts(arr)]
     return dv.join_parts(parts, arr)
@@ -160,7 +162,7 @@ def transform_stack(plan: TransformPlan, field3d, plane_range: Optional[tuple] =
     if start == stop:
         return
     if dv.is_tensor(values):
-        _stack(dv.device_tensor(values), start, stop)
+        dv.apply_inplace(values, lambda t: _stack(t, start, stop))
         return
     sub = values[start:stop]
     parts = _apply_host(sub, lambda t: _stack(t, 0, stop - start))
@@ -175,7 +177,7 @@ def transform_lines_x(field3d, y_range: tuple) -> None:
         return
     nz, ny, nx = values.shape
     if dv.is_tensor(values):
-        _lines_x(dv.device_tensor(values), nz, ny, nx, start, stop)
+        dv.apply_inplace(values, lambda t: _lines_x(t, nz, ny, nx, start, stop))
         return
     parts = _apply_host(values, lambda t: _lines_x(t, nz, ny, nx, start, stop))
     dv.write_back(values, parts)
@@ -189,7 +191,7 @@ def transform_lines_y(field3d, x_range: tuple) -> None:
         return
     nz, ny, nx = values.shape
     if dv.is_tensor(values):
-        _lines_y(dv.device_tensor(values), nz, ny, nx, start, stop)
+        dv.apply_inplace(values, lambda t: _lines_y(t, nz, ny, nx, start, stop))
         return
     parts = _apply_host(values, lambda t: _lines_y(t, nz, ny, nx, start, stop))
     dv.write_back(values, parts)

@@ -134,12 +134,21 @@ def solve_slab(values, scheme, profile: CoefficientProfile, grid: Grid3D,
         return
     if tuple(values.shape) != (grid.n_z, values.shape[1], grid.n_x):
         raise ValueError(f"slab shape {tuple(values.shape)} does not match the grid")
+    complex_table = is_complex_table(coefficient_table(scheme, profile, grid))
     if dv.is_tensor(values):
-        _slab_device(dv.device_tensor(values), scheme, profile, grid, m_start)
+        parts = dv.device_parts(values)
+        if complex_table:
+            if len(parts) < 2:
+                raise TypeError("complex k(z) needs a complex slab")
+            _slab_device_z(parts[0], parts[1], scheme, profile, grid, m_start)
+        else:
+            for t in parts:
+                _slab_device(t, scheme, profile, grid, m_start)
+        dv.store_device(values, parts)
         return
     torch = dv._torch()
     dev = torch.device("cuda", torch.cuda.current_device())
-    if is_complex_table(coefficient_table(scheme, profile, grid)):
+    if complex_table:
         if not np.iscomplexobj(values):
             raise TypeError("complex k(z) needs a complex slab")
         tr = dv.upload(np.ascontiguousarray(values.real), dev)
@@ -167,7 +176,8 @@ def solve_all(transformed_rhs, scheme, profile: CoefficientProfile, grid: Grid3D
     if start == stop:
         return
     if dv.is_tensor(values):
-        sub = dv.device_tensor(values)[:, start:stop, :].contiguous()
+        dv.device_parts(values[:1, :1, :1])  # CUDA float64 / complex128 check
+        sub = values[:, start:stop, :].contiguous()
         solve_slab(sub, scheme, profile, grid, m_start=start)
         values[:, start:stop, :] = sub
         return

@@ -1376,3 +1376,67 @@ def test_carry_ipc_two_processes_one_gpu(cuda, world, cplx):
     solve1 = _one_call_z if cplx else _one_call
     ref = solve1(F, hb.SchemeKind.FOURTH_ORDER, _ipc_profile(g, cplx), g)
     assert np.array_equal(U, ref.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["z4", "zb"])
+def test_complex_k_on_device_tensors(golden, cuda, name):
+    """complex128 CUDA tensors through the drop-in (round-1 verdict: complex k(z)
+    with device fields raised): solve_discrete, fold_dirichlet, residual_l2 and
+    apply_stencil return complex CUDA tensors equal to the numpy path's results,
+    and the caller's tensor is not modified."""
+    import torch
+    g, prof, scheme, F, bnd = z_inputs(golden, name)
+    Ft = torch.from_numpy(np.ascontiguousarray(F, dtype=complex)).to(cuda)
+    keep = Ft.clone()
+    ut, t = hb.solve_discrete(hb.Field3D(Ft), bnd, scheme, prof, g)
+    assert ut.values.is_cuda and ut.values.dtype == torch.complex128
+    assert torch.equal(Ft, keep)
+    u, _ = hb.solve_discrete(hb.Field3D(F), bnd, scheme, prof, g)
+    assert np.array_equal(ut.values.cpu().numpy(), u.values)
+    assert rel_l2(u.values, golden[f"{name}_U"]) < PARITY
+    assert t.transform_s > 0 and t.tridiag_s > 0
+    Fft = hb.fold_dirichlet(hb.Field3D(Ft), bnd, scheme, prof, g)
+    Ff = hb.fold_dirichlet(hb.Field3D(F), bnd, scheme, prof, g)
+    assert Fft.values.is_cuda
+    assert np.array_equal(Fft.values.cpu().numpy(), np.asarray(Ff.values, dtype=complex))
+    assert hb.residual_l2(ut, Fft, scheme, prof, g) < 1e-11 * np.linalg.norm(Ff.values)
+    Au = hb.apply_stencil(ut, bnd, scheme, prof, g)
+    assert Au.values.is_cuda and rel_l2(Au.values.cpu().numpy(), F) < 1e-12
+
+
+def test_real_k_complex_device_tensor_and_stage_operators(cuda):
+    """A complex128 CUDA rhs with a real table is two real solves (bitwise the
+    numpy path); the in-place stage operators (transform_stack, solve_all,
+    transform_lines_x/y) work on complex and on non-contiguous CUDA views."""
+    import torch
+    w = wl.workload(1)
+    g = w.grid
+    rng = np.random.default_rng(11)
+    F = rng.uniform(-1, 1, g.shape) + 1j * rng.uniform(-1, 1, g.shape)
+    Ft = torch.from_numpy(F).to(cuda)
+    ut, _ = hb.solve_discrete(hb.Field3D(Ft), hb.BoundaryData.zero(), w.scheme, w.profile, g)
+    u, _ = hb.solve_discrete(hb.Field3D(F), hb.BoundaryData.zero(), w.scheme, w.profile, g)
+    assert ut.values.dtype == torch.complex128
+    assert np.array_equal(ut.values.cpu().numpy(), u.values)
+    plan = hb.make_plan(g.n_x, g.n_y)
+    a = F.copy()
+    hb.transform_stack(plan, a)
+    at = Ft.clone()
+    hb.transform_stack(plan, at)
+    assert np.array_equal(at.cpu().numpy(), a)
+    hb.solve_all(a, w.scheme, w.profile, g)
+    hb.solve_all(at, w.scheme, w.profile, g)
+    assert np.array_equal(at.cpu().numpy(), a)
+    # a non-contiguous float64 view (every other plane of a bigger tensor) is
+    # transformed in place, not in a discarded copy
+    big = torch.from_numpy(np.ascontiguousarray(
+        np.stack([F.real, F.imag], axis=1).reshape(2 * g.n_z, g.n_y, g.n_x))).to(cuda)
+    view = big[::2]
+    assert not view.is_contiguous()
+    hb.transform_lines_x(view, (0, g.n_y))
+    hb.transform_lines_y(view, (0, g.n_x))
+    ref = F.real.copy()
+    hb.transform_lines_x(ref, (0, g.n_y))
+    hb.transform_lines_y(ref, (0, g.n_x))
+    assert np.array_equal(view.cpu().numpy(), ref)
+    assert np.array_equal(big[1::2].cpu().numpy(), F.imag)
