@@ -582,7 +582,7 @@ def emit(line):
     if _STDOUT_FD is not None:
         os.write(_STDOUT_FD, (json.dumps(line) + "\n").encode())
     else:
-        emit(line)
+        print(json.dumps(line), flush=True)
 
 
 def self_launch(args):
