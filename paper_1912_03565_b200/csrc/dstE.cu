@@ -103,6 +103,7 @@ struct StreamArgs {
   int dbg;  // measurement only (tuning key 22): 1 no waits, 2 acq_rel fences, 4 no fences
   int late;               // issue the next batch's prefetch after this batch's pre-processing
                           // (tuning key 29) instead of before waiting for this batch
+  int gshift;             // log2(G) when G is a power of two, else -1
   long long per;          // batches per CTA (one contiguous run), 0 = interleaved
   int run;                // > 1: interleaved runs of `run` consecutive batches
 };
@@ -131,8 +132,17 @@ __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long
     b = blockIdx.x + it * gridDim.x;
   }
   if (b >= (long long)a.nz * a.G) return false;
-  plane = a.desc ? a.z0 + a.nz - 1 - b / a.G : a.z0 + b / a.G;
-  g = a.g0 + (int)(b % a.G);
+  long long q;
+  int r;
+  if (a.gshift >= 0) {  // G a power of two (every power-of-two line count)
+    q = b >> a.gshift;
+    r = (int)b & (a.G - 1);
+  } else {
+    q = b / a.G;
+    r = (int)(b % a.G);
+  }
+  plane = a.desc ? a.z0 + a.nz - 1 - q : a.z0 + q;
+  g = a.g0 + r;
   return true;
 }
 
@@ -419,10 +429,29 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         if (a.late) prefetch_next(it);
       } else {
         const double2* bx = reinterpret_cast<const double2*>(gbuf(s, 0));
-        dstE_pre<P, E>(v, c.sn, etw, t, [&](int e) -> double2 {
-          const int gr = ((e + M - 1) & (M - 1)) * a.NF + f;
-          return bx[gr ^ ((gr >> 3) & (a.NF - 1))];
-        });
+        if (E == 16 && T >= 8 && a.NF == 2) {
+          // granule 2 pos + f of position pos = e - 1, XOR term bit 2 of pos: for
+          // e = t + T i that bit is bit 2 of t - 1, for e = M - t - T i bit 2 of
+          // M - 1 - t (T i leaves bit 2 alone): two per-thread bases plus
+          // compile-time offsets +-2 T i (the same slots as the generic form
+          // below; e = 0 and e = M keep it — their values are selected away)
+          const int lo = t - 1, hi = M - 1 - t;
+          const double2* pl = bx + 2 * lo + (f ^ ((lo >> 2) & 1));
+          const double2* ph = bx + 2 * hi + (f ^ ((hi >> 2) & 1));
+          dstE_pre_idx<P, E>(v, c.sn, etw, t, [&](int i, bool mirror) -> double2 {
+            if (i == 0) {  // e = t (t = 0: unused) or e = M - t (t = 0: unused)
+              const int e = mirror ? M - t : t;
+              const int gr = ((e + M - 1) & (M - 1)) * 2 + f;
+              return bx[gr ^ ((gr >> 3) & 1)];
+            }
+            return mirror ? ph[-2 * T * i] : pl[2 * T * i];
+          });
+        } else {
+          dstE_pre<P, E>(v, c.sn, etw, t, [&](int e) -> double2 {
+            const int gr = ((e + M - 1) & (M - 1)) * a.NF + f;
+            return bx[gr ^ ((gr >> 3) & (a.NF - 1))];
+          });
+        }
         __syncthreads();  // the box interleaves all groups' lines
         if (a.late) prefetch_next(it);
       }
@@ -466,9 +495,25 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
       }
       const double* r0 = gb + meta.delta[s][2 * f] - 1;  // a_e at r0[e]
       const double* r1 = gb + a.rowslot + meta.delta[s][2 * f + 1] - 1;
-      dstE_pre<P, E>(v, c.sn, etw, t, [&](int e) -> double2 {
-        return make_double2(v0 ? r0[e] : 0.0, v1 ? r1[e] : 0.0);
-      });
+      if constexpr (T >= 32) {
+        // (groups of whole warps: the group barrier below is legal in a branch
+        // that is uniform per group)
+        if (!(v0 && v1)) {
+          // an absent line (the odd line out at the end of a plane) is a staged
+          // row of zeros, so the loads below carry no per-element select
+          if (!v0)
+            for (int e = 1 + t; e <= a.N; e += T) const_cast<double*>(r0)[e] = 0.0;
+          if (!v1)
+            for (int e = 1 + t; e <= a.N; e += T) const_cast<double*>(r1)[e] = 0.0;
+          group_sync<T>(f);
+        }
+        dstE_pre<P, E>(v, c.sn, etw, t,
+                       [&](int e) -> double2 { return make_double2(r0[e], r1[e]); });
+      } else {
+        dstE_pre<P, E>(v, c.sn, etw, t, [&](int e) -> double2 {
+          return make_double2(v0 ? r0[e] : 0.0, v1 ? r1[e] : 0.0);
+        });
+      }
       group_sync<T>(f);  // staged rows consumed: the group buffer becomes FFT scratch
       if (a.late) prefetch_next(it);
     }
@@ -612,14 +657,22 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         constexpr int NSEG = M / 16;
 #pragma unroll
         for (int L = 0; L < 2; ++L) {
+          // Q = 16: thread t owns box row L NSEG + t; granule h of it sits at
+          // h ^ (row & 7): double2 slot (8 row ^ (row & 7)) ^ h
+          const int rowq = L * NSEG + t;
+          const int bq = (8 * rowq) ^ (rowq & 7);
 #pragma unroll
           for (int h = 0; h < Q / 2; ++h) {
-            const int pos = Q * t + 2 * h;
-            const int row = L * NSEG + (pos >> 4);
-            const int phys = row * 16 + 2 * (((pos >> 1) & 7) ^ (row & 7));
             const double2 val = L == 0 ? make_double2(out[2 * h].x, out[2 * h + 1].x)
                                        : make_double2(out[2 * h].y, out[2 * h + 1].y);
-            *reinterpret_cast<double2*>(gb + phys) = val;
+            if constexpr (Q == 16) {
+              reinterpret_cast<double2*>(gb)[bq ^ h] = val;
+            } else {
+              const int pos = Q * t + 2 * h;
+              const int row = L * NSEG + (pos >> 4);
+              const int phys = row * 16 + 2 * (((pos >> 1) & 7) ^ (row & 7));
+              *reinterpret_cast<double2*>(gb + phys) = val;
+            }
           }
         }
         fence_proxy_async_smem();
@@ -894,6 +947,9 @@ static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMa
   StreamArgs b = a;
   b.per = 0;
   b.run = 1;
+  b.gshift = -1;
+  if (a.G > 0 && (a.G & (a.G - 1)) == 0)
+    for (b.gshift = 0; (1 << b.gshift) < a.G;) ++b.gshift;
   if (MODE == kYF) {
     // one CTA per column block, walking the levels in order (the Thomas carry)
     blocks = a.G;

@@ -299,17 +299,54 @@ __device__ __forceinline__ void pass_regs(double2* v, double2 w1, double2 w4, do
 }
 
 // Store a radix-E pass's outputs in Stockham order, then reload cyclic.
+// Swizzled slot of the cyclic element t + T i in closed form (S = LE or LE - 1,
+// T a multiple of 2^S): the XOR term ((t >> S) + (T >> S) i) & 7 takes at most
+// 8 / gcd(8, T >> S) values over i, so the slots are a few per-thread bases plus
+// compile-time offsets T i (base + immediate addressing, no per-element
+// integer arithmetic; the same slots as swz<S>(t + T i)).
+template <int T, int S>
+struct CyclicSlots {
+  static constexpr int STEP = (T >> S) & 7;
+  static constexpr int NC = STEP == 0 ? 1 : (STEP & 1) ? 8 : (STEP & 2) ? 4 : 2;
+  int base[NC];
+  __device__ __forceinline__ explicit CyclicSlots(int t) {
+    static_assert(T >= (1 << S) && T >= 8, "closed form needs T >= max(8, 2^S)");
+    const int a = (t >> S) & 7;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) base[c] = t ^ ((a + STEP * c) & 7);
+  }
+  __device__ __forceinline__ int at(int i) const { return base[i % NC] + T * i; }
+};
+
 template <int P, int E, int L>
 __device__ __forceinline__ void exchangeE(double2* v, double2* sb, int t, int f) {
   constexpr int T = FE<P, E>::T;
+  constexpr int LE = FE<P, E>::LE;
   const int k = t & (L - 1);
   const int base = (t - k) * E + k;
-  constexpr int LE = FE<P, E>::LE;
+  if constexpr (E == 16 && L == 1) {
+    // slot 16 t + u, XOR term t & 7: (16 t ^ (t & 7)) ^ u
+    const int b0 = (16 * t) ^ (t & 7);
 #pragma unroll
-  for (int u = 0; u < E; ++u) sb[swz<LE>(base + u * L)] = v[u];
+    for (int u = 0; u < E; ++u) sb[b0 ^ u] = v[u];
+  } else if constexpr (E == 16 && L == 16) {
+    // slot base + 16 u with base = 16 (t - k) + k, k < 16: XOR term u & 7 on
+    // k's low bits: (base ^ (u & 7)) + 16 u
+#pragma unroll
+    for (int u = 0; u < E; ++u) sb[(base ^ (u & 7)) + u * L] = v[u];
+  } else {
+#pragma unroll
+    for (int u = 0; u < E; ++u) sb[swz<LE>(base + u * L)] = v[u];
+  }
   group_sync<T>(f);
+  if constexpr (E == 16 && T >= 16) {
+    const CyclicSlots<T, LE> cs(t);
 #pragma unroll
-  for (int i = 0; i < E; ++i) v[i] = sb[swz<LE>(t + T * i)];
+    for (int i = 0; i < E; ++i) v[i] = sb[cs.at(i)];
+  } else {
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = sb[swz<LE>(t + T * i)];
+  }
   group_sync<T>(f);
 }
 
@@ -362,6 +399,51 @@ __device__ __forceinline__ double2 group_scanE(double2 v, int t, int f, double2*
   return ex;
 }
 
+// Post-processing slots (swizzle S = LE - 1, SEG = 2^S values per thread).
+// post_store: B_{t + T i} at swz<S>(t + T i). PostSlots: thread t's segment
+// values B_k, k = SEG t + s (s <= SEG), and their mirrors B_{(M - k) mod M}, at
+// swz<S>(.) — for E = 16 in closed form: k and M - k stay inside one 8-slot row
+// for s in [0, 8) resp. [1, 8], where the XOR term is the row's low bits, so a
+// slot is (row base ^ row bits) ^ column: one XOR with a compile-time column.
+template <int P, int E>
+__device__ __forceinline__ void post_store(const double2* v, double2* sb, int t) {
+  constexpr int T = FE<P, E>::T, LS = FE<P, E>::LE - 1;
+  if constexpr (E == 16 && T >= 8) {
+    const CyclicSlots<T, LS> cs(t);
+#pragma unroll
+    for (int i = 0; i < E; ++i) sb[cs.at(i)] = v[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < E; ++i) sb[swz<LS>(t + T * i)] = v[i];
+  }
+}
+
+template <int P, int E>
+struct PostSlots {
+  static constexpr int M = FE<P, E>::M, SEG = FE<P, E>::SEG, LS = FE<P, E>::LE - 1;
+  static constexpr bool FAST = (E == 16);
+  int t, f0, f1, m0, m1;
+  __device__ __forceinline__ explicit PostSlots(int tt) : t(tt) {
+    if constexpr (FAST) {
+      const int R = M / 8;  // 8-slot rows of the buffer
+      f0 = (8 * t) ^ (t & 7);                    // row t: k = 8 t + s, s < 8
+      f1 = (8 * (t + 1)) ^ ((t + 1) & 7);        // k = 8 (t + 1) <= M/2
+      const int r0 = (R - t) & (R - 1);          // M - 8 t (mod M) = 8 r0
+      m0 = (8 * r0) ^ (r0 & 7);
+      const int r1 = R - 1 - t;                  // M - 8 t - s = 8 r1 + (8 - s), 1 <= s <= 8
+      m1 = (8 * r1) ^ (r1 & 7);
+    }
+  }
+  __device__ __forceinline__ int fwd(int s) const {
+    if constexpr (FAST) return s < 8 ? (f0 ^ s) : f1;
+    return swz<LS>((SEG * t + s) & (M - 1));
+  }
+  __device__ __forceinline__ int mir(int s) const {
+    if constexpr (FAST) return s == 0 ? m0 : (m1 ^ (8 - s));
+    return swz<LS>((M - SEG * t - s) & (M - 1));
+  }
+};
+
 // DST post-processing: v = B (cyclic) -> the 2*SEG outputs of thread t, i.e.
 // positions 2k-1 and 2k for k in [SEG t, SEG t + SEG), scaled by sqrt(2/M):
 // out[2s] = S_{2k} (position 2k-1; meaningless for k = 0), out[2s+1] =
@@ -370,16 +452,16 @@ template <int P, int E>
 __device__ __forceinline__ void dstE_post(const double2* v, double2* sb, double2* wsum,
                                           double scale, int t, int f, double2* out) {
   constexpr int M = FE<P, E>::M, T = FE<P, E>::T, SEG = FE<P, E>::SEG, LS = FE<P, E>::LE - 1;
-#pragma unroll
-  for (int i = 0; i < E; ++i) sb[swz<LS>(t + T * i)] = v[i];
+  post_store<P, E>(v, sb, t);
   group_sync<T>(f);
   const int k0 = SEG * t;
+  const PostSlots<P, E> ps(t);
   double2 run = make_double2(0.0, 0.0);
 #pragma unroll
   for (int s = 0; s < SEG; ++s) {
     const int k = k0 + s;
-    const double2 bk = sb[swz<LS>(k)];
-    const double2 bm = sb[swz<LS>((M - k) & (M - 1))];
+    const double2 bk = sb[ps.fwd(s)];
+    const double2 bm = sb[ps.mir(s)];
     double2 C = make_double2(0.5 * (bk.x + bm.x), 0.5 * (bk.y + bm.y));
     if (k == 0) C = cscale(C, 0.5);
     run = cadd(run, C);
@@ -401,16 +483,16 @@ template <int P, int E>
 __device__ __forceinline__ void dstE_post_aligned(const double2* v, double2* sb, double2* wsum,
                                                   double scale, int t, int f, double2* out) {
   constexpr int M = FE<P, E>::M, T = FE<P, E>::T, SEG = FE<P, E>::SEG, LS = FE<P, E>::LE - 1;
-#pragma unroll
-  for (int i = 0; i < E; ++i) sb[swz<LS>(t + T * i)] = v[i];
+  post_store<P, E>(v, sb, t);
   group_sync<T>(f);
   const int k0 = SEG * t;
+  const PostSlots<P, E> ps(t);
   double2 run = make_double2(0.0, 0.0);
 #pragma unroll
   for (int s = 0; s <= SEG; ++s) {
     const int k = k0 + s;  // k <= M/2
-    const double2 bk = sb[swz<LS>(k & (M - 1))];
-    const double2 bm = sb[swz<LS>((M - k) & (M - 1))];
+    const double2 bk = sb[ps.fwd(s)];
+    const double2 bm = sb[ps.mir(s)];
     if (s > 0)
       out[2 * s - 1] = make_double2(-0.5 * scale * (bk.y - bm.y), 0.5 * scale * (bk.x - bm.x));
     if (s < SEG) {
@@ -428,16 +510,19 @@ __device__ __forceinline__ void dstE_post_aligned(const double2* v, double2* sb,
 
 // Pre-processing: v[i] = b_{t + T i} from a loader of a_e (e in [1, M-1]); the
 // loader may return garbage for e = 0 and e = M (selected away here).
+// dstE_pre_idx: the loader gets (i, mirror) — a_e for e = t + T i, or for
+// e = M - t - T i when mirror — so a caller whose addresses are a per-thread base
+// plus a compile-time multiple of i can say so. dstE_pre: a loader of e.
 template <int P, int E, class Load>
-__device__ __forceinline__ void dstE_pre(double2* v, const double* __restrict__ sn,
-                                         const EngineTw<P, E>& tw, int t, Load&& load) {
+__device__ __forceinline__ void dstE_pre_idx(double2* v, const double* __restrict__ sn,
+                                             const EngineTw<P, E>& tw, int t, Load&& load) {
   constexpr int M = FE<P, E>::M, T = FE<P, E>::T, H = M / 2;
   // E = 16: sin(pi (t + T i)/M) = sin(pi t/M) cos(pi i/16) + cos(pi t/M) sin(pi i/16)
   const double st = tw.st, ct = tw.ct;
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const int e = t + T * i;
-    double2 p = load(e), q = load(M - e);
+    double2 p = load(i, false), q = load(i, true);
     if (i == 0) {
       const bool z = (t == 0);
       p = z ? make_double2(0.0, 0.0) : p;
@@ -452,6 +537,16 @@ __device__ __forceinline__ void dstE_pre(double2* v, const double* __restrict__ 
     const double sx = (p.x + q.x) * s, sy = (p.y + q.y) * s;
     v[i] = make_double2(fma(0.5, p.x - q.x, sx), fma(0.5, p.y - q.y, sy));
   }
+}
+
+template <int P, int E, class Load>
+__device__ __forceinline__ void dstE_pre(double2* v, const double* __restrict__ sn,
+                                         const EngineTw<P, E>& tw, int t, Load&& load) {
+  constexpr int M = FE<P, E>::M, T = FE<P, E>::T;
+  dstE_pre_idx<P, E>(v, sn, tw, t, [&](int i, bool mirror) -> double2 {
+    const int e = t + T * i;
+    return load(mirror ? M - e : e);
+  });
 }
 
 }  // namespace hfb
