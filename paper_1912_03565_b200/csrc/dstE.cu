@@ -106,6 +106,7 @@ struct StreamArgs {
   int gshift;             // log2(G) when G is a power of two, else -1
   long long per;          // batches per CTA (one contiguous run), 0 = interleaved
   int run;                // > 1: interleaved runs of `run` consecutive batches
+  int runshift;           // log2(run) when run is a power of two > 1, else 0
 };
 
 constexpr int kMaxRows = 16;  // 2 * NF
@@ -126,6 +127,8 @@ __device__ __forceinline__ bool batch_of(const StreamArgs& a, long long it, long
   if (a.per > 0) {
     if (it >= a.per) return false;
     b = (long long)blockIdx.x * a.per + it;
+  } else if (a.runshift > 0) {  // runs of 2^runshift batches
+    b = ((((it >> a.runshift) * gridDim.x + blockIdx.x)) << a.runshift) + (it & (a.run - 1));
   } else if (a.run > 1) {
     b = ((it / a.run) * gridDim.x + blockIdx.x) * a.run + it % a.run;
   } else {
@@ -665,7 +668,9 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
           for (int h = 0; h < Q / 2; ++h) {
             const double2 val = L == 0 ? make_double2(out[2 * h].x, out[2 * h + 1].x)
                                        : make_double2(out[2 * h].y, out[2 * h + 1].y);
-            if constexpr (Q == 16) {
+            if constexpr (Q == 16 && kXorAddr<P, E>) {
+              sh_st2((sh_addr(gb) + 16u * (uint32_t)bq) ^ (16u * h), val);
+            } else if constexpr (Q == 16) {
               reinterpret_cast<double2*>(gb)[bq ^ h] = val;
             } else {
               const int pos = Q * t + 2 * h;
@@ -965,6 +970,9 @@ static int launch_stream(const StreamArgs& a, const FftArgs& c, const CUtensorMa
   } else if (MODE == kTload) {
     b.run = 2;  // pairs of neighbouring column blocks (measured best at W = 4)
   }
+  b.runshift = 0;
+  if (b.run > 1 && (b.run & (b.run - 1)) == 0)
+    while ((1 << b.runshift) < b.run) ++b.runshift;
   kern<<<(unsigned)blocks, threads, sm, st>>>(b, c, tmap, omap, umap);
   return HFB_OK;
 }
@@ -1022,6 +1030,8 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   if (a.ustore) gb = std::max(gb, 128 + ((2 * a.N) / 16 + 3) * 16);
   if (a.tstore || a.ustore) {
     gb = (gb + 127) & ~127;  // every group box 1-KB aligned (128B swizzle atoms)
+  } else if (T >= 32) {
+    gb = (gb + 31) & ~31;  // 256-byte aligned group buffers (the engine's XOR byte addresses)
   } else {
     const int want = 16 / a.NF;  // group offsets spread over the 8 16-byte bank groups
     while (gb % 16 != want % 16) ++gb;

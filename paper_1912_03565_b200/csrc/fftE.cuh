@@ -161,6 +161,30 @@ __device__ __forceinline__ constexpr int swz(int i) {
   return i ^ ((i >> S) & 7);
 }
 
+// Shared-memory accesses by 32-bit shared address. For groups of whole warps
+// (T >= 32) the launch code keeps every group buffer 256-byte aligned, so a
+// swizzled slot "base ^ column" is one XOR on the byte address (no separate
+// index-to-address step). volatile keeps these in program order with the
+// group barriers (also volatile asm); the stores clobber memory.
+__device__ __forceinline__ uint32_t sh_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void sh_st2(uint32_t addr, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void sh_st2_off(uint32_t addr, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0+%3], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y), "n"(OFF)
+               : "memory");
+}
+__device__ __forceinline__ double2 sh_ld2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+template <int P, int E>
+constexpr bool kXorAddr = (E == 16 && FE<P, E>::T >= 32);
+
 // multiply by w_N^e for an e that is a compile-time constant after unrolling
 template <int N>
 __device__ __forceinline__ double2 mul_wn_at(double2 a, int e) {
@@ -327,13 +351,29 @@ __device__ __forceinline__ void exchangeE(double2* v, double2* sb, int t, int f)
   if constexpr (E == 16 && L == 1) {
     // slot 16 t + u, XOR term t & 7: (16 t ^ (t & 7)) ^ u
     const int b0 = (16 * t) ^ (t & 7);
+    if constexpr (kXorAddr<P, E>) {
+      const uint32_t a0 = sh_addr(sb) + 16u * (uint32_t)b0;
 #pragma unroll
-    for (int u = 0; u < E; ++u) sb[b0 ^ u] = v[u];
+      for (int u = 0; u < E; ++u) sh_st2(a0 ^ (16u * u), v[u]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < E; ++u) sb[b0 ^ u] = v[u];
+    }
   } else if constexpr (E == 16 && L == 16) {
     // slot base + 16 u with base = 16 (t - k) + k, k < 16: XOR term u & 7 on
     // k's low bits: (base ^ (u & 7)) + 16 u
+    if constexpr (kXorAddr<P, E>) {
+      const uint32_t a0 = sh_addr(sb) + 16u * (uint32_t)base;
 #pragma unroll
-    for (int u = 0; u < E; ++u) sb[(base ^ (u & 7)) + u * L] = v[u];
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t au = a0 ^ (16u * u);
+        sh_st2(au + 256u * u, v[u]);
+        sh_st2(au + 256u * (u + 8), v[u + 8]);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < E; ++u) sb[(base ^ (u & 7)) + u * L] = v[u];
+    }
   } else {
 #pragma unroll
     for (int u = 0; u < E; ++u) sb[swz<LE>(base + u * L)] = v[u];
@@ -434,6 +474,13 @@ struct PostSlots {
       m1 = (8 * r1) ^ (r1 & 7);
     }
   }
+  // byte-address forms (128-byte aligned buffer at shared address a)
+  __device__ __forceinline__ uint32_t fwd_addr(uint32_t a, int s) const {
+    return s < 8 ? ((a + 16u * (uint32_t)f0) ^ (16u * s)) : a + 16u * (uint32_t)f1;
+  }
+  __device__ __forceinline__ uint32_t mir_addr(uint32_t a, int s) const {
+    return s == 0 ? a + 16u * (uint32_t)m0 : ((a + 16u * (uint32_t)m1) ^ (16u * (8 - s)));
+  }
   __device__ __forceinline__ int fwd(int s) const {
     if constexpr (FAST) return s < 8 ? (f0 ^ s) : f1;
     return swz<LS>((SEG * t + s) & (M - 1));
@@ -460,8 +507,14 @@ __device__ __forceinline__ void dstE_post(const double2* v, double2* sb, double2
 #pragma unroll
   for (int s = 0; s < SEG; ++s) {
     const int k = k0 + s;
-    const double2 bk = sb[ps.fwd(s)];
-    const double2 bm = sb[ps.mir(s)];
+    double2 bk, bm;
+    if constexpr (kXorAddr<P, E>) {
+      bk = sh_ld2(ps.fwd_addr(sh_addr(sb), s));
+      bm = sh_ld2(ps.mir_addr(sh_addr(sb), s));
+    } else {
+      bk = sb[ps.fwd(s)];
+      bm = sb[ps.mir(s)];
+    }
     double2 C = make_double2(0.5 * (bk.x + bm.x), 0.5 * (bk.y + bm.y));
     if (k == 0) C = cscale(C, 0.5);
     run = cadd(run, C);
@@ -491,8 +544,14 @@ __device__ __forceinline__ void dstE_post_aligned(const double2* v, double2* sb,
 #pragma unroll
   for (int s = 0; s <= SEG; ++s) {
     const int k = k0 + s;  // k <= M/2
-    const double2 bk = sb[ps.fwd(s)];
-    const double2 bm = sb[ps.mir(s)];
+    double2 bk, bm;
+    if constexpr (kXorAddr<P, E>) {
+      bk = sh_ld2(ps.fwd_addr(sh_addr(sb), s));
+      bm = sh_ld2(ps.mir_addr(sh_addr(sb), s));
+    } else {
+      bk = sb[ps.fwd(s)];
+      bm = sb[ps.mir(s)];
+    }
     if (s > 0)
       out[2 * s - 1] = make_double2(-0.5 * scale * (bk.y - bm.y), 0.5 * scale * (bk.x - bm.x));
     if (s < SEG) {
