@@ -115,8 +115,8 @@ uint64_t hfb_launch_count(void);
  * by cp.async (1, default) or read them from registers (0); key 28 = TMA
  * z-solve blocks of 128 modes everywhere (1) or 256 where the slab is wide
  * (0, default); key 29 = the DST passes prefetch the next batch after the
- * current one's pre-processing: 1 every pass, 2 (default) the passes that
- * store into the user's odd-pitch array, 0 none; key 30 = TMA z-solve chunks
+ * current one's pre-processing: 1 every pass, 2 (default) the M = 1024 passes
+ * that store into the user's odd-pitch array, 0 none; key 30 = TMA z-solve chunks
  * of 16 levels with 3 (1) or 2 (2) stages, or 8 levels (0, default); key 31 =
  * z-invariant weight tables (every level's weights bitwise equal) get their
  * eigenvalues once per mode block in the z-solves (1, default) or per level

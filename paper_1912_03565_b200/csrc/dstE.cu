@@ -1058,7 +1058,11 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   // late prefetch (key 29: 1 all passes, 2 the flat-row-store passes only).
   // Measured at 1023^3 (same box): final pass 4.87 -> 4.62 ms, the other
   // passes 0.05-0.12 ms slower.
-  a.late = tuning(29) == 1 || (tuning(29) == 2 && a.ustore);
+  // After the engine's address-generation work the M = 2048 final pass is
+  // faster with the early prefetch again (47.0 -> 38.9 ms at 2047^3, same box),
+  // the M = 1024 one still with the late one (3.97 vs 4.11 ms): key 29 = 2 now
+  // means the M = 1024 flat-row-store passes only.
+  a.late = tuning(29) == 1 || (tuning(29) == 2 && a.ustore && M == 1024);
   // key 14 = 2: also decouple the groups of the M = 1024 column pass that stores
   // into the user's array (flat-row stores; the final inverse-x pass)
   a.indep = (k.mode == kRow || k.mode == kYB || (k.mode == kTload && M == 2048) ||

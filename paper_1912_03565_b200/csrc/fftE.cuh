@@ -182,8 +182,11 @@ __device__ __forceinline__ double2 sh_ld2(uint32_t addr) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
   return v;
 }
+#ifndef HFB_XOR_ADDR
+#define HFB_XOR_ADDR 1  // 0: index forms everywhere (A/B builds)
+#endif
 template <int P, int E>
-constexpr bool kXorAddr = (E == 16 && FE<P, E>::T >= 32);
+constexpr bool kXorAddr = (HFB_XOR_ADDR && E == 16 && FE<P, E>::T >= 32);
 
 // multiply by w_N^e for an e that is a compile-time constant after unrolling
 template <int N>
