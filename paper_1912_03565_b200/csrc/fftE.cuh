@@ -37,11 +37,35 @@ __host__ __device__ __forceinline__ constexpr double c32(int k) {
   return m <= 8 ? tab[m] : m <= 16 ? -tab[16 - m] : m <= 24 ? -tab[m - 16] : tab[32 - m];
 }
 
+// HFB_CONST_BANK: the same cosines from a __constant__ table, so the FP64
+// instructions take them as constant-bank operands instead of 64-bit
+// immediates moved through uniform registers (two UMOV each).
+#ifndef HFB_CONST_BANK
+#define HFB_CONST_BANK 0
+#endif
+#if HFB_CONST_BANK
+__constant__ double kC32[9] = {1.0,
+                               0.98078528040323044913,
+                               0.92387953251128675613,
+                               0.83146961230254523708,
+                               0.70710678118654752440,
+                               0.55557023301960222474,
+                               0.38268343236508977173,
+                               0.19509032201612826785,
+                               0.0};
+__device__ __forceinline__ double c32v(int k) {  // k a compile-time constant after unrolling
+  const int m = ((k % 32) + 32) % 32;
+  return m <= 8 ? kC32[m] : m <= 16 ? -kC32[16 - m] : m <= 24 ? -kC32[m - 16] : kC32[32 - m];
+}
+#else
+__device__ __forceinline__ constexpr double c32v(int k) { return c32(k); }
+#endif
+
 // multiply by w_N^E = exp(-2 pi i E / N) for a compile-time (N, E), N | 32
 template <int N, int E>
 __device__ __forceinline__ double2 mul_wn(double2 a) {
   constexpr int e = ((E % N) + N) % N;
-  constexpr double r = 0.70710678118654752440;
+  const double r = c32v(4);
   if constexpr (e == 0) {
     return a;
   } else if constexpr (4 * e == N) {  // -i
@@ -56,7 +80,7 @@ __device__ __forceinline__ double2 mul_wn(double2 a) {
     return make_double2(r * (a.y - a.x), -r * (a.x + a.y));
   } else {
     constexpr int K = e * (32 / N);  // angle 2 pi e / N = pi K / 16
-    constexpr double wc = c32(K), ws = c32(K - 8);  // cos, sin
+    const double wc = c32v(K), ws = c32v(K - 8);  // cos, sin
     return make_double2(fma(a.x, wc, a.y * ws), fma(a.y, wc, -a.x * ws));
   }
 }
@@ -592,7 +616,7 @@ __device__ __forceinline__ void dstE_pre_idx(double2* v, const double* __restric
     }
     double s;
     if constexpr (E == 16) {
-      s = fma(st, c32(i), ct * c32(i - 8));
+      s = fma(st, c32v(i), ct * c32v(i - 8));
     } else {
       s = __ldg(&sn[e <= H ? e : M - e]);
     }
