@@ -548,7 +548,13 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int l0 = blockIdx.z * lz, l1 = min(nz, l0 + lz);
   const int i = x0 + lane, jw = y0 + warp * RJ;
-  for (int e = threadIdx.x; e < (l1 - l0) * 12; e += 256) wsm[e] = __ldg(raw + l0 * 12LL + e);
+  // weights of levels l0 - 2 .. l1 + 1 with the out-of-range levels replicated
+  // from the nearest level of the CTA: plane P then reads its three weight rows
+  // (levels P - 2, P - 1, P, clamped as before) at fixed offsets from one pointer
+  for (int e = threadIdx.x; e < (l1 - l0 + 4) * 12; e += 256) {
+    const int lev = min(max(l0 - 2 + e / 12, l0), l1 - 1);
+    wsm[e] = __ldg(raw + lev * 12LL + e % 12);
+  }
   // this thread's (at most 5) elements of the 34 x 34 input tile: byte offset
   // in a stage, offset from the plane base (coordinates clamped into the array,
   // so every copy reads a valid address) and whether the element lies in the
@@ -578,11 +584,22 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
   // rhs / F of output level P - 2 rides with plane P: this thread's own 4 values
   const uint32_t rbase = smem_u32(smt + NS * kT27Stage) + 8 * (warp * RJ * 32 + lane);
   const bool icol = i < nx;
+  // the next plane to load (a running pointer: one 64-bit add per plane instead
+  // of a 64-bit product); the residual's planes outside the array are never read
+  // (zero-filled copies of size 0 from a valid address)
+  const double* nextp = src + (long long)(KIND == 2 ? l0 - 1 : l0) * pstride;
+  // rhs / F rows of level P - 2 and the output rows: plane stride of the interior
+  // arrays, this thread's row offsets (clamped into the plane)
+  const long long ostep = (long long)ny * nx;
+  const double* nextr = KIND == 0 ? nullptr : rhs + (long long)(l0 - 2) * ostep + min(i, nx - 1);
+  int roff[RJ];
+#pragma unroll
+  for (int q = 0; q < RJ; ++q) roff[q] = min(jw + q, ny - 1) * nx;
   auto load_plane = [&](int P, int st) {
     const uint32_t dst = sbase + st * (kT27Stage * 8);
     const bool pok = KIND != 2 || (P >= 1 && P <= nz);
-    const int pc = KIND == 2 ? min(max(P - 1, 0), nz - 1) : P;
-    const double* base = src + (long long)pc * pstride;
+    const double* base = pok ? nextp : src;
+    nextp += pstride;
 #pragma unroll
     for (int q = 0; q < NE; ++q) {
       if (soff[q] < 0) continue;
@@ -591,15 +608,12 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
     if constexpr (KIND != 0) {
       const int L = P - 2;
       const bool lok = L >= l0 && L < l1 && icol;
-      const int Lc = min(max(L, 0), nz - 1);
-      const double* rb = rhs + ((long long)Lc * ny) * nx + min(i, nx - 1);
+      const double* rb = lok ? nextr : rhs;  // level L's rows (a running pointer)
+      nextr += ostep;
       const uint32_t rd = rbase + st * (1024 * 8);
 #pragma unroll
-      for (int q = 0; q < RJ; ++q) {
-        const int j = jw + q;
-        cp_async8_s(rd + q * 32 * 8, rb + (long long)min(j, ny - 1) * nx,
-                    (lok && j < ny) ? 8 : 0);
-      }
+      for (int q = 0; q < RJ; ++q)
+        cp_async8_s(rd + q * 32 * 8, rb + roff[q], (lok && jw + q < ny) ? 8 : 0);
     }
   };
   const int Pend = l1 + 1;  // planes l0 .. l1 + 1 serve levels l0 .. l1 - 1
@@ -615,6 +629,8 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
   bool rowok[RJ];
 #pragma unroll
   for (int q = 0; q < RJ; ++q) rowok[q] = icol && jw + q < ny;
+  // output row of level L = P - 2, this thread's column: advanced by a plane per step
+  double* op = KIND == 2 ? nullptr : out + ((long long)l0 * ny + jw) * nx + i - 2 * ostep;
   auto plane_step = [&](int P) {
     cp_async_wait<NS - 2>();
     __syncthreads();  // plane P staged for everyone; stage (P - 1) free
@@ -622,9 +638,10 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
     cp_async_commit();
     const double* pl = smt + ((P - l0) % NS) * kT27Stage + warp * RJ * PT + lane;
     const double* rl = smt + NS * kT27Stage + ((P - l0) % NS) * 1024 + warp * RJ * 32 + lane;
-    const double* w0 = wsm + (min(P, l1 - 1) - l0) * 12;                  // level P, k = 0
-    const double* w1 = wsm + (min(max(P - 1, l0), l1 - 1) - l0) * 12 + 4;  // level P-1, k = 1
-    const double* w2 = wsm + (max(P - 2, l0) - l0) * 12 + 8;               // level P-2, k = 2
+    const double* wp = wsm + (P - l0) * 12;  // the row of level P - 2 (replicated table)
+    const double* w0 = wp + 24;              // level P, k = 0
+    const double* w1 = wp + 12 + 4;          // level P-1, k = 1
+    const double* w2 = wp + 8;               // level P-2, k = 2
     double wk0[4], wk1[4], wk2[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -633,7 +650,8 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
       wk2[q] = w2[q];
     }
     const int L = P - 2;
-    double* orow = KIND == 0 ? out + ((long long)max(L, 0) * ny + jw) * nx + i : nullptr;
+    double* orow = op;  // out + ((L ny) + jw) nx + i: a running pointer (valid once L >= l0)
+    if constexpr (KIND != 2) op += ostep;
 #pragma unroll
     for (int q = 0; q < RJ; ++q) {
       double v[9];
@@ -655,8 +673,7 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
         // registers for the twice-unrolled apply loop)
         if (L >= l0 && rowok[q]) orow[q * nx] = t2;
       } else if (L >= l0 && i < nx && j < ny) {
-        const long long oo = ((long long)L * ny + j) * nx + i;
-        if constexpr (KIND == 1) out[oo] = __dsub_rn(rl[q * 32], t2);
+        if constexpr (KIND == 1) orow[q * nx] = __dsub_rn(rl[q * 32], t2);
         if constexpr (KIND == 2) {
           const double rr = t2 - rl[q * 32];
           ssq = fma(rr, rr, ssq);
@@ -666,10 +683,14 @@ __global__ void __launch_bounds__(256, 2) s27_tile_kernel(
       a1[q] = t0;
     }
   };
-  // the apply kernel's plane loop is unrolled twice (the (a0, a1) <- (t1, t0)
-  // rotation then needs no register moves); the fold / residual keep the
-  // compiler's choice (unrolling them spills)
-  if constexpr (KIND == 0) {
+  // the plane loop is unrolled twice (the (a0, a1) <- (t1, t0) rotation then
+  // needs no register moves); with the running pointers all three kinds fit
+  // the 128-register budget without spills (fold 5.4 -> 5.1-5.2 ms, residual
+  // 4.75 -> 4.61 ms at 1023^3)
+#ifndef HFB_S27_UNROLL2
+#define HFB_S27_UNROLL2 7  // bit 0: apply, bit 1: fold, bit 2: residual (all: no spills since the running pointers)
+#endif
+  if constexpr (((HFB_S27_UNROLL2) >> KIND) & 1) {
 #pragma unroll 2
     for (int P = l0; P <= Pend; ++P) plane_step(P);
   } else {
@@ -709,7 +730,7 @@ static int s27_launch(const hfb_plan* p, int lz, const double* src, const double
   const double* raw = p->coef + 12LL * p->nz;
   if (tuning(27)) {  // shared-memory staged planes (32 x 32 tiles = the rj = 4 grid)
     const size_t sm = sizeof(double) * ((size_t)kT27NS * (kT27Stage + (KIND ? 1024 : 0)) +
-                                        12 * (size_t)lz);
+                                        12 * ((size_t)lz + 4));
     auto kern = mask == kMask27 ? s27_tile_kernel<KIND, kMask27>
                 : mask == kMask19 ? s27_tile_kernel<KIND, kMask19>
                                   : s27_tile_kernel<KIND, 0>;
