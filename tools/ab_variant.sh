@@ -1,3 +1,8 @@
+#!/bin/bash
+# Same-box check of a variant build (tools/build_variant.sh NAME ...) against the
+# default library: bitwise fingerprints of cfg1-4 solves in both workspace layouts
+# (tools/bits.py), alternating timed runs (tools/ab.py) and per-launch stage times.
+#   bash tools/ab_variant.sh NAME        (writes gpurun_out/bits_*.txt, ab_NAME*.txt)
 A=paper_1912_03565_b200/_lib/libhelmfft_b200.so
 B=paper_1912_03565_b200/_lib/libhelmfft_b200_${1:-addr}.so
 HFB_LIBRARY=$A timeout 200 python tools/bits.py 1 2 3:63 3:255 3 4 > gpurun_out/bits_A.txt 2>&1
