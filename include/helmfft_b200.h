@@ -120,7 +120,11 @@ uint64_t hfb_launch_count(void);
  * of 16 levels with 3 (1) or 2 (2) stages, or 8 levels (0, default); key 31 =
  * z-invariant weight tables (every level's weights bitwise equal) get their
  * eigenvalues once per mode block in the z-solves (1, default) or per level
- * (0). Key 14 = 2 also decouples the groups of the flat-row-store column pass.
+ * (0); key 32 = the one-call z-solve keeps its cp checkpoints (matrix-only data,
+ * one plane per 8 levels) in a plan-owned array across solves with the same
+ * coefficients, so only the first solve after a coefficient upload writes them
+ * (1, default; 0 = every solve writes them into the caller's workspace).
+ * Key 14 = 2 also decouples the groups of the flat-row-store column pass.
  * Keys 5, 6, 9, 21, 26 = 4, 28 and 30 keep measured-slower variants for A/B
  * runs; keys 17 and 22 are measurement knobs (22 bit 0 skips the waits: wrong
  * results). All of them keep the bits of the default path except keys 0, 17,

@@ -129,6 +129,7 @@ extern "C" int hfb_plan_destroy(hfb_plan* p) {
   cudaFree(p->coef);
   cudaFree(p->coef_i);
   cudaFree(p->pq);
+  cudaFree(p->ck_cache);
   cudaFree(p->cx);
   cudaFree(p->cy);
   cudaFree(p->err);
@@ -237,6 +238,8 @@ extern "C" int hfb_plan_set_coefficients(hfb_plan* p, const double* table, const
   HFB_CUDA(cudaMemcpy(p->cy, cy, sizeof(double) * p->ny, cudaMemcpyHostToDevice));
   p->thr = thr;
   p->have_coef = 1;
+  p->coef_epoch++;  // cached cp checkpoints (ck_cache) belong to the previous table
+  p->ck_valid = 0;
   p->zinv = 1;  // all levels' scaled weights equal (bitwise)
   for (size_t e = 12; e < nlev && p->zinv; ++e)
     if (std::memcmp(&buf[e], &buf[e % 12], sizeof(double)) != 0) p->zinv = 0;

@@ -752,7 +752,9 @@ int solve_fused(hfb_plan* p, const double* rhs, double* out, double* work, cudaS
     if ((rc = launch_dst16_mode(y, st))) return rc;
     mark(2);
     // 3
-    if ((rc = launch_thomas_tma(p, S2, CP, ldt, pst, st, fuse ? 1 : 0))) return rc;
+    if ((rc = fuse ? launch_thomas_tma(p, S2, CP, ldt, pst, st, 1)
+                   : launch_thomas_tma_cached(p, S2, CP, ldt, pst, st)))
+      return rc;
     mark(3);
     // 4
     y.mode = 0;

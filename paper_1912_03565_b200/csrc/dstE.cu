@@ -927,6 +927,7 @@ static int g_tune_late = 2;  // DST passes: prefetch after the pre-processing (k
 static int g_tune_thomas_narrow = 0;  // TMA z-solve with 128-mode blocks (key 28)
 static int g_tune_thomas_kc = 0;  // TMA z-solve chunks (key 30: 0 = 8 levels, 1 = 16 levels 3 stages, 2 = 16 levels 2 stages)
 static int g_tune_zinv = 1;  // TMA z-solve: eigenvalues once per mode for z-invariant weights (key 31)
+static int g_tune_ckcache = 1;  // one-call z-solve: cp checkpoints cached in the plan across solves (key 32)
 static int g_tune_wave_dbg = 0;  // its measurement variants (key 22; wrong results for bit 1)
 
 template <int P, int E, int MODE>
@@ -1208,6 +1209,7 @@ int tuning(int key) {
     case 29: return g_tune_late;
     case 30: return g_tune_thomas_kc;
     case 31: return g_tune_zinv;
+    case 32: return g_tune_ckcache;
     default: return 0;
   }
 }
@@ -1244,6 +1246,7 @@ void set_tuning(int key, int value) {
   if (key == 29) g_tune_late = value;
   if (key == 30) g_tune_thomas_kc = value;
   if (key == 31) g_tune_zinv = value ? 1 : 0;
+  if (key == 32) g_tune_ckcache = value ? 1 : 0;
 }
 
 int launch_dst16_mode(const Dst16Call& k, cudaStream_t st) {

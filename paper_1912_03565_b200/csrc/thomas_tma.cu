@@ -39,6 +39,7 @@ struct TmaArgs {
   int row0;      // first row (x-mode) of this launch
   const int* lvl;  // level -> plane of the data (null: identity), e.g. a chunked y-slab
   int xsparse;     // forward stores x' only at each chunk's first level (see below)
+  int ck_ro;       // cpk already holds this matrix's checkpoints: the forward stores none
 };
 
 __device__ __forceinline__ double eig_s(const double* co, double cx, double cy, double cxy) {
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
             if (keep_all || i == 0) sdat[s][i][tid] = x;
             c = up * rr;
           }
-          if (live) ck[(long long)cidx * a.ps] = c;
+          if (live && !a.ck_ro) ck[(long long)cidx * a.ps] = c;
           if (live && bad < K) {
             const unsigned long long key =
                 ((unsigned long long)(l0 + bad) * (unsigned long long)a.ny_total +
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(BM) thomas_tma_kernel(TmaArgs a) {
               if (keep_all || i == 0) sdat[s][i][tid] = x;
               if (l < a.nz - 1) {
                 c = up * rr;
-                if (i == K - 1 && live) ck[(long long)cidx * a.ps] = c;
+                if (i == K - 1 && live && !a.ck_ro) ck[(long long)cidx * a.ps] = c;
               }
             }
           }
@@ -379,8 +380,41 @@ __global__ void __launch_bounds__(32) thomas_smem_kernel(TmaArgs a) {
     for (int l = 0; l < a.nz; ++l) base[(long long)l * a.ps] = sd[l * 32 + t];
 }
 
+int launch_thomas_tma_cached(hfb_plan* p, double* data, double* cpk, long long ld, long long ps,
+                             cudaStream_t st) {
+  if (!tuning(32) || p->nz <= 256) return launch_thomas_tma(p, data, cpk, ld, ps, st, 0);
+  // what the cached checkpoints depend on: the coefficients, the layout and the
+  // chunk length
+  const unsigned long long sig = (p->coef_epoch << 20) ^ ((unsigned long long)ld << 44) ^
+                                 ((unsigned long long)ps * 0x9E3779B97F4A7C15ull) ^
+                                 (unsigned long long)(tuning(30) ? 16 : K);
+  const int kc = tuning(30) ? 16 : K;
+  const size_t need = sizeof(double) * (size_t)((p->nz + kc - 1) / kc) * (size_t)ps;
+  if (!p->ck_cache || p->ck_cache_bytes < need) {
+    if (p->ck_cache) cudaFree(p->ck_cache);
+    p->ck_cache = nullptr;
+    p->ck_cache_bytes = 0;
+    p->ck_valid = 0;
+    if (cudaMalloc(&p->ck_cache, need) == cudaSuccess) {
+      p->ck_cache_bytes = need;
+    } else {
+      (void)cudaGetLastError();  // no room: solve with the workspace's checkpoints
+      p->ck_cache = nullptr;
+    }
+  }
+  if (!p->ck_cache) return launch_thomas_tma(p, data, cpk, ld, ps, st, 0);
+  const int ro = p->ck_valid && p->ck_sig == sig && p->ck_stream == st;
+  const int rc = launch_thomas_tma(p, data, p->ck_cache, ld, ps, st, 0, ro);
+  if (rc == HFB_OK && !ro) {
+    p->ck_valid = 1;
+    p->ck_sig = sig;
+    p->ck_stream = st;
+  }
+  return rc;
+}
+
 int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, long long ps,
-                      cudaStream_t st, int bwd_only) {
+                      cudaStream_t st, int bwd_only, int ck_ro) {
   // the whole column on chip (tuning key 19, default on) when the modes fit in
   // a few waves of it; many modes keep the bandwidth-bound copy ring
   const size_t sm_small = sizeof(double) * ((size_t)p->nz * 64 + (size_t)p->nz * 12);
@@ -414,12 +448,13 @@ int launch_thomas_tma(hfb_plan* p, double* data, double* cpk, long long ld, long
     HFB_LAUNCHED();
     return HFB_OK;
   }
-  return launch_thomas_tma_cols(p, data, cpk, ld, ps, p->ny, 0, st, bwd_only);
+  return launch_thomas_tma_cols(p, data, cpk, ld, ps, p->ny, 0, st, bwd_only, 0, -1, 0, nullptr,
+                                ck_ro);
 }
 
 int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld, long long ps,
                            int ncols, int m_off, cudaStream_t st, int bwd_only, int row0,
-                           int row1, int max_per_sm, const int* lvl) {
+                           int row1, int max_per_sm, const int* lvl, int ck_ro) {
   if (row1 < 0) row1 = p->nx;
   if (p->nz < 1 || ncols < 1 || row1 <= row0) return HFB_OK;
   TmaArgs a;
@@ -428,6 +463,7 @@ int launch_thomas_tma_cols(hfb_plan* p, double* data, double* cpk, long long ld,
   a.row0 = row0;
   a.lvl = lvl;
   a.xsparse = tuning(23);
+  a.ck_ro = ck_ro && !bwd_only;
   a.w = data;
   a.cpk = cpk;
   a.coef = p->coef;

@@ -269,6 +269,61 @@ def test_zsolve_variants_bitwise(cuda, shape):
         assert np.array_equal(u, ref), knobs
 
 
+@pytest.mark.parametrize("shape", [(63, 127, 300), (255, 64, 257), (31, 600, 515)])
+def test_checkpoint_cache_bitwise(cuda, shape):
+    """Tuning key 32 (default on): the one-call z-solve keeps its cp checkpoints
+    in a plan-owned array across solves with the same coefficients. Repeated
+    solves (the second reads the cache), a change of chunk length or workspace
+    layout (the cache is refilled) and a coefficient upload (the cache is
+    invalidated) all give the bits of the uncached solve (key 32 = 0), on plans
+    with n_z > 256 (below that the shared-memory z-solve needs no checkpoints)."""
+    import torch
+    nx, ny, nz = shape
+    h = 1.0 / 64
+    g = hb.make_grid(hb.Domain(0, (nx + 1) * h, 0, (ny + 1) * h, 0, (nz + 1) * h), nx, ny, nz)
+    tables = [(hb.SchemeKind.SIXTH_ORDER, wl.profile_a(g)),
+              (hb.SchemeKind.CONVECTION_DIFFUSION_4, hb.constant_profile(0.0, g, gamma=-1.5))]
+    lib = _native.load_library()
+    plan = _native.get_plan(nx, ny, nz, torch.device("cuda", 0))
+    F = torch.from_numpy(np.random.default_rng(5).standard_normal((nz, ny, nx))).cuda()
+
+    def solve(lean=False):
+        plan.set_workspace_mode(lean)
+        X = F.clone()
+        U = X if lean else torch.empty_like(F)
+        work = plan.workspace(0)
+        work.fill_(0x7f)  # the workspace's own checkpoint planes are scratch either way
+        _native.check(lib.hfb_solve(plan.handle, _native.ptr(X), _native.ptr(U),
+                                    _native.ptr(work), plan.stream()), "solve")
+        plan.fetch_status()
+        return U.cpu().numpy()
+
+    try:
+        refs = {}
+        for t, (sk, prof) in enumerate(tables):  # uncached references
+            lib.hfb_set_tuning(32, 0)
+            device_coefficients(plan, sk, prof, g)
+            refs[t] = solve()
+            refs[t, "lean"] = solve(lean=True)
+        lib.hfb_set_tuning(32, 1)
+        for t in (0, 1, 0):  # every upload invalidates what the last table cached
+            device_coefficients(plan, *tables[t], g)
+            assert np.array_equal(solve(), refs[t]), ("fill", t)
+            assert np.array_equal(solve(), refs[t]), ("cached", t)
+            lib.hfb_set_tuning(30, 1)  # 16-level chunks: other checkpoints, refilled
+            assert np.array_equal(solve(), refs[t]), ("16-level chunks", t)
+            assert np.array_equal(solve(), refs[t]), ("16-level chunks, cached", t)
+            lib.hfb_set_tuning(30, 0)
+            assert np.array_equal(solve(), refs[t]), ("8-level chunks again", t)
+            assert np.array_equal(solve(lean=True), refs[t, "lean"]), ("lean layout", t)
+            assert np.array_equal(solve(lean=True), refs[t, "lean"]), ("lean layout, cached", t)
+            assert np.array_equal(solve(), refs[t]), ("fast layout again", t)
+    finally:
+        lib.hfb_set_tuning(30, 0)
+        lib.hfb_set_tuning(32, 1)
+        plan.set_workspace_mode(False)
+
+
 @pytest.mark.parametrize("scheme", ["6", "cd4"])
 def test_zsolve_default_vs_oracle(cuda, scheme):
     """The default z-solve (sparse x', guard-free interior chunks; for the
