@@ -349,7 +349,6 @@ __device__ __forceinline__ void pass_regs(double2* v, double2 w1, double2 w4, do
   }
 }
 
-// Store a radix-E pass's outputs in Stockham order, then reload cyclic.
 // Swizzled slot of the cyclic element t + T i in closed form (S = LE or LE - 1,
 // T a multiple of 2^S): the XOR term ((t >> S) + (T >> S) i) & 7 takes at most
 // 8 / gcd(8, T >> S) values over i, so the slots are a few per-thread bases plus
@@ -369,6 +368,7 @@ struct CyclicSlots {
   __device__ __forceinline__ int at(int i) const { return base[i % NC] + T * i; }
 };
 
+// Store a radix-E pass's outputs in Stockham order, then reload cyclic.
 template <int P, int E, int L>
 __device__ __forceinline__ void exchangeE(double2* v, double2* sb, int t, int f) {
   constexpr int T = FE<P, E>::T;
