@@ -330,7 +330,19 @@ int hfb_unpack_yblocks(hfb_plan* plan, const double* recv, double* slab, int kpz
  *   hfb_solve_modes: z-solve of a y-slab of mode rows (n_z levels of the plan,
  *     row stride ld even, columns = y-modes m_offset .. m_offset + m_count - 1),
  *     cp_work = ceil(n_z / 8) * n_x * ld doubles;
- *   hfb_pack_modes / hfb_unpack_modes: mode rows <-> exchange blocks. */
+ *   hfb_pack_modes / hfb_unpack_modes: mode rows <-> exchange blocks;
+ *   hfb_forward_blocks / hfb_inverse_blocks: the transforms with the exchange
+ *     layout on their far side, so no pack / unpack pass runs — the forward y-pass
+ *     stores every mode row straight into the blocks of `send` (one 5D tensor
+ *     store per line pair), the inverse y-pass gathers its rows from the blocks of
+ *     `back` (one bulk copy per block and row) into `modes` (scratch of
+ *     kpz * n_x * ldm doubles). Same bits as forward_modes + pack_modes /
+ *     unpack_modes + inverse_modes. They need the uniform exchange geometry —
+ *     y_starts[q] = q * kp with parts * kp = n_y + 1 and kp a multiple of 16
+ *     (every power-of-two n_y + 1 split over a power-of-two rank count) — and
+ *     return HFB_ERR_PARTITION otherwise (callers then use the pack path). This
+ *     replaces the strided block copies of exchange_forward / exchange_inverse
+ *     (reference solver.py:146-201). */
 int hfb_modes_ld(const hfb_plan* plan);
 int hfb_forward_modes(hfb_plan* plan, const double* src, double* modes, void* work, void* stream);
 int hfb_inverse_modes(hfb_plan* plan, double* modes, double* out, void* stream);
@@ -345,6 +357,10 @@ int hfb_pack_modes(hfb_plan* plan, const double* modes, double* send, const int*
                    int parts, void* stream);
 int hfb_unpack_modes(hfb_plan* plan, const double* recv, double* modes, const int* y_starts,
                      int parts, void* stream);
+int hfb_forward_blocks(hfb_plan* plan, const double* src, double* send, void* work,
+                       const int* y_starts, int parts, void* stream);
+int hfb_inverse_blocks(hfb_plan* plan, const double* back, double* modes, double* out,
+                       const int* y_starts, int parts, void* stream);
 
 /* ---- transpose-free distributed z-solve ("alternative to
  * measure next"; replaces the exchange_forward / solve / exchange_inverse

@@ -58,6 +58,8 @@ SIGNATURES = {
     "hfb_solve_modes_perm": (_i, [_vp, _vp, _i, _i, _i, _ip, _vp, _vp]),
     "hfb_pack_modes": (_i, [_vp, _vp, _vp, _ip, _i, _vp]),
     "hfb_unpack_modes": (_i, [_vp, _vp, _vp, _ip, _i, _vp]),
+    "hfb_forward_blocks": (_i, [_vp, _vp, _vp, _vp, _ip, _i, _vp]),
+    "hfb_inverse_blocks": (_i, [_vp, _vp, _vp, _vp, _ip, _i, _vp]),
     "hfb_solve_host_async": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "hfb_host_sync": (_i, [_vp, _vp]),
     "hfb_plan_set_coefficients_z": (_i, [_vp, _vp, _vp, _vp, _vp, ctypes.c_double]),

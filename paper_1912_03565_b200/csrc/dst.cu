@@ -903,10 +903,12 @@ size_t modes_work_elems(const hfb_plan* p) {
   return tran_path(p) ? (size_t)p->nz * p->ny * x_ld(p) : 0;
 }
 
-int forward_modes(hfb_plan* p, const double* src, double* modes, double* S1, cudaStream_t st) {
+int forward_modes(hfb_plan* p, const double* src, double* modes, double* S1, cudaStream_t st,
+                  int parts, int kp) {
   if (!tran_path(p) || !S1) return HFB_ERR_ARGUMENT;
   const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), ldx = x_ld(p);
   if (dmma2d_np(p)) {  // small N: the one-call solve's DMMA transform (bitwise the same)
+    if (parts > 1) return HFB_ERR_ARGUMENT;  // no packed output on this path
     D2Layout fw = {p->nx, ps, ldt, ldt * p->nx, 0, 1};
     return launch_dmma2d(p, src, modes, 0, p->nz, st, &fw);
   }
@@ -942,6 +944,13 @@ int forward_modes(hfb_plan* p, const double* src, double* modes, double* S1, cud
   y.dst = modes;
   y.out_ld = ldt;
   y.out_ps = ldt * p->nx;
+  if (parts > 1) {
+    // straight into the exchange blocks: block q = (n_z, n_x, kp), the line's
+    // positions [q kp, (q + 1) kp) (modes is the send buffer)
+    y.pack_parts = parts;
+    y.pack_kp = kp;
+    y.pack_bstride = (long long)p->nz * p->nx * kp;
+  }
   return launch_dst16_mode(y, st);
 }
 
@@ -964,6 +973,46 @@ int inverse_modes(hfb_plan* p, double* modes, double* out, cudaStream_t st) {
   y.nrow = p->nx;
   y.in_ld = ldt;
   y.in_ps = pst;
+  y.dst = modes;
+  y.out_ld = ldt;
+  y.out_ps = pst;
+  int rc = launch_dst16_mode(y, st);
+  if (rc) return rc;
+  Dst16Call x = {};
+  x.tw = p->tw_x;
+  x.sn = p->sn_x;
+  x.scale = p->scale_x;
+  x.M = p->nx + 1;
+  x.nz = p->nz;
+  x.mode = 2;
+  x.src = modes;
+  x.src_end = modes + p->nz * pst;
+  x.nrow = p->ny;
+  x.in_ld = ldt;
+  x.in_ps = pst;
+  x.dst = out;
+  x.out_ld = p->nx;
+  x.out_ps = ps;
+  return launch_dst16_mode(x, st);
+}
+
+int inverse_modes_blocks(hfb_plan* p, const double* back, double* modes, double* out, int parts,
+                         int kp, cudaStream_t st) {
+  if (!tran_path(p) || dmma2d_np(p) || parts < 2) return HFB_ERR_ARGUMENT;
+  const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), pst = ldt * p->nx;
+  Dst16Call y = {};
+  y.tw = p->tw_y;
+  y.sn = p->sn_y;
+  y.scale = p->scale_y;
+  y.M = p->ny + 1;
+  y.nz = p->nz;
+  y.mode = 0;
+  y.src = back;  // rows gathered from the blocks by the row copies themselves
+  y.src_end = back;
+  y.nrow = p->nx;
+  y.split_parts = parts;
+  y.split_kp = kp;
+  y.split_bstride = (long long)p->nz * p->nx * kp;
   y.dst = modes;
   y.out_ld = ldt;
   y.out_ps = pst;

@@ -53,7 +53,9 @@ namespace hfb {
 // and an item waits only for an item G (the items per plane) before it, so the
 // wait always ends (the smallest unfinished item never waits on a later one).
 // The arithmetic is thomas_tma_kernel's expression for expression: bitwise equal.
-enum { kRow = 0, kTran = 1, kTload = 2, kYF = 3, kYF2 = 4, kYB = 5 };
+// kRowS = ROW whose input lines are split over exchange blocks (Dst16Call::split_*):
+// every staged row arrives as sp_parts bulk copies of sp_kp doubles.
+enum { kRow = 0, kTran = 1, kTload = 2, kYF = 3, kYF2 = 4, kYB = 5, kRowS = 6 };
 
 struct FftArgs {
   const double2* __restrict__ tw;  // tw[k] = exp(-2 pi i k/M)
@@ -103,6 +105,9 @@ struct StreamArgs {
   int dbg;  // measurement only (tuning key 22): 1 no waits, 2 acq_rel fences, 4 no fences
   int late;               // issue the next batch's prefetch after this batch's pre-processing
                           // (tuning key 29) instead of before waiting for this batch
+  int packed;             // tensor stores through a 5D map of the exchange blocks (omap)
+  int sp_parts, sp_kp;    // kRowS: pieces per input line and their length
+  long long sp_bstride;   // kRowS: doubles between the blocks of consecutive pieces
   int gshift;             // log2(G) when G is a power of two, else -1
   long long per;          // batches per CTA (one contiguous run), 0 = interleaved
   int run;                // > 1: interleaved runs of `run` consecutive batches
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
   }
 
   __shared__ uint64_t gbar[2][kMaxRows / 2];  // indep: per stage and group
-  const bool indep = (MODE == kRow || MODE == kTload || MODE == kYB) && a.indep;
+  const bool indep = (MODE == kRow || MODE == kRowS || MODE == kTload || MODE == kYB) && a.indep;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -274,6 +279,27 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
       for (int b = 0; b < a.nbox; ++b)
         tensor_g2s_3d(gbuf(s, 0) + (long long)b * a.boxn * W, &tmap, g * W, b * a.boxn,
                       (int)plane, &bar[s]);
+    } else if constexpr (MODE == kRowS) {
+      // every present row arrives as sp_parts pieces of sp_kp doubles (16-byte
+      // aligned at both ends), staged contiguously at gbuf(s, r/2) + (r&1)*rowslot + 2
+      uint32_t total = 0;
+      for (int r = 0; r < W; ++r) {
+        const int k = g * a.NF + (r >> 1);
+        const int row = 2 * k + (r & 1);
+        const bool ok = k < a.ppp && row < a.nrow;
+        meta.row[s][r] = ok ? row : -1;
+        meta.delta[s][r] = 2;
+        if (ok) total += (uint32_t)(a.sp_parts * a.sp_kp * 8);
+      }
+      mbar_arrive_expect_tx(&bar[s], total);
+      for (int r = 0; r < W; ++r) {
+        const int row = meta.row[s][r];
+        if (row < 0) continue;
+        const double* A = a.src + (plane * a.nrow + row) * a.sp_kp;
+        double* dstrow = gbuf(s, r >> 1) + (r & 1) * a.rowslot + 2;
+        for (int q = 0; q < a.sp_parts; ++q)
+          bulk_g2s(dstrow + q * a.sp_kp, A + q * a.sp_bstride, (uint32_t)(a.sp_kp * 8), &bar[s]);
+      }
     } else {
       // staged row r at gbuf(s, r/2) + (r&1)*rowslot + 2 (16-B aligned)
       uint32_t total = 0;
@@ -318,6 +344,28 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
     long long plane;
     int g;
     batch_of(a, it, plane, g);
+    if constexpr (MODE == kRowS) {
+      uint32_t tot = 0;
+      for (int r = 2 * f; r < 2 * f + 2; ++r) {
+        const int k = g * a.NF + (r >> 1);
+        const int row = 2 * k + (r & 1);
+        const bool ok = k < a.ppp && row < a.nrow;
+        meta.row[s][r] = ok ? row : -1;
+        meta.delta[s][r] = 2;
+        if (ok) tot += (uint32_t)(a.sp_parts * a.sp_kp * 8);
+      }
+      mbar_arrive_expect_tx(&gbar[s][f], tot);
+      for (int r = 2 * f; r < 2 * f + 2; ++r) {
+        const int row = meta.row[s][r];
+        if (row < 0) continue;
+        const double* A = a.src + (plane * a.nrow + row) * a.sp_kp;
+        double* dstrow = gbuf(s, f) + (r & 1) * a.rowslot + 2;
+        for (int q = 0; q < a.sp_parts; ++q)
+          bulk_g2s(dstrow + q * a.sp_kp, A + q * a.sp_bstride, (uint32_t)(a.sp_kp * 8),
+                   &gbar[s][f]);
+      }
+      return;
+    }
     uint32_t total = 0;
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {
@@ -684,7 +732,10 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
         if (indep) {
           group_sync<T>(f);
           if (t == 0) {
-            if (row0 >= 0) tensor_s2g_4d(&omap, 0, 0, row0, (int)plane, gb);
+            if (row0 >= 0) {
+              if (a.packed) tensor_s2g_5d(&omap, 0, 0, 0, row0, (int)plane, gb);
+              else tensor_s2g_4d(&omap, 0, 0, row0, (int)plane, gb);
+            }
             bulk_commit();
           }
         } else {
@@ -692,7 +743,10 @@ __global__ void __launch_bounds__(kMaxThreads<P, E, MODE>, (kMinBlocks<P, E, MOD
           if (threadIdx.x == 0) {
             for (int gg = 0; gg < a.NF; ++gg) {
               const int r0 = meta.row[s][2 * gg];
-              if (r0 >= 0) tensor_s2g_4d(&omap, 0, 0, r0, (int)plane, gbuf(s, gg));
+              if (r0 >= 0) {
+                if (a.packed) tensor_s2g_5d(&omap, 0, 0, 0, r0, (int)plane, gbuf(s, gg));
+                else tensor_s2g_4d(&omap, 0, 0, r0, (int)plane, gbuf(s, gg));
+              }
             }
             bulk_commit();
           }
@@ -1016,10 +1070,18 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   a.wc = k.wc;
   a.desc = k.mode == kYB;
   a.dbg = g_tune_wave_dbg;
-  a.tstore = (k.mode != kTran && k.mode != kYF2) &&
-             (g_tune_tstore || k.mode == kYF || k.mode == kYB) && M >= 16 &&
-             a.out_ld >= M && !(reinterpret_cast<uintptr_t>(a.dst) & 15) && !(a.out_ld & 1) &&
-             !(a.out_ps & 1);
+  // packed output: the line's M positions as pack_parts pieces of pack_kp in the
+  // exchange blocks (whole 128-byte segments per piece)
+  a.packed = k.pack_parts > 1;
+  if (a.packed && ((k.mode != kRow && k.mode != kTload) || k.pack_kp % 16 ||
+                   (long long)k.pack_kp * k.pack_parts != M || (k.pack_bstride & 1) ||
+                   (reinterpret_cast<uintptr_t>(a.dst) & 15) || k.pack_parts > 256))
+    return HFB_ERR_ARGUMENT;
+  a.tstore = a.packed ||
+             ((k.mode != kTran && k.mode != kYF2) &&
+              (g_tune_tstore || k.mode == kYF || k.mode == kYB) && M >= 16 &&
+              a.out_ld >= M && !(reinterpret_cast<uintptr_t>(a.dst) & 15) && !(a.out_ld & 1) &&
+              !(a.out_ps & 1));
   if ((k.mode == kYF || k.mode == kYB) && !a.tstore) return HFB_ERR_ARGUMENT;
   a.pbulk = !a.tstore && (k.mode == kRow || k.mode == kTload) && E == 16 && g_tune_pbulk &&
             a.out_ld == a.N && !(reinterpret_cast<uintptr_t>(a.dst) & 7);
@@ -1040,7 +1102,21 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   a.gbuf = gb;
   CUtensorMap omap;
   memset(&omap, 0, sizeof(omap));
-  if (a.tstore) {
+  if (a.packed) {
+    auto enc = tensor_encoder();
+    if (!enc) return HFB_ERR_CUDA;
+    const cuuint64_t kp = (cuuint64_t)k.pack_kp;
+    cuuint64_t dims[5] = {16, kp / 16, (cuuint64_t)k.pack_parts, (cuuint64_t)a.nrow,
+                          (cuuint64_t)(a.z0 + a.nz)};
+    cuuint64_t strides[4] = {128, (cuuint64_t)k.pack_bstride * 8, kp * 8,
+                             (cuuint64_t)a.nrow * kp * 8};
+    cuuint32_t box[5] = {16, (cuuint32_t)(kp / 16), (cuuint32_t)k.pack_parts, 2, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = enc(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, a.dst, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return HFB_ERR_ARGUMENT;
+  } else if (a.tstore) {
     auto enc = tensor_encoder();
     if (!enc) return HFB_ERR_CUDA;
     cuuint64_t dims[4] = {16, (cuuint64_t)(M / 16), (cuuint64_t)a.nrow,
@@ -1161,6 +1237,18 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   }
   if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, tmap, omap, umap, threads, sm, st);
   if (k.mode == kTload) return launch_stream<P, E, kTload>(a, c, tmap, omap, umap, threads, sm, st);
+  if (k.split_parts > 1) {
+    // input lines split over exchange blocks: whole 16-byte aligned pieces
+    if ((long long)k.split_kp * k.split_parts != M || (k.split_kp & 1) || (k.split_bstride & 1) ||
+        (reinterpret_cast<uintptr_t>(a.src) & 15))
+      return HFB_ERR_ARGUMENT;
+    a.sp_parts = k.split_parts;
+    a.sp_kp = k.split_kp;
+    a.sp_bstride = k.split_bstride;
+    if constexpr (E == 16 && P >= 6)
+      return launch_stream<P, E, kRowS>(a, c, tmap, omap, umap, threads, sm, st);
+    return HFB_ERR_ARGUMENT;
+  }
   return launch_stream<P, E, kRow>(a, c, tmap, omap, umap, threads, sm, st);
 }
 

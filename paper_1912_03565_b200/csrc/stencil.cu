@@ -1124,6 +1124,37 @@ extern "C" int hfb_forward_modes(hfb_plan* p, const double* src, double* modes, 
   return forward_modes(p, src, modes, (double*)work, (cudaStream_t)stream);
 }
 
+// kp of the uniform exchange geometry (every part's y-range rounded up to even is
+// the same kp and parts * kp = n_y + 1, whole 128-byte segments), else 0
+static int uniform_kp(const hfb_plan* p, const int* ys, int parts) {
+  if (!ys || parts < 2 || ys[0] != 0 || ys[parts] != p->ny) return 0;
+  const int kp = (p->ny + 1) / parts;
+  if (kp * parts != p->ny + 1 || kp % 16) return 0;
+  for (int q = 0; q < parts; ++q)
+    if (ys[q] != q * kp) return 0;
+  return kp;
+}
+
+extern "C" int hfb_forward_blocks(hfb_plan* p, const double* src, double* send, void* work,
+                                  const int* ys, int parts, void* stream) {
+  const NvtxRange nvtx_("hfb_forward_blocks");
+  if (!p || !src || !send || !work) return HFB_ERR_ARGUMENT;
+  const int kp = uniform_kp(p, ys, parts);
+  if (!kp) return HFB_ERR_PARTITION;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return forward_modes(p, src, send, (double*)work, (cudaStream_t)stream, parts, kp);
+}
+
+extern "C" int hfb_inverse_blocks(hfb_plan* p, const double* back, double* modes, double* out,
+                                  const int* ys, int parts, void* stream) {
+  const NvtxRange nvtx_("hfb_inverse_blocks");
+  if (!p || !back || !modes || !out) return HFB_ERR_ARGUMENT;
+  const int kp = uniform_kp(p, ys, parts);
+  if (!kp) return HFB_ERR_PARTITION;
+  HFB_CUDA(cudaSetDevice(p->device));
+  return inverse_modes_blocks(p, back, modes, out, parts, kp, (cudaStream_t)stream);
+}
+
 extern "C" int hfb_inverse_modes(hfb_plan* p, double* modes, double* out, void* stream) {
   const NvtxRange nvtx_("hfb_inverse_modes");
   if (!p || !modes || !out) return HFB_ERR_ARGUMENT;

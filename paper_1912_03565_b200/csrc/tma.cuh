@@ -132,6 +132,15 @@ __device__ __forceinline__ void tensor_s2g_4d(const void* tmap, int c0, int c1, 
       "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
       : "memory");
 }
+// 5D tiled tensor store of a shared-memory box (bulk-group completion).
+__device__ __forceinline__ void tensor_s2g_5d(const void* tmap, int c0, int c1, int c2, int c3,
+                                              int c4, const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], "
+      "[%6];" ::"l"(reinterpret_cast<uint64_t>(tmap)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(src))
+      : "memory");
+}
 // 3D tiled tensor store of a shared-memory box (bulk-group completion).
 __device__ __forceinline__ void tensor_s2g_3d(const void* tmap, int c0, int c1, int c2,
                                               const void* src) {

@@ -30,6 +30,7 @@ block extents are exactly (n_x, kpy(q), kpz(p)) as in ExchangePlan.
 """
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -52,6 +53,24 @@ def split_sizes(ex, rank):
 
 def y_starts(ex):
     return np.array([r[0] for r in ex.partition.y_ranges] + [ex.n_y], dtype=np.int32)
+
+
+# The transforms write / read the exchange blocks themselves (hfb_forward_blocks,
+# hfb_inverse_blocks: no pack / unpack pass) whenever the exchange geometry is
+# uniform; False keeps the pack / unpack kernels everywhere (A/B and tests).
+FUSED_BLOCKS = os.environ.get("HFB_FUSED_BLOCKS", "1") != "0"
+
+
+def fused_blocks(ex):
+    """True when the block transforms apply: every part owns kp = (n_y + 1) / parts
+    y-modes (the last one kp - 1 plus the padding column), kp a multiple of 16, and
+    both line lengths run on the FFT engine (n + 1 >= 64)."""
+    if not FUSED_BLOCKS or ex.n_parts < 2:
+        return False
+    kp, rem = divmod(ex.n_y + 1, ex.n_parts)
+    if rem or kp % 16 or ex.n_x + 1 < 64 or ex.n_y + 1 < 64:
+        return False
+    return all(y0 == q * kp for q, (y0, _) in enumerate(ex.partition.y_ranges))
 
 
 def pack_blocks_reference(z_slab, ex):
@@ -121,13 +140,17 @@ def forward_to_blocks(z_slab, grid, ex, rank):
     modes = torch.empty(kpz * grid.n_x * ldm, dtype=torch.float64, device=dev)
     with tplan.lock:
         work = tplan.workspace(5)
-        check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(z_slab), ptr(modes), ptr(work), st),
-              "forward_modes")
         send = torch.empty(sum(mode_split_sizes(ex, rank)[0]), dtype=torch.float64, device=dev)
         ys = y_starts(ex)
-        check(tplan.lib.hfb_pack_modes(tplan.handle, ptr(modes), ptr(send),
-                                       ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
-                                       ex.n_parts, st), "pack_modes")
+        ysp = ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+        if fused_blocks(ex):  # `modes` stays scratch for the way back
+            check(tplan.lib.hfb_forward_blocks(tplan.handle, ptr(z_slab), ptr(send), ptr(work),
+                                               ysp, ex.n_parts, st), "forward_blocks")
+        else:
+            check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(z_slab), ptr(modes), ptr(work),
+                                              st), "forward_modes")
+            check(tplan.lib.hfb_pack_modes(tplan.handle, ptr(modes), ptr(send), ysp, ex.n_parts,
+                                           st), "pack_modes")
     return send, modes
 
 
@@ -161,11 +184,15 @@ def blocks_to_solution(back, modes, grid, ex, rank, out=None):
     with tplan.lock:
         st = tplan.stream()
         ys = y_starts(ex)
-        check(tplan.lib.hfb_unpack_modes(tplan.handle, ptr(back), ptr(modes),
-                                         ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
-                                         ex.n_parts, st), "unpack_modes")
-        check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(modes), ptr(out), st),
-              "inverse_modes")
+        ysp = ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+        if fused_blocks(ex):
+            check(tplan.lib.hfb_inverse_blocks(tplan.handle, ptr(back), ptr(modes), ptr(out), ysp,
+                                               ex.n_parts, st), "inverse_blocks")
+        else:
+            check(tplan.lib.hfb_unpack_modes(tplan.handle, ptr(back), ptr(modes), ysp,
+                                             ex.n_parts, st), "unpack_modes")
+            check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(modes), ptr(out), st),
+                  "inverse_modes")
     return out
 
 
@@ -230,14 +257,18 @@ def forward_chunk(z_slab, modes, grid, ex, rank, c0, c1):
     with tplan.lock:
         st = tplan.stream()
         work = tplan.workspace(5)
-        check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(z_slab[c0:c1]), ptr(m), ptr(work), st),
-              "forward_modes")
         kp = [((y1 - y0) + 1) & ~1 for y0, y1 in ex.partition.y_ranges]
         send = torch.empty((c1 - c0) * grid.n_x * sum(kp), dtype=torch.float64, device=dev)
         ys = y_starts(ex)
-        check(tplan.lib.hfb_pack_modes(tplan.handle, ptr(m), ptr(send),
-                                       ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
-                                       ex.n_parts, st), "pack_modes")
+        ysp = ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+        if fused_blocks(ex):
+            check(tplan.lib.hfb_forward_blocks(tplan.handle, ptr(z_slab[c0:c1]), ptr(send),
+                                               ptr(work), ysp, ex.n_parts, st), "forward_blocks")
+        else:
+            check(tplan.lib.hfb_forward_modes(tplan.handle, ptr(z_slab[c0:c1]), ptr(m), ptr(work),
+                                              st), "forward_modes")
+            check(tplan.lib.hfb_pack_modes(tplan.handle, ptr(m), ptr(send), ysp, ex.n_parts, st),
+                  "pack_modes")
     return send
 
 
@@ -250,11 +281,15 @@ def inverse_chunk(back, modes, out, grid, ex, c0, c1):
     with tplan.lock:
         st = tplan.stream()
         ys = y_starts(ex)
-        check(tplan.lib.hfb_unpack_modes(tplan.handle, ptr(back), ptr(m),
-                                         ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
-                                         ex.n_parts, st), "unpack_modes")
-        check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(m), ptr(out[c0:c1]), st),
-              "inverse_modes")
+        ysp = ys.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+        if fused_blocks(ex):
+            check(tplan.lib.hfb_inverse_blocks(tplan.handle, ptr(back), ptr(m), ptr(out[c0:c1]),
+                                               ysp, ex.n_parts, st), "inverse_blocks")
+        else:
+            check(tplan.lib.hfb_unpack_modes(tplan.handle, ptr(back), ptr(m), ysp, ex.n_parts, st),
+                  "unpack_modes")
+            check(tplan.lib.hfb_inverse_modes(tplan.handle, ptr(m), ptr(out[c0:c1]), st),
+                  "inverse_modes")
 
 
 def solve_received_chunked(recv, level_plane, scheme, profile, grid, ex, rank):

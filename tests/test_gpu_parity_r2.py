@@ -324,6 +324,67 @@ def test_checkpoint_cache_bitwise(cuda, shape):
         plan.set_workspace_mode(False)
 
 
+@pytest.mark.parametrize("shape,parts", [((127, 127, 16), 4), ((255, 511, 12), 8),
+                                         ((1023, 1023, 8), 8), ((63, 63, 9), 2),
+                                         ((2047, 511, 5), 4), ((511, 2047, 16), 8)])
+def test_block_transforms_bitwise(cuda, shape, parts):
+    """hfb_forward_blocks / hfb_inverse_blocks (the y-pass stores mode rows straight
+    into the exchange blocks through a 5D tensor map; the inverse y-pass gathers
+    its rows from the returned blocks) against forward_modes + pack_modes and
+    unpack_modes + inverse_modes: the same bits in every valid block entry and in
+    the solution planes, whole slabs and plane chunks, for every rank's slab."""
+    import torch
+    from paper_1912_03565_b200 import distributed as hd
+    nx, ny, nz = shape
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+    ex = hb.make_exchange_plan(g, parts)
+    assert hd.fused_blocks(ex)
+    rng = np.random.default_rng(17)
+    kp = (ny + 1) // parts
+    try:
+        for rank in (0, parts - 1):
+            z0, z1 = ex.partition.z_ranges[rank]
+            kpz = z1 - z0
+            if kpz == 0:
+                continue
+            slab = torch.from_numpy(rng.standard_normal((kpz, ny, nx))).cuda()
+            back = torch.from_numpy(rng.standard_normal(kpz * nx * kp * parts)).cuda()
+
+            def valid(buf, planes):  # drop the padding column of the last block
+                return [buf.reshape(parts, planes, nx, kp)[q, :, :, :y1 - y0].cpu().numpy()
+                        for q, (y0, y1) in enumerate(ex.partition.y_ranges)]
+
+            res = {}
+            for fused in (False, True):
+                hd.FUSED_BLOCKS = fused
+                send, modes = hd.forward_to_blocks(slab, g, ex, rank)
+                out = hd.blocks_to_solution(back, modes, g, ex, rank)
+                c0, c1 = kpz // 3, kpz  # a plane chunk through the chunked helpers
+                m2 = torch.empty_like(modes)
+                csend = hd.forward_chunk(slab, m2, g, ex, rank, c0, c1)
+                cout = torch.zeros((kpz, ny, nx), dtype=torch.float64, device="cuda")
+                hd.inverse_chunk(back[:(c1 - c0) * nx * kp * parts], m2, cout, g, ex, c0, c1)
+                torch.cuda.synchronize()
+                res[fused] = (valid(send, kpz), out.cpu().numpy(), valid(csend, c1 - c0),
+                              cout.cpu().numpy())
+            for a, b in zip(res[False], res[True]):
+                if isinstance(a, list):
+                    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+                else:
+                    assert np.array_equal(a, b)
+            assert np.isfinite(res[True][1]).all()
+    finally:
+        hd.FUSED_BLOCKS = True
+
+
+def test_block_transforms_need_uniform_geometry(cuda):
+    """Ragged exchange geometries (3 parts of 1023 modes) keep the pack path."""
+    from paper_1912_03565_b200 import distributed as hd
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), 1023, 1023, 9)
+    assert not hd.fused_blocks(hb.make_exchange_plan(g, 3))
+    assert hd.fused_blocks(hb.make_exchange_plan(g, 8))
+
+
 @pytest.mark.parametrize("scheme", ["6", "cd4"])
 def test_zsolve_default_vs_oracle(cuda, scheme):
     """The default z-solve (sparse x', guard-free interior chunks; for the
