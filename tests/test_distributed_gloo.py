@@ -81,6 +81,30 @@ def test_split_sizes_match_exchange_plan_blocks():
     assert list(hd.y_starts(ex)) == [0, 128, 256, 384, 512, 640, 768, 896, 1023]
 
 
+def test_fused_block_geometry_predicate():
+    """distributed.fused_blocks: the block transforms (no pack / unpack pass) apply
+    exactly to the uniform exchange geometry — kp = (n_y + 1) / parts for every
+    part, a multiple of 16, FFT-engine line lengths — which covers every BASELINE
+    config at 2, 4 and 8 ranks; everything else keeps the pack kernels. The block
+    sizes of mode_split_sizes are then parts equal blocks of kpz * n_x * kp."""
+    from paper_1912_03565_b200 import distributed as hd
+    mk = lambda nx, ny, nz: hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+    for n in (511, 1023, 2047):
+        for parts in (2, 4, 8):
+            ex = hb.make_exchange_plan(mk(n, n, n), parts)
+            assert hd.fused_blocks(ex), (n, parts)
+            kp = (n + 1) // parts
+            for r in range(parts):
+                z0, z1 = ex.partition.z_ranges[r]
+                assert hd.mode_split_sizes(ex, r)[0] == [(z1 - z0) * n * kp] * parts
+    assert not hd.fused_blocks(hb.make_exchange_plan(mk(1023, 1023, 1023), 3))   # ragged
+    assert not hd.fused_blocks(hb.make_exchange_plan(mk(1023, 1023, 1023), 1))   # one part
+    assert not hd.fused_blocks(hb.make_exchange_plan(mk(1023, 100, 64), 4))      # not 2^p
+    assert not hd.fused_blocks(hb.make_exchange_plan(mk(31, 31, 31), 2))         # DMMA sizes
+    assert not hd.fused_blocks(hb.make_exchange_plan(mk(1023, 127, 64), 16))     # kp = 8
+    assert hd.fused_blocks(hb.make_exchange_plan(mk(63, 255, 64), 16))           # kp = 16
+
+
 @pytest.mark.parametrize("parts", [1, 2, 3, 8])
 def test_mode_split_sizes_consistent(parts):
     """Mode-space exchange: what p sends to q is what q expects from p, blocks
