@@ -685,6 +685,88 @@ def _nccl_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _a2a_worker(rank, world, port, q, shape):
+    """One rank of solve_partitioned in its own process (all ranks on GPU 0): a gloo
+    group, and all_to_all_single staged through host tensors (gloo has no CUDA
+    all-to-all; NCCL refuses two ranks on one GPU) — everything else is the code
+    path of a real multi-GPU run: plan_partition, chunked block transforms,
+    chunk-ordered y-slab z-solve, split sizes."""
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1912_03565_b200 import distributed as hd
+        torch.cuda.set_device(0)
+        nx, ny, nz = shape
+        g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+        prof = hb.constant_profile(-20.0, g)
+        F = torch.from_numpy(np.random.default_rng(3).standard_normal((nz, ny, nx))).cuda()
+        z0, z1 = hb.plan_partition(nz, world)[rank]
+        real_a2a = dist.all_to_all_single
+
+        class Done:
+            def wait(self):
+                return True
+
+        def staged(out, inp, output_split_sizes=None, input_split_sizes=None, group=None,
+                   async_op=False):
+            torch.cuda.synchronize()
+            host_out = torch.empty(out.numel(), dtype=out.dtype)
+            real_a2a(host_out, inp.cpu(), output_split_sizes, input_split_sizes, group=group)
+            out.copy_(host_out)
+            torch.cuda.synchronize()
+            return Done() if async_op else None
+
+        dist.all_to_all_single = staged
+        fused = hd.fused_blocks(hb.make_exchange_plan(g, world))
+        outs = []
+        for _ in range(2):  # twice: buffers and plans reused
+            U = hd.solve_partitioned(F[z0:z1].contiguous(), hb.SchemeKind.FOURTH_ORDER, prof, g,
+                                     check=False)
+            torch.cuda.synchronize()
+            outs.append(U.cpu().numpy())
+        hb._native.get_plan(nx, ny, nz, torch.device("cuda", 0)).fetch_status()
+        assert np.array_equal(outs[0], outs[1])
+        q.put((rank, outs[0], fused))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape", [(2, (127, 127, 24)), (4, (127, 255, 19)),
+                                         (3, (127, 127, 17))])
+def test_solve_partitioned_processes_one_gpu(cuda, world, shape):
+    """solve_partitioned with one PROCESS per rank (2 and 4 ranks: the fused block
+    transforms; 3 ranks: the ragged geometry with the pack kernels), the exchange
+    staged through the host: the concatenated slabs equal the one-call solve bit
+    for bit."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, world, port, q, shape))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in range(world)), key=lambda x: x[0])
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(r[2] == (world != 3) for r in res)
+    U = np.concatenate([r[1] for r in res])
+    nx, ny, nz = shape
+    g = hb.make_grid(hb.Domain(0, 1, 0, 1, 0, 1), nx, ny, nz)
+    F = torch.from_numpy(np.random.default_rng(3).standard_normal((nz, ny, nx))).cuda()
+    ref = _one_call(F, hb.SchemeKind.FOURTH_ORDER, hb.constant_profile(-20.0, g), g)
+    assert np.array_equal(U, ref.cpu().numpy())
+
+
 def test_solve_partitioned_nccl_single_rank(cuda):
     """solve_partitioned through a real NCCL communicator (one rank: this box has
     one GPU) against the one-call solve."""
