@@ -161,6 +161,12 @@ size_t hfb_workspace_bytes(const hfb_plan* plan, int op);
  * the current mode, which hfb_solve then expects. Default 0. */
 int hfb_plan_set_workspace_mode(hfb_plan* plan, int lean);
 
+/* Give back the device memory the plan allocated on its own for reuse across
+ * solves: the z-solve's cached cp checkpoints (tuning key 32; one plane per 8
+ * levels, 1.07 GB at 1023^3). The next hfb_solve allocates and fills them again.
+ * For callers that keep many plans alive and run short of memory. */
+int hfb_plan_trim(hfb_plan* plan);
+
 /* Per-stage CUDA events of the one-call solve (measurement only). With a ring
  * of R > 0 slots, each hfb_solve records an event before its first and after
  * each of its five launches on the caller's stream, in slot (solve count mod

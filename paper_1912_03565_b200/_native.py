@@ -47,6 +47,7 @@ SIGNATURES = {
     "hfb_launch_count": (ctypes.c_uint64, []),
     "hfb_set_tuning": (None, [_i, _i]),
     "hfb_plan_set_workspace_mode": (_i, [_vp, _i]),
+    "hfb_plan_trim": (_i, [_vp]),
     "hfb_stage_timing": (_i, [_vp, _i]),
     "hfb_modes_ld": (_i, [_vp]),
     "hfb_rhs_sixth_z": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_double, _vp, _vp,
@@ -235,8 +236,13 @@ class DevicePlan:
         try:
             return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         except torch.OutOfMemoryError:
-            if op not in (0, 3):
-                raise
+            trim_plans()  # the other cached plans' own device memory (checkpoint caches)
+            torch.cuda.empty_cache()
+            try:
+                return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            except torch.OutOfMemoryError:
+                if op not in (0, 3):
+                    raise
         torch.cuda.empty_cache()
         self.set_workspace_mode(True)
         nbytes = int(self.lib.hfb_workspace_bytes(self.handle, op))
@@ -260,6 +266,15 @@ class DevicePlan:
 
 _plans = {}
 _plans_lock = threading.Lock()
+
+
+def trim_plans():
+    """hfb_plan_trim on every cached plan: frees the memory the plans allocated
+    themselves (the z-solve's cached checkpoints); the next solve rebuilds it."""
+    with _plans_lock:
+        plans = list(_plans.values())
+    for plan in plans:
+        plan.lib.hfb_plan_trim(plan.handle)
 
 
 def get_plan(n_x, n_y, n_z, device=None) -> DevicePlan:

@@ -282,6 +282,18 @@ extern "C" int hfb_plan_set_workspace_mode(hfb_plan* p, int lean) {
   return HFB_OK;
 }
 
+extern "C" int hfb_plan_trim(hfb_plan* p) {
+  if (!p) return HFB_ERR_ARGUMENT;
+  HFB_CUDA(cudaSetDevice(p->device));
+  if (p->ck_cache) {
+    HFB_CUDA(cudaFree(p->ck_cache));  // waits for the work that still reads it
+    p->ck_cache = nullptr;
+    p->ck_cache_bytes = 0;
+    p->ck_valid = 0;
+  }
+  return HFB_OK;
+}
+
 extern "C" size_t hfb_workspace_bytes(const hfb_plan* p, int op) {
   if (!p) return 0;
   const size_t vol = (size_t)p->nx * p->ny * p->nz;
