@@ -318,6 +318,9 @@ def test_checkpoint_cache_bitwise(cuda, shape):
             assert np.array_equal(solve(lean=True), refs[t, "lean"]), ("lean layout", t)
             assert np.array_equal(solve(lean=True), refs[t, "lean"]), ("lean layout, cached", t)
             assert np.array_equal(solve(), refs[t]), ("fast layout again", t)
+            _native.check(lib.hfb_plan_trim(plan.handle), "trim")  # cache freed, rebuilt
+            assert np.array_equal(solve(), refs[t]), ("after hfb_plan_trim", t)
+            assert np.array_equal(solve(), refs[t]), ("after hfb_plan_trim, cached", t)
     finally:
         lib.hfb_set_tuning(30, 0)
         lib.hfb_set_tuning(32, 1)
