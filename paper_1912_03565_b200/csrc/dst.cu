@@ -908,7 +908,7 @@ int forward_modes(hfb_plan* p, const double* src, double* modes, double* S1, cud
   if (!tran_path(p) || !S1) return HFB_ERR_ARGUMENT;
   const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), ldx = x_ld(p);
   if (dmma2d_np(p)) {  // small N: the one-call solve's DMMA transform (bitwise the same)
-    if (parts > 1) return HFB_ERR_ARGUMENT;  // no packed output on this path
+    if (parts > 0) return HFB_ERR_ARGUMENT;  // no packed output on this path
     D2Layout fw = {p->nx, ps, ldt, ldt * p->nx, 0, 1};
     return launch_dmma2d(p, src, modes, 0, p->nz, st, &fw);
   }
@@ -944,7 +944,7 @@ int forward_modes(hfb_plan* p, const double* src, double* modes, double* S1, cud
   y.dst = modes;
   y.out_ld = ldt;
   y.out_ps = ldt * p->nx;
-  if (parts > 1) {
+  if (parts > 0) {
     // straight into the exchange blocks: block q = (n_z, n_x, kp), the line's
     // positions [q kp, (q + 1) kp) (modes is the send buffer)
     y.pack_parts = parts;
@@ -998,7 +998,7 @@ int inverse_modes(hfb_plan* p, double* modes, double* out, cudaStream_t st) {
 
 int inverse_modes_blocks(hfb_plan* p, const double* back, double* modes, double* out, int parts,
                          int kp, cudaStream_t st) {
-  if (!tran_path(p) || dmma2d_np(p) || parts < 2) return HFB_ERR_ARGUMENT;
+  if (!tran_path(p) || dmma2d_np(p) || parts < 1) return HFB_ERR_ARGUMENT;
   const long long ps = (long long)p->ny * p->nx, ldt = tran_ld(p), pst = ldt * p->nx;
   Dst16Call y = {};
   y.tw = p->tw_y;

@@ -1072,7 +1072,7 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   a.dbg = g_tune_wave_dbg;
   // packed output: the line's M positions as pack_parts pieces of pack_kp in the
   // exchange blocks (whole 128-byte segments per piece)
-  a.packed = k.pack_parts > 1;
+  a.packed = k.pack_parts > 0;
   if (a.packed && ((k.mode != kRow && k.mode != kTload) || k.pack_kp % 16 ||
                    (long long)k.pack_kp * k.pack_parts != M || (k.pack_bstride & 1) ||
                    (reinterpret_cast<uintptr_t>(a.dst) & 15) || k.pack_parts > 256))
@@ -1237,7 +1237,7 @@ static int launch_pe(const Dst16Call& k, StreamArgs a, const FftArgs& c, cudaStr
   }
   if (k.mode == kTran) return launch_stream<P, E, kTran>(a, c, tmap, omap, umap, threads, sm, st);
   if (k.mode == kTload) return launch_stream<P, E, kTload>(a, c, tmap, omap, umap, threads, sm, st);
-  if (k.split_parts > 1) {
+  if (k.split_parts > 0) {
     // input lines split over exchange blocks: whole 16-byte aligned pieces
     if ((long long)k.split_kp * k.split_parts != M || (k.split_kp & 1) || (k.split_bstride & 1) ||
         (reinterpret_cast<uintptr_t>(a.src) & 15))

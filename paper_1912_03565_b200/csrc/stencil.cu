@@ -1127,7 +1127,7 @@ extern "C" int hfb_forward_modes(hfb_plan* p, const double* src, double* modes, 
 // kp of the uniform exchange geometry (every part's y-range rounded up to even is
 // the same kp and parts * kp = n_y + 1, whole 128-byte segments), else 0
 static int uniform_kp(const hfb_plan* p, const int* ys, int parts) {
-  if (!ys || parts < 2 || ys[0] != 0 || ys[parts] != p->ny) return 0;
+  if (!ys || parts < 1 || ys[0] != 0 || ys[parts] != p->ny) return 0;
   const int kp = (p->ny + 1) / parts;
   if (kp * parts != p->ny + 1 || kp % 16) return 0;
   for (int q = 0; q < parts; ++q)

@@ -65,7 +65,7 @@ def fused_blocks(ex):
     """True when the block transforms apply: every part owns kp = (n_y + 1) / parts
     y-modes (the last one kp - 1 plus the padding column), kp a multiple of 16, and
     both line lengths run on the FFT engine (n + 1 >= 64)."""
-    if not FUSED_BLOCKS or ex.n_parts < 2:
+    if not FUSED_BLOCKS:
         return False
     kp, rem = divmod(ex.n_y + 1, ex.n_parts)
     if rem or kp % 16 or ex.n_x + 1 < 64 or ex.n_y + 1 < 64:

@@ -98,7 +98,7 @@ def test_fused_block_geometry_predicate():
                 z0, z1 = ex.partition.z_ranges[r]
                 assert hd.mode_split_sizes(ex, r)[0] == [(z1 - z0) * n * kp] * parts
     assert not hd.fused_blocks(hb.make_exchange_plan(mk(1023, 1023, 1023), 3))   # ragged
-    assert not hd.fused_blocks(hb.make_exchange_plan(mk(1023, 1023, 1023), 1))   # one part
+    assert hd.fused_blocks(hb.make_exchange_plan(mk(1023, 1023, 1023), 1))       # one part
     assert not hd.fused_blocks(hb.make_exchange_plan(mk(1023, 100, 64), 4))      # not 2^p
     assert not hd.fused_blocks(hb.make_exchange_plan(mk(31, 31, 31), 2))         # DMMA sizes
     assert not hd.fused_blocks(hb.make_exchange_plan(mk(1023, 127, 64), 16))     # kp = 8
